@@ -1,0 +1,179 @@
+/*
+ * mgauss_b200.h -- C ABI of the B200 (sm_100a) M-Gaussian rendering path.
+ *
+ * Every entry point takes raw DEVICE pointers, element counts and a
+ * cudaStream_t passed as void*; none allocates (scratch comes from the
+ * caller's `ws` buffer, sized by the matching *_workspace_bytes query); all
+ * are asynchronous on `stream` and return 0 on success, a negative CUDA
+ * error code on a launch failure, or a positive MG_E* code for an argument
+ * error (message via mg_last_error()).  Domain errors raised by the
+ * reference's Python wrappers (DegenerateQuaternion, InconsistentGrid,
+ * OutOfMemoryRequest, ValueError) are raised by the host layer, exactly as
+ * the reference raises them outside its kernels.
+ *
+ * Reference interfaces each group replaces (paths under
+ * /root/reference/pkg/src/mgauss):
+ *   mg_block_forward / mg_block_backward / mg_dense_forward
+ *        -> _kernels.block_forward (_kernels.py:24-27), block_backward
+ *           (_kernels.py:73-76), dense_forward (_kernels.py:147-148):
+ *           same argument list and meaning, float64/int64 device arrays.
+ *   mg_bin_f32 / mg_bin_f64 / mg_cell_keys_f64
+ *        -> spatial.cell_index / spatial.build (spatial.py:18-66)
+ *   mg_activate / mg_activate_f64
+ *        -> render.activated_parameters (render.py:122-142)
+ *   mg_bin_points + mg_forward + mg_forward_finish
+ *        -> render.render_points (render.py:161-187), plus the slice-PSF
+ *           tap expansion
+ *   mg_backward_points + mg_backward + mg_backward_epilogue /
+ *   mg_backward_accumulators
+ *        -> render.render_backward (render.py:276-354)
+ *   mg_transform_grads -> render.transform_grads_from_points (render.py:246-273)
+ *   mg_sample_volume   -> render.sample_volume (render.py:379-408)
+ *   mg_smooth_l1 / mg_gauss_update / mg_transform_adam / mg_upsample
+ *        -> train.smooth_l1(_grad) (train.py:108-120), AdamState.step +
+ *           aniso_loss_grad (train.py:128-147, 239-271), progressive_upsample
+ *           (train.py:157-218)
+ */
+#ifndef MGAUSS_B200_H
+#define MGAUSS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MG_ABI_VERSION 1
+#define MG_EINVAL 1
+
+int mg_abi_version(void);
+const char *mg_last_error(void);
+int mg_device_sm_count(void);
+
+/* ---- binning: spatial.py:18-66 ------------------------------------------ */
+/* keys[i] = (ci*G + cj)*G + ck with c = clamp(floor((x+1)*(G/2)), 0, G-1) in float64 */
+int mg_cell_keys_f64(const double *pos, int64_t n, int64_t grid_res, uint32_t *keys, void *stream);
+size_t mg_bin_workspace_bytes(int64_t n, int64_t grid_res);
+/* Stable bucket sort: keys_sorted (n), cell_indices (n, ascending primitive id
+ * within a cell), cell_starts (G^3+1).  int32 on device. */
+int mg_bin_f32(const float *pos, int64_t n, int64_t grid_res, uint32_t *keys_sorted, int32_t *cell_indices,
+               int32_t *cell_starts, void *ws, size_t ws_bytes, void *stream);
+int mg_bin_f64(const double *pos, int64_t n, int64_t grid_res, uint32_t *keys_sorted, int32_t *cell_indices,
+               int32_t *cell_starts, void *ws, size_t ws_bytes, void *stream);
+/* keys_sorted[p] = the cell c with cell_starts[c] <= p < cell_starts[c+1]
+ * (follows a caller-supplied CSR exactly, like the reference kernels do). */
+int mg_keys_from_csr(const int32_t *cell_starts, int64_t ncell, uint32_t *keys_sorted, void *stream);
+/* int64 -> int32 copy (device CSR from the reference's int64 arrays). */
+int mg_i64_to_i32(const int64_t *src, int64_t n, int32_t *dst, void *stream);
+/* int32 -> int64 copies in the reference dtype (PartitionGrid fields). */
+int mg_i32_to_i64(const int32_t *src, int64_t n, int64_t *dst, void *stream);
+
+/* ---- preprocessing: render.py:122-142 ----------------------------------- */
+/* Packed records (48 B each, cell order: rec[p] describes primitive
+ * cell_indices[p]).  err_flag |= 1 when some |q| <= 1e-12. */
+int mg_activate(const float *pos, const float *quat, const float *log_scales, const float *logits, int64_t n,
+                const int32_t *cell_indices, void *grec, int32_t *err_flag, void *stream);
+/* Records from float64 prepared (mu (n,3), prec6 (n,6), alpha (n)) in cell order. */
+int mg_pack_records(const double *mu, const double *prec6, const double *alpha, const int32_t *cell_indices,
+                    int64_t n, void *grec, void *stream);
+/* float64 activated_parameters: qn (n,4), rot (n,3,3), inv_var (n,3), prec6 (n,6), alpha (n) */
+int mg_activate_f64(const double *quat, const double *log_scales, const double *logits, int64_t n, double *qn,
+                    double *rot, double *inv_var, double *prec6, double *alpha, int32_t *err_flag, void *stream);
+
+/* ---- sample points: transform (+ PSF taps) and bin ---------------------- */
+size_t mg_points_workspace_bytes(int64_t n_sub, int64_t grid_res);
+/* n_sub = b * ntaps.  tap_offsets (ntaps) and through_dirs (k,3) may be NULL
+ * (no PSF, ntaps = 1).  rot (k,3,3), trans (k,3) float64; slice_ids < 0 mean
+ * identity.  Outputs: pkey_sorted (n_sub), pinv (n_sub: sorted position of
+ * sub-point b*ntaps+t), pstart (G^3+1), prec (n_sub float4 records), and
+ * optionally transformed (n_sub,3) float64 in input order. */
+int mg_bin_points(const double *coords, const int64_t *slice_ids, int64_t b, int32_t ntaps,
+                  const double *tap_offsets, const double *through_dirs, const double *rot, const double *trans,
+                  int64_t k, int64_t grid_res, uint32_t *pkey_sorted, int32_t *pinv, int32_t *pstart, void *prec,
+                  double *transformed, void *ws, size_t ws_bytes, void *stream);
+
+/* ---- forward: _kernels.py:24-70 ----------------------------------------- */
+size_t mg_forward_workspace_bytes(int64_t n_sub);
+/* out4[p] = {H.x, H.y, H.z, I} per sorted sub-point (H = sum alpha g P d,
+ * only when with_h != 0); counts[p] = candidate count (sorted order). */
+int mg_forward(const void *grec, const int32_t *gstart, int64_t grid_res, int64_t radius, const void *prec,
+               const uint32_t *pkey_sorted, const int32_t *pstart, int64_t n_sub, int32_t with_h, void *out4,
+               int32_t *counts, void *ws, size_t ws_bytes, void *stream);
+/* I_b = sum_t w_t I_(b,t) (tap_weights NULL = single tap); counts summed. */
+int mg_forward_finish(const void *out4, const int32_t *counts, const int32_t *pinv, int64_t b, int32_t ntaps,
+                      const double *tap_weights, double *intensity, float *intensity_f32, int64_t *counts_out,
+                      void *stream);
+
+/* ---- backward: _kernels.py:73-144, render.py:276-354 -------------------- */
+/* upstream (b) float64 (or upstream_f32) -> prec[].w and d_points (n_sub,3, input order, may be NULL) */
+int mg_backward_points(const double *upstream, const float *upstream_f32, int64_t b, int32_t ntaps,
+                       const double *tap_weights, const int32_t *pinv, const void *out4, void *prec,
+                       double *d_points, void *stream);
+size_t mg_backward_workspace_bytes(int64_t n);
+/* Gaussian-major pair pass: acc10[p] = {S, T(3), A6(6)} per sorted Gaussian. */
+int mg_backward(const void *grec, const uint32_t *gkey_sorted, const int32_t *gstart, int64_t n, int64_t grid_res,
+                int64_t radius, const void *prec, const int32_t *pstart, float *acc10, void *ws, size_t ws_bytes,
+                void *stream);
+/* RenderGradients parameter fields (float64, primitive order). */
+int mg_backward_epilogue(const float *acc10, const int32_t *cell_indices, int64_t n, const float *quat,
+                         const float *log_scales, const float *logits, double *d_positions, double *d_quaternions,
+                         double *d_log_scales, double *d_logits, void *stream);
+/* render.py:319-340 chain rule from reference-convention float64 accumulators
+ * (d_mu, d_abar6, d_alpha) and float64 parameters; primitive order. */
+int mg_epilogue_f64(const double *d_mu, const double *d_abar6, const double *d_alpha, const double *quat,
+                    const double *log_scales, const double *logits, int64_t n, double *d_positions,
+                    double *d_quaternions, double *d_log_scales, double *d_logits, void *stream);
+/* Reference block_backward accumulators, ADDED into d_mu (n,3), d_abar6 (n,6), d_alpha (n). */
+int mg_backward_accumulators(const float *acc10, const int32_t *cell_indices, int64_t n, const double *alpha,
+                             double *d_mu, double *d_abar6, double *d_alpha, void *stream);
+/* (k,7) transform gradients; scratch12 is (k,12) float64. */
+int mg_transform_grads(const double *d_points, const double *coords, const int64_t *slice_ids, int64_t b,
+                       int32_t ntaps, const double *tap_offsets, const double *through_dirs, const double *t_quats,
+                       int64_t k, double *scratch12, double *out7, int32_t accumulate, void *stream);
+
+/* ---- inference: render.py:357-408 --------------------------------------- */
+size_t mg_volume_workspace_bytes(int64_t nx, int64_t ny, int64_t nz);
+/* Slab [i0, i1) of a node-inclusive (nx,ny,nz) grid over [lo, hi]; out is
+ * (i1-i0, ny, nz) float32 clipped to [0,1]; residual (same shape) optional. */
+int mg_sample_volume(const void *grec, const int32_t *gstart, int64_t grid_res, int64_t radius, int64_t nx,
+                     int64_t ny, int64_t nz, const double *lo3_host, const double *hi3_host, int64_t i0, int64_t i1,
+                     const float *residual, float *out, void *ws, size_t ws_bytes, void *stream);
+
+/* ---- training: train.py ------------------------------------------------- */
+int mg_smooth_l1(const void *out4, const int32_t *pinv, int64_t b, int32_t ntaps, const double *tap_weights,
+                 const float *target, const float *residual, void *prec, float *pred_out, double *loss_acc,
+                 void *stream);
+int mg_counter_incr(int32_t *counters, int32_t n, void *stream);
+/* hyper (host, 9 doubles): lr_pos, lr_quat, lr_scale, lr_logit, beta1, beta2, eps, lambda_aniso, lambda_ratio.
+ * t_dev: device int32 post-increment Adam step.  Moments m, v are (n, 11) float32. */
+int mg_gauss_update(const float *acc10, const int32_t *cell_indices, int64_t n, float *pos, float *quat,
+                    float *log_scales, float *logits, float *m, float *v, const double *hyper_host,
+                    int32_t use_aniso, const int32_t *t_dev, double *aniso_acc, void *stream);
+int mg_transform_adam(double *t_quats, double *t_trans, const double *grad7, double *m7, double *v7, int64_t k,
+                      double lr, double beta1, double beta2, double eps, const int32_t *t_dev, void *stream);
+/* node_of_old[(i*R+j)*R+k] = primitive id at lattice node (i,j,k) */
+int mg_upsample(const float *quat_old, const float *log_scales_old, const float *logits_old,
+                const int32_t *node_of_old, int64_t r_old, int64_t r_new, float *pos, float *quat,
+                float *log_scales, float *logits, void *stream);
+
+/* ---- drop-in reference kernel ABI: _kernels.py -------------------------- */
+size_t mg_block_workspace_bytes(int64_t b, int64_t n, int64_t grid_res);
+int mg_block_forward(const double *points, const int64_t *slice_ids, int64_t b, const double *rot,
+                     const double *trans, int64_t k, const double *mu, const double *prec6, const double *alpha,
+                     int64_t n, const int64_t *cell_starts, const int64_t *cell_indices, int64_t grid_res,
+                     int64_t radius, double *out_intensity, int64_t *out_counts, double *out_transformed, void *ws,
+                     size_t ws_bytes, void *stream);
+int mg_block_backward(const double *points, const int64_t *slice_ids, int64_t b, const double *rot,
+                      const double *trans, int64_t k, const double *mu, const double *prec6, const double *alpha,
+                      int64_t n, const int64_t *cell_starts, const int64_t *cell_indices, int64_t grid_res,
+                      int64_t radius, const double *upstream, double *d_mu, double *d_abar6, double *d_alpha,
+                      double *out_dpoint, void *ws, size_t ws_bytes, void *stream);
+size_t mg_dense_workspace_bytes(int64_t n);
+int mg_dense_forward(const double *points, int64_t b, const double *mu, const double *prec6, const double *alpha,
+                     int64_t n, double *out_intensity, void *ws, size_t ws_bytes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MGAUSS_B200_H */

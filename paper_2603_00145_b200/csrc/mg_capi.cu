@@ -1,0 +1,476 @@
+// mg_capi.cu -- extern "C" entry points (include/mgauss_b200.h).
+#include <stdio.h>
+#include <string.h>
+
+#include "../../include/mgauss_b200.h"
+#include "mg_render.cuh"
+#include "mg_sort.cuh"
+
+using namespace mg;
+
+namespace {
+thread_local char g_err[512] = "";
+
+int fail(const char* msg) {
+  snprintf(g_err, sizeof(g_err), "%s", msg);
+  return MG_EINVAL;
+}
+
+int cuda_status() {
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) {
+    snprintf(g_err, sizeof(g_err), "CUDA: %s", cudaGetErrorString(e));
+    cudaGetLastError();
+    return -(int)e;
+  }
+  return 0;
+}
+
+inline size_t al(size_t b) { return (b + 255) & ~(size_t)255; }
+
+struct Bump {
+  char* p;
+  size_t left;
+  bool ok = true;
+  Bump(void* base, size_t n) : p((char*)base), left(n) {}
+  template <class T>
+  T* take(size_t count) {
+    size_t b = al(count * sizeof(T) + (count == 0 ? 1 : 0));
+    if (b > left) {
+      ok = false;
+      return nullptr;
+    }
+    T* r = (T*)p;
+    p += b;
+    left -= b;
+    return r;
+  }
+  void* rest() { return p; }
+};
+
+inline cudaStream_t S(void* s) { return (cudaStream_t)s; }
+
+int64_t ncell_of(int64_t g) { return g * g * g; }
+
+// ---- small kernels local to the ABI layer ----
+__global__ void csr64_to_32_kernel(const int64_t* __restrict__ cs, int64_t ncell1, const int64_t* __restrict__ ci,
+                                   int64_t n, int* __restrict__ cs32, int* __restrict__ ci32) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ncell1 || i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < ncell1) cs32[i] = (int)cs[i];
+    if (i < n) ci32[i] = (int)ci[i];
+  }
+}
+
+// gkey[p] = cell c with cs[c] <= p < cs[c+1]  (follows the caller's CSR exactly)
+__global__ void keys_from_csr_kernel(const int* __restrict__ cs, int64_t ncell, uint32_t* __restrict__ gkey) {
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < ncell; c += (int64_t)gridDim.x * blockDim.x) {
+    for (int p = cs[c]; p < cs[c + 1]; ++p) gkey[p] = (uint32_t)c;
+  }
+}
+
+__global__ void iota32_kernel(int* __restrict__ v, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    v[i] = (int)i;
+}
+
+__global__ void i32_to_i64_kernel(const int* __restrict__ s, int64_t n, int64_t* __restrict__ d) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    d[i] = s[i];
+}
+
+__global__ void activate_f64_kernel(const double* __restrict__ quat, const double* __restrict__ ls,
+                                    const double* __restrict__ lg, int64_t n, double* __restrict__ qn,
+                                    double* __restrict__ rot, double* __restrict__ inv_var,
+                                    double* __restrict__ prec6, double* __restrict__ alpha, int* __restrict__ err) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double q[4] = {quat[4 * i], quat[4 * i + 1], quat[4 * i + 2], quat[4 * i + 3]};
+    double nrm = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+    if (!(nrm > 1e-12)) {
+      atomicOr(err, MG_ERR_DEGENERATE_QUAT);
+      nrm = 1.0;
+    }
+    double w = q[0] / nrm, x = q[1] / nrm, y = q[2] / nrm, z = q[3] / nrm;
+    qn[4 * i] = w;
+    qn[4 * i + 1] = x;
+    qn[4 * i + 2] = y;
+    qn[4 * i + 3] = z;
+    double R[9] = {1.0 - 2.0 * (y * y + z * z), 2.0 * (x * y - w * z), 2.0 * (x * z + w * y),
+                   2.0 * (x * y + w * z),       1.0 - 2.0 * (x * x + z * z), 2.0 * (y * z - w * x),
+                   2.0 * (x * z - w * y),       2.0 * (y * z + w * x),       1.0 - 2.0 * (x * x + y * y)};
+    for (int a = 0; a < 9; ++a) rot[9 * i + a] = R[a];
+    double e[3];
+    for (int a = 0; a < 3; ++a) {
+      double s = ls[3 * i + a];
+      s = s < -20.0 ? -20.0 : (s > 20.0 ? 20.0 : s);
+      e[a] = exp(-2.0 * s);
+      inv_var[3 * i + a] = e[a];
+    }
+    const int ia[6] = {0, 0, 0, 1, 1, 2}, ib[6] = {0, 1, 2, 1, 2, 2};
+    for (int k = 0; k < 6; ++k) {
+      int a = ia[k], b = ib[k];
+      prec6[6 * i + k] = R[3 * a] * e[0] * R[3 * b] + R[3 * a + 1] * e[1] * R[3 * b + 1] + R[3 * a + 2] * e[2] * R[3 * b + 2];
+    }
+    alpha[i] = 1.0 / (1.0 + exp(-lg[i]));
+  }
+}
+
+// All-pairs evaluation (_kernels.py:147-162) over fp32 records, smem-tiled.
+__global__ void dense_kernel(const double* __restrict__ pts, int64_t b, const float4* __restrict__ grec, int64_t n,
+                             double* __restrict__ out) {
+  __shared__ float4 tile[3 * 128];
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  float x = 0.f, y = 0.f, z = 0.f;
+  if (q < b) {
+    x = (float)pts[3 * q];
+    y = (float)pts[3 * q + 1];
+    z = (float)pts[3 * q + 2];
+  }
+  float acc = 0.f;
+  for (int64_t t0 = 0; t0 < n; t0 += 128) {
+    int cnt = (int)min((int64_t)128, n - t0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < 3 * cnt; i += blockDim.x) tile[i] = grec[3 * t0 + i];
+    __syncthreads();
+    for (int i = 0; i < cnt; ++i) {
+      float4 A = tile[3 * i], B = tile[3 * i + 1], C = tile[3 * i + 2];
+      float dx = x - A.x, dy = y - A.y, dz = z - A.z;
+      float m = dx * (B.x * dx + 2.f * B.w * dy + 2.f * C.x * dz) + dy * (B.y * dy + 2.f * C.y * dz) + B.z * dz * dz;
+      acc += A.w * gauss_w(m);
+    }
+  }
+  if (q < b) out[q] = acc;
+}
+
+unsigned grid_of(int64_t n) {
+  int64_t b = (n + 255) / 256;
+  int64_t cap = (int64_t)num_sms() * 16;
+  if (b > cap) b = cap;
+  return (unsigned)(b < 1 ? 1 : b);
+}
+
+// ---- composite workspace layouts ----
+size_t bin_ws(int64_t n, int64_t g) {
+  return al((size_t)n * 4) + radix_workspace_bytes(n) + csr_workspace_bytes(ncell_of(g)) + 1024;
+}
+
+size_t points_ws(int64_t ns, int64_t g) {
+  return al((size_t)ns * 4) * 2 + al((size_t)ns * 16) + radix_workspace_bytes(ns) + csr_workspace_bytes(ncell_of(g)) +
+         2048;
+}
+
+size_t fwd_ws(int64_t ns) { return al((size_t)ns * 4) + 256 + items_workspace_bytes(ns) + 1024; }
+
+int do_bin(const float* pos32, const double* pos64, int64_t n, int64_t g, uint32_t* keys_sorted, int* order,
+           int* starts, void* ws, size_t wsb, cudaStream_t st) {
+  Bump b(ws, wsb);
+  uint32_t* keys = b.take<uint32_t>(n);
+  if (!b.ok) return fail("mg_bin: workspace too small");
+  if (pos32)
+    launch_gauss_keys(pos32, n, (int)g, keys, st);
+  else
+    launch_gauss_keys_f64(pos64, n, (int)g, keys, st);
+  int bits = bits_for(ncell_of(g) - 1);
+  radix_sort_pairs(keys, keys_sorted, order, n, bits, b.rest(), st);
+  csr_starts(keys_sorted, n, ncell_of(g), starts, b.rest(), st);
+  return cuda_status();
+}
+
+}  // namespace
+
+extern "C" {
+
+int mg_abi_version(void) { return MG_ABI_VERSION; }
+const char* mg_last_error(void) { return g_err; }
+int mg_device_sm_count(void) { return num_sms(); }
+
+int mg_cell_keys_f64(const double* pos, int64_t n, int64_t g, uint32_t* keys, void* stream) {
+  if (g < 1 || n < 0) return fail("mg_cell_keys_f64: bad sizes");
+  launch_gauss_keys_f64(pos, n, (int)g, keys, S(stream));
+  return cuda_status();
+}
+
+size_t mg_bin_workspace_bytes(int64_t n, int64_t g) { return bin_ws(n, g); }
+
+int mg_bin_f32(const float* pos, int64_t n, int64_t g, uint32_t* keys_sorted, int32_t* cell_indices,
+               int32_t* cell_starts, void* ws, size_t wsb, void* stream) {
+  if (g < 1 || n < 0 || ncell_of(g) >= (1ll << 31)) return fail("mg_bin_f32: bad sizes");
+  return do_bin(pos, nullptr, n, g, keys_sorted, cell_indices, cell_starts, ws, wsb, S(stream));
+}
+
+int mg_bin_f64(const double* pos, int64_t n, int64_t g, uint32_t* keys_sorted, int32_t* cell_indices,
+               int32_t* cell_starts, void* ws, size_t wsb, void* stream) {
+  if (g < 1 || n < 0 || ncell_of(g) >= (1ll << 31)) return fail("mg_bin_f64: bad sizes");
+  return do_bin(nullptr, pos, n, g, keys_sorted, cell_indices, cell_starts, ws, wsb, S(stream));
+}
+
+int mg_keys_from_csr(const int32_t* cs, int64_t ncell, uint32_t* keys, void* stream) {
+  if (ncell > 0) keys_from_csr_kernel<<<grid_of(ncell), 256, 0, S(stream)>>>(cs, ncell, keys);
+  return cuda_status();
+}
+
+int mg_i64_to_i32(const int64_t* src, int64_t n, int32_t* dst, void* stream) {
+  if (n > 0) csr64_to_32_kernel<<<grid_of(n), 256, 0, S(stream)>>>(src, n, nullptr, 0, dst, nullptr);
+  return cuda_status();
+}
+
+int mg_i32_to_i64(const int32_t* src, int64_t n, int64_t* dst, void* stream) {
+  if (n > 0) i32_to_i64_kernel<<<grid_of(n), 256, 0, S(stream)>>>(src, n, dst);
+  return cuda_status();
+}
+
+int mg_activate(const float* pos, const float* quat, const float* ls, const float* lg, int64_t n,
+                const int32_t* cell_indices, void* grec, int32_t* err_flag, void* stream) {
+  launch_gauss_activate(pos, quat, ls, lg, cell_indices, n, (float4*)grec, err_flag, S(stream));
+  return cuda_status();
+}
+
+int mg_activate_f64(const double* quat, const double* ls, const double* lg, int64_t n, double* qn, double* rot,
+                    double* inv_var, double* prec6, double* alpha, int32_t* err_flag, void* stream) {
+  if (n > 0)
+    activate_f64_kernel<<<grid_of(n), 256, 0, S(stream)>>>(quat, ls, lg, n, qn, rot, inv_var, prec6, alpha, err_flag);
+  return cuda_status();
+}
+
+size_t mg_points_workspace_bytes(int64_t ns, int64_t g) { return points_ws(ns, g); }
+
+int mg_bin_points(const double* coords, const int64_t* sids, int64_t b, int32_t ntaps, const double* tap_off,
+                  const double* dirs, const double* rot, const double* trans, int64_t k, int64_t g,
+                  uint32_t* pkey_sorted, int32_t* pinv, int32_t* pstart, void* prec, double* transformed, void* ws,
+                  size_t wsb, void* stream) {
+  if (g < 1 || b < 0 || ntaps < 1) return fail("mg_bin_points: bad sizes");
+  if (ntaps > 1 && (!tap_off || !dirs)) return fail("mg_bin_points: PSF taps need offsets and directions");
+  cudaStream_t st = S(stream);
+  int64_t ns = b * ntaps;
+  Bump w(ws, wsb);
+  uint32_t* keys = w.take<uint32_t>(ns);
+  int* perm = w.take<int>(ns);
+  float4* xf = w.take<float4>(ns);
+  if (!w.ok) return fail("mg_bin_points: workspace too small");
+  launch_points_prepare(coords, sids, nullptr, b, ntaps, ntaps > 1 ? tap_off : nullptr, dirs, rot, trans, (int)k,
+                        (int)g, keys, xf, transformed, st);
+  radix_sort_pairs(keys, pkey_sorted, perm, ns, bits_for(ncell_of(g) - 1), w.rest(), st);
+  launch_points_gather(xf, perm, ns, (float4*)prec, pinv, st);
+  csr_starts(pkey_sorted, ns, ncell_of(g), pstart, w.rest(), st);
+  return cuda_status();
+}
+
+size_t mg_forward_workspace_bytes(int64_t ns) { return fwd_ws(ns); }
+
+int mg_forward(const void* grec, const int32_t* gstart, int64_t g, int64_t r, const void* prec,
+               const uint32_t* pkey_sorted, const int32_t* pstart, int64_t ns, int32_t with_h, void* out4,
+               int32_t* counts, void* ws, size_t wsb, void* stream) {
+  if (g < 1 || r < 0 || ns < 0) return fail("mg_forward: bad sizes");
+  cudaStream_t st = S(stream);
+  Bump w(ws, wsb);
+  int* items = w.take<int>(ns);
+  int* nitems = w.take<int>(1);
+  if (!w.ok) return fail("mg_forward: workspace too small");
+  if (ns == 0) return 0;
+  build_items(pkey_sorted, pstart, ns, 8, items, nitems, w.rest(), st);
+  launch_forward(with_h != 0, (const float4*)grec, gstart, (int)g, (int)r, (const float4*)prec, pkey_sorted, pstart,
+                 items, nitems, ns, (float4*)out4, counts, st);
+  return cuda_status();
+}
+
+int mg_forward_finish(const void* out4, const int32_t* counts, const int32_t* pinv, int64_t b, int32_t ntaps,
+                      const double* tap_w, double* intensity, float* intensity_f32, int64_t* counts_out,
+                      void* stream) {
+  launch_forward_finish((const float4*)out4, counts, pinv, b, ntaps, ntaps > 1 ? tap_w : nullptr, intensity,
+                        intensity_f32, counts_out, S(stream));
+  return cuda_status();
+}
+
+int mg_backward_points(const double* up, const float* up32, int64_t b, int32_t ntaps, const double* tap_w,
+                       const int32_t* pinv, const void* out4, void* prec, double* d_points, void* stream) {
+  if (!up && !up32) return fail("mg_backward_points: no upstream");
+  launch_backward_points(up, up32, pinv, b, ntaps, ntaps > 1 ? tap_w : nullptr, (const float4*)out4, (float4*)prec,
+                         d_points, S(stream));
+  return cuda_status();
+}
+
+size_t mg_backward_workspace_bytes(int64_t n) { return fwd_ws(n); }
+
+int mg_backward(const void* grec, const uint32_t* gkey_sorted, const int32_t* gstart, int64_t n, int64_t g, int64_t r,
+                const void* prec, const int32_t* pstart, float* acc10, void* ws, size_t wsb, void* stream) {
+  if (g < 1 || r < 0 || n < 0) return fail("mg_backward: bad sizes");
+  cudaStream_t st = S(stream);
+  Bump w(ws, wsb);
+  int* items = w.take<int>(n);
+  int* nitems = w.take<int>(1);
+  if (!w.ok) return fail("mg_backward: workspace too small");
+  if (n == 0) return 0;
+  build_items(gkey_sorted, gstart, n, 4, items, nitems, w.rest(), st);
+  launch_backward((const float4*)grec, gkey_sorted, gstart, (int)g, (int)r, (const float4*)prec, pstart, items,
+                  nitems, n, acc10, st);
+  return cuda_status();
+}
+
+int mg_backward_epilogue(const float* acc10, const int32_t* order, int64_t n, const float* quat, const float* ls,
+                         const float* lg, double* d_pos, double* d_q, double* d_s, double* d_l, void* stream) {
+  launch_epilogue(acc10, order, n, quat, ls, lg, d_pos, d_q, d_s, d_l, S(stream));
+  return cuda_status();
+}
+
+int mg_epilogue_f64(const double* d_mu, const double* d_abar6, const double* d_alpha, const double* quat,
+                    const double* ls, const double* lg, int64_t n, double* d_pos, double* d_q, double* d_s,
+                    double* d_l, void* stream) {
+  launch_epilogue_f64(d_mu, d_abar6, d_alpha, quat, ls, lg, n, d_pos, d_q, d_s, d_l, S(stream));
+  return cuda_status();
+}
+
+int mg_pack_records(const double* mu, const double* prec6, const double* alpha, const int32_t* order, int64_t n,
+                    void* grec, void* stream) {
+  launch_gauss_pack_prepared(mu, prec6, alpha, order, n, (float4*)grec, S(stream));
+  return cuda_status();
+}
+
+int mg_backward_accumulators(const float* acc10, const int32_t* order, int64_t n, const double* alpha, double* d_mu,
+                             double* d_abar6, double* d_alpha, void* stream) {
+  launch_acc_to_ref(acc10, order, n, alpha, d_mu, d_abar6, d_alpha, S(stream));
+  return cuda_status();
+}
+
+int mg_transform_grads(const double* d_points, const double* coords, const int64_t* sids, int64_t b, int32_t ntaps,
+                       const double* tap_off, const double* dirs, const double* t_quats, int64_t k, double* scratch12,
+                       double* out7, int32_t accumulate, void* stream) {
+  launch_transform_grads(d_points, coords, sids, b, ntaps, ntaps > 1 ? tap_off : nullptr, dirs, t_quats, (int)k,
+                         scratch12, out7, accumulate, S(stream));
+  return cuda_status();
+}
+
+size_t mg_volume_workspace_bytes(int64_t nx, int64_t ny, int64_t nz) {
+  return volume_workspace_bytes((int)nx, (int)ny, (int)nz);
+}
+
+int mg_sample_volume(const void* grec, const int32_t* gstart, int64_t g, int64_t r, int64_t nx, int64_t ny,
+                     int64_t nz, const double* lo, const double* hi, int64_t i0, int64_t i1, const float* residual,
+                     float* out, void* ws, size_t wsb, void* stream) {
+  if (nx < 1 || ny < 1 || nz < 1 || i0 < 0 || i1 > nx || i1 <= i0 || g < 1 || r < 0)
+    return fail("mg_sample_volume: bad sizes");
+  if (wsb < volume_workspace_bytes((int)nx, (int)ny, (int)nz)) return fail("mg_sample_volume: workspace too small");
+  int dims[3] = {(int)nx, (int)ny, (int)nz};
+  launch_sample_volume((const float4*)grec, gstart, (int)g, (int)r, dims, lo, hi, (int)i0, (int)i1, residual, out, ws,
+                       S(stream));
+  return cuda_status();
+}
+
+int mg_smooth_l1(const void* out4, const int32_t* pinv, int64_t b, int32_t ntaps, const double* tap_w,
+                 const float* target, const float* residual, void* prec, float* pred_out, double* loss_acc,
+                 void* stream) {
+  launch_smooth_l1((const float4*)out4, pinv, b, ntaps, ntaps > 1 ? tap_w : nullptr, target, residual, (float4*)prec,
+                   pred_out, loss_acc, S(stream));
+  return cuda_status();
+}
+
+int mg_counter_incr(int32_t* c, int32_t n, void* stream) {
+  launch_counter_incr(c, n, S(stream));
+  return cuda_status();
+}
+
+int mg_gauss_update(const float* acc10, const int32_t* order, int64_t n, float* pos, float* quat, float* ls,
+                    float* lg, float* m, float* v, const double* hyper, int32_t use_aniso, const int32_t* t_dev,
+                    double* aniso_acc, void* stream) {
+  launch_gauss_update(acc10, order, n, pos, quat, ls, lg, m, v, hyper, use_aniso, t_dev, aniso_acc, S(stream));
+  return cuda_status();
+}
+
+int mg_transform_adam(double* tq, double* tt, const double* g7, double* m7, double* v7, int64_t k, double lr,
+                      double b1, double b2, double eps, const int32_t* t_dev, void* stream) {
+  launch_transform_adam(tq, tt, g7, m7, v7, (int)k, lr, b1, b2, eps, t_dev, S(stream));
+  return cuda_status();
+}
+
+int mg_upsample(const float* q_old, const float* s_old, const float* l_old, const int32_t* node_of_old, int64_t ro,
+                int64_t rn, float* pos, float* q, float* s, float* l, void* stream) {
+  if (rn < ro || ro < 1) return fail("mg_upsample: bad resolutions");
+  launch_upsample(q_old, s_old, l_old, node_of_old, (int)ro, (int)rn, pos, q, s, l, S(stream));
+  return cuda_status();
+}
+
+// ---- drop-in reference kernel ABI ----
+size_t mg_block_workspace_bytes(int64_t b, int64_t n, int64_t g) {
+  int64_t nc1 = ncell_of(g) + 1;
+  return al((size_t)nc1 * 4) * 2 + al((size_t)n * 4) * 2 + al((size_t)n * 48) + al((size_t)b * 4) * 3 +
+         al((size_t)b * 16) * 2 + al((size_t)n * 40) + points_ws(b, g) + fwd_ws(b > n ? b : n) + 4096;
+}
+
+static int block_common(const double* points, const int64_t* sids, int64_t b, const double* rot, const double* trans,
+                        int64_t k, const double* mu, const double* prec6, const double* alpha, int64_t n,
+                        const int64_t* cs, const int64_t* ci, int64_t g, int64_t r, bool with_h, double* out_i,
+                        int64_t* out_cnt, double* out_x, const double* upstream, double* d_mu, double* d_abar6,
+                        double* d_alpha, double* out_dp, void* ws, size_t wsb, cudaStream_t st) {
+  if (g < 1 || r < 0 || b < 0 || n < 0) return fail("mg_block: bad sizes");
+  if (ncell_of(g) >= (1ll << 31)) return fail("mg_block: grid too large");
+  int64_t nc1 = ncell_of(g) + 1;
+  Bump w(ws, wsb);
+  int* gstart = w.take<int>(nc1);
+  int* pstart = w.take<int>(nc1);
+  int* gorder = w.take<int>(n);
+  uint32_t* gkey = w.take<uint32_t>(n);
+  float4* grec = w.take<float4>(3 * n);
+  uint32_t* pkey = w.take<uint32_t>(b);
+  int* pinv = w.take<int>(b);
+  int* cnt = w.take<int>(b);
+  float4* prec = w.take<float4>(b);
+  float4* out4 = w.take<float4>(b);
+  float* acc10 = w.take<float>(10 * n);
+  char* rest = (char*)w.rest();
+  size_t restb = w.left;
+  if (!w.ok || restb < points_ws(b, g)) return fail("mg_block: workspace too small");
+  csr64_to_32_kernel<<<grid_of(nc1 > n ? nc1 : n), 256, 0, st>>>(cs, nc1, ci, n, gstart, gorder);
+  keys_from_csr_kernel<<<grid_of(nc1 - 1), 256, 0, st>>>(gstart, nc1 - 1, gkey);
+  launch_gauss_pack_prepared(mu, prec6, alpha, gorder, n, grec, st);
+  int rc = mg_bin_points(points, sids, b, 1, nullptr, nullptr, rot, trans, k, g, pkey, pinv, pstart, prec, out_x,
+                         rest, restb, st);
+  if (rc) return rc;
+  if (b == 0) return cuda_status();
+  rc = mg_forward(grec, gstart, g, r, prec, pkey, pstart, b, with_h ? 1 : 0, out4, cnt, rest, restb, st);
+  if (rc) return rc;
+  if (!upstream) {
+    launch_forward_finish(out4, cnt, pinv, b, 1, nullptr, out_i, nullptr, out_cnt, st);
+    return cuda_status();
+  }
+  launch_backward_points(upstream, nullptr, pinv, b, 1, nullptr, out4, prec, out_dp, st);
+  rc = mg_backward(grec, gkey, gstart, n, g, r, prec, pstart, acc10, rest, restb, st);
+  if (rc) return rc;
+  launch_acc_to_ref(acc10, gorder, n, alpha, d_mu, d_abar6, d_alpha, st);
+  return cuda_status();
+}
+
+int mg_block_forward(const double* points, const int64_t* sids, int64_t b, const double* rot, const double* trans,
+                     int64_t k, const double* mu, const double* prec6, const double* alpha, int64_t n,
+                     const int64_t* cs, const int64_t* ci, int64_t g, int64_t r, double* out_i, int64_t* out_cnt,
+                     double* out_x, void* ws, size_t wsb, void* stream) {
+  return block_common(points, sids, b, rot, trans, k, mu, prec6, alpha, n, cs, ci, g, r, false, out_i, out_cnt, out_x,
+                      nullptr, nullptr, nullptr, nullptr, nullptr, ws, wsb, S(stream));
+}
+
+int mg_block_backward(const double* points, const int64_t* sids, int64_t b, const double* rot, const double* trans,
+                      int64_t k, const double* mu, const double* prec6, const double* alpha, int64_t n,
+                      const int64_t* cs, const int64_t* ci, int64_t g, int64_t r, const double* upstream,
+                      double* d_mu, double* d_abar6, double* d_alpha, double* out_dp, void* ws, size_t wsb,
+                      void* stream) {
+  if (!upstream) return fail("mg_block_backward: upstream is required");
+  return block_common(points, sids, b, rot, trans, k, mu, prec6, alpha, n, cs, ci, g, r, true, nullptr, nullptr,
+                      nullptr, upstream, d_mu, d_abar6, d_alpha, out_dp, ws, wsb, S(stream));
+}
+
+size_t mg_dense_workspace_bytes(int64_t n) { return al((size_t)n * 48) + al((size_t)n * 4) + 512; }
+
+int mg_dense_forward(const double* points, int64_t b, const double* mu, const double* prec6, const double* alpha,
+                     int64_t n, double* out, void* ws, size_t wsb, void* stream) {
+  cudaStream_t st = S(stream);
+  Bump w(ws, wsb);
+  float4* grec = w.take<float4>(3 * n);
+  int* ident = w.take<int>(n);
+  if (!w.ok) return fail("mg_dense_forward: workspace too small");
+  if (n > 0) {
+    iota32_kernel<<<grid_of(n), 256, 0, st>>>(ident, n);
+    launch_gauss_pack_prepared(mu, prec6, alpha, ident, n, grec, st);
+  }
+  if (b > 0) dense_kernel<<<(unsigned)((b + 127) / 128), 128, 0, st>>>(points, b, grec, n, out);
+  return cuda_status();
+}
+
+}  // extern "C"

@@ -1,0 +1,130 @@
+// mg_common.cuh -- shared device helpers for the B200 (sm_100a) Gaussian path.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define MG_WARP 32
+#define MG_FULL 0xffffffffu
+
+// Reference cutoff m <= 64 (_kernels.py:21).  Precisions are stored pre-scaled
+// by kMScale = -0.5*log2(e), so m' = d^T P' d = -0.5*log2(e)*m and
+// exp(-m/2) = 2^{m'}; the cutoff becomes m' >= kCutScaled.
+#define MG_LOG2E 1.4426950408889634
+static constexpr double kMScaleD = -0.5 * MG_LOG2E;
+static constexpr float kMScale = (float)(-0.5 * MG_LOG2E);
+static constexpr float kCutScaled = (float)(-32.0 * MG_LOG2E);  // = kMScale * 64
+
+// ---------------------------------------------------------------------------
+// Packed f32x2 arithmetic (sm_100a FFMA2/FMUL2/FADD2).  A scalar operand that
+// is shared by both halves is passed as a float and ptxas encodes it as a
+// broadcast (.F32) operand, so no duplicate register is needed.
+// ---------------------------------------------------------------------------
+struct f2 {
+  float x, y;
+};
+
+__device__ __forceinline__ uint64_t f2_bits(f2 a) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+  return r;
+}
+__device__ __forceinline__ f2 f2_from(uint64_t b) {
+  f2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2 mk2(float a, float b) { return f2{a, b}; }
+__device__ __forceinline__ f2 bc2(float a) { return f2{a, a}; }
+
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)), "l"(f2_bits(c)));
+  return f2_from(d);
+}
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+  return f2_from(d);
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+  return f2_from(d);
+}
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+  return f2_from(d);
+}
+
+// 2^x on the MUFU (SFU) pipe, flush-to-zero: one MUFU.EX2.
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Cutoff-masked weight: 2^{m'} if m' >= cut (i.e. m <= 64) else exactly 0.
+__device__ __forceinline__ float gauss_w(float ms) {
+  float e = ex2(ms);
+  return ms >= kCutScaled ? e : 0.0f;
+}
+
+// ---------------------------------------------------------------------------
+// Warp reductions
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(MG_FULL, v, o);
+  return v;
+}
+
+__device__ __forceinline__ int warp_excl_scan(int v, int lane, int* total) {
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(MG_FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  *total = __shfl_sync(MG_FULL, x, 31);
+  return x - v;
+}
+
+// Transposed ("reduce-scatter") warp reduction of 32 per-lane values:
+// afterwards lane l holds sum over lanes of v[l].  31 shuffles instead of 160.
+__device__ __forceinline__ float warp_transpose_reduce32(float (&v)[32], int lane) {
+#pragma unroll
+  for (int half = 16; half >= 1; half >>= 1) {
+    const bool upper = (lane & half) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      // keep the half of the values this lane is responsible for
+      float send = upper ? v[i] : v[i + half];
+      float keep = upper ? v[i + half] : v[i];
+      float recv = __shfl_xor_sync(MG_FULL, send, half);
+      v[i] = keep + recv;
+    }
+  }
+  return v[0];
+}
+
+// ---------------------------------------------------------------------------
+// Cell math, bit-exact with spatial.py:18-27 evaluated in float64.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int cell_of_d(double v, int g) {
+  double half = (double)g / 2.0;
+  double f = floor(__dmul_rn(__dadd_rn(v, 1.0), half));
+  // clamp in floating point first so huge values do not overflow the int cast
+  if (f < 0.0) f = 0.0;
+  if (f > (double)(g - 1)) f = (double)(g - 1);
+  return (int)f;
+}
+
+__device__ __forceinline__ int flat_cell(int ci, int cj, int ck, int g) { return (ci * g + cj) * g + ck; }
+
+// Device-side error codes (read by the host wrappers).
+enum MgErr : int {
+  MG_OK = 0,
+  MG_ERR_DEGENERATE_QUAT = 1,
+  MG_ERR_NONFINITE = 2,
+};

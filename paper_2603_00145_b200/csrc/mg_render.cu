@@ -1,0 +1,630 @@
+// mg_render.cu -- Gaussian preprocessing, point binning and the block
+// forward / backward pair kernels for sm_100a.
+//
+// Reference semantics (cited per kernel):
+//   activated_parameters   render.py:122-142, core.py:36-67
+//   block_forward          _kernels.py:24-70   (+ render.py:161-187)
+//   block_backward         _kernels.py:73-144  (+ render.py:276-317)
+//
+// Candidate rule: Gaussian i is a candidate of point x iff the Chebyshev
+// distance between cell(mu_i) and cell(x) is <= r (both clamped cells,
+// spatial.py:18-27, _kernels.py:43-58).  The relation is symmetric, which
+// lets the backward run Gaussian-major with no atomics.
+//
+// Layout in HBM (all in cell-sorted order):
+//   grec[3*p + {0,1,2}]  float4 {mu.xyz, alpha}, {P'00,P'11,P'22,P'01}, {P'02,P'12,-,-}
+//                        with P' = -0.5*log2(e) * P  (exp(-m/2) = 2^{d^T P' d})
+//   prec[p]              float4 {x, y, z, upstream} of sub-point p (fp32)
+//   gstart / pstart      int32 CSR over the G^3 cells
+#include "mg_render.cuh"
+#include "mg_sort.cuh"
+
+namespace mg {
+
+// ---------------------------------------------------------------------------
+// Gaussian keys and activation
+// ---------------------------------------------------------------------------
+__global__ void gauss_keys_kernel(const float* __restrict__ pos, int64_t n, int g, uint32_t* __restrict__ keys) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int ci = cell_of_d((double)pos[3 * i + 0], g);
+    int cj = cell_of_d((double)pos[3 * i + 1], g);
+    int ck = cell_of_d((double)pos[3 * i + 2], g);
+    keys[i] = (uint32_t)flat_cell(ci, cj, ck, g);
+  }
+}
+
+// Same key math on float64 positions (the reference drop-in ABI passes f64).
+__global__ void gauss_keys_f64_kernel(const double* __restrict__ pos, int64_t n, int g, uint32_t* __restrict__ keys) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int ci = cell_of_d(pos[3 * i + 0], g);
+    int cj = cell_of_d(pos[3 * i + 1], g);
+    int ck = cell_of_d(pos[3 * i + 2], g);
+    keys[i] = (uint32_t)flat_cell(ci, cj, ck, g);
+  }
+}
+
+// Quaternion -> rotation exactly as core.py:48-67 (w-first), in float64.
+__device__ __forceinline__ void quat_rot_d(double w, double x, double y, double z, double R[9]) {
+  R[0] = 1.0 - 2.0 * (y * y + z * z);
+  R[1] = 2.0 * (x * y - w * z);
+  R[2] = 2.0 * (x * z + w * y);
+  R[3] = 2.0 * (x * y + w * z);
+  R[4] = 1.0 - 2.0 * (x * x + z * z);
+  R[5] = 2.0 * (y * z - w * x);
+  R[6] = 2.0 * (x * z - w * y);
+  R[7] = 2.0 * (y * z + w * x);
+  R[8] = 1.0 - 2.0 * (x * x + y * y);
+}
+
+__device__ __forceinline__ void activate_one(const float* pos, const float* quat, const float* ls, const float* lg,
+                                             int64_t i, float4* rec, int* err) {
+  double qw = quat[4 * i], qx = quat[4 * i + 1], qy = quat[4 * i + 2], qz = quat[4 * i + 3];
+  double nrm = sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
+  if (!(nrm > 1e-12)) {  // core.py:43-44 (DegenerateQuaternion); NaN also flags
+    atomicOr(err, MG_ERR_DEGENERATE_QUAT);
+    nrm = 1.0;
+  }
+  double R[9];
+  quat_rot_d(qw / nrm, qx / nrm, qy / nrm, qz / nrm, R);
+  double e[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    double s = (double)ls[3 * i + a];
+    s = s < -20.0 ? -20.0 : (s > 20.0 ? 20.0 : s);  // LOG_SCALE_LIMIT clamp, render.py:131
+    e[a] = exp(-2.0 * s);
+  }
+  // P = R diag(e) R^T, scaled by -0.5*log2(e)
+  double P[6];
+  const int ia[6] = {0, 1, 2, 0, 0, 1}, ib[6] = {0, 1, 2, 1, 2, 2};
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    int a = ia[k], b = ib[k];
+    P[k] = kMScaleD * (R[3 * a] * e[0] * R[3 * b] + R[3 * a + 1] * e[1] * R[3 * b + 1] + R[3 * a + 2] * e[2] * R[3 * b + 2]);
+  }
+  double alpha = 1.0 / (1.0 + exp(-(double)lg[i]));  // core.py:21-26
+  rec[0] = make_float4(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], (float)alpha);
+  rec[1] = make_float4((float)P[0], (float)P[1], (float)P[2], (float)P[3]);
+  rec[2] = make_float4((float)P[4], (float)P[5], 0.f, 0.f);
+}
+
+__global__ void gauss_activate_kernel(const float* __restrict__ pos, const float* __restrict__ quat,
+                                      const float* __restrict__ ls, const float* __restrict__ lg,
+                                      const int* __restrict__ order, int64_t n, float4* __restrict__ grec,
+                                      int* __restrict__ err) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = order ? order[p] : p;
+    activate_one(pos, quat, ls, lg, i, grec + 3 * p, err);
+  }
+}
+
+// Records straight from precomputed float64 (mu, prec6, alpha) -- the
+// reference kernel ABI (_kernels.py:24-27) hands these in already activated.
+__global__ void gauss_pack_prepared_kernel(const double* __restrict__ mu, const double* __restrict__ prec6,
+                                           const double* __restrict__ alpha, const int* __restrict__ order,
+                                           int64_t n, float4* __restrict__ grec) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = order[p];
+    const double* P = prec6 + 6 * i;
+    grec[3 * p + 0] = make_float4((float)mu[3 * i], (float)mu[3 * i + 1], (float)mu[3 * i + 2], (float)alpha[i]);
+    grec[3 * p + 1] = make_float4((float)(kMScaleD * P[0]), (float)(kMScaleD * P[3]), (float)(kMScaleD * P[5]),
+                                  (float)(kMScaleD * P[1]));
+    grec[3 * p + 2] = make_float4((float)(kMScaleD * P[2]), (float)(kMScaleD * P[4]), 0.f, 0.f);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Point preparation: PSF tap expansion, rigid transform (float64, same
+// operation order as _kernels.py:33-38), cell key.
+// ---------------------------------------------------------------------------
+__global__ void points_prepare_kernel(const double* __restrict__ coords, const int64_t* __restrict__ sids64,
+                                      const int* __restrict__ sids32, int64_t b, int ntaps,
+                                      const double* __restrict__ tap_off, const double* __restrict__ dirs,
+                                      const double* __restrict__ rot, const double* __restrict__ trans,
+                                      int nslices, int g, uint32_t* __restrict__ keys, float4* __restrict__ xf,
+                                      double* __restrict__ xout) {
+  const int64_t total = b * ntaps;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < total; j += (int64_t)gridDim.x * blockDim.x) {
+    int64_t pb = j / ntaps;
+    int t = (int)(j - pb * ntaps);
+    int64_t s = sids64 ? sids64[pb] : (sids32 ? sids32[pb] : -1);
+    double px = coords[3 * pb], py = coords[3 * pb + 1], pz = coords[3 * pb + 2];
+    if (s >= 0 && tap_off) {
+      double o = tap_off[t];
+      px = __dadd_rn(px, __dmul_rn(o, dirs[3 * s]));
+      py = __dadd_rn(py, __dmul_rn(o, dirs[3 * s + 1]));
+      pz = __dadd_rn(pz, __dmul_rn(o, dirs[3 * s + 2]));
+    }
+    double x, y, z;
+    if (s >= 0 && s < nslices) {
+      const double* R = rot + 9 * s;
+      const double* T = trans + 3 * s;
+      x = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(R[0], px), __dmul_rn(R[1], py)), __dmul_rn(R[2], pz)), T[0]);
+      y = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(R[3], px), __dmul_rn(R[4], py)), __dmul_rn(R[5], pz)), T[1]);
+      z = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(R[6], px), __dmul_rn(R[7], py)), __dmul_rn(R[8], pz)), T[2]);
+    } else {
+      x = px;
+      y = py;
+      z = pz;
+    }
+    keys[j] = (uint32_t)flat_cell(cell_of_d(x, g), cell_of_d(y, g), cell_of_d(z, g), g);
+    xf[j] = make_float4((float)x, (float)y, (float)z, 0.f);
+    if (xout) {
+      xout[3 * j] = x;
+      xout[3 * j + 1] = y;
+      xout[3 * j + 2] = z;
+    }
+  }
+}
+
+// Gather point records into cell order; inv[j] = sorted position of j.
+__global__ void points_gather_kernel(const float4* __restrict__ xf, const int* __restrict__ perm, int64_t n,
+                                     float4* __restrict__ prec, int* __restrict__ inv) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    int j = perm[p];
+    prec[p] = xf[j];
+    inv[j] = (int)p;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Work items: runs of equal cell key chunked into groups of <= Q.
+// flag[p] = 1 if p starts an item.
+// ---------------------------------------------------------------------------
+__global__ void item_flags_kernel(const uint32_t* __restrict__ keys, const int* __restrict__ starts, int64_t n, int q,
+                                  int* __restrict__ flags) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    int s = starts[keys[p]];
+    flags[p] = ((p - s) % q) == 0 ? 1 : 0;
+  }
+}
+
+__global__ void item_compact_kernel(const int* __restrict__ flags, const int* __restrict__ scan, int64_t n,
+                                    int* __restrict__ items, int* __restrict__ nitems) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    if (flags[p]) items[scan[p]] = (int)p;
+    if (p == n - 1) *nitems = scan[p] + flags[p];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Segment table: the (2r+1)^2 (clipped) neighbor columns of a cell, each a
+// contiguous CSR range over the k-window [klo, khi].  Built 128 columns at a
+// time into per-warp shared memory.
+// ---------------------------------------------------------------------------
+struct Window {
+  int ilo, jlo, klo, khi, nj, ncol;
+};
+
+__device__ __forceinline__ Window make_window(int cell, int g, int r) {
+  int ck = cell % g;
+  int t = cell / g;
+  int cj = t % g;
+  int ci = t / g;
+  Window w;
+  w.ilo = max(ci - r, 0);
+  int ihi = min(ci + r, g - 1);
+  w.jlo = max(cj - r, 0);
+  int jhi = min(cj + r, g - 1);
+  w.klo = max(ck - r, 0);
+  w.khi = min(ck + r, g - 1);
+  w.nj = jhi - w.jlo + 1;
+  w.ncol = (ihi - w.ilo + 1) * w.nj;
+  return w;
+}
+
+// Fills s_start[0..127], s_pre[0..128] for columns [c0, c0+128); returns total.
+__device__ __forceinline__ int build_segments(const Window& w, int c0, int g, const int* __restrict__ starts,
+                                              int* s_start, int* s_pre, int lane) {
+  int st[4], ln[4], sum = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    int col = c0 + lane * 4 + k;
+    st[k] = 0;
+    ln[k] = 0;
+    if (col < w.ncol) {
+      int ii = w.ilo + col / w.nj;
+      int jj = w.jlo + col % w.nj;
+      int base = (ii * g + jj) * g;
+      int a = __ldg(starts + base + w.klo);
+      int b = __ldg(starts + base + w.khi + 1);
+      st[k] = a;
+      ln[k] = b - a;
+    }
+    sum += ln[k];
+  }
+  int tot;
+  int off = warp_excl_scan(sum, lane, &tot);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    s_start[lane * 4 + k] = st[k];
+    s_pre[lane * 4 + k] = off;
+    off += ln[k];
+  }
+  if (lane == 31) s_pre[128] = tot;
+  __syncwarp();
+  return tot;
+}
+
+// Monotone virtual-index -> element map within the current segment batch.
+__device__ __forceinline__ int seg_lookup(int v, int& s, const int* s_start, const int* s_pre) {
+  while (v >= s_pre[s + 1]) ++s;
+  return s_start[s] + (v - s_pre[s]);
+}
+
+// ---------------------------------------------------------------------------
+// Forward: one warp per (point cell, <= Q sub-points of that cell); lanes
+// stride over the flattened candidate Gaussians; sub-points are warp-uniform
+// and packed two per f32x2 register.  Every point of the item shares the
+// exact candidate set, so contributor_counts is the total candidate count.
+// ---------------------------------------------------------------------------
+constexpr int kFwdWarps = 4;
+
+template <int Q, bool WITH_H>
+__device__ __forceinline__ void fwd_item(const float4* __restrict__ grec, const int* __restrict__ gstart, int g, int r,
+                                         const float4* __restrict__ prec, int p0, int np, int cell,
+                                         float4* __restrict__ out4, int* __restrict__ cnt_out, int* s_start,
+                                         int* s_pre, int lane) {
+  constexpr int QP = Q / 2;
+  f2 px[QP], py[QP], pz[QP];
+#pragma unroll
+  for (int q = 0; q < QP; ++q) {
+    float4 a = prec[p0 + min(2 * q, np - 1)];
+    float4 b = prec[p0 + min(2 * q + 1, np - 1)];
+    px[q] = mk2(a.x, b.x);
+    py[q] = mk2(a.y, b.y);
+    pz[q] = mk2(a.z, b.z);
+  }
+  f2 accI[QP], hx[QP], hy[QP], hz[QP];
+#pragma unroll
+  for (int q = 0; q < QP; ++q) {
+    accI[q] = bc2(0.f);
+    hx[q] = hy[q] = hz[q] = bc2(0.f);
+  }
+  const Window w = make_window(cell, g, r);
+  int total = 0;
+  for (int c0 = 0; c0 < w.ncol; c0 += 128) {
+    const int tot = build_segments(w, c0, g, gstart, s_start, s_pre, lane);
+    total += tot;
+    int s = 0;
+    for (int v = lane; v < tot; v += 32) {
+      const int gi = seg_lookup(v, s, s_start, s_pre);
+      const float4 A = __ldg(grec + 3 * gi);
+      const float4 B = __ldg(grec + 3 * gi + 1);
+      const float4 C = __ldg(grec + 3 * gi + 2);
+      const float p00 = B.x, p11 = B.y, p22 = B.z, p01 = B.w, p02 = C.x, p12 = C.y;
+      if (WITH_H) {
+#pragma unroll
+        for (int q = 0; q < QP; ++q) {
+          f2 dx = sub2(px[q], bc2(A.x)), dy = sub2(py[q], bc2(A.y)), dz = sub2(pz[q], bc2(A.z));
+          f2 pdx = fma2(bc2(p02), dz, fma2(bc2(p01), dy, mul2(bc2(p00), dx)));
+          f2 pdy = fma2(bc2(p12), dz, fma2(bc2(p11), dy, mul2(bc2(p01), dx)));
+          f2 pdz = fma2(bc2(p22), dz, fma2(bc2(p12), dy, mul2(bc2(p02), dx)));
+          f2 m = fma2(dz, pdz, fma2(dy, pdy, mul2(dx, pdx)));
+          f2 wv = mul2(bc2(A.w), mk2(gauss_w(m.x), gauss_w(m.y)));
+          accI[q] = add2(accI[q], wv);
+          hx[q] = fma2(wv, pdx, hx[q]);
+          hy[q] = fma2(wv, pdy, hy[q]);
+          hz[q] = fma2(wv, pdz, hz[q]);
+        }
+      } else {
+        const float a01 = 2.f * p01, a02 = 2.f * p02, a12 = 2.f * p12;
+#pragma unroll
+        for (int q = 0; q < QP; ++q) {
+          f2 dx = sub2(px[q], bc2(A.x)), dy = sub2(py[q], bc2(A.y)), dz = sub2(pz[q], bc2(A.z));
+          f2 t1 = fma2(bc2(a02), dz, fma2(bc2(a01), dy, mul2(bc2(p00), dx)));
+          f2 m = mul2(dx, t1);
+          f2 t2 = fma2(bc2(a12), dz, mul2(bc2(p11), dy));
+          m = fma2(dy, t2, m);
+          m = fma2(dz, mul2(bc2(p22), dz), m);
+          accI[q] = fma2(bc2(A.w), mk2(gauss_w(m.x), gauss_w(m.y)), accI[q]);
+        }
+      }
+    }
+    __syncwarp();
+  }
+  // Transposed reduction: 4 values per point -> lane 4q+c (Q=8) holds point q comp c.
+  constexpr int NV = 4 * Q;  // 8, 16 or 32
+  float v[32];
+#pragma unroll
+  for (int q = 0; q < QP; ++q) {
+    v[8 * q + 0] = accI[q].x;
+    v[8 * q + 1] = hx[q].x;
+    v[8 * q + 2] = hy[q].x;
+    v[8 * q + 3] = hz[q].x;
+    v[8 * q + 4] = accI[q].y;
+    v[8 * q + 5] = hx[q].y;
+    v[8 * q + 6] = hy[q].y;
+    v[8 * q + 7] = hz[q].y;
+  }
+#pragma unroll
+  for (int i = NV; i < 32; ++i) v[i] = 0.f;
+  // halving levels first (each lane keeps half of the remaining values)
+  int nrem = NV;
+#pragma unroll
+  for (int half = 16; half >= 1; half >>= 1) {
+    if (nrem > 1) {
+      const bool upper = (lane & half) != 0;
+      const int h2 = nrem / 2;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        if (i < h2) {
+          float send = upper ? v[i] : v[i + h2];
+          float keep = upper ? v[i + h2] : v[i];
+          v[i] = keep + __shfl_xor_sync(MG_FULL, send, half);
+        }
+      }
+      nrem = h2;
+    } else {
+      v[0] += __shfl_xor_sync(MG_FULL, v[0], half);
+    }
+  }
+  // After log2(NV) halving levels on lane bits 4..(5-log2 NV), value index = lane >> (5 - log2 NV).
+  constexpr int SH = (NV == 32) ? 0 : (NV == 16 ? 1 : 2);
+  const int idx = lane >> SH;
+  const int q = idx >> 2, comp = idx & 3;
+  const bool writer = (lane & ((1 << SH) - 1)) == 0;
+  if (writer && q < np) {
+    float* o = reinterpret_cast<float*>(out4 + p0 + q);
+    // comp 0 = I -> .w ; comps 1..3 = H' -> .xyz (unscale P')
+    if (comp == 0)
+      o[3] = v[0];
+    else
+      o[comp - 1] = v[0] * (1.0f / kMScale);
+    if (comp == 0) cnt_out[p0 + q] = total;
+  }
+}
+
+template <bool WITH_H>
+__global__ void __launch_bounds__(kFwdWarps * 32) forward_kernel(const float4* __restrict__ grec,
+                                                                 const int* __restrict__ gstart, int g, int r,
+                                                                 const float4* __restrict__ prec,
+                                                                 const uint32_t* __restrict__ pkey,
+                                                                 const int* __restrict__ pstart,
+                                                                 const int* __restrict__ items,
+                                                                 const int* __restrict__ nitems_dev,
+                                                                 float4* __restrict__ out4, int* __restrict__ cnt_out) {
+  __shared__ int s_start[kFwdWarps][128];
+  __shared__ int s_pre[kFwdWarps][132];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nitems = *nitems_dev;
+  for (int it = blockIdx.x * kFwdWarps + warp; it < nitems; it += gridDim.x * kFwdWarps) {
+    const int p0 = items[it];
+    const int cell = (int)pkey[p0];
+    const int np = min(8, pstart[cell + 1] - p0);
+    if (np > 4)
+      fwd_item<8, WITH_H>(grec, gstart, g, r, prec, p0, np, cell, out4, cnt_out, s_start[warp], s_pre[warp], lane);
+    else if (np > 2)
+      fwd_item<4, WITH_H>(grec, gstart, g, r, prec, p0, np, cell, out4, cnt_out, s_start[warp], s_pre[warp], lane);
+    else
+      fwd_item<2, WITH_H>(grec, gstart, g, r, prec, p0, np, cell, out4, cnt_out, s_start[warp], s_pre[warp], lane);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Backward, Gaussian-major: one warp per (Gaussian cell, <= QG Gaussians of
+// that cell); lanes stride over the flattened candidate sub-points, two per
+// lane packed in f32x2.  Per Gaussian it accumulates (register-resident, no
+// atomics):  S = sum u*g,  T = sum u*g*(P'd),  A6 = sum u*g*(d d^T)
+// from which the epilogue forms d_alpha = S, d_mu = alpha*T/kMScale,
+// d_abar6 = -0.5*alpha*A6 (_kernels.py:118-141).
+// ---------------------------------------------------------------------------
+constexpr int kBwdWarps = 4;
+
+template <int QG>
+__device__ __forceinline__ void bwd_item(const float4* __restrict__ grec, int g0, int ng, int cell, int g, int r,
+                                         const float4* __restrict__ prec, const int* __restrict__ pstart,
+                                         float* __restrict__ acc10, int* s_start, int* s_pre, int lane) {
+  float mx[QG], my[QG], mz[QG], P[QG][6];
+#pragma unroll
+  for (int k = 0; k < QG; ++k) {
+    int gi = g0 + min(k, ng - 1);
+    float4 A = grec[3 * gi], B = grec[3 * gi + 1], C = grec[3 * gi + 2];
+    mx[k] = A.x;
+    my[k] = A.y;
+    mz[k] = A.z;
+    P[k][0] = B.x;  // P00
+    P[k][1] = B.y;  // P11
+    P[k][2] = B.z;  // P22
+    P[k][3] = B.w;  // P01
+    P[k][4] = C.x;  // P02
+    P[k][5] = C.y;  // P12
+  }
+  f2 S[QG], T[QG][3], A6[QG][6];
+#pragma unroll
+  for (int k = 0; k < QG; ++k) {
+    S[k] = bc2(0.f);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) T[k][c] = bc2(0.f);
+#pragma unroll
+    for (int c = 0; c < 6; ++c) A6[k][c] = bc2(0.f);
+  }
+  const Window w = make_window(cell, g, r);
+  for (int c0 = 0; c0 < w.ncol; c0 += 128) {
+    const int tot = build_segments(w, c0, g, pstart, s_start, s_pre, lane);
+    int s = 0;
+    for (int v = 2 * lane; v < tot; v += 64) {
+      const int ia = seg_lookup(v, s, s_start, s_pre);
+      float4 a = __ldg(prec + ia);
+      float4 b;
+      if (v + 1 < tot) {
+        int s2 = s;
+        b = __ldg(prec + seg_lookup(v + 1, s2, s_start, s_pre));
+      } else {
+        b = make_float4(a.x, a.y, a.z, 0.f);  // dummy partner: zero upstream
+      }
+      const f2 px = mk2(a.x, b.x), py = mk2(a.y, b.y), pz = mk2(a.z, b.z), u = mk2(a.w, b.w);
+#pragma unroll
+      for (int k = 0; k < QG; ++k) {
+        f2 dx = sub2(px, bc2(mx[k])), dy = sub2(py, bc2(my[k])), dz = sub2(pz, bc2(mz[k]));
+        f2 pdx = fma2(bc2(P[k][4]), dz, fma2(bc2(P[k][3]), dy, mul2(bc2(P[k][0]), dx)));
+        f2 pdy = fma2(bc2(P[k][5]), dz, fma2(bc2(P[k][1]), dy, mul2(bc2(P[k][3]), dx)));
+        f2 pdz = fma2(bc2(P[k][2]), dz, fma2(bc2(P[k][5]), dy, mul2(bc2(P[k][4]), dx)));
+        f2 m = fma2(dz, pdz, fma2(dy, pdy, mul2(dx, pdx)));
+        f2 ug = mul2(u, mk2(gauss_w(m.x), gauss_w(m.y)));
+        S[k] = add2(S[k], ug);
+        T[k][0] = fma2(ug, pdx, T[k][0]);
+        T[k][1] = fma2(ug, pdy, T[k][1]);
+        T[k][2] = fma2(ug, pdz, T[k][2]);
+        f2 cx = mul2(ug, dx), cy = mul2(ug, dy), cz = mul2(ug, dz);
+        A6[k][0] = fma2(cx, dx, A6[k][0]);
+        A6[k][1] = fma2(cx, dy, A6[k][1]);
+        A6[k][2] = fma2(cx, dz, A6[k][2]);
+        A6[k][3] = fma2(cy, dy, A6[k][3]);
+        A6[k][4] = fma2(cy, dz, A6[k][4]);
+        A6[k][5] = fma2(cz, dz, A6[k][5]);
+      }
+    }
+    __syncwarp();
+  }
+  // Per Gaussian: 10 sums (pad to 16) -> transposed reduction; value index = lane >> 1.
+#pragma unroll
+  for (int k = 0; k < QG; ++k) {
+    if (k < ng) {
+      float v[16];
+      v[0] = S[k].x + S[k].y;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) v[1 + c] = T[k][c].x + T[k][c].y;
+#pragma unroll
+      for (int c = 0; c < 6; ++c) v[4 + c] = A6[k][c].x + A6[k][c].y;
+#pragma unroll
+      for (int c = 10; c < 16; ++c) v[c] = 0.f;
+      int nrem = 16;
+#pragma unroll
+      for (int half = 16; half >= 1; half >>= 1) {
+        if (nrem > 1) {
+          const bool upper = (lane & half) != 0;
+          const int h2 = nrem / 2;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            if (i < h2) {
+              float send = upper ? v[i] : v[i + h2];
+              float keep = upper ? v[i + h2] : v[i];
+              v[i] = keep + __shfl_xor_sync(MG_FULL, send, half);
+            }
+          }
+          nrem = h2;
+        } else {
+          v[0] += __shfl_xor_sync(MG_FULL, v[0], half);
+        }
+      }
+      const int idx = lane >> 1;
+      if ((lane & 1) == 0 && idx < 10) acc10[(int64_t)(g0 + k) * 10 + idx] = v[0];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kBwdWarps * 32) backward_kernel(const float4* __restrict__ grec,
+                                                                  const uint32_t* __restrict__ gkey,
+                                                                  const int* __restrict__ gstart, int g, int r,
+                                                                  const float4* __restrict__ prec,
+                                                                  const int* __restrict__ pstart,
+                                                                  const int* __restrict__ items,
+                                                                  const int* __restrict__ nitems_dev,
+                                                                  float* __restrict__ acc10) {
+  __shared__ int s_start[kBwdWarps][128];
+  __shared__ int s_pre[kBwdWarps][132];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nitems = *nitems_dev;
+  for (int it = blockIdx.x * kBwdWarps + warp; it < nitems; it += gridDim.x * kBwdWarps) {
+    const int g0 = items[it];
+    const int cell = (int)gkey[g0];
+    const int ng = min(4, gstart[cell + 1] - g0);
+    if (ng > 2)
+      bwd_item<4>(grec, g0, ng, cell, g, r, prec, pstart, acc10, s_start[warp], s_pre[warp], lane);
+    else if (ng == 2)
+      bwd_item<2>(grec, g0, ng, cell, g, r, prec, pstart, acc10, s_start[warp], s_pre[warp], lane);
+    else
+      bwd_item<1>(grec, g0, ng, cell, g, r, prec, pstart, acc10, s_start[warp], s_pre[warp], lane);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host launchers
+// ---------------------------------------------------------------------------
+static int g_num_sms = 0;
+int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+static inline unsigned grid_for(int64_t n, int threads = 256) {
+  int64_t b = (n + threads - 1) / threads;
+  int64_t cap = (int64_t)num_sms() * 16;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (unsigned)b;
+}
+
+void launch_gauss_keys(const float* pos, int64_t n, int g, uint32_t* keys, cudaStream_t st) {
+  if (n > 0) gauss_keys_kernel<<<grid_for(n), 256, 0, st>>>(pos, n, g, keys);
+}
+void launch_gauss_keys_f64(const double* pos, int64_t n, int g, uint32_t* keys, cudaStream_t st) {
+  if (n > 0) gauss_keys_f64_kernel<<<grid_for(n), 256, 0, st>>>(pos, n, g, keys);
+}
+void launch_gauss_activate(const float* pos, const float* quat, const float* ls, const float* lg, const int* order,
+                           int64_t n, float4* grec, int* err, cudaStream_t st) {
+  if (n > 0) gauss_activate_kernel<<<grid_for(n), 256, 0, st>>>(pos, quat, ls, lg, order, n, grec, err);
+}
+void launch_gauss_pack_prepared(const double* mu, const double* prec6, const double* alpha, const int* order,
+                                int64_t n, float4* grec, cudaStream_t st) {
+  if (n > 0) gauss_pack_prepared_kernel<<<grid_for(n), 256, 0, st>>>(mu, prec6, alpha, order, n, grec);
+}
+void launch_points_prepare(const double* coords, const int64_t* sids64, const int* sids32, int64_t b, int ntaps,
+                           const double* tap_off, const double* dirs, const double* rot, const double* trans,
+                           int nslices, int g, uint32_t* keys, float4* xf, double* xout, cudaStream_t st) {
+  if (b * ntaps > 0)
+    points_prepare_kernel<<<grid_for(b * ntaps), 256, 0, st>>>(coords, sids64, sids32, b, ntaps, tap_off, dirs, rot,
+                                                               trans, nslices, g, keys, xf, xout);
+}
+void launch_points_gather(const float4* xf, const int* perm, int64_t n, float4* prec, int* inv, cudaStream_t st) {
+  if (n > 0) points_gather_kernel<<<grid_for(n), 256, 0, st>>>(xf, perm, n, prec, inv);
+}
+
+size_t items_workspace_bytes(int64_t n) { return 2 * (((size_t)n * 4 + 255) & ~(size_t)255) + scan_workspace_bytes(n); }
+
+void build_items(const uint32_t* keys, const int* starts, int64_t n, int q, int* items, int* nitems, void* ws,
+                 cudaStream_t st) {
+  if (n <= 0) {
+    cudaMemsetAsync(nitems, 0, sizeof(int), st);
+    return;
+  }
+  int* flags = (int*)ws;
+  int* scan = (int*)((char*)ws + (((size_t)n * 4 + 255) & ~(size_t)255));
+  void* sws = (char*)ws + 2 * (((size_t)n * 4 + 255) & ~(size_t)255);
+  item_flags_kernel<<<grid_for(n), 256, 0, st>>>(keys, starts, n, q, flags);
+  excl_scan(flags, scan, n, sws, st);
+  item_compact_kernel<<<grid_for(n), 256, 0, st>>>(flags, scan, n, items, nitems);
+}
+
+void launch_forward(bool with_h, const float4* grec, const int* gstart, int g, int r, const float4* prec,
+                    const uint32_t* pkey, const int* pstart, const int* items, const int* nitems, int64_t max_items,
+                    float4* out4, int* cnt, cudaStream_t st) {
+  if (max_items <= 0) return;
+  int64_t blocks = (max_items + kFwdWarps - 1) / kFwdWarps;
+  int64_t cap = (int64_t)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  if (with_h)
+    forward_kernel<true><<<(unsigned)blocks, kFwdWarps * 32, 0, st>>>(grec, gstart, g, r, prec, pkey, pstart, items,
+                                                                      nitems, out4, cnt);
+  else
+    forward_kernel<false><<<(unsigned)blocks, kFwdWarps * 32, 0, st>>>(grec, gstart, g, r, prec, pkey, pstart, items,
+                                                                       nitems, out4, cnt);
+}
+
+void launch_backward(const float4* grec, const uint32_t* gkey, const int* gstart, int g, int r, const float4* prec,
+                     const int* pstart, const int* items, const int* nitems, int64_t max_items, float* acc10,
+                     cudaStream_t st) {
+  if (max_items <= 0) return;
+  int64_t blocks = (max_items + kBwdWarps - 1) / kBwdWarps;
+  int64_t cap = (int64_t)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  backward_kernel<<<(unsigned)blocks, kBwdWarps * 32, 0, st>>>(grec, gkey, gstart, g, r, prec, pstart, items, nitems,
+                                                              acc10);
+}
+
+}  // namespace mg

@@ -1,0 +1,63 @@
+// mg_render.cuh -- host launchers for the Gaussian path kernels.
+#pragma once
+#include "mg_common.cuh"
+
+namespace mg {
+int num_sms();
+
+// preprocessing / binning
+void launch_gauss_keys(const float* pos, int64_t n, int g, uint32_t* keys, cudaStream_t st);
+void launch_gauss_keys_f64(const double* pos, int64_t n, int g, uint32_t* keys, cudaStream_t st);
+void launch_gauss_activate(const float* pos, const float* quat, const float* ls, const float* lg, const int* order,
+                           int64_t n, float4* grec, int* err, cudaStream_t st);
+void launch_gauss_pack_prepared(const double* mu, const double* prec6, const double* alpha, const int* order,
+                                int64_t n, float4* grec, cudaStream_t st);
+void launch_points_prepare(const double* coords, const int64_t* sids64, const int* sids32, int64_t b, int ntaps,
+                           const double* tap_off, const double* dirs, const double* rot, const double* trans,
+                           int nslices, int g, uint32_t* keys, float4* xf, double* xout, cudaStream_t st);
+void launch_points_gather(const float4* xf, const int* perm, int64_t n, float4* prec, int* inv, cudaStream_t st);
+size_t items_workspace_bytes(int64_t n);
+void build_items(const uint32_t* keys, const int* starts, int64_t n, int q, int* items, int* nitems, void* ws,
+                 cudaStream_t st);
+
+// pair kernels
+void launch_forward(bool with_h, const float4* grec, const int* gstart, int g, int r, const float4* prec,
+                    const uint32_t* pkey, const int* pstart, const int* items, const int* nitems, int64_t max_items,
+                    float4* out4, int* cnt, cudaStream_t st);
+void launch_backward(const float4* grec, const uint32_t* gkey, const int* gstart, int g, int r, const float4* prec,
+                     const int* pstart, const int* items, const int* nitems, int64_t max_items, float* acc10,
+                     cudaStream_t st);
+
+// epilogues / training
+void launch_forward_finish(const float4* out4, const int* cnt, const int* inv, int64_t b, int ntaps,
+                           const double* tap_w, double* out_i, float* out_i32, int64_t* out_cnt, cudaStream_t st);
+void launch_backward_points(const double* up64, const float* up32, const int* inv, int64_t b, int ntaps,
+                            const double* tap_w, const float4* out4, float4* prec, double* dpoints, cudaStream_t st);
+void launch_acc_to_ref(const float* acc10, const int* order, int64_t n, const double* alpha64, double* d_mu,
+                       double* d_abar6, double* d_alpha, cudaStream_t st);
+void launch_epilogue(const float* acc10, const int* order, int64_t n, const float* quat, const float* ls,
+                     const float* lg, double* d_pos, double* d_q, double* d_s, double* d_l, cudaStream_t st);
+void launch_epilogue_f64(const double* d_mu, const double* d_abar6, const double* d_alpha, const double* quat,
+                         const double* ls, const double* lg, int64_t n, double* d_pos, double* d_q, double* d_s,
+                         double* d_l, cudaStream_t st);
+void launch_transform_grads(const double* dpoints, const double* coords, const int64_t* sids, int64_t b, int ntaps,
+                            const double* tap_off, const double* dirs, const double* tq, int k, double* acc12,
+                            double* out7, int accumulate, cudaStream_t st);
+void launch_smooth_l1(const float4* out4, const int* inv, int64_t b, int ntaps, const double* tap_w,
+                      const float* target, const float* residual, float4* prec, float* pred_out, double* loss_acc,
+                      cudaStream_t st);
+void launch_counter_incr(int* c, int n, cudaStream_t st);
+void launch_gauss_update(const float* acc10, const int* order, int64_t n, float* pos, float* quat, float* ls,
+                         float* lg, float* mom_m, float* mom_v, const double* hyper, int use_aniso,
+                         const int* t_dev, double* aniso_acc, cudaStream_t st);
+void launch_transform_adam(double* tq, double* tt, const double* g7, double* m7, double* v7, int k, double lr,
+                           double b1, double b2, double eps, const int* t_dev, cudaStream_t st);
+void launch_upsample(const float* q_old, const float* s_old, const float* l_old, const int* node_of_old, int ro, int rn,
+                     float* pos, float* q, float* s, float* l, cudaStream_t st);
+
+// inference
+size_t volume_workspace_bytes(int nx, int ny, int nz);
+void launch_sample_volume(const float4* grec, const int* gstart, int g, int r, const int dims[3], const double lo[3],
+                          const double hi[3], int i0, int i1, const float* residual, float* out, void* ws,
+                          cudaStream_t st);
+}  // namespace mg

@@ -1,0 +1,500 @@
+// mg_train.cu -- O(N) / O(B) kernels around the pair kernels:
+//   forward finish (PSF tap reduction)
+//   backward point prep (upstream, d_points)      _kernels.py:131-144
+//   backward epilogue chain rule                  render.py:319-340, 207-243
+//   transform gradients                           render.py:246-273
+//   smooth-L1 loss + gradient                     train.py:108-120
+//   fused epilogue + aniso + Adam                 train.py:128-147, 239-271, 457-474
+//   progressive lattice upsample                  train.py:157-218
+#include "mg_render.cuh"
+
+namespace mg {
+
+static inline unsigned gridn(int64_t n, int t = 256) {
+  int64_t b = (n + t - 1) / t;
+  int64_t cap = (int64_t)num_sms() * 16;
+  if (b > cap) b = cap;
+  return (unsigned)(b < 1 ? 1 : b);
+}
+
+#define GRID_LOOP(i, n) for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
+
+// ---------------------------------------------------------------------------
+// Forward finish: I_b = sum_t w_t I_(b,t); counts summed over taps.
+// ---------------------------------------------------------------------------
+__global__ void forward_finish_kernel(const float4* __restrict__ out4, const int* __restrict__ cnt,
+                                      const int* __restrict__ inv, int64_t b, int ntaps,
+                                      const double* __restrict__ tap_w, double* __restrict__ out_i,
+                                      float* __restrict__ out_i32, int64_t* __restrict__ out_cnt) {
+  GRID_LOOP(pb, b) {
+    double acc = 0.0;
+    int64_t c = 0;
+    for (int t = 0; t < ntaps; ++t) {
+      int p = inv[pb * ntaps + t];
+      double w = tap_w ? tap_w[t] : 1.0;
+      acc += w * (double)out4[p].w;
+      c += cnt[p];
+    }
+    if (out_i) out_i[pb] = acc;
+    if (out_i32) out_i32[pb] = (float)acc;
+    if (out_cnt) out_cnt[pb] = c;
+  }
+}
+
+// Upstream per sub-point u_(b,t) = w_t * u_b into the point records; the
+// gradient w.r.t. the transformed sub-point is h = -u * H (H from forward).
+__global__ void backward_points_kernel(const double* __restrict__ up64, const float* __restrict__ up32,
+                                       const int* __restrict__ inv, int64_t b, int ntaps,
+                                       const double* __restrict__ tap_w, const float4* __restrict__ out4,
+                                       float4* __restrict__ prec, double* __restrict__ dpoints) {
+  GRID_LOOP(j, b * ntaps) {
+    int64_t pb = j / ntaps;
+    int t = (int)(j - pb * ntaps);
+    double u = up64 ? up64[pb] : (double)up32[pb];
+    double us = u * (tap_w ? tap_w[t] : 1.0);
+    int p = inv[j];
+    prec[p].w = (float)us;
+    if (dpoints) {
+      float4 H = out4[p];
+      dpoints[3 * j + 0] = -us * (double)H.x;
+      dpoints[3 * j + 1] = -us * (double)H.y;
+      dpoints[3 * j + 2] = -us * (double)H.z;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Epilogue helpers (float64)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void rot_quat_grad(const double g[9], double w, double x, double y, double z,
+                                              double out[4]) {
+  // render.py:207-235, g row-major (a, b) -> g[3a+b]
+  out[0] = 2.0 * (-z * g[1] + y * g[2] + z * g[3] - x * g[5] - y * g[6] + x * g[7]);
+  out[1] = 2.0 * (y * g[1] + z * g[2] + y * g[3] - 2.0 * x * g[4] - w * g[5] + z * g[6] + w * g[7] - 2.0 * x * g[8]);
+  out[2] = 2.0 * (-2.0 * y * g[0] + x * g[1] + w * g[2] + x * g[3] + z * g[5] - w * g[6] + z * g[7] - 2.0 * y * g[8]);
+  out[3] = 2.0 * (-2.0 * z * g[0] - w * g[1] + x * g[2] + w * g[3] - 2.0 * z * g[4] + y * g[5] + x * g[6] + y * g[7]);
+}
+
+__device__ __forceinline__ void quat_rot_d2(double w, double x, double y, double z, double R[9]) {
+  R[0] = 1.0 - 2.0 * (y * y + z * z);
+  R[1] = 2.0 * (x * y - w * z);
+  R[2] = 2.0 * (x * z + w * y);
+  R[3] = 2.0 * (x * y + w * z);
+  R[4] = 1.0 - 2.0 * (x * x + z * z);
+  R[5] = 2.0 * (y * z - w * x);
+  R[6] = 2.0 * (x * z - w * y);
+  R[7] = 2.0 * (y * z + w * x);
+  R[8] = 1.0 - 2.0 * (x * x + y * y);
+}
+
+struct GaussGrad {
+  double dmu[3], dq[4], ds[3], dl;
+};
+
+// Full chain for one Gaussian from the reference-convention accumulators.
+__device__ __forceinline__ GaussGrad chain_one(const double dmu[3], const double dab[6], double dalpha, double qw,
+                                               double qx, double qy, double qz, const double s_raw[3],
+                                               double logit) {
+  GaussGrad o;
+  double nrm = sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
+  double w = qw / nrm, x = qx / nrm, y = qy / nrm, z = qz / nrm;
+  double R[9];
+  quat_rot_d2(w, x, y, z, R);
+  double e[3];
+  for (int a = 0; a < 3; ++a) {
+    double s = s_raw[a] < -20.0 ? -20.0 : (s_raw[a] > 20.0 ? 20.0 : s_raw[a]);
+    e[a] = exp(-2.0 * s);
+  }
+  double A[9] = {dab[0], dab[1], dab[2], dab[1], dab[3], dab[4], dab[2], dab[4], dab[5]};
+  double AR[9];
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) AR[3 * a + b] = A[3 * a] * R[b] + A[3 * a + 1] * R[3 + b] + A[3 * a + 2] * R[6 + b];
+  for (int k = 0; k < 3; ++k) {
+    double de = R[k] * AR[k] + R[3 + k] * AR[3 + k] + R[6 + k] * AR[6 + k];
+    o.ds[k] = (fabs(s_raw[k]) > 20.0) ? 0.0 : -2.0 * e[k] * de;
+  }
+  double grot[9];
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) grot[3 * a + b] = 2.0 * AR[3 * a + b] * e[b];
+  double dqh[4];
+  rot_quat_grad(grot, w, x, y, z, dqh);
+  double inner = dqh[0] * w + dqh[1] * x + dqh[2] * y + dqh[3] * z;
+  o.dq[0] = (dqh[0] - inner * w) / nrm;
+  o.dq[1] = (dqh[1] - inner * x) / nrm;
+  o.dq[2] = (dqh[2] - inner * y) / nrm;
+  o.dq[3] = (dqh[3] - inner * z) / nrm;
+  double alpha = 1.0 / (1.0 + exp(-logit));
+  o.dl = dalpha * alpha * (1.0 - alpha);
+  o.dmu[0] = dmu[0];
+  o.dmu[1] = dmu[1];
+  o.dmu[2] = dmu[2];
+  return o;
+}
+
+// acc10 (kernel convention, sorted order) -> reference accumulators.
+__device__ __forceinline__ void acc_to_ref(const float* a, double alpha, double dmu[3], double dab[6], double* dal) {
+  *dal = (double)a[0];
+  const double sc = alpha / kMScaleD;
+  dmu[0] = sc * (double)a[1];
+  dmu[1] = sc * (double)a[2];
+  dmu[2] = sc * (double)a[3];
+  for (int k = 0; k < 6; ++k) dab[k] = -0.5 * alpha * (double)a[4 + k];
+}
+
+// Reference block_backward ABI: d_mu/d_abar6/d_alpha are ACCUMULATED into
+// (caller-zeroed, render.py:300-302), alpha given as float64.
+__global__ void acc_to_ref_kernel(const float* __restrict__ acc10, const int* __restrict__ order, int64_t n,
+                                  const double* __restrict__ alpha64, double* __restrict__ d_mu,
+                                  double* __restrict__ d_abar6, double* __restrict__ d_alpha) {
+  GRID_LOOP(p, n) {
+    int64_t i = order[p];
+    double dmu[3], dab[6], dal;
+    acc_to_ref(acc10 + 10 * p, alpha64[i], dmu, dab, &dal);
+    for (int a = 0; a < 3; ++a) d_mu[3 * i + a] += dmu[a];
+    for (int k = 0; k < 6; ++k) d_abar6[6 * i + k] += dab[k];
+    d_alpha[i] += dal;
+  }
+}
+
+// Full epilogue to parameter gradients (RenderGradients fields, float64).
+__global__ void epilogue_kernel(const float* __restrict__ acc10, const int* __restrict__ order, int64_t n,
+                                const float* __restrict__ quat, const float* __restrict__ ls,
+                                const float* __restrict__ lg, double* __restrict__ d_pos, double* __restrict__ d_q,
+                                double* __restrict__ d_s, double* __restrict__ d_l) {
+  GRID_LOOP(p, n) {
+    int64_t i = order[p];
+    double logit = lg[i];
+    double alpha = 1.0 / (1.0 + exp(-logit));
+    double dmu[3], dab[6], dal;
+    acc_to_ref(acc10 + 10 * p, alpha, dmu, dab, &dal);
+    double s[3] = {ls[3 * i], ls[3 * i + 1], ls[3 * i + 2]};
+    GaussGrad gg = chain_one(dmu, dab, dal, quat[4 * i], quat[4 * i + 1], quat[4 * i + 2], quat[4 * i + 3], s, logit);
+    for (int a = 0; a < 3; ++a) d_pos[3 * i + a] = gg.dmu[a];
+    for (int a = 0; a < 4; ++a) d_q[4 * i + a] = gg.dq[a];
+    for (int a = 0; a < 3; ++a) d_s[3 * i + a] = gg.ds[a];
+    d_l[i] = gg.dl;
+  }
+}
+
+// Chain rule from float64 reference-convention accumulators (primitive order).
+__global__ void epilogue_f64_kernel(const double* __restrict__ d_mu, const double* __restrict__ d_abar6,
+                                    const double* __restrict__ d_alpha, const double* __restrict__ quat,
+                                    const double* __restrict__ ls, const double* __restrict__ lg, int64_t n,
+                                    double* __restrict__ d_pos, double* __restrict__ d_q, double* __restrict__ d_s,
+                                    double* __restrict__ d_l) {
+  GRID_LOOP(i, n) {
+    double s[3] = {ls[3 * i], ls[3 * i + 1], ls[3 * i + 2]};
+    GaussGrad gg = chain_one(d_mu + 3 * i, d_abar6 + 6 * i, d_alpha[i], quat[4 * i], quat[4 * i + 1], quat[4 * i + 2],
+                             quat[4 * i + 3], s, lg[i]);
+    for (int a = 0; a < 3; ++a) d_pos[3 * i + a] = gg.dmu[a];
+    for (int a = 0; a < 4; ++a) d_q[4 * i + a] = gg.dq[a];
+    for (int a = 0; a < 3; ++a) d_s[3 * i + a] = gg.ds[a];
+    d_l[i] = gg.dl;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Transform gradients: per slice sums of h and h (x) c over sub-points
+// (render.py:246-273), then the quaternion chain.
+// ---------------------------------------------------------------------------
+__global__ void transform_reduce_kernel(const double* __restrict__ dpoints, const double* __restrict__ coords,
+                                        const int64_t* __restrict__ sids, int64_t b, int ntaps,
+                                        const double* __restrict__ tap_off, const double* __restrict__ dirs, int k,
+                                        double* __restrict__ out12) {
+  extern __shared__ double s_acc[];  // 12 * k
+  const bool use_smem = k <= 256;
+  if (use_smem) {
+    for (int i = threadIdx.x; i < 12 * k; i += blockDim.x) s_acc[i] = 0.0;
+    __syncthreads();
+  }
+  GRID_LOOP(j, b * ntaps) {
+    int64_t pb = j / ntaps;
+    int t = (int)(j - pb * ntaps);
+    int64_t s = sids[pb];
+    if (s < 0 || s >= k) continue;
+    double c[3] = {coords[3 * pb], coords[3 * pb + 1], coords[3 * pb + 2]};
+    if (tap_off) {
+      double o = tap_off[t];
+      for (int a = 0; a < 3; ++a) c[a] = __dadd_rn(c[a], __dmul_rn(o, dirs[3 * s + a]));
+    }
+    double h[3] = {dpoints[3 * j], dpoints[3 * j + 1], dpoints[3 * j + 2]};
+    double* dst = use_smem ? s_acc + 12 * s : out12 + 12 * s;
+    for (int a = 0; a < 3; ++a) {
+      atomicAdd(dst + a, h[a]);
+      for (int bb = 0; bb < 3; ++bb) atomicAdd(dst + 3 + 3 * a + bb, h[a] * c[bb]);
+    }
+  }
+  if (use_smem) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < 12 * k; i += blockDim.x)
+      if (s_acc[i] != 0.0) atomicAdd(out12 + i, s_acc[i]);
+  }
+}
+
+__global__ void transform_chain_kernel(const double* __restrict__ acc12, const double* __restrict__ tq, int k,
+                                       double* __restrict__ out7, int accumulate) {
+  GRID_LOOP(s, k) {
+    const double* a = acc12 + 12 * s;
+    double qw = tq[4 * s], qx = tq[4 * s + 1], qy = tq[4 * s + 2], qz = tq[4 * s + 3];
+    double nrm = sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
+    double w = qw / nrm, x = qx / nrm, y = qy / nrm, z = qz / nrm;
+    double dqh[4];
+    rot_quat_grad(a + 3, w, x, y, z, dqh);
+    double inner = dqh[0] * w + dqh[1] * x + dqh[2] * y + dqh[3] * z;
+    double o[7] = {(dqh[0] - inner * w) / nrm, (dqh[1] - inner * x) / nrm, (dqh[2] - inner * y) / nrm,
+                   (dqh[3] - inner * z) / nrm, a[0], a[1], a[2]};
+    for (int c = 0; c < 7; ++c) out7[7 * s + c] = accumulate ? out7[7 * s + c] + o[c] : o[c];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Smooth-L1 (train.py:108-120) over the batch, fused with the tap reduction.
+// Writes upstream u_(b,t) = w_t * dL/dpred_b into the point records.
+// ---------------------------------------------------------------------------
+__global__ void smooth_l1_kernel(const float4* __restrict__ out4, const int* __restrict__ inv, int64_t b, int ntaps,
+                                 const double* __restrict__ tap_w, const float* __restrict__ target,
+                                 const float* __restrict__ residual, double scale, float4* __restrict__ prec,
+                                 float* __restrict__ pred_out, double* __restrict__ loss_acc) {
+  double local = 0.0;
+  GRID_LOOP(pb, b) {
+    double pred = 0.0;
+    for (int t = 0; t < ntaps; ++t) pred += (tap_w ? tap_w[t] : 1.0) * (double)out4[inv[pb * ntaps + t]].w;
+    if (residual) pred += (double)residual[pb];
+    if (pred_out) pred_out[pb] = (float)pred;
+    double x = pred - (double)target[pb];
+    double ax = fabs(x);
+    local += ax < 1.0 ? 0.5 * x * x : ax - 0.5;
+    double gr = (ax < 1.0 ? x : (x > 0 ? 1.0 : (x < 0 ? -1.0 : 0.0))) * scale;
+    for (int t = 0; t < ntaps; ++t) prec[inv[pb * ntaps + t]].w = (float)(gr * (tap_w ? tap_w[t] : 1.0));
+  }
+  // block reduce the loss
+  __shared__ double s_red[32];
+  for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(MG_FULL, local, o);
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = local;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? s_red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(MG_FULL, v, o);
+    if (threadIdx.x == 0) atomicAdd(loss_acc, v * scale);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Fused: epilogue chain + aniso penalty + Adam on the four Gaussian groups.
+// Adam in float64 math, float32 state (train.py:251-271); groups share t.
+// ---------------------------------------------------------------------------
+struct AdamHyper {
+  double lr_pos, lr_quat, lr_scale, lr_logit;
+  double beta1, beta2, eps;
+  double lambda_aniso, lambda_ratio;
+  int use_aniso;
+  double bc1, bc2;  // filled in-kernel from the device step counter
+};
+
+__device__ __forceinline__ float adam_upd(float& p, float& m, float& v, double g, double lr, const AdamHyper& h) {
+  double mm = h.beta1 * (double)m + (1.0 - h.beta1) * g;
+  double vv = h.beta2 * (double)v + (1.0 - h.beta2) * g * g;
+  m = (float)mm;
+  v = (float)vv;
+  double np = (double)p - lr * (mm / h.bc1) / (sqrt(vv / h.bc2) + h.eps);
+  p = (float)np;
+  return p;
+}
+
+__global__ void gauss_update_kernel(const float* __restrict__ acc10, const int* __restrict__ order, int64_t n,
+                                    float* __restrict__ pos, float* __restrict__ quat, float* __restrict__ ls,
+                                    float* __restrict__ lg, float* __restrict__ mom_m, float* __restrict__ mom_v,
+                                    AdamHyper h, const int* __restrict__ t_dev, double* __restrict__ aniso_acc) {
+  double aniso_local = 0.0;
+  {
+    const double t = (double)*t_dev;
+    h.bc1 = 1.0 - pow(h.beta1, t);
+    h.bc2 = 1.0 - pow(h.beta2, t);
+  }
+  GRID_LOOP(p, n) {
+    int64_t i = order[p];
+    double logit = lg[i];
+    double alpha = 1.0 / (1.0 + exp(-logit));
+    double dmu[3], dab[6], dal;
+    acc_to_ref(acc10 + 10 * p, alpha, dmu, dab, &dal);
+    double s[3] = {ls[3 * i], ls[3 * i + 1], ls[3 * i + 2]};
+    GaussGrad gg = chain_one(dmu, dab, dal, quat[4 * i], quat[4 * i + 1], quat[4 * i + 2], quat[4 * i + 3], s, logit);
+    if (h.use_aniso) {
+      // train.py:128-147: ratio = exp(s_max - s_min), first index on ties
+      int hi = 0, lo = 0;
+      for (int a = 1; a < 3; ++a) {
+        if (s[a] > s[hi]) hi = a;
+        if (s[a] < s[lo]) lo = a;
+      }
+      double ratio = exp(s[hi] - s[lo]);
+      double excess = ratio - h.lambda_ratio;
+      if (excess > 0) {
+        aniso_local += excess;
+        double c = h.lambda_aniso * ratio / (double)n;
+        gg.ds[hi] += c;
+        gg.ds[lo] -= c;
+      }
+    }
+    // state layout: m/v [N][11] = pos(3) quat(4) scale(3) logit(1)
+    float* m = mom_m + 11 * i;
+    float* v = mom_v + 11 * i;
+    for (int a = 0; a < 3; ++a) adam_upd(pos[3 * i + a], m[a], v[a], gg.dmu[a], h.lr_pos, h);
+    for (int a = 0; a < 4; ++a) adam_upd(quat[4 * i + a], m[3 + a], v[3 + a], gg.dq[a], h.lr_quat, h);
+    for (int a = 0; a < 3; ++a) adam_upd(ls[3 * i + a], m[7 + a], v[7 + a], gg.ds[a], h.lr_scale, h);
+    adam_upd(lg[i], m[10], v[10], gg.dl, h.lr_logit, h);
+  }
+  if (aniso_acc && h.use_aniso) {
+    for (int o = 16; o > 0; o >>= 1) aniso_local += __shfl_xor_sync(MG_FULL, aniso_local, o);
+    if ((threadIdx.x & 31) == 0 && aniso_local != 0.0) atomicAdd(aniso_acc, aniso_local / (double)n);
+  }
+}
+
+// Transform group: quats (K,4) + trans (K,3) fp64, one Adam group.
+__global__ void transform_adam_kernel(double* __restrict__ tq, double* __restrict__ tt, const double* __restrict__ g7,
+                                      double* __restrict__ m7, double* __restrict__ v7, int k, double lr, double b1,
+                                      double b2, double eps, const int* __restrict__ t_dev) {
+  const double bc1 = 1.0 - pow(b1, (double)*t_dev), bc2 = 1.0 - pow(b2, (double)*t_dev);
+  GRID_LOOP(j, (int64_t)k * 7) {
+    int64_t s = j / 7;
+    int c = (int)(j - s * 7);
+    double g = g7[j];
+    double m = b1 * m7[j] + (1.0 - b1) * g;
+    double v = b2 * v7[j] + (1.0 - b2) * g * g;
+    m7[j] = m;
+    v7[j] = v;
+    double upd = lr * (m / bc1) / (sqrt(v / bc2) + eps);
+    if (c < 4)
+      tq[4 * s + c] -= upd;
+    else
+      tt[3 * s + c - 4] -= upd;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Progressive upsample (train.py:157-218), lattice-index addressed.
+// Input arrays are indexed by the (C-ordered) lattice node id old_id.
+// ---------------------------------------------------------------------------
+__global__ void upsample_kernel(const float* __restrict__ q_old, const float* __restrict__ s_old,
+                                const float* __restrict__ l_old, const int* __restrict__ node_of_old, int ro,
+                                int rn, float* __restrict__ pos, float* __restrict__ q, float* __restrict__ s,
+                                float* __restrict__ l) {
+  const int64_t nn = (int64_t)rn * rn * rn;
+  GRID_LOOP(id, nn) {
+    int c3[3] = {(int)(id / ((int64_t)rn * rn)), (int)((id / rn) % rn), (int)(id % rn)};
+    double f[3], t[3];
+    int base[3];
+    for (int a = 0; a < 3; ++a) {
+      double fr = ((double)c3[a] + 0.5) * ((double)ro / (double)rn) - 0.5;
+      fr = fr < 0.0 ? 0.0 : (fr > ro - 1.0 ? ro - 1.0 : fr);
+      f[a] = fr;
+      int bs = ro > 1 ? (int)floor(fr) : 0;
+      if (ro > 1 && bs > ro - 2) bs = ro - 2;
+      base[a] = bs;
+      t[a] = fr - bs;
+    }
+    int ref[3];
+    for (int a = 0; a < 3; ++a) ref[a] = min(base[a] + (t[a] >= 0.5 ? 1 : 0), ro - 1);
+    int rid = node_of_old[((int64_t)ref[0] * ro + ref[1]) * ro + ref[2]];
+    double rq[4] = {q_old[4 * rid], q_old[4 * rid + 1], q_old[4 * rid + 2], q_old[4 * rid + 3]};
+    double lo = 0.0, sc[3] = {0, 0, 0}, qs[4] = {0, 0, 0, 0};
+    for (int da = 0; da < 2; ++da)
+      for (int db = 0; db < 2; ++db)
+        for (int dc = 0; dc < 2; ++dc) {
+          int ia = min(base[0] + da, ro - 1), ib = min(base[1] + db, ro - 1), ic = min(base[2] + dc, ro - 1);
+          double w = (da ? t[0] : 1.0 - t[0]) * (db ? t[1] : 1.0 - t[1]) * (dc ? t[2] : 1.0 - t[2]);
+          int src = node_of_old[((int64_t)ia * ro + ib) * ro + ic];
+          lo += w * (double)l_old[src];
+          for (int a = 0; a < 3; ++a) sc[a] += w * (double)s_old[3 * src + a];
+          double qq[4] = {q_old[4 * src], q_old[4 * src + 1], q_old[4 * src + 2], q_old[4 * src + 3]};
+          double dot = qq[0] * rq[0] + qq[1] * rq[1] + qq[2] * rq[2] + qq[3] * rq[3];
+          double sg = dot < 0.0 ? -1.0 : 1.0;
+          for (int a = 0; a < 4; ++a) qs[a] += w * sg * qq[a];
+        }
+    double nrm = sqrt(qs[0] * qs[0] + qs[1] * qs[1] + qs[2] * qs[2] + qs[3] * qs[3]);
+    if (!(nrm > 1e-12)) nrm = 1.0;
+    for (int a = 0; a < 4; ++a) q[4 * id + a] = (float)(qs[a] / nrm);
+    for (int a = 0; a < 3; ++a) s[3 * id + a] = (float)sc[a];
+    l[id] = (float)lo;
+    for (int a = 0; a < 3; ++a) pos[3 * id + a] = (float)(-1.0 + ((double)c3[a] + 0.5) * (2.0 / rn));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Launchers
+// ---------------------------------------------------------------------------
+void launch_forward_finish(const float4* out4, const int* cnt, const int* inv, int64_t b, int ntaps,
+                           const double* tap_w, double* out_i, float* out_i32, int64_t* out_cnt, cudaStream_t st) {
+  if (b > 0) forward_finish_kernel<<<gridn(b), 256, 0, st>>>(out4, cnt, inv, b, ntaps, tap_w, out_i, out_i32, out_cnt);
+}
+void launch_backward_points(const double* up64, const float* up32, const int* inv, int64_t b, int ntaps,
+                            const double* tap_w, const float4* out4, float4* prec, double* dpoints, cudaStream_t st) {
+  if (b > 0)
+    backward_points_kernel<<<gridn(b * ntaps), 256, 0, st>>>(up64, up32, inv, b, ntaps, tap_w, out4, prec, dpoints);
+}
+void launch_acc_to_ref(const float* acc10, const int* order, int64_t n, const double* alpha64, double* d_mu,
+                       double* d_abar6, double* d_alpha, cudaStream_t st) {
+  if (n > 0) acc_to_ref_kernel<<<gridn(n), 256, 0, st>>>(acc10, order, n, alpha64, d_mu, d_abar6, d_alpha);
+}
+void launch_epilogue(const float* acc10, const int* order, int64_t n, const float* quat, const float* ls,
+                     const float* lg, double* d_pos, double* d_q, double* d_s, double* d_l, cudaStream_t st) {
+  if (n > 0) epilogue_kernel<<<gridn(n), 256, 0, st>>>(acc10, order, n, quat, ls, lg, d_pos, d_q, d_s, d_l);
+}
+void launch_epilogue_f64(const double* d_mu, const double* d_abar6, const double* d_alpha, const double* quat,
+                         const double* ls, const double* lg, int64_t n, double* d_pos, double* d_q, double* d_s,
+                         double* d_l, cudaStream_t st) {
+  if (n > 0) epilogue_f64_kernel<<<gridn(n), 256, 0, st>>>(d_mu, d_abar6, d_alpha, quat, ls, lg, n, d_pos, d_q, d_s, d_l);
+}
+void launch_transform_grads(const double* dpoints, const double* coords, const int64_t* sids, int64_t b, int ntaps,
+                            const double* tap_off, const double* dirs, const double* tq, int k, double* acc12,
+                            double* out7, int accumulate, cudaStream_t st) {
+  if (k <= 0) return;
+  cudaMemsetAsync(acc12, 0, sizeof(double) * 12 * k, st);
+  if (b > 0) {
+    size_t sm = k <= 256 ? sizeof(double) * 12 * k : 0;
+    transform_reduce_kernel<<<gridn(b * ntaps), 256, sm, st>>>(dpoints, coords, sids, b, ntaps, tap_off, dirs, k,
+                                                               acc12);
+  }
+  transform_chain_kernel<<<gridn(k), 256, 0, st>>>(acc12, tq, k, out7, accumulate);
+}
+void launch_smooth_l1(const float4* out4, const int* inv, int64_t b, int ntaps, const double* tap_w,
+                      const float* target, const float* residual, float4* prec, float* pred_out, double* loss_acc,
+                      cudaStream_t st) {
+  if (b > 0)
+    smooth_l1_kernel<<<gridn(b), 256, 0, st>>>(out4, inv, b, ntaps, tap_w, target, residual, 1.0 / (double)b, prec,
+                                               pred_out, loss_acc);
+}
+__global__ void counter_incr_kernel(int* c, int n) {
+  if (threadIdx.x < n) c[threadIdx.x] += 1;
+}
+void launch_counter_incr(int* c, int n, cudaStream_t st) { counter_incr_kernel<<<1, 32, 0, st>>>(c, n); }
+
+void launch_gauss_update(const float* acc10, const int* order, int64_t n, float* pos, float* quat, float* ls,
+                         float* lg, float* mom_m, float* mom_v, const double* hyper, int use_aniso,
+                         const int* t_dev, double* aniso_acc, cudaStream_t st) {
+  AdamHyper h;
+  h.lr_pos = hyper[0];
+  h.lr_quat = hyper[1];
+  h.lr_scale = hyper[2];
+  h.lr_logit = hyper[3];
+  h.beta1 = hyper[4];
+  h.beta2 = hyper[5];
+  h.eps = hyper[6];
+  h.lambda_aniso = hyper[7];
+  h.lambda_ratio = hyper[8];
+  h.use_aniso = use_aniso;
+  h.bc1 = h.bc2 = 1.0;
+  if (n > 0)
+    gauss_update_kernel<<<gridn(n), 256, 0, st>>>(acc10, order, n, pos, quat, ls, lg, mom_m, mom_v, h, t_dev,
+                                                  aniso_acc);
+}
+void launch_transform_adam(double* tq, double* tt, const double* g7, double* m7, double* v7, int k, double lr,
+                           double b1, double b2, double eps, const int* t_dev, cudaStream_t st) {
+  if (k > 0) transform_adam_kernel<<<gridn((int64_t)k * 7), 256, 0, st>>>(tq, tt, g7, m7, v7, k, lr, b1, b2, eps, t_dev);
+}
+void launch_upsample(const float* q_old, const float* s_old, const float* l_old, const int* node_of_old, int ro, int rn,
+                     float* pos, float* q, float* s, float* l, cudaStream_t st) {
+  int64_t nn = (int64_t)rn * rn * rn;
+  if (nn > 0) upsample_kernel<<<gridn(nn), 256, 0, st>>>(q_old, s_old, l_old, node_of_old, ro, rn, pos, q, s, l);
+}
+
+}  // namespace mg

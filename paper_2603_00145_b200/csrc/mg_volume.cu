@@ -1,0 +1,207 @@
+// mg_volume.cu -- inference-time sampling of the Gaussian field on a dense,
+// node-inclusive voxel grid (render.py:357-408: grid_coordinates +
+// sample_volume, clip to [0, 1]).
+//
+// Voxel (i, j, k) sits at lo + i*spacing (float64, numpy order of
+// operations).  Along each axis the voxels of one partition cell form a
+// contiguous run, so a work item is a box of voxels that all share one
+// cell -- and therefore one exact candidate set.  A warp owns an item:
+// lanes hold voxels (V per lane, packed in f32x2), the candidate Gaussians
+// stream through warp-uniform (broadcast) loads.  Slabs [i0, i1) of axis 0
+// are independent, which is how inference shards across GPUs.
+#include "mg_render.cuh"
+#include "mg_sort.cuh"
+
+namespace mg {
+
+// Per-axis voxel coordinate (render.py:357-376).
+__device__ __forceinline__ double axis_coord(int i, int n, double lo, double hi, double sp) {
+  if (n == 1) return __dmul_rn(0.5, __dadd_rn(lo, hi));
+  return __dadd_rn(lo, __dmul_rn((double)i, sp));
+}
+
+// axis a voxels [v0, v1): cell per voxel and "starts a run" flags.
+__global__ void axis_cells_kernel(int n_all, int v0, int v1, double lo, double hi, double sp, int g,
+                                  int* __restrict__ cells, int* __restrict__ flags) {
+  int n = v1 - v0;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    int c = cell_of_d(axis_coord(v0 + t, n_all, lo, hi, sp), g);
+    int cp = t > 0 ? cell_of_d(axis_coord(v0 + t - 1, n_all, lo, hi, sp), g) : -1;
+    cells[t] = c;
+    flags[t] = (c != cp) ? 1 : 0;
+  }
+}
+
+__global__ void axis_runs_kernel(const int* __restrict__ cells, const int* __restrict__ flags,
+                                 const int* __restrict__ scan, int n, int* __restrict__ run_start,
+                                 int* __restrict__ run_cell, int* __restrict__ nruns) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    if (flags[t]) {
+      run_start[scan[t]] = t;
+      run_cell[scan[t]] = cells[t];
+    }
+    if (t == n - 1) {
+      int nr = scan[t] + flags[t];
+      *nruns = nr;
+      run_start[nr] = n;  // sentinel
+    }
+  }
+}
+
+struct VolAxes {
+  const int* rs[3];  // run starts (relative to axis origin), with sentinel
+  const int* rc[3];  // run cells
+  const int* nr;     // nruns[3]
+  int v0[3];         // axis origins (slab offset on axis 0)
+  int n[3];          // total voxels per axis
+  double lo[3], hi[3], sp[3];
+};
+
+constexpr int kVolWarps = 4;
+
+template <int V>
+__device__ __forceinline__ void vol_chunk(const float4* __restrict__ grec, const int* __restrict__ gstart, int g,
+                                          int r, const VolAxes& ax, int bx0, int by0, int bz0, int nbx, int nby,
+                                          int nbz, int cell, int l0, int nvox, const float* __restrict__ residual,
+                                          float* __restrict__ out, int64_t slab_i0, int lane) {
+  constexpr int VP = V / 2;
+  f2 px[VP], py[VP], pz[VP], acc[VP];
+  int vid[V];
+  const int nyz = nby * nbz;
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    int l = l0 + lane + 32 * v;
+    int lc = l < nvox ? l : 0;
+    int bx = lc / nyz, rem = lc - bx * nyz, by = rem / nbz, bz = rem - by * nbz;
+    int i = bx0 + bx, j = by0 + by, k = bz0 + bz;
+    float x = (float)axis_coord(ax.v0[0] + i, ax.n[0], ax.lo[0], ax.hi[0], ax.sp[0]);
+    float y = (float)axis_coord(j, ax.n[1], ax.lo[1], ax.hi[1], ax.sp[1]);
+    float z = (float)axis_coord(k, ax.n[2], ax.lo[2], ax.hi[2], ax.sp[2]);
+    vid[v] = l < nvox ? ((i * ax.n[1] + j) * ax.n[2] + k) : -1;
+    if (v & 1) {
+      px[v / 2].y = x;
+      py[v / 2].y = y;
+      pz[v / 2].y = z;
+    } else {
+      px[v / 2].x = x;
+      py[v / 2].x = y;
+      pz[v / 2].x = z;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < VP; ++q) acc[q] = bc2(0.f);
+  // candidate Gaussians: clipped (2r+1)^2 columns x k-window, warp-uniform walk
+  int ck = cell % g, t = cell / g, cj = t % g, ci = t / g;
+  int ilo = max(ci - r, 0), ihi = min(ci + r, g - 1), jlo = max(cj - r, 0), jhi = min(cj + r, g - 1);
+  int klo = max(ck - r, 0), khi = min(ck + r, g - 1);
+  for (int ii = ilo; ii <= ihi; ++ii) {
+    for (int jj = jlo; jj <= jhi; ++jj) {
+      int base = (ii * g + jj) * g;
+      int a = __ldg(gstart + base + klo), b = __ldg(gstart + base + khi + 1);
+      for (int gi = a; gi < b; ++gi) {
+        const float4 A = __ldg(grec + 3 * gi), B = __ldg(grec + 3 * gi + 1), C = __ldg(grec + 3 * gi + 2);
+        const float a01 = 2.f * B.w, a02 = 2.f * C.x, a12 = 2.f * C.y;
+#pragma unroll
+        for (int q = 0; q < VP; ++q) {
+          f2 dx = sub2(px[q], bc2(A.x)), dy = sub2(py[q], bc2(A.y)), dz = sub2(pz[q], bc2(A.z));
+          f2 t1 = fma2(bc2(a02), dz, fma2(bc2(a01), dy, mul2(bc2(B.x), dx)));
+          f2 m = mul2(dx, t1);
+          f2 t2 = fma2(bc2(a12), dz, mul2(bc2(B.y), dy));
+          m = fma2(dy, t2, m);
+          m = fma2(dz, mul2(bc2(B.z), dz), m);
+          acc[q] = fma2(bc2(A.w), mk2(gauss_w(m.x), gauss_w(m.y)), acc[q]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    if (vid[v] >= 0) {
+      float val = (v & 1) ? acc[v / 2].y : acc[v / 2].x;
+      int64_t o = (int64_t)vid[v];
+      if (residual) val += residual[o];
+      val = fminf(fmaxf(val, 0.f), 1.f);
+      out[o] = val;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kVolWarps * 32) volume_kernel(const float4* __restrict__ grec,
+                                                                const int* __restrict__ gstart, int g, int r,
+                                                                VolAxes ax, const float* __restrict__ residual,
+                                                                float* __restrict__ out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nrx = ax.nr[0], nry = ax.nr[1], nrz = ax.nr[2];
+  const int64_t nitems = (int64_t)nrx * nry * nrz;
+  for (int64_t it = (int64_t)blockIdx.x * kVolWarps + warp; it < nitems; it += (int64_t)gridDim.x * kVolWarps) {
+    int rz = (int)(it % nrz);
+    int64_t t = it / nrz;
+    int ry = (int)(t % nry);
+    int rx = (int)(t / nry);
+    int bx0 = ax.rs[0][rx], nbx = ax.rs[0][rx + 1] - bx0;
+    int by0 = ax.rs[1][ry], nby = ax.rs[1][ry + 1] - by0;
+    int bz0 = ax.rs[2][rz], nbz = ax.rs[2][rz + 1] - bz0;
+    int cell = flat_cell(ax.rc[0][rx], ax.rc[1][ry], ax.rc[2][rz], g);
+    int nvox = nbx * nby * nbz;
+    if (nvox <= 64) {
+      vol_chunk<2>(grec, gstart, g, r, ax, bx0, by0, bz0, nbx, nby, nbz, cell, 0, nvox, residual, out, 0, lane);
+    } else {
+      for (int l0 = 0; l0 < nvox; l0 += 128)
+        vol_chunk<4>(grec, gstart, g, r, ax, bx0, by0, bz0, nbx, nby, nbz, cell, l0, nvox, residual, out, 0, lane);
+    }
+  }
+}
+
+size_t volume_workspace_bytes(int nx, int ny, int nz) {
+  int m = nx > ny ? nx : ny;
+  m = m > nz ? m : nz;
+  size_t per = (((size_t)(m + 1) * 4 + 255) & ~(size_t)255);
+  return 3 * 5 * per + 256 + scan_workspace_bytes(m);
+}
+
+// Samples voxels [i0, i1) x [0, ny) x [0, nz); out is the slab (i1-i0, ny, nz),
+// float32, clipped to [0, 1].  residual (optional) is added before the clip.
+void launch_sample_volume(const float4* grec, const int* gstart, int g, int r, const int dims[3], const double lo[3],
+                          const double hi[3], int i0, int i1, const float* residual, float* out, void* ws,
+                          cudaStream_t st) {
+  int n[3] = {dims[0], dims[1], dims[2]};
+  int m = n[0] > n[1] ? n[0] : n[1];
+  m = m > n[2] ? m : n[2];
+  size_t per = (((size_t)(m + 1) * 4 + 255) & ~(size_t)255);
+  char* w = (char*)ws;
+  int* nr = (int*)w;
+  w += 256;
+  VolAxes ax;
+  ax.nr = nr;
+  void* sws = w + 3 * 5 * per;
+  for (int a = 0; a < 3; ++a) {
+    int* cells = (int*)(w + (5 * a + 0) * per);
+    int* flags = (int*)(w + (5 * a + 1) * per);
+    int* scan = (int*)(w + (5 * a + 2) * per);
+    int* rs = (int*)(w + (5 * a + 3) * per);
+    int* rc = (int*)(w + (5 * a + 4) * per);
+    int v0 = a == 0 ? i0 : 0, v1 = a == 0 ? i1 : n[a];
+    ax.n[a] = n[a];
+    ax.lo[a] = lo[a];
+    ax.hi[a] = hi[a];
+    ax.sp[a] = n[a] == 1 ? (hi[a] - lo[a]) : (hi[a] - lo[a]) / (double)(n[a] - 1);
+    ax.v0[a] = 0;
+    ax.rs[a] = rs;
+    ax.rc[a] = rc;
+    int cnt = v1 - v0;
+    axis_cells_kernel<<<(cnt + 255) / 256, 256, 0, st>>>(n[a], v0, v1, lo[a], hi[a], ax.sp[a], g, cells, flags);
+    excl_scan(flags, scan, cnt, sws, st);
+    axis_runs_kernel<<<(cnt + 255) / 256, 256, 0, st>>>(cells, flags, scan, cnt, rs, rc, nr + a);
+  }
+  // axis-0 voxel indices inside the kernel are slab-relative; shift coordinates by i0
+  ax.v0[0] = i0;
+  int64_t maxitems = (int64_t)(i1 - i0) * n[1] * n[2];
+  int64_t blocks = (maxitems + kVolWarps - 1) / kVolWarps;
+  int64_t cap = (int64_t)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  // write offsets: kernel computes vid relative to the slab (i in [0, i1-i0))
+  volume_kernel<<<(unsigned)blocks, kVolWarps * 32, 0, st>>>(grec, gstart, g, r, ax, residual, out);
+}
+
+}  // namespace mg

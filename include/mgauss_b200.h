@@ -81,6 +81,9 @@ int mg_pack_records(const double *mu, const double *prec6, const double *alpha, 
 int mg_activate_f64(const double *quat, const double *log_scales, const double *logits, int64_t n, double *qn,
                     double *rot, double *inv_var, double *prec6, double *alpha, int32_t *err_flag, void *stream);
 
+/* Per-slice rotations R(q/|q|) (k,3,3) from w-first quats (k,4), float64 (core.py:48-67). */
+int mg_quat_to_rot_f64(const double *quats, int64_t k, double *rot, void *stream);
+
 /* ---- sample points: transform (+ PSF taps) and bin ---------------------- */
 size_t mg_points_workspace_bytes(int64_t n_sub, int64_t grid_res);
 /* n_sub = b * ntaps.  tap_offsets (ntaps) and through_dirs (k,3) may be NULL
@@ -141,9 +144,12 @@ int mg_sample_volume(const void *grec, const int32_t *gstart, int64_t grid_res, 
                      const float *residual, float *out, void *ws, size_t ws_bytes, void *stream);
 
 /* ---- training: train.py ------------------------------------------------- */
+/* Smooth-L1 data loss (mean over b) fused with the PSF tap reduction:
+ * pred_out = sum_t w_t I_(b,t) (+ residual), upstream_out = dL/dpred (b),
+ * loss_acc += loss (float64 device scalar). */
 int mg_smooth_l1(const void *out4, const int32_t *pinv, int64_t b, int32_t ntaps, const double *tap_weights,
-                 const float *target, const float *residual, void *prec, float *pred_out, double *loss_acc,
-                 void *stream);
+                 const float *target, const float *residual, float *pred_out, float *upstream_out,
+                 double *loss_acc, void *stream);
 int mg_counter_incr(int32_t *counters, int32_t n, void *stream);
 /* hyper (host, 9 doubles): lr_pos, lr_quat, lr_scale, lr_logit, beta1, beta2, eps, lambda_aniso, lambda_ratio.
  * t_dev: device int32 post-increment Adam step.  Moments m, v are (n, 11) float32. */

@@ -356,10 +356,15 @@ int mg_sample_volume(const void* grec, const int32_t* gstart, int64_t g, int64_t
 }
 
 int mg_smooth_l1(const void* out4, const int32_t* pinv, int64_t b, int32_t ntaps, const double* tap_w,
-                 const float* target, const float* residual, void* prec, float* pred_out, double* loss_acc,
+                 const float* target, const float* residual, float* pred_out, float* up_out, double* loss_acc,
                  void* stream) {
-  launch_smooth_l1((const float4*)out4, pinv, b, ntaps, ntaps > 1 ? tap_w : nullptr, target, residual, (float4*)prec,
-                   pred_out, loss_acc, S(stream));
+  launch_smooth_l1((const float4*)out4, pinv, b, ntaps, ntaps > 1 ? tap_w : nullptr, target, residual, pred_out,
+                   up_out, loss_acc, S(stream));
+  return cuda_status();
+}
+
+int mg_quat_to_rot_f64(const double* q, int64_t k, double* rot, void* stream) {
+  launch_quat_to_rot(q, k, rot, S(stream));
   return cuda_status();
 }
 

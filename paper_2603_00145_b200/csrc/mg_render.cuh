@@ -44,8 +44,9 @@ void launch_transform_grads(const double* dpoints, const double* coords, const i
                             const double* tap_off, const double* dirs, const double* tq, int k, double* acc12,
                             double* out7, int accumulate, cudaStream_t st);
 void launch_smooth_l1(const float4* out4, const int* inv, int64_t b, int ntaps, const double* tap_w,
-                      const float* target, const float* residual, float4* prec, float* pred_out, double* loss_acc,
+                      const float* target, const float* residual, float* pred_out, float* up_out, double* loss_acc,
                       cudaStream_t st);
+void launch_quat_to_rot(const double* q, int64_t k, double* rot, cudaStream_t st);
 void launch_counter_incr(int* c, int n, cudaStream_t st);
 void launch_gauss_update(const float* acc10, const int* order, int64_t n, float* pos, float* quat, float* ls,
                          float* lg, float* mom_m, float* mom_v, const double* hyper, int use_aniso,

@@ -253,8 +253,8 @@ __global__ void transform_chain_kernel(const double* __restrict__ acc12, const d
 // ---------------------------------------------------------------------------
 __global__ void smooth_l1_kernel(const float4* __restrict__ out4, const int* __restrict__ inv, int64_t b, int ntaps,
                                  const double* __restrict__ tap_w, const float* __restrict__ target,
-                                 const float* __restrict__ residual, double scale, float4* __restrict__ prec,
-                                 float* __restrict__ pred_out, double* __restrict__ loss_acc) {
+                                 const float* __restrict__ residual, double scale, float* __restrict__ pred_out,
+                                 float* __restrict__ up_out, double* __restrict__ loss_acc) {
   double local = 0.0;
   GRID_LOOP(pb, b) {
     double pred = 0.0;
@@ -265,7 +265,7 @@ __global__ void smooth_l1_kernel(const float4* __restrict__ out4, const int* __r
     double ax = fabs(x);
     local += ax < 1.0 ? 0.5 * x * x : ax - 0.5;
     double gr = (ax < 1.0 ? x : (x > 0 ? 1.0 : (x < 0 ? -1.0 : 0.0))) * scale;
-    for (int t = 0; t < ntaps; ++t) prec[inv[pb * ntaps + t]].w = (float)(gr * (tap_w ? tap_w[t] : 1.0));
+    up_out[pb] = (float)gr;
   }
   // block reduce the loss
   __shared__ double s_red[32];
@@ -457,11 +457,22 @@ void launch_transform_grads(const double* dpoints, const double* coords, const i
   transform_chain_kernel<<<gridn(k), 256, 0, st>>>(acc12, tq, k, out7, accumulate);
 }
 void launch_smooth_l1(const float4* out4, const int* inv, int64_t b, int ntaps, const double* tap_w,
-                      const float* target, const float* residual, float4* prec, float* pred_out, double* loss_acc,
+                      const float* target, const float* residual, float* pred_out, float* up_out, double* loss_acc,
                       cudaStream_t st) {
   if (b > 0)
-    smooth_l1_kernel<<<gridn(b), 256, 0, st>>>(out4, inv, b, ntaps, tap_w, target, residual, 1.0 / (double)b, prec,
-                                               pred_out, loss_acc);
+    smooth_l1_kernel<<<gridn(b), 256, 0, st>>>(out4, inv, b, ntaps, tap_w, target, residual, 1.0 / (double)b,
+                                               pred_out, up_out, loss_acc);
+}
+
+__global__ void quat_to_rot_kernel(const double* __restrict__ q, int64_t k, double* __restrict__ rot) {
+  GRID_LOOP(s, k) {
+    double qw = q[4 * s], qx = q[4 * s + 1], qy = q[4 * s + 2], qz = q[4 * s + 3];
+    double nrm = sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
+    quat_rot_d2(qw / nrm, qx / nrm, qy / nrm, qz / nrm, rot + 9 * s);
+  }
+}
+void launch_quat_to_rot(const double* q, int64_t k, double* rot, cudaStream_t st) {
+  if (k > 0) quat_to_rot_kernel<<<gridn(k), 256, 0, st>>>(q, k, rot);
 }
 __global__ void counter_incr_kernel(int* c, int n) {
   if (threadIdx.x < n) c[threadIdx.x] += 1;

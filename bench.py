@@ -1,0 +1,419 @@
+"""Benchmark: Gaussian-sample (candidate-pair) evaluations per second, forward +
+backward, for one training step of the M-Gaussian hot path on B200.
+
+Workload (BASELINE.json configs[1], "C2"): 160^3 phantom at 0.8 mm, three
+orthogonal stacks of 3 mm slices (3 x 42 x 160^2 = 3,225,600 samples), 3-tap
+Gaussian slice PSF, 100k Gaussians (R = G = 46 lattice, N = 97,336), a step =
+65,536 batch points + one 160x160 SSIM slice, each expanded to 3 PSF taps.
+One step = Gaussian binning + activation, point transform/binning, forward,
+smooth-L1 + SSIM gradients, Gaussian-major backward, transform gradients,
+fused chain-rule + aniso + Adam.  Synthetic data (paper_2603_00145_b200.synth).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+N > 1 is launched with torch.distributed.run: one rank per GPU, weak scaling
+(each rank its own 65,536-point batch), NCCL all-reduce of the per-Gaussian
+gradient accumulators.  Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Gaussian-sample evals/sec fwd+bwd"
+UNIT = "pairs/s"
+FLOP_FWD, FLOP_BWD = 20, 56  # algorithmic FP32 FLOP per candidate pair
+CONFIG = "C2"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=CONFIG)
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--cpu-sample-points", type=int, default=65536)
+    return ap.parse_args()
+
+
+def dist_info():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        rows = [r for r in self.rows if len(r) >= 7]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def make_workload(cfg_name, rank):
+    from paper_2603_00145_b200.render import SlicePSF
+    from paper_2603_00145_b200.synth import CONFIGS, make_config
+    from paper_2603_00145_b200.train import TrainConfig
+
+    data = make_config(cfg_name, seed=7)
+    _, _, _, _, lattice, use_nrf, batch = CONFIGS[cfg_name]
+    grids = []
+    for k in range(data.num_slices):
+        c, t = data.slice_grid(k)
+        grids.append(type("SG", (), {"coords": c, "target": t, "slice_id": k})())
+    psf = SlicePSF(data.psf_offsets, data.psf_weights, data.through_dirs)
+    cfg = TrainConfig(resolution_schedule=((0, lattice),), use_nrf=use_nrf, use_ssim=True, batch_points=batch,
+                      seed=7 + rank, total_iters=10 ** 9)
+    cloud = type("Cloud", (), {"coords": data.coords, "intensities": data.intensities,
+                               "slice_ids": data.slice_ids})()
+    return data, cloud, grids, psf, cfg
+
+
+def peak_fp32(sm_count, mhz):
+    return 2.0 * 128 * sm_count * mhz * 1e6  # FFMA = 2 FLOP, 128 FP32 lanes per SM
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def count_graph_kernels(graph):
+    """Kernel nodes in a captured torch CUDA graph (cudaGraphGetNodes + node types)."""
+    try:
+        import ctypes
+
+        raw = graph.raw_cuda_graph()
+        rt = ctypes.CDLL("libcudart.so")
+    except Exception:
+        try:
+            import ctypes
+            import glob
+
+            import torch
+
+            libs = glob.glob(os.path.join(os.path.dirname(torch.__file__), "lib", "libcudart*.so*"))
+            libs += glob.glob("/usr/local/cuda/lib64/libcudart.so*")
+            rt = ctypes.CDLL(libs[0])
+            raw = graph.raw_cuda_graph()
+        except Exception:
+            return None
+    n = ctypes.c_size_t(0)
+    if rt.cudaGraphGetNodes(ctypes.c_void_p(raw), None, ctypes.byref(n)) != 0:
+        return None
+    nodes = (ctypes.c_void_p * n.value)()
+    rt.cudaGraphGetNodes(ctypes.c_void_p(raw), nodes, ctypes.byref(n))
+    kernels = 0
+    for i in range(n.value):
+        t = ctypes.c_int(0)
+        rt.cudaGraphNodeGetType(ctypes.c_void_p(nodes[i]), ctypes.byref(t))
+        kernels += int(t.value == 0)  # cudaGraphNodeTypeKernel
+    return kernels
+
+
+def cpu_baseline(trainer, data, psf, sample_points, threads):
+    """Oracle (C restatement of the reference kernels + numpy host math), all host
+    threads, on a bounded sample of one step: render + backward over the first
+    `sample_points` batch points with the same field, transforms and PSF."""
+    from oracle import oracle as O
+
+    f = trainer.field.to_host()
+    ts = trainer.transforms_host()
+    g = trainer.field.resolution
+    idx = trainer._next_batch()[:sample_points]
+    coords, sids = data.coords[idx], data.slice_ids[idx]
+    up = np.random.default_rng(0).normal(size=len(idx)) * 1e-5
+    t0 = time.perf_counter()
+    inten, cnt = O.psf_render(f.positions, f.quaternions, f.log_scales, f.intensity_logits, g, 5, coords, sids,
+                              ts.quats, ts.translations, psf.offsets, psf.weights, psf.through_dirs, threads)
+    O.psf_backward(f.positions, f.quaternions, f.log_scales, f.intensity_logits, g, 5, coords, sids, ts.quats,
+                   ts.translations, psf.offsets, psf.weights, psf.through_dirs, up, threads)
+    dt = time.perf_counter() - t0
+    pairs = int(cnt.sum())
+    return pairs / dt, pairs, dt, len(idx)
+
+
+def run_reference(args):
+    rank, world, _ = dist_info()
+    if rank != 0:
+        return
+    import torch  # noqa: F401  (workload generator imports it)
+
+    from oracle import oracle as O
+
+    threads = os.cpu_count() or 1
+    data, cloud, grids, psf, cfg = make_workload(args.config, 0)
+    from paper_2603_00145_b200.core import uniform_lattice_field
+
+    r = cfg.resolution_schedule[0][1]
+    f = uniform_lattice_field(r)
+    f.intensity_logits[:] = O.init_logits(data.coords, data.intensities, r)
+    rng = np.random.default_rng(7)
+    per_step = max(1024, args.cpu_sample_points)
+    total_pairs, total_t = 0, 0.0
+    for s in range(args.warmup + args.steps):
+        idx = rng.choice(data.coords.shape[0], per_step, replace=False)
+        coords, sids = data.coords[idx], data.slice_ids[idx]
+        up = rng.normal(size=per_step) * 1e-5
+        t0 = time.perf_counter()
+        _, cnt = O.psf_render(f.positions, f.quaternions, f.log_scales, f.intensity_logits, r, 5, coords, sids,
+                              data.transforms.quats, data.transforms.translations, psf.offsets, psf.weights,
+                              psf.through_dirs, threads)
+        O.psf_backward(f.positions, f.quaternions, f.log_scales, f.intensity_logits, r, 5, coords, sids,
+                       data.transforms.quats, data.transforms.translations, psf.offsets, psf.weights,
+                       psf.through_dirs, up, threads)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            total_pairs += int(cnt.sum())
+            total_t += dt
+    v = total_pairs / total_t
+    sample = (f"{per_step} batch points x {psf.ntaps} PSF taps per step (of 65,536 + 25,600), fwd+bwd incl. "
+              f"activation/binning/epilogue, C2 field R={r}")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000 * total_t / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: 160^3 @0.8mm, 3 stacks x 42 slices 3mm, PSF 3 taps, N=97,336",
+                   "cpu_threads": threads},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def run_ours(args):
+    import torch
+
+    rank, world, local = dist_info()
+    torch.cuda.set_device(local)
+    group = None
+    if world > 1:
+        import torch.distributed as tdist
+
+        tdist.init_process_group("nccl")
+        group = tdist.group.WORLD
+    from paper_2603_00145_b200 import _native as N
+    from paper_2603_00145_b200.train import Trainer
+
+    data, cloud, grids, psf, cfg = make_workload(args.config, rank)
+    tr = Trainer(cloud, data.transforms, cfg, slice_grids=grids, slice_psf=psf, graph=not args.no_graph,
+                 dist=group)
+    # warm-up (eager first step, then graph capture + replays)
+    for _ in range(max(args.warmup, 3)):
+        tr.step(sync=True)
+    # pre-generate the timed steps' indices on the host RNG, upload -> device-resident inputs
+    steps_idx = []
+    for _ in range(args.steps):
+        idx = tr._next_batch()
+        j = int(tr.rng.integers(len(tr.slice_grids)))
+        all_idx, hw = tr.host_indices(idx, j)
+        steps_idx.append(torch.from_numpy(all_idx).cuda())
+    nb = cfg.batch_points
+    B = tr._buffers(len(steps_idx[0]))
+    B.pairs.zero_()
+    sampler = ClockSampler(local)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    time.sleep(0.3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for k in range(args.steps):
+        tr.load_indices(steps_idx[k])
+        if tr._graph is not None and world == 1:
+            tr._graph.replay()
+        else:
+            tr._body(B, nb, hw)
+        tr.iteration += 1
+    e1.record()
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    if world > 1:
+        torch.distributed.barrier()
+    ms = e0.elapsed_time(e1)
+    pairs_local = int(B.pairs.item())
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    pt = torch.tensor([pairs_local], dtype=torch.float64, device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(pt)
+    ms_max = float(t.item())
+    pairs_total = float(pt.item())
+    value = pairs_total / (ms_max / 1000.0)
+
+    # --- kernel-level timing (CUDA events around the pair kernels, eager, same stream) ---
+    kt = kernel_times(tr, steps_idx[: min(5, len(steps_idx))], nb, hw)
+
+    # --- end to end through the public API: Trainer.step() with host RNG batches (H2D) + loss D2H ---
+    e2e_steps = max(3, min(args.steps, 10))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    p_before = int(B.pairs.item())
+    for _ in range(e2e_steps):
+        tr.step(sync=True)
+    torch.cuda.synchronize()
+    e2e_dt = time.perf_counter() - t0
+    e2e_pairs = int(B.pairs.item()) - p_before
+    e2e_t = torch.tensor([e2e_dt], dtype=torch.float64, device="cuda")
+    e2e_p = torch.tensor([e2e_pairs], dtype=torch.float64, device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(e2e_t, op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(e2e_p)
+    e2e_val = float(e2e_p.item()) / float(e2e_t.item())
+
+    if rank != 0:
+        torch.distributed.destroy_process_group()
+        return
+    peaks = load_peaks()
+    sms = N.lib().mg_device_sm_count()
+    mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
+    peak = peak_fp32(sms, mhz)
+    fwd_ms, bwd_ms, kpairs = kt["forward_ms"], kt["backward_ms"], kt["pairs_per_launch"]
+    achieved_fwd = kpairs * FLOP_FWD / (fwd_ms / 1e3)
+    achieved_bwd = kpairs * FLOP_BWD / (bwd_ms / 1e3)
+    achieved_pair = kpairs * (FLOP_FWD + FLOP_BWD) / ((fwd_ms + bwd_ms) / 1e3)
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("backward_kernel_dram_bytes")
+        except Exception:
+            traffic = None
+    nlaunch = count_graph_kernels(tr._graph) if tr._graph is not None else None
+    cpu = None
+    if world == 1 or rank == 0:
+        threads = os.cpu_count() or 1
+        v, p, dt, npts = cpu_baseline(tr, data, psf, args.cpu_sample_points, threads)
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"{npts} batch points x {psf.ntaps} taps of one C2 step ({p} pairs, {dt:.1f} s), "
+                         f"fwd+bwd incl. host epilogue"}
+    bytes_h2d = int(steps_idx[0].numel() * 8)
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "C2: 160^3 @0.8mm phantom, 3 stacks x 42 slices of 160^2 at 3mm, 3-tap slab PSF, "
+                               "N=97,336 Gaussians (R=G=46), r=5, step = 65,536 batch + 25,600 SSIM-slice points",
+                   "global_batch": nb * world, "pairs_per_step": pairs_total / args.steps,
+                   "parallelism": f"dp{world}", "l2": "inputs and per-step working set fit in L2 (126 MB); "
+                   "steps differ in batch, no flush", "cuda_graph": tr._graph is not None},
+        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": bytes_h2d, "d2h_bytes_per_step": 32 + 4,
+                "path": "Trainer.step(): host RNG batch -> pinned H2D -> graph replay -> loss D2H"},
+        "roofline": {"bound": "fp32", "achieved": achieved_pair / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
+                     "frac": achieved_pair / peak, "traffic": traffic,
+                     "peak_source": f"nominal 256 FLOP/clk/SM x {sms} SMs x {mhz:.0f} MHz (measured SM clock); "
+                                    "MEASURED_PEAKS.json has no FP32 figure",
+                     "kernels": {"forward": {"ms": fwd_ms, "tflops": achieved_fwd / 1e12,
+                                             "frac": achieved_fwd / peak},
+                                 "backward": {"ms": bwd_ms, "tflops": achieved_bwd / 1e12,
+                                              "frac": achieved_bwd / peak},
+                                 "pairs_per_launch": kpairs, "flop_per_pair": [FLOP_FWD, FLOP_BWD]}},
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+        "gpu_launches": (nlaunch * args.steps) if nlaunch else None,
+    }
+    print(json.dumps(out))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def kernel_times(tr, idx_list, nb, hw):
+    """Average device time of the forward and backward pair kernels, via CUDA
+    events on the launching (current) stream, eager replays of timed batches."""
+    import torch
+
+    from paper_2603_00145_b200 import _native as N
+
+    L = N.lib()
+    fwd, bwd, pairs = [], [], []
+    orig_fwd, orig_bwd = L.mg_forward, L.mg_backward
+
+    class Timed:
+        def __init__(self, fn, sink):
+            self.fn, self.sink = fn, sink
+
+        def __call__(self, *a):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            rc = self.fn(*a)
+            e1.record()
+            self.sink.append((e0, e1))
+            return rc
+
+    B = tr._buffers(len(idx_list[0]))
+    try:
+        L.mg_forward, L.mg_backward = Timed(orig_fwd, fwd), Timed(orig_bwd, bwd)
+        for ix in idx_list:
+            tr.load_indices(ix)
+            tr._body(B, nb, hw)
+            torch.cuda.synchronize()
+            pairs.append(int(B.cnt.sum().item()))
+    finally:
+        L.mg_forward, L.mg_backward = orig_fwd, orig_bwd
+    torch.cuda.synchronize()
+    f = float(np.mean([a.elapsed_time(b) for a, b in fwd]))
+    b = float(np.mean([a.elapsed_time(c) for a, c in bwd]))
+    return {"forward_ms": f, "backward_ms": b, "pairs_per_launch": float(np.mean(pairs))}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

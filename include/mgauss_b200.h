@@ -144,12 +144,15 @@ int mg_sample_volume(const void *grec, const int32_t *gstart, int64_t grid_res, 
                      const float *residual, float *out, void *ws, size_t ws_bytes, void *stream);
 
 /* ---- training: train.py ------------------------------------------------- */
-/* Smooth-L1 data loss (mean over b) fused with the PSF tap reduction:
- * pred_out = sum_t w_t I_(b,t) (+ residual), upstream_out = dL/dpred (b),
- * loss_acc += loss (float64 device scalar). */
-int mg_smooth_l1(const void *out4, const int32_t *pinv, int64_t b, int32_t ntaps, const double *tap_weights,
-                 const float *target, const float *residual, float *pred_out, float *upstream_out,
-                 double *loss_acc, void *stream);
+/* Smooth-L1 data loss (train.py:108-120): upstream_out = dL/dpred over the b
+ * predictions (mean), loss_acc += L (float64 device scalar). */
+int mg_smooth_l1(const float *pred, const float *target, int64_t b, float *upstream_out, double *loss_acc,
+                 void *stream);
+/* 2D SSIM (ssim.py:59-122) of an (H,W) slice: upstream_out = scale * d(1-SSIM)/dpred,
+ * ssim_sum += sum of the SSIM map over the (H-10)(W-10) valid windows. */
+size_t mg_ssim_workspace_bytes(int64_t h, int64_t w);
+int mg_ssim_loss_grad(const float *pred, const float *target, int64_t h, int64_t w, double scale,
+                      float *upstream_out, double *ssim_sum, void *ws, size_t ws_bytes, void *stream);
 int mg_counter_incr(int32_t *counters, int32_t n, void *stream);
 /* hyper (host, 9 doubles): lr_pos, lr_quat, lr_scale, lr_logit, beta1, beta2, eps, lambda_aniso, lambda_ratio.
  * t_dev: device int32 post-increment Adam step.  Moments m, v are (n, 11) float32. */

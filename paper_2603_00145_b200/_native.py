@@ -50,7 +50,9 @@ SIGNATURES = {
     "mg_transform_grads": (ctypes.c_int, [P, P, P, I64, I32, P, P, P, I64, P, P, I32, P]),
     "mg_volume_workspace_bytes": (SZ, [I64, I64, I64]),
     "mg_sample_volume": (ctypes.c_int, [P, P, I64, I64, I64, I64, I64, P, P, I64, I64, P, P, P, SZ, P]),
-    "mg_smooth_l1": (ctypes.c_int, [P, P, I64, I32, P, P, P, P, P, P, P]),
+    "mg_smooth_l1": (ctypes.c_int, [P, P, I64, P, P, P]),
+    "mg_ssim_workspace_bytes": (SZ, [I64, I64]),
+    "mg_ssim_loss_grad": (ctypes.c_int, [P, P, I64, I64, D, P, P, P, SZ, P]),
     "mg_quat_to_rot_f64": (ctypes.c_int, [P, I64, P, P]),
     "mg_counter_incr": (ctypes.c_int, [P, I32, P]),
     "mg_gauss_update": (ctypes.c_int, [P, P, I64, P, P, P, P, P, P, P, I32, P, P, P]),

@@ -355,11 +355,18 @@ int mg_sample_volume(const void* grec, const int32_t* gstart, int64_t g, int64_t
   return cuda_status();
 }
 
-int mg_smooth_l1(const void* out4, const int32_t* pinv, int64_t b, int32_t ntaps, const double* tap_w,
-                 const float* target, const float* residual, float* pred_out, float* up_out, double* loss_acc,
-                 void* stream) {
-  launch_smooth_l1((const float4*)out4, pinv, b, ntaps, ntaps > 1 ? tap_w : nullptr, target, residual, pred_out,
-                   up_out, loss_acc, S(stream));
+int mg_smooth_l1(const float* pred, const float* target, int64_t b, float* up_out, double* loss_acc, void* stream) {
+  launch_smooth_l1(pred, target, b, up_out, loss_acc, S(stream));
+  return cuda_status();
+}
+
+size_t mg_ssim_workspace_bytes(int64_t h, int64_t w) { return ssim_workspace_bytes((int)h, (int)w); }
+
+int mg_ssim_loss_grad(const float* pred, const float* target, int64_t h, int64_t w, double scale, float* up,
+                      double* ssim_sum, void* ws, size_t wsb, void* stream) {
+  if (h < 11 || w < 11) return fail("mg_ssim_loss_grad: slice smaller than the 11-tap window");
+  if (wsb < ssim_workspace_bytes((int)h, (int)w)) return fail("mg_ssim_loss_grad: workspace too small");
+  launch_ssim(pred, target, (int)h, (int)w, scale, up, ssim_sum, ws, S(stream));
   return cuda_status();
 }
 

@@ -43,9 +43,11 @@ void launch_epilogue_f64(const double* d_mu, const double* d_abar6, const double
 void launch_transform_grads(const double* dpoints, const double* coords, const int64_t* sids, int64_t b, int ntaps,
                             const double* tap_off, const double* dirs, const double* tq, int k, double* acc12,
                             double* out7, int accumulate, cudaStream_t st);
-void launch_smooth_l1(const float4* out4, const int* inv, int64_t b, int ntaps, const double* tap_w,
-                      const float* target, const float* residual, float* pred_out, float* up_out, double* loss_acc,
+void launch_smooth_l1(const float* pred, const float* target, int64_t b, float* up_out, double* loss_acc,
                       cudaStream_t st);
+size_t ssim_workspace_bytes(int H, int W);
+void launch_ssim(const float* pred, const float* tgt, int H, int W, double scale, float* up, double* ssim_sum,
+                 void* ws, cudaStream_t st);
 void launch_quat_to_rot(const double* q, int64_t k, double* rot, cudaStream_t st);
 void launch_counter_incr(int* c, int n, cudaStream_t st);
 void launch_gauss_update(const float* acc10, const int* order, int64_t n, float* pos, float* quat, float* ls,

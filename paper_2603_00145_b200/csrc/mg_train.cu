@@ -248,26 +248,17 @@ __global__ void transform_chain_kernel(const double* __restrict__ acc12, const d
 }
 
 // ---------------------------------------------------------------------------
-// Smooth-L1 (train.py:108-120) over the batch, fused with the tap reduction.
-// Writes upstream u_(b,t) = w_t * dL/dpred_b into the point records.
+// Smooth-L1 (train.py:108-120): mean Huber (delta 1) and its gradient.
 // ---------------------------------------------------------------------------
-__global__ void smooth_l1_kernel(const float4* __restrict__ out4, const int* __restrict__ inv, int64_t b, int ntaps,
-                                 const double* __restrict__ tap_w, const float* __restrict__ target,
-                                 const float* __restrict__ residual, double scale, float* __restrict__ pred_out,
-                                 float* __restrict__ up_out, double* __restrict__ loss_acc) {
+__global__ void smooth_l1_kernel(const float* __restrict__ pred, const float* __restrict__ target, int64_t b,
+                                 double scale, float* __restrict__ up_out, double* __restrict__ loss_acc) {
   double local = 0.0;
   GRID_LOOP(pb, b) {
-    double pred = 0.0;
-    for (int t = 0; t < ntaps; ++t) pred += (tap_w ? tap_w[t] : 1.0) * (double)out4[inv[pb * ntaps + t]].w;
-    if (residual) pred += (double)residual[pb];
-    if (pred_out) pred_out[pb] = (float)pred;
-    double x = pred - (double)target[pb];
+    double x = (double)pred[pb] - (double)target[pb];
     double ax = fabs(x);
     local += ax < 1.0 ? 0.5 * x * x : ax - 0.5;
-    double gr = (ax < 1.0 ? x : (x > 0 ? 1.0 : (x < 0 ? -1.0 : 0.0))) * scale;
-    up_out[pb] = (float)gr;
+    up_out[pb] = (float)((ax < 1.0 ? x : (x > 0 ? 1.0 : (x < 0 ? -1.0 : 0.0))) * scale);
   }
-  // block reduce the loss
   __shared__ double s_red[32];
   for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(MG_FULL, local, o);
   if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = local;
@@ -456,12 +447,9 @@ void launch_transform_grads(const double* dpoints, const double* coords, const i
   }
   transform_chain_kernel<<<gridn(k), 256, 0, st>>>(acc12, tq, k, out7, accumulate);
 }
-void launch_smooth_l1(const float4* out4, const int* inv, int64_t b, int ntaps, const double* tap_w,
-                      const float* target, const float* residual, float* pred_out, float* up_out, double* loss_acc,
+void launch_smooth_l1(const float* pred, const float* target, int64_t b, float* up_out, double* loss_acc,
                       cudaStream_t st) {
-  if (b > 0)
-    smooth_l1_kernel<<<gridn(b), 256, 0, st>>>(out4, inv, b, ntaps, tap_w, target, residual, 1.0 / (double)b,
-                                               pred_out, up_out, loss_acc);
+  if (b > 0) smooth_l1_kernel<<<gridn(b), 256, 0, st>>>(pred, target, b, 1.0 / (double)b, up_out, loss_acc);
 }
 
 __global__ void quat_to_rot_kernel(const double* __restrict__ q, int64_t k, double* __restrict__ rot) {

@@ -1,0 +1,127 @@
+"""Neural Residual Field on the device (/root/reference/pkg/src/mgauss/nrf.py).
+
+r(x) = 0.1 * tanh(MLP(enc(x))), enc = [x, sin(2^k pi x), cos(2^k pi x)]_{k<6}
+(39 dims), hidden widths (64, 64, 64, 64) with SiLU, zero-initialised last
+layer.  The four dense layers are plain fp32 GEMMs (cuBLAS through torch);
+SURVEY §8(a) A16 allows tensor cores only once ncu shows the MLP is a
+dense-contraction bottleneck, and bf16/tf32 would break the 1e-4 parity.
+Manual backward identical to nrf.py:147-182 (including d/dx into transforms).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field as dc_field
+
+import numpy as np
+import torch
+
+from . import _device as dv
+from .errors import UninitializedField
+
+OUTPUT_BOUND = 0.1
+DEFAULT_BANDS = 6
+DEFAULT_HIDDEN = (64, 64, 64, 64)
+
+
+@dataclass
+class ResidualField:
+    frequency_bands: int = DEFAULT_BANDS
+    layer_widths: tuple = ()
+    weights: list = dc_field(default_factory=list)  # (fan_in, fan_out) float32 device tensors
+    biases: list = dc_field(default_factory=list)
+    output_bound: float = OUTPUT_BOUND
+
+    @classmethod
+    def create(cls, rng=None, frequency_bands=DEFAULT_BANDS, hidden=DEFAULT_HIDDEN):
+        """Same initialisation stream as nrf.py:58-83 (uniform +-sqrt(6/(fi+fo)), last layer 0)."""
+        rng = np.random.default_rng(rng)
+        widths = (3 + 6 * int(frequency_bands),) + tuple(hidden) + (1,)
+        ws, bs = [], []
+        for li in range(len(widths) - 1):
+            fi, fo = widths[li], widths[li + 1]
+            if li == len(widths) - 2:
+                w = np.zeros((fi, fo))
+            else:
+                bound = np.sqrt(6.0 / (fi + fo))
+                w = rng.uniform(-bound, bound, size=(fi, fo))
+            ws.append(dv.to_dev(w, torch.float32))
+            bs.append(dv.zeros((fo,), torch.float32))
+        return cls(int(frequency_bands), widths, ws, bs)
+
+    @classmethod
+    def from_numpy(cls, weights, biases, frequency_bands=DEFAULT_BANDS):
+        ws = [dv.to_dev(np.asarray(w), torch.float32) for w in weights]
+        bs = [dv.to_dev(np.asarray(b), torch.float32) for b in biases]
+        widths = (ws[0].shape[0],) + tuple(w.shape[1] for w in ws)
+        return cls(int(frequency_bands), widths, ws, bs)
+
+    def parameter_arrays(self):
+        out = {}
+        for li, (w, b) in enumerate(zip(self.weights, self.biases)):
+            out[f"w{li}"] = w
+            out[f"b{li}"] = b
+        return out
+
+
+def fourier_encode(x: torch.Tensor, bands: int) -> torch.Tensor:
+    """nrf.py:23-36 on device."""
+    parts = [x]
+    for k in range(bands):
+        s = x * ((2.0 ** k) * np.pi)
+        parts.append(torch.sin(s))
+        parts.append(torch.cos(s))
+    return torch.cat(parts, dim=1)
+
+
+def nrf_forward_cached(field: ResidualField, x: torch.Tensor):
+    if not field.weights:
+        raise UninitializedField("residual field has no weights")
+    h = fourier_encode(x, field.frequency_bands)
+    pre, post = [], [h]
+    depth = len(field.weights)
+    for li in range(depth):
+        z = torch.addmm(field.biases[li], h, field.weights[li])
+        pre.append(z)
+        if li < depth - 1:
+            h = z * torch.sigmoid(z)
+            post.append(h)
+    t = torch.tanh(pre[-1][:, 0])
+    return field.output_bound * t, (t, pre, post)
+
+
+def nrf_forward_device(field: ResidualField, x: torch.Tensor, chunk=1 << 20):
+    out = torch.empty(x.shape[0], dtype=torch.float32, device=x.device)
+    for lo in range(0, x.shape[0], chunk):
+        out[lo:lo + chunk] = nrf_forward_cached(field, x[lo:lo + chunk])[0]
+    return out
+
+
+def nrf_backward(field: ResidualField, x: torch.Tensor, upstream: torch.Tensor, cache):
+    """(d_weights, d_biases, d_points) of sum_b upstream_b r(x_b)."""
+    t, pre, post = cache
+    depth = len(field.weights)
+    dws, dbs = [None] * depth, [None] * depth
+    dz = (upstream * field.output_bound * (1.0 - t * t))[:, None]
+    d_enc = None
+    for li in range(depth - 1, -1, -1):
+        dws[li] = post[li].T @ dz
+        dbs[li] = dz.sum(dim=0)
+        dh = dz @ field.weights[li].T
+        if li > 0:
+            s = torch.sigmoid(pre[li - 1])
+            dz = dh * (s * (1.0 + pre[li - 1] * (1.0 - s)))
+        else:
+            d_enc = dh
+    dp = d_enc[:, :3].clone()
+    for k in range(field.frequency_bands):
+        f = (2.0 ** k) * np.pi
+        dp += f * torch.cos(f * x) * d_enc[:, 3 + 6 * k:6 + 6 * k]
+        dp -= f * torch.sin(f * x) * d_enc[:, 6 + 6 * k:9 + 6 * k]
+    return dws, dbs, dp
+
+
+def nrf_forward(field: ResidualField, x):
+    """Host-facing r(x) (numpy in, numpy out), nrf.py:132-137."""
+    xt = dv.to_dev(np.atleast_2d(np.asarray(x, dtype=np.float64)), torch.float32)
+    r = dv.to_host(nrf_forward_cached(field, xt)[0]).astype(np.float64)
+    return float(r[0]) if np.asarray(x).ndim == 1 else r

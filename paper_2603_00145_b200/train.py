@@ -1,0 +1,610 @@
+"""Device-resident training step -- drop-in for the hot part of
+/root/reference/pkg/src/mgauss/train.py (TrainConfig, losses, AdamState,
+progressive_upsample, init_field, Trainer.step / run / render_volume).
+
+One step runs entirely on the B200: Gaussian binning (radix sort) and
+activation, point transform + PSF taps + binning, the cell-exact forward
+(with H = sum alpha g P d for d_points), smooth-L1 and SSIM gradients,
+the Gaussian-major backward, transform gradients, and one fused kernel for
+the chain rule + anisotropy penalty + Adam on the four Gaussian groups.
+The host only draws batch indices from the reference's RNG stream
+(SeedSequence(seed).spawn(2), train.py:332-335,348-363,408) so batches are
+identical to the reference's.  With ``graph=True`` the step is captured
+once per lattice level and replayed as a CUDA graph.
+
+Multi-GPU: Gaussians replicated, sample points sharded; the
+only exchange is an all-reduce(sum) of the per-Gaussian accumulators, the
+transform accumulators and the loss partials.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field as dc_field, replace  # noqa: F401
+
+import numpy as np
+import torch
+
+from . import _device as dv
+from . import _native as N
+from .core import TransformSet, lattice_node_index, lattice_node_positions  # noqa: F401
+from .errors import NonFiniteLoss, ShrinkNotAllowed
+from .render import SlicePSF, sample_volume_device
+
+DEFAULT_SCHEDULE = ((0, 70), (500, 100), (1000, 130), (2000, 165), (3000, 200))
+
+
+@dataclass
+class TrainConfig:
+    """Hyperparameters with the reference defaults (train.py:40-66)."""
+
+    lr_position: float = 0.001
+    lr_intensity: float = 0.05
+    lr_scale: float = 0.005
+    lr_rotation: float = 0.001
+    lr_nrf: float = 0.0001
+    lr_transform: float = 0.0001
+    lambda_ssim: float = 0.5
+    lambda_aniso: float = 0.1
+    lambda_ratio: float = 1.5
+    block_radius: int = 5
+    resolution_schedule: tuple = DEFAULT_SCHEDULE
+    nrf_activation_iter: int = 2000
+    total_iters: int = 4000
+    batch_points: int = 65536
+    adam_beta1: float = 0.9
+    adam_beta2: float = 0.999
+    adam_eps: float = 1e-8
+    seed: int = 0
+    use_ssim: bool = True
+    use_nrf: bool = True
+    use_aniso: bool = True
+    use_progressive: bool = True
+
+    def validate(self):
+        for name in ("lr_position", "lr_intensity", "lr_scale", "lr_rotation", "lr_nrf", "lr_transform"):
+            if getattr(self, name) <= 0:
+                raise ValueError(f"{name} must be > 0")
+        sched = tuple((int(i), int(r)) for i, r in self.resolution_schedule)
+        if not sched or sched[0][0] != 0:
+            raise ValueError("resolution_schedule must start at iteration 0")
+        its = [i for i, _ in sched]
+        if any(b <= a for a, b in zip(its, its[1:])):
+            raise ValueError("schedule iterations must be strictly increasing")
+        res = [r for _, r in sched]
+        if any(b < a for a, b in zip(res, res[1:])):
+            raise ValueError("schedule resolutions must be non-decreasing")
+        if self.batch_points < 1 or self.total_iters < 0:
+            raise ValueError("batch_points >= 1 and total_iters >= 0 required")
+        return self
+
+    def resolution_at(self, iteration):
+        res = self.resolution_schedule[0][1]
+        for it, r in self.resolution_schedule:
+            if iteration >= it:
+                res = r
+        return res
+
+    @property
+    def final_resolution(self):
+        return max(r for _, r in self.resolution_schedule)
+
+
+@dataclass
+class LossReport:
+    iteration: int
+    total: float
+    data: float
+    ssim: float
+    aniso: float
+    resolution: int
+    nrf_active: bool
+    pairs: int = 0
+
+    def to_line(self):
+        return (f"iter={self.iteration} total={self.total:.10g} l1={self.data:.10g} ssim={self.ssim:.10g} "
+                f"aniso={self.aniso:.10g} res={self.resolution} nrf={int(self.nrf_active)}")
+
+
+@dataclass
+class DeviceField:
+    """Learnable Gaussian parameters (float32 device tensors) on an R^3 lattice.
+    node_of[(i*R + j)*R + k] = primitive id at lattice node (i, j, k)."""
+
+    positions: torch.Tensor
+    quaternions: torch.Tensor
+    log_scales: torch.Tensor
+    logits: torch.Tensor
+    resolution: int
+    node_of: torch.Tensor
+
+    @property
+    def count(self):
+        return int(self.positions.shape[0])
+
+    def to_host(self):
+        from .core import GaussianField
+
+        r = self.resolution
+        node = dv.to_host(self.node_of).astype(np.int64)
+        lat = np.empty((self.count, 3), np.int64)
+        lat[node] = lattice_node_index(r)
+        return GaussianField(dv.to_host(self.positions).astype(np.float64),
+                             dv.to_host(self.quaternions).astype(np.float64),
+                             dv.to_host(self.log_scales).astype(np.float64),
+                             dv.to_host(self.logits).astype(np.float64), (r, r, r), lat)
+
+    @classmethod
+    def from_host(cls, field):
+        r = int(field.lattice_dims[0])
+        li = np.asarray(field.lattice_index, dtype=np.int64)
+        node_of = np.empty(field.count, np.int32)
+        node_of[(li[:, 0] * r + li[:, 1]) * r + li[:, 2]] = np.arange(field.count, dtype=np.int32)
+        return cls(dv.to_dev(field.positions, torch.float32), dv.to_dev(field.quaternions, torch.float32),
+                   dv.to_dev(field.log_scales, torch.float32), dv.to_dev(field.intensity_logits, torch.float32),
+                   r, dv.to_dev(node_of, torch.int32))
+
+
+def uniform_lattice_device(r, logits=None):
+    """uniform_lattice_field on the device (core.py:318-342)."""
+    n = r ** 3
+    pos = dv.to_dev(lattice_node_positions(r), torch.float32)
+    q = dv.zeros((n, 4), torch.float32)
+    q[:, 0] = 1.0
+    s = torch.full((n, 3), float(np.log(1.0 / r)), dtype=torch.float32, device=pos.device)
+    lg = dv.zeros((n,), torch.float32) if logits is None else logits.to(torch.float32)
+    return DeviceField(pos, q, s, lg, r, torch.arange(n, dtype=torch.int32, device=pos.device))
+
+
+def init_field_device(coords: torch.Tensor, intensities: torch.Tensor, r: int, logit_eps=1e-4):
+    """Logit of the mean sample intensity per lattice cell, 0 where empty (train.py:221-236)."""
+    n = r ** 3
+    keys = dv.empty((coords.shape[0],), torch.int32)
+    N.check(N.lib().mg_cell_keys_f64(N.ptr(coords), coords.shape[0], r, N.ptr(keys), dv.sptr()), "cell_keys")
+    k = keys.to(torch.int64)
+    sums = torch.zeros(n, dtype=torch.float64, device=coords.device).index_add_(0, k, intensities.double())
+    cnts = torch.bincount(k, minlength=n).double()
+    occ = cnts > 0
+    mean = torch.where(occ, sums / cnts.clamp(min=1), torch.full_like(sums, 0.5))
+    mean = mean.clamp(logit_eps, 1.0 - logit_eps)
+    lg = torch.where(occ, torch.log(mean) - torch.log1p(-mean), torch.zeros_like(mean))
+    return uniform_lattice_device(r, lg)
+
+
+def progressive_upsample_device(field: DeviceField, new_r: int) -> DeviceField:
+    """train.py:157-218 on the device: trilinear logits/log-scales, sign-aligned
+    NLERP quaternions, positions reseeded on the new lattice."""
+    old_r = field.resolution
+    if new_r < old_r:
+        raise ShrinkNotAllowed(f"cannot shrink lattice {old_r} -> {new_r}")
+    n = new_r ** 3
+    pos = dv.empty((n, 3), torch.float32)
+    q = dv.empty((n, 4), torch.float32)
+    s = dv.empty((n, 3), torch.float32)
+    lg = dv.empty((n,), torch.float32)
+    N.check(N.lib().mg_upsample(N.ptr(field.quaternions), N.ptr(field.log_scales), N.ptr(field.logits),
+                                N.ptr(field.node_of), old_r, new_r, N.ptr(pos), N.ptr(q), N.ptr(s), N.ptr(lg),
+                                dv.sptr()), "upsample")
+    return DeviceField(pos, q, s, lg, new_r, torch.arange(n, dtype=torch.int32, device=pos.device))
+
+
+class _StepBuffers:
+    """Fixed-shape device buffers for one (N, B, HW, taps) configuration."""
+
+    def __init__(self, n, g, b_total, ntaps, k):
+        L = N.lib()
+        ns = b_total * ntaps
+        self.gkey = dv.empty((n,), torch.int32)
+        self.gorder = dv.empty((n,), torch.int32)
+        self.gstart = dv.empty((g ** 3 + 1,), torch.int32)
+        self.grec = dv.empty((n, 12), torch.float32)
+        self.acc10 = dv.empty((n, 10), torch.float32)
+        self.pkey = dv.empty((ns,), torch.int32)
+        self.pinv = dv.empty((ns,), torch.int32)
+        self.pstart = dv.empty((g ** 3 + 1,), torch.int32)
+        self.prec = dv.empty((ns, 4), torch.float32)
+        self.xout = dv.empty((ns, 3), torch.float64)
+        self.out4 = dv.empty((ns, 4), torch.float32)
+        self.cnt = dv.empty((ns,), torch.int32)
+        self.pred = dv.empty((b_total,), torch.float32)
+        self.up = dv.empty((b_total,), torch.float32)
+        self.dpts = dv.empty((ns, 3), torch.float64)
+        self.rot = dv.empty((max(k, 1), 3, 3), torch.float64)
+        self.g7 = dv.empty((max(k, 1), 7), torch.float64)
+        self.scratch12 = dv.empty((max(k, 1), 12), torch.float64)
+        self.scalars = dv.zeros((4,), torch.float64)  # data loss, aniso loss, ssim sum, spare
+        self.err = dv.zeros((1,), torch.int32)
+        wsb = max(L.mg_bin_workspace_bytes(n, g), L.mg_points_workspace_bytes(ns, g),
+                  L.mg_forward_workspace_bytes(ns), L.mg_backward_workspace_bytes(n))
+        self.ws = dv.empty((wsb,), torch.uint8)
+        self.ssim_ws = None
+
+
+class Trainer:
+    """Owns the device field, transforms, optimizer state and the batch stream."""
+
+    def __init__(self, cloud, transforms: TransformSet, config: TrainConfig, slice_grids=None,
+                 slice_psf: SlicePSF | None = None, graph=False, dist=None):
+        config.validate()
+        if config.use_ssim and not slice_grids:
+            raise ValueError("use_ssim requires slice sample grids")
+        self.config = config
+        self.psf = slice_psf
+        self.graph = graph
+        self.dist = dist  # optional torch.distributed group for gradient all-reduce
+        self.coords = dv.to_dev(cloud.coords, torch.float64)
+        self.intens = dv.to_dev(cloud.intensities, torch.float32)
+        self.sids = dv.to_dev(cloud.slice_ids, torch.int64)
+        self.m_points = int(self.coords.shape[0])
+        self.slice_grids = list(slice_grids or [])
+        self._prepare_sources()
+        ts = transforms.copy()
+        self.k = len(ts)
+        self.tq = dv.to_dev(ts.quats, torch.float64, (self.k, 4))
+        self.tt = dv.to_dev(ts.translations, torch.float64, (self.k, 3))
+        self.tm = dv.zeros((max(self.k, 1), 7), torch.float64)
+        self.tv = dv.zeros((max(self.k, 1), 7), torch.float64)
+        root = np.random.SeedSequence(config.seed)
+        batch_ss, nrf_ss = root.spawn(2)
+        self.rng = np.random.default_rng(batch_ss)
+        self.nrf = None
+        if config.use_nrf:
+            from .nrf import ResidualField
+
+            self.nrf = ResidualField.create(np.random.default_rng(nrf_ss))
+            self.nrf_m = {k: torch.zeros_like(v) for k, v in self.nrf.parameter_arrays().items()}
+            self.nrf_v = {k: torch.zeros_like(v) for k, v in self.nrf.parameter_arrays().items()}
+            self.nrf_t = 0
+        start = config.resolution_at(0) if config.use_progressive else config.final_resolution
+        self.field = init_field_device(self.coords, self.intens, start)
+        self._reset_gauss_adam()
+        self.counters = dv.zeros((2,), torch.int32)  # [gauss t, transform t]
+        self.iteration = 0
+        self._perm = None
+        self._cursor = 0
+        self.reports = []
+        self._bufs = None
+        self._bufs_key = None
+        self._graph = None
+        self._graph_key = None
+        self._hyper = np.array([config.lr_position, config.lr_rotation, config.lr_scale, config.lr_intensity,
+                                config.adam_beta1, config.adam_beta2, config.adam_eps, config.lambda_aniso,
+                                config.lambda_ratio], dtype=np.float64)
+        if slice_psf is not None:
+            self._psf_off = dv.to_dev(np.asarray(slice_psf.offsets, dtype=np.float64), torch.float64)
+            self._psf_w = dv.to_dev(np.asarray(slice_psf.weights, dtype=np.float64), torch.float64)
+            self._psf_dirs = dv.to_dev(np.asarray(slice_psf.through_dirs, dtype=np.float64).reshape(-1, 3),
+                                       torch.float64)
+
+    # -- state --------------------------------------------------------------
+    def _reset_gauss_adam(self):
+        n = self.field.count
+        self.m = dv.zeros((n, 11), torch.float32)
+        self.v = dv.zeros((n, 11), torch.float32)
+        if hasattr(self, "counters"):
+            self.counters[0].zero_()
+
+    @property
+    def nrf_active(self):
+        return self.config.use_nrf and self.iteration >= self.config.nrf_activation_iter
+
+    @property
+    def ntaps(self):
+        return 1 if self.psf is None else self.psf.ntaps
+
+    # -- batching (train.py:348-363) ------------------------------------------
+    def _next_batch(self):
+        m = self.m_points
+        b = min(self.config.batch_points, m)
+        if b == m:
+            return np.arange(m)
+        picked, need = [], b
+        while need > 0:
+            if self._perm is None or self._cursor >= m:
+                self._perm = self.rng.permutation(m)
+                self._cursor = 0
+            take = min(need, m - self._cursor)
+            picked.append(self._perm[self._cursor:self._cursor + take])
+            self._cursor += take
+            need -= take
+        return np.concatenate(picked) if len(picked) > 1 else picked[0]
+
+    def _apply_milestones(self):
+        if not self.config.use_progressive:
+            return
+        for it, res in self.config.resolution_schedule:
+            if it == self.iteration and res > self.field.resolution:
+                self.field = progressive_upsample_device(self.field, res)
+                self._reset_gauss_adam()
+                self._graph = None
+
+    def _prepare_sources(self):
+        """Cloud + every slice grid in one device pool, so a step's points are a
+        single index gather (graph-replayable with a fixed index buffer)."""
+        cs, ss, ts = [self.coords], [self.sids], [self.intens]
+        self._sg_off, self._sg_shape = [], []
+        base = self.m_points
+        for sg in self.slice_grids:
+            c = dv.to_dev(np.asarray(sg.coords, np.float64).reshape(-1, 3), torch.float64)
+            t = dv.to_dev(np.asarray(sg.target, np.float64).ravel(), torch.float32)
+            cs.append(c)
+            ts.append(t)
+            ss.append(torch.full((c.shape[0],), int(sg.slice_id), dtype=torch.int64, device=c.device))
+            self._sg_off.append(base)
+            self._sg_shape.append(tuple(np.asarray(sg.target).shape))
+            base += c.shape[0]
+        if len(cs) > 1:
+            self.src_coords, self.src_sids, self.src_tgt = torch.cat(cs), torch.cat(ss), torch.cat(ts)
+        else:
+            self.src_coords, self.src_sids, self.src_tgt = self.coords, self.sids, self.intens
+
+    def host_indices(self, idx, slice_j):
+        """Pool indices of one step: the batch, then the SSIM slice's pixels."""
+        idx = np.asarray(idx, dtype=np.int64)
+        if slice_j is None:
+            return idx, None
+        hw = self._sg_shape[slice_j]
+        return np.concatenate([idx, self._sg_off[slice_j] + np.arange(hw[0] * hw[1], dtype=np.int64)]), hw
+
+    # -- one optimizer step ----------------------------------------------------
+    def step(self, sync=True):
+        cfg = self.config
+        self._apply_milestones()
+        idx = self._next_batch()
+        slice_j = int(self.rng.integers(len(self.slice_grids))) if cfg.use_ssim else None
+        all_idx, hw = self.host_indices(idx, slice_j)
+        report = self._device_step(all_idx, len(idx), hw, sync)
+        self.iteration += 1
+        self.reports.append(report)
+        return report
+
+    def _buffers(self, b_total):
+        g = self.field.resolution
+        key = (self.field.count, g, b_total, self.ntaps, self.k)
+        if self._bufs_key != key:
+            self._bufs = _StepBuffers(self.field.count, g, b_total, self.ntaps, self.k)
+            self._bufs.idx = dv.empty((b_total,), torch.int64)
+            self._bufs.coords = dv.empty((b_total, 3), torch.float64)
+            self._bufs.sids = dv.empty((b_total,), torch.int64)
+            self._bufs.tgt = dv.empty((b_total,), torch.float32)
+            self._bufs.pairs = dv.zeros((1,), torch.int64)
+            self._bufs_key = key
+            self._graph = None
+        return self._bufs
+
+    def load_indices(self, all_idx):
+        """Stage one step's pool indices (host array or device tensor) into the
+        fixed index buffer, on the current stream."""
+        B = self._buffers(len(all_idx))
+        if isinstance(all_idx, torch.Tensor):
+            B.idx.copy_(all_idx, non_blocking=True)
+        else:
+            B.idx.copy_(torch.from_numpy(np.ascontiguousarray(all_idx, dtype=np.int64)).pin_memory(),
+                        non_blocking=True)
+        return B
+
+    def _body(self, B, nb, hw):
+        torch.index_select(self.src_coords, 0, B.idx, out=B.coords)
+        torch.index_select(self.src_sids, 0, B.idx, out=B.sids)
+        torch.index_select(self.src_tgt, 0, B.idx, out=B.tgt)
+        self._launch(B, B.coords, B.sids, B.tgt, nb, hw)
+        B.pairs.add_(B.cnt.sum(dtype=torch.int64))
+
+    def _device_step(self, all_idx, nb, hw, sync):
+        cfg = self.config
+        B = self.load_indices(all_idx)
+        use_graph = self.graph and not self.nrf_active and self.dist is None
+        if use_graph:
+            key = (nb, hw)
+            if self._graph is None or self._graph_key != key:
+                self._body(B, nb, hw)  # eager warm-up of this shape (also lazily inits kernels)
+                torch.cuda.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    self._body(B, nb, hw)
+                self._graph, self._graph_key = g, key
+                # the warm-up already performed this step's update; undo nothing: the
+                # captured graph is replayed from the next step on.
+            else:
+                self._graph.replay()
+        else:
+            self._body(B, nb, hw)
+        if not sync:
+            return LossReport(self.iteration, float("nan"), float("nan"), float("nan"), float("nan"),
+                              self.field.resolution, self.nrf_active)
+        sc = dv.to_host(B.scalars)
+        err = int(B.err.item())
+        if err:
+            from .errors import DegenerateQuaternion
+
+            raise DegenerateQuaternion("quaternion norm <= 1e-12 during training")
+        data = float(sc[0])
+        aniso = float(sc[1]) if cfg.use_aniso else 0.0
+        ssim = 0.0
+        if hw is not None:
+            ssim = 1.0 - float(sc[2]) / ((hw[0] - 10) * (hw[1] - 10))
+        total = data + cfg.lambda_ssim * ssim + cfg.lambda_aniso * aniso
+        if not np.isfinite(total):
+            raise NonFiniteLoss(f"non-finite loss at iteration {self.iteration}")
+        return LossReport(self.iteration, total, data, ssim, aniso, self.field.resolution, self.nrf_active)
+
+    def _launch(self, B, coords, sids, tgt, nb, hw):
+        """Enqueue the whole step on the current stream (graph-capturable)."""
+        cfg = self.config
+        L = N.lib()
+        st = dv.sptr()
+        f = self.field
+        n, g, r = f.count, f.resolution, cfg.block_radius
+        bt = coords.shape[0]
+        t = self.ntaps
+        ns = bt * t
+        ws = B.ws
+        B.scalars.zero_()
+        # Gaussians: bin + activate (spatial.py:46-66, render.py:122-142)
+        N.check(L.mg_bin_f32(N.ptr(f.positions), n, g, N.ptr(B.gkey), N.ptr(B.gorder), N.ptr(B.gstart), N.ptr(ws),
+                             ws.numel(), st), "bin")
+        N.check(L.mg_activate(N.ptr(f.positions), N.ptr(f.quaternions), N.ptr(f.log_scales), N.ptr(f.logits), n,
+                              N.ptr(B.gorder), N.ptr(B.grec), N.ptr(B.err), st), "activate")
+        # points: transforms, PSF taps, bin
+        if self.k:
+            N.check(L.mg_quat_to_rot_f64(N.ptr(self.tq), self.k, N.ptr(B.rot), st))
+        off = self._psf_off if self.psf is not None else None
+        wts = self._psf_w if self.psf is not None else None
+        dirs = self._psf_dirs if self.psf is not None else None
+        N.check(L.mg_bin_points(N.ptr(coords), N.ptr(sids), bt, t, N.ptr(off), N.ptr(dirs), N.ptr(B.rot),
+                                N.ptr(self.tt), self.k, g, N.ptr(B.pkey), N.ptr(B.pinv), N.ptr(B.pstart),
+                                N.ptr(B.prec), N.ptr(B.xout), N.ptr(ws), ws.numel(), st), "bin_points")
+        # forward with H (render_points, _kernels.py:24-70)
+        N.check(L.mg_forward(N.ptr(B.grec), N.ptr(B.gstart), g, r, N.ptr(B.prec), N.ptr(B.pkey), N.ptr(B.pstart),
+                             ns, 1, N.ptr(B.out4), N.ptr(B.cnt), N.ptr(ws), ws.numel(), st), "forward")
+        N.check(L.mg_forward_finish(N.ptr(B.out4), N.ptr(B.cnt), N.ptr(B.pinv), bt, t, N.ptr(wts), None,
+                                    N.ptr(B.pred), None, st), "finish")
+        nrf_cache = None
+        if self.nrf_active:
+            from .nrf import nrf_forward_cached
+
+            xc = self._centre_points(B, bt, t)
+            res, nrf_cache = nrf_forward_cached(self.nrf, xc)
+            B.pred.add_(res)
+        # losses (train.py:424-436)
+        N.check(L.mg_smooth_l1(N.ptr(B.pred), N.ptr(tgt), nb, N.ptr(B.up), N.ptr(B.scalars[0:1]), st), "smooth_l1")
+        if hw is not None:
+            h, w = hw
+            need = L.mg_ssim_workspace_bytes(h, w)
+            if B.ssim_ws is None or B.ssim_ws.numel() < need:
+                B.ssim_ws = dv.empty((need,), torch.uint8)
+            N.check(L.mg_ssim_loss_grad(N.ptr(B.pred[nb:]), N.ptr(tgt[nb:]), h, w, cfg.lambda_ssim,
+                                        N.ptr(B.up[nb:]), N.ptr(B.scalars[2:3]), N.ptr(B.ssim_ws),
+                                        B.ssim_ws.numel(), st), "ssim")
+        # backward (render_backward): upstream -> point records, d_points; Gaussian-major pass
+        N.check(L.mg_backward_points(None, N.ptr(B.up), bt, t, N.ptr(wts), N.ptr(B.pinv), N.ptr(B.out4),
+                                     N.ptr(B.prec), N.ptr(B.dpts), st), "backward_points")
+        N.check(L.mg_backward(N.ptr(B.grec), N.ptr(B.gkey), N.ptr(B.gstart), n, g, r, N.ptr(B.prec),
+                              N.ptr(B.pstart), N.ptr(B.acc10), N.ptr(ws), ws.numel(), st), "backward")
+        if self.k:
+            N.check(L.mg_transform_grads(N.ptr(B.dpts), N.ptr(coords), N.ptr(sids), bt, t, N.ptr(off), N.ptr(dirs),
+                                         N.ptr(self.tq), self.k, N.ptr(B.scratch12), N.ptr(B.g7), 0, st),
+                    "transform_grads")
+        ng = None
+        if nrf_cache is not None:
+            from .nrf import nrf_backward
+
+            dws, dbs, dp = nrf_backward(self.nrf, self._centre_x, B.up, nrf_cache)
+            ng = (dws, dbs)
+            if self.k:
+                dp64 = dp.double().contiguous()
+                N.check(L.mg_transform_grads(N.ptr(dp64), N.ptr(coords), N.ptr(sids), bt, 1, None, None,
+                                             N.ptr(self.tq), self.k, N.ptr(B.scratch12), N.ptr(B.g7), 1, st),
+                        "nrf_transform_grads")
+        if self.dist is not None:
+            self._allreduce(B)
+        # updates (train.py:461-477): epilogue + aniso + Adam fused; transforms; NRF
+        N.check(L.mg_counter_incr(N.ptr(self.counters), 2, st))
+        hyper = self._hyper
+        N.check(L.mg_gauss_update(N.ptr(B.acc10), N.ptr(B.gorder), n, N.ptr(f.positions), N.ptr(f.quaternions),
+                                  N.ptr(f.log_scales), N.ptr(f.logits), N.ptr(self.m), N.ptr(self.v),
+                                  hyper.ctypes.data_as(N.P), 1 if cfg.use_aniso else 0, N.ptr(self.counters[0:1]),
+                                  N.ptr(B.scalars[1:2]), st), "gauss_update")
+        if self.k:
+            N.check(L.mg_transform_adam(N.ptr(self.tq), N.ptr(self.tt), N.ptr(B.g7), N.ptr(self.tm), N.ptr(self.tv),
+                                        self.k, cfg.lr_transform, cfg.adam_beta1, cfg.adam_beta2, cfg.adam_eps,
+                                        N.ptr(self.counters[1:2]), st), "transform_adam")
+        if ng is not None:
+            self._nrf_adam(*ng)
+
+    def _centre_points(self, B, bt, t):
+        """Transformed (un-shifted) sample positions for the NRF (train.py:414-419)."""
+        if t == 1:
+            x = B.xout.view(bt, 3)
+        else:
+            c = int(np.argmin(np.abs(np.asarray(self.psf.offsets))))
+            x = B.xout.view(bt, t, 3)[:, c, :]
+        self._centre_x = x.to(torch.float32).contiguous()
+        return self._centre_x
+
+    def _nrf_adam(self, dws, dbs):
+        cfg = self.config
+        self.nrf_t += 1
+        bc1 = 1.0 - cfg.adam_beta1 ** self.nrf_t
+        bc2 = 1.0 - cfg.adam_beta2 ** self.nrf_t
+        params = self.nrf.parameter_arrays()
+        grads = {}
+        for li, (dw, db) in enumerate(zip(dws, dbs)):
+            grads[f"w{li}"], grads[f"b{li}"] = dw, db
+        for k, p in params.items():
+            g = grads[k]
+            m, v = self.nrf_m[k], self.nrf_v[k]
+            m.mul_(cfg.adam_beta1).add_(g, alpha=1.0 - cfg.adam_beta1)
+            v.mul_(cfg.adam_beta2).addcmul_(g, g, value=1.0 - cfg.adam_beta2)
+            p.sub_(cfg.lr_nrf * (m / bc1) / (torch.sqrt(v / bc2) + cfg.adam_eps))
+
+    def _allreduce(self, B):
+        import torch.distributed as tdist
+
+        tdist.all_reduce(B.acc10, group=self.dist)
+        if self.k:
+            tdist.all_reduce(B.g7, group=self.dist)
+        tdist.all_reduce(B.scalars, group=self.dist)
+
+    def run(self, iterations=None):
+        target = self.config.total_iters if iterations is None else self.iteration + iterations
+        while self.iteration < target:
+            self.step()
+        return self.reports
+
+    # -- inference (train.py:509-512, render.py:379-408) -------------------------
+    def render_volume(self, dims, bounds, include_nrf=True):
+        from .core import Volume
+        from .render import grid_coordinates
+
+        f = self.field
+        g, r = f.resolution, self.config.block_radius
+        B = self._buffers(1)
+        L = N.lib()
+        N.check(L.mg_bin_f32(N.ptr(f.positions), f.count, g, N.ptr(B.gkey), N.ptr(B.gorder), N.ptr(B.gstart),
+                             N.ptr(B.ws), B.ws.numel(), dv.sptr()), "bin")
+        N.check(L.mg_activate(N.ptr(f.positions), N.ptr(f.quaternions), N.ptr(f.log_scales), N.ptr(f.logits),
+                              f.count, N.ptr(B.gorder), N.ptr(B.grec), N.ptr(B.err), dv.sptr()), "activate")
+        dims = tuple(int(d) for d in dims)
+        axes, spacing = grid_coordinates(dims, bounds)
+        res = None
+        if include_nrf and self.nrf_active:
+            from .nrf import nrf_forward_device
+
+            gx, gy, gz = np.meshgrid(axes[0], axes[1], axes[2], indexing="ij")
+            pts = dv.to_dev(np.stack([gx.ravel(), gy.ravel(), gz.ravel()], 1), torch.float32)
+            res = nrf_forward_device(self.nrf, pts).reshape(dims)
+        out = sample_volume_device(B.grec, B.gstart, g, r, dims, bounds, residual=res)
+        return Volume(data=dv.to_host(out).astype(np.float64), spacing=spacing,
+                      origin=np.array([axes[0][0], axes[1][0], axes[2][0]]))
+
+    def transforms_host(self):
+        return TransformSet(dv.to_host(self.tq), dv.to_host(self.tt))
+
+
+# ---------------------------------------------------------------------------
+# host-facing loss helpers (train.py:108-120, ssim.py:82-122), device-computed
+# ---------------------------------------------------------------------------
+
+
+def smooth_l1_loss_grad(pred, target):
+    """(mean Huber loss, d/dpred) computed by the device kernel."""
+    p = dv.to_dev(np.asarray(pred, dtype=np.float64).ravel(), torch.float32)
+    t = dv.to_dev(np.asarray(target, dtype=np.float64).ravel(), torch.float32)
+    up = dv.empty(p.shape, torch.float32)
+    acc = dv.zeros((1,), torch.float64)
+    N.check(N.lib().mg_smooth_l1(N.ptr(p), N.ptr(t), p.numel(), N.ptr(up), N.ptr(acc), dv.sptr()), "smooth_l1")
+    return float(acc.item()), dv.to_host(up).astype(np.float64)
+
+
+def ssim_loss_grad(pred, target):
+    """(1 - mean SSIM, d/dpred) of an (H, W) slice computed by the device kernels."""
+    pred = np.asarray(pred, dtype=np.float64)
+    h, w = pred.shape
+    p = dv.to_dev(pred.ravel(), torch.float32)
+    t = dv.to_dev(np.asarray(target, dtype=np.float64).ravel(), torch.float32)
+    up = dv.empty(p.shape, torch.float32)
+    acc = dv.zeros((1,), torch.float64)
+    ws = dv.empty((N.lib().mg_ssim_workspace_bytes(h, w),), torch.uint8)
+    N.check(N.lib().mg_ssim_loss_grad(N.ptr(p), N.ptr(t), h, w, 1.0, N.ptr(up), N.ptr(acc), N.ptr(ws), ws.numel(),
+                                      dv.sptr()), "ssim")
+    return 1.0 - float(acc.item()) / ((h - 10) * (w - 10)), dv.to_host(up).astype(np.float64).reshape(h, w)

@@ -257,7 +257,51 @@ def make_trainer_case():
     )
 
 
+def make_ssim_case():
+    from mgauss import ssim as mssim
+
+    rng = np.random.default_rng(9)
+    tgt = np.clip(rng.uniform(0, 1, (40, 33)), 0, 1)
+    pred = np.clip(tgt + rng.normal(0, 0.1, tgt.shape), 0, 1)
+    loss, grad = mssim.ssim_loss_grad(pred, tgt)
+    np.savez_compressed(os.path.join(OUT, "ssim.npz"), pred=pred, tgt=tgt, loss=loss, grad=grad)
+
+
+def make_trainer_full_case():
+    """Reference Trainer with SSIM + NRF (active from step 2) + a milestone at 3."""
+    from mgauss.cli import simulate_stacks
+    from mgauss.io import SimSettings
+    from mgauss.simdata import build_slice_grids, devoxelize, normalized_transforms
+
+    sim = SimSettings(phantom="nested-ellipsoids", phantom_dims=24, phantom_spacing=1.0,
+                      in_plane_spacing=1.0, slice_thickness=4.0, motion_sigma=0.5,
+                      noise_sigma=0.01, reg_error_sigma=0.0, foreground_threshold=-1.0)
+    _, stacks = simulate_stacks(sim, 7)
+    cloud = devoxelize(stacks, -1.0)
+    ts = normalized_transforms(stacks, cloud.world_map, "estimated")
+    grids = build_slice_grids(stacks, cloud.world_map, cloud.intensity_scale)
+    cfg = train.TrainConfig(resolution_schedule=((0, 8), (3, 10)), use_nrf=True, nrf_activation_iter=2,
+                            use_ssim=True, batch_points=2048, seed=11, total_iters=6)
+    tr = train.Trainer(cloud, ts, cfg, slice_grids=grids)
+    losses = []
+    for _ in range(6):
+        rep = tr.step()
+        losses.append([rep.total, rep.data, rep.ssim, rep.aniso])
+    sg_coords = np.stack([g.coords for g in grids])
+    sg_target = np.stack([g.target for g in grids])
+    np.savez_compressed(
+        os.path.join(OUT, "trainer_full.npz"),
+        coords=cloud.coords, intensities=cloud.intensities, slice_ids=cloud.slice_ids,
+        t_quats0=ts.quats, t_trans0=ts.translations, sg_coords=sg_coords, sg_target=sg_target,
+        sg_ids=np.array([g.slice_id for g in grids]), losses=np.array(losses), **field_arrays(tr.field),
+        t_quats=tr.transforms.quats, t_trans=tr.transforms.translations,
+        nrf_w4=tr.nrf.weights[4], nrf_b4=tr.nrf.biases[4], nrf_w0=tr.nrf.weights[0],
+    )
+
+
 if __name__ == "__main__":
+    make_ssim_case()
+    make_trainer_full_case()
     make_spatial_cases()
     make_render_cases()
     make_volume_case()

@@ -134,3 +134,10 @@ def test_nrf_golden():
         np.testing.assert_allclose(dws[i], z[f"dw{i}"], rtol=1e-10, atol=1e-14)
         np.testing.assert_allclose(dbs[i], z[f"db{i}"], rtol=1e-10, atol=1e-14)
     np.testing.assert_allclose(dp, z["d_points"], rtol=1e-10, atol=1e-14)
+
+
+def test_ssim_golden():
+    z = load_golden("ssim")
+    loss, grad = O.ssim_loss_grad(z["pred"], z["tgt"])
+    np.testing.assert_allclose(loss, z["loss"], rtol=1e-13)
+    np.testing.assert_allclose(grad, z["grad"], rtol=1e-10, atol=1e-15)

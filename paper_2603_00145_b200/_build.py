@@ -33,16 +33,18 @@ def needs_build():
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force=False, verbose=False):
-    if not force and not needs_build():
+def build(force=False, verbose=False, out=None, defines=()):
+    out = out or LIB
+    if not force and out == LIB and not needs_build():
         return LIB
-    os.makedirs(OUT_DIR, exist_ok=True)
-    cmd = [NVCC, *FLAGS, "-o", LIB + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-o", out + ".tmp",
+           *[os.path.join(CSRC, s) for s in SOURCES]]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True, cwd=CSRC)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":

@@ -13,7 +13,7 @@ import threading
 from .errors import NativeLibraryMissing
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libmgauss_b200.so")
+LIB_PATH = os.environ.get("MGAUSS_B200_LIB") or os.path.join(_HERE, "_lib", "libmgauss_b200.so")
 
 P = ctypes.c_void_p
 I64 = ctypes.c_int64

@@ -300,7 +300,7 @@ int mg_backward(const void* grec, const uint32_t* gkey_sorted, const int32_t* gs
   int* nitems = w.take<int>(1);
   if (!w.ok) return fail("mg_backward: workspace too small");
   if (n == 0) return 0;
-  build_items(gkey_sorted, gstart, n, 4, items, nitems, w.rest(), st);
+  build_items(gkey_sorted, gstart, n, 2, items, nitems, w.rest(), st);
   launch_backward((const float4*)grec, gkey_sorted, gstart, (int)g, (int)r, (const float4*)prec, pstart, items,
                   nitems, n, acc10, st);
   return cuda_status();

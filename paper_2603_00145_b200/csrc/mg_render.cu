@@ -252,93 +252,99 @@ __device__ __forceinline__ int seg_lookup(int v, int& s, const int* s_start, con
 }
 
 // ---------------------------------------------------------------------------
-// Forward: one warp per (point cell, <= Q sub-points of that cell); lanes
-// stride over the flattened candidate Gaussians; sub-points are warp-uniform
-// and packed two per f32x2 register.  Every point of the item shares the
-// exact candidate set, so contributor_counts is the total candidate count.
+// Bitmap segment cursor.  For a batch of <= 128 columns the candidate list is
+// the concatenation of the non-empty column segments.  Each warp keeps, in
+// shared memory, delta[seg] = (segment start element) - (segment start in the
+// flattened index) for the compacted non-empty segments, and a bitmap with one
+// bit per flattened index that starts a segment, over a window of
+// kBmWords*32 indices.  A lane then maps its flattened index v to its element
+// with one broadcast LDS + popc + one LDS: no loops, no divergence.
 // ---------------------------------------------------------------------------
-constexpr int kFwdWarps = 4;
+constexpr int kBmWords = 128;  // window of 4096 flattened indices
 
-template <int Q, bool WITH_H>
-__device__ __forceinline__ void fwd_item(const float4* __restrict__ grec, const int* __restrict__ gstart, int g, int r,
-                                         const float4* __restrict__ prec, int p0, int np, int cell,
-                                         float4* __restrict__ out4, int* __restrict__ cnt_out, int* s_start,
-                                         int* s_pre, int lane) {
-  constexpr int QP = Q / 2;
-  f2 px[QP], py[QP], pz[QP];
+struct SegSmem {
+  int start[128];
+  int pre[132];
+  int delta[128];
+  uint32_t bits[kBmWords];
+};
+
+// Per-lane copy of its 4 columns' (pre, len, start) for window rebuilds.
+struct LaneSegs {
+  int pre[4], len[4], st[4];
+  int nonempty_before;  // # non-empty segments owned by lower lanes
+  int tot;
+};
+
+__device__ __forceinline__ LaneSegs build_lane_segs(const Window& w, int c0, int g, const int* __restrict__ starts,
+                                                    SegSmem& sm, int lane) {
+  LaneSegs L;
+  int sum = 0, ne = 0;
 #pragma unroll
-  for (int q = 0; q < QP; ++q) {
-    float4 a = prec[p0 + min(2 * q, np - 1)];
-    float4 b = prec[p0 + min(2 * q + 1, np - 1)];
-    px[q] = mk2(a.x, b.x);
-    py[q] = mk2(a.y, b.y);
-    pz[q] = mk2(a.z, b.z);
-  }
-  f2 accI[QP], hx[QP], hy[QP], hz[QP];
-#pragma unroll
-  for (int q = 0; q < QP; ++q) {
-    accI[q] = bc2(0.f);
-    hx[q] = hy[q] = hz[q] = bc2(0.f);
-  }
-  const Window w = make_window(cell, g, r);
-  int total = 0;
-  for (int c0 = 0; c0 < w.ncol; c0 += 128) {
-    const int tot = build_segments(w, c0, g, gstart, s_start, s_pre, lane);
-    total += tot;
-    int s = 0;
-    for (int v = lane; v < tot; v += 32) {
-      const int gi = seg_lookup(v, s, s_start, s_pre);
-      const float4 A = __ldg(grec + 3 * gi);
-      const float4 B = __ldg(grec + 3 * gi + 1);
-      const float4 C = __ldg(grec + 3 * gi + 2);
-      const float p00 = B.x, p11 = B.y, p22 = B.z, p01 = B.w, p02 = C.x, p12 = C.y;
-      if (WITH_H) {
-#pragma unroll
-        for (int q = 0; q < QP; ++q) {
-          f2 dx = sub2(px[q], bc2(A.x)), dy = sub2(py[q], bc2(A.y)), dz = sub2(pz[q], bc2(A.z));
-          f2 pdx = fma2(bc2(p02), dz, fma2(bc2(p01), dy, mul2(bc2(p00), dx)));
-          f2 pdy = fma2(bc2(p12), dz, fma2(bc2(p11), dy, mul2(bc2(p01), dx)));
-          f2 pdz = fma2(bc2(p22), dz, fma2(bc2(p12), dy, mul2(bc2(p02), dx)));
-          f2 m = fma2(dz, pdz, fma2(dy, pdy, mul2(dx, pdx)));
-          f2 wv = mul2(bc2(A.w), mk2(gauss_w(m.x), gauss_w(m.y)));
-          accI[q] = add2(accI[q], wv);
-          hx[q] = fma2(wv, pdx, hx[q]);
-          hy[q] = fma2(wv, pdy, hy[q]);
-          hz[q] = fma2(wv, pdz, hz[q]);
-        }
-      } else {
-        const float a01 = 2.f * p01, a02 = 2.f * p02, a12 = 2.f * p12;
-#pragma unroll
-        for (int q = 0; q < QP; ++q) {
-          f2 dx = sub2(px[q], bc2(A.x)), dy = sub2(py[q], bc2(A.y)), dz = sub2(pz[q], bc2(A.z));
-          f2 t1 = fma2(bc2(a02), dz, fma2(bc2(a01), dy, mul2(bc2(p00), dx)));
-          f2 m = mul2(dx, t1);
-          f2 t2 = fma2(bc2(a12), dz, mul2(bc2(p11), dy));
-          m = fma2(dy, t2, m);
-          m = fma2(dz, mul2(bc2(p22), dz), m);
-          accI[q] = fma2(bc2(A.w), mk2(gauss_w(m.x), gauss_w(m.y)), accI[q]);
-        }
-      }
+  for (int k = 0; k < 4; ++k) {
+    int col = c0 + lane * 4 + k;
+    L.st[k] = 0;
+    L.len[k] = 0;
+    if (col < w.ncol) {
+      int ii = w.ilo + col / w.nj;
+      int jj = w.jlo + col % w.nj;
+      int base = (ii * g + jj) * g;
+      int a = __ldg(starts + base + w.klo);
+      int b = __ldg(starts + base + w.khi + 1);
+      L.st[k] = a;
+      L.len[k] = b - a;
     }
-    __syncwarp();
+    sum += L.len[k];
+    ne += L.len[k] > 0;
   }
-  // Transposed reduction: 4 values per point -> lane 4q+c (Q=8) holds point q comp c.
-  constexpr int NV = 4 * Q;  // 8, 16 or 32
-  float v[32];
+  int tot, netot;
+  int off = warp_excl_scan(sum, lane, &tot);
+  int nbefore = warp_excl_scan(ne, lane, &netot);
+  int e = nbefore;
 #pragma unroll
-  for (int q = 0; q < QP; ++q) {
-    v[8 * q + 0] = accI[q].x;
-    v[8 * q + 1] = hx[q].x;
-    v[8 * q + 2] = hy[q].x;
-    v[8 * q + 3] = hz[q].x;
-    v[8 * q + 4] = accI[q].y;
-    v[8 * q + 5] = hx[q].y;
-    v[8 * q + 6] = hy[q].y;
-    v[8 * q + 7] = hz[q].y;
+  for (int k = 0; k < 4; ++k) {
+    L.pre[k] = off;
+    sm.start[lane * 4 + k] = L.st[k];
+    sm.pre[lane * 4 + k] = off;
+    if (L.len[k] > 0) sm.delta[e++] = L.st[k] - off;
+    off += L.len[k];
+  }
+  if (lane == 31) sm.pre[128] = tot;
+  L.nonempty_before = nbefore;
+  L.tot = tot;
+  return L;
+}
+
+// Fill the bitmap for flattened window [w0, w0 + 32*kBmWords); returns the
+// number of non-empty segments that start before w0 (the window's seg base).
+__device__ __forceinline__ int build_window(const LaneSegs& L, int w0, SegSmem& sm, int lane) {
+#pragma unroll
+  for (int i = 0; i < kBmWords / 32; ++i) sm.bits[lane + 32 * i] = 0u;
+  __syncwarp();
+  int before = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (L.len[k] > 0) {
+      int p = L.pre[k] - w0;
+      if (p < 0)
+        ++before;
+      else if (p < 32 * kBmWords)
+        atomicOr(&sm.bits[p >> 5], 1u << (p & 31));
+    }
   }
 #pragma unroll
-  for (int i = NV; i < 32; ++i) v[i] = 0.f;
-  // halving levels first (each lane keeps half of the remaining values)
+  for (int o = 16; o > 0; o >>= 1) before += __shfl_xor_sync(MG_FULL, before, o);
+  __syncwarp();
+  return before;
+}
+
+// ---------------------------------------------------------------------------
+// Transposed ("reduce-scatter") warp reduction of NV <= 32 per-lane values:
+// after it, lane l holds the warp sum of value index (l >> (5 - log2 NV)).
+// NV - 1 + (5 - log2 NV) shuffles instead of 5 * NV.
+// ---------------------------------------------------------------------------
+template <int NV>
+__device__ __forceinline__ float transpose_reduce(float (&v)[32], int lane) {
   int nrem = NV;
 #pragma unroll
   for (int half = 16; half >= 1; half >>= 1) {
@@ -358,24 +364,218 @@ __device__ __forceinline__ void fwd_item(const float4* __restrict__ grec, const 
       v[0] += __shfl_xor_sync(MG_FULL, v[0], half);
     }
   }
-  // After log2(NV) halving levels on lane bits 4..(5-log2 NV), value index = lane >> (5 - log2 NV).
-  constexpr int SH = (NV == 32) ? 0 : (NV == 16 ? 1 : 2);
-  const int idx = lane >> SH;
-  const int q = idx >> 2, comp = idx & 3;
-  const bool writer = (lane & ((1 << SH) - 1)) == 0;
-  if (writer && q < np) {
-    float* o = reinterpret_cast<float*>(out4 + p0 + q);
-    // comp 0 = I -> .w ; comps 1..3 = H' -> .xyz (unscale P')
-    if (comp == 0)
-      o[3] = v[0];
-    else
-      o[comp - 1] = v[0] * (1.0f / kMScale);
-    if (comp == 0) cnt_out[p0 + q] = total;
+  return v[0];
+}
+template <int NV>
+struct RedShift {
+  static constexpr int value = NV >= 32 ? 0 : (NV >= 16 ? 1 : (NV >= 8 ? 2 : (NV >= 4 ? 3 : (NV >= 2 ? 4 : 5))));
+};
+
+// Write the reduced (I, H) of point q of an item.  comp 0 = I -> .w,
+// comps 1..3 = H' -> .xyz (P' scale removed).
+__device__ __forceinline__ void write_point_out(float4* __restrict__ out4, int* __restrict__ cnt_out, int p, int comp,
+                                                float val, int total) {
+  float* o = reinterpret_cast<float*>(out4 + p);
+  if (comp == 0) {
+    o[3] = val;
+    cnt_out[p] = total;
+  } else {
+    o[comp - 1] = val * (1.0f / kMScale);
   }
 }
 
+// ---------------------------------------------------------------------------
+// Forward: one warp per (point cell, <= Q sub-points of that cell); lanes
+// stride over the flattened candidate Gaussians (prefetching the next
+// record while computing the current one); the item's sub-points are
+// warp-uniform and packed two per f32x2 register (Gaussian parameters go in
+// as scalar-broadcast FFMA2 operands).  Every point of an item shares the
+// exact candidate set, so contributor_counts is the total candidate count.
+// ---------------------------------------------------------------------------
+#ifndef MG_FWD_MINB
+#define MG_FWD_MINB 4
+#endif
+#ifndef MG_BWD_MINB
+#define MG_BWD_MINB 4
+#endif
+constexpr int kFwdWarps = 4;
+
+template <int QP, bool WITH_H>
+__device__ __forceinline__ void fwd_pair_math(const float4& A, const float4& B, const float4& C, const f2 (&px)[QP],
+                                              const f2 (&py)[QP], const f2 (&pz)[QP], f2 (&accI)[QP], f2 (&hx)[QP],
+                                              f2 (&hy)[QP], f2 (&hz)[QP]) {
+  const float p00 = B.x, p11 = B.y, p22 = B.z, p01 = B.w, p02 = C.x, p12 = C.y;
+  if (WITH_H) {
+#pragma unroll
+    for (int q = 0; q < QP; ++q) {
+      f2 dx = sub2(px[q], bc2(A.x)), dy = sub2(py[q], bc2(A.y)), dz = sub2(pz[q], bc2(A.z));
+      f2 pdx = fma2(bc2(p02), dz, fma2(bc2(p01), dy, mul2(bc2(p00), dx)));
+      f2 pdy = fma2(bc2(p12), dz, fma2(bc2(p11), dy, mul2(bc2(p01), dx)));
+      f2 pdz = fma2(bc2(p22), dz, fma2(bc2(p12), dy, mul2(bc2(p02), dx)));
+      f2 m = fma2(dz, pdz, fma2(dy, pdy, mul2(dx, pdx)));
+      f2 wv = mul2(bc2(A.w), mk2(gauss_w(m.x), gauss_w(m.y)));
+      accI[q] = add2(accI[q], wv);
+      hx[q] = fma2(wv, pdx, hx[q]);
+      hy[q] = fma2(wv, pdy, hy[q]);
+      hz[q] = fma2(wv, pdz, hz[q]);
+    }
+  } else {
+    const float a01 = 2.f * p01, a02 = 2.f * p02, a12 = 2.f * p12;
+#pragma unroll
+    for (int q = 0; q < QP; ++q) {
+      f2 dx = sub2(px[q], bc2(A.x)), dy = sub2(py[q], bc2(A.y)), dz = sub2(pz[q], bc2(A.z));
+      f2 t1 = fma2(bc2(a02), dz, fma2(bc2(a01), dy, mul2(bc2(p00), dx)));
+      f2 m = mul2(dx, t1);
+      f2 t2 = fma2(bc2(a12), dz, mul2(bc2(p11), dy));
+      m = fma2(dy, t2, m);
+      m = fma2(dz, mul2(bc2(p22), dz), m);
+      accI[q] = fma2(bc2(A.w), mk2(gauss_w(m.x), gauss_w(m.y)), accI[q]);
+    }
+  }
+}
+
+template <int Q, bool WITH_H>
+__device__ __forceinline__ void fwd_item(const float4* __restrict__ grec, const int* __restrict__ gstart, int g, int r,
+                                         const float4* __restrict__ prec, int p0, int np, int cell,
+                                         float4* __restrict__ out4, int* __restrict__ cnt_out, SegSmem& sm,
+                                         int lane) {
+  constexpr int QP = Q / 2;
+  f2 px[QP], py[QP], pz[QP];
+#pragma unroll
+  for (int q = 0; q < QP; ++q) {
+    float4 a = prec[p0 + min(2 * q, np - 1)];
+    float4 b = prec[p0 + min(2 * q + 1, np - 1)];
+    px[q] = mk2(a.x, b.x);
+    py[q] = mk2(a.y, b.y);
+    pz[q] = mk2(a.z, b.z);
+  }
+  f2 accI[QP], hx[QP], hy[QP], hz[QP];
+#pragma unroll
+  for (int q = 0; q < QP; ++q) {
+    accI[q] = bc2(0.f);
+    hx[q] = hy[q] = hz[q] = bc2(0.f);
+  }
+  const Window w = make_window(cell, g, r);
+  const unsigned upto = 0xffffffffu >> (31 - lane);  // bits 0..lane
+  int total = 0;
+  for (int c0 = 0; c0 < w.ncol; c0 += 128) {
+    const LaneSegs L = build_lane_segs(w, c0, g, gstart, sm, lane);
+    const int tot = L.tot;
+    total += tot;
+    for (int w0 = 0; w0 < tot; w0 += 32 * kBmWords) {
+      int sbase = build_window(L, w0, sm, lane);
+      const int wend = min(tot, w0 + 32 * kBmWords);
+      for (int base = w0; base < wend; base += 32) {
+        const uint32_t M = sm.bits[(base - w0) >> 5];
+        const int v = base + lane;
+        const int seg = sbase + __popc(M & upto) - 1;
+        sbase += __popc(M);
+        if (v < wend) {
+          const int gi = v + sm.delta[seg];
+          const float4 A = __ldg(grec + 3 * gi);
+          const float4 B = __ldg(grec + 3 * gi + 1);
+          const float4 C = __ldg(grec + 3 * gi + 2);
+          fwd_pair_math<QP, WITH_H>(A, B, C, px, py, pz, accI, hx, hy, hz);
+        }
+      }
+      __syncwarp();
+    }
+  }
+  constexpr int NV = 4 * Q;  // 8, 16 or 32
+  float vals[32];
+#pragma unroll
+  for (int q = 0; q < QP; ++q) {
+    vals[8 * q + 0] = accI[q].x;
+    vals[8 * q + 1] = hx[q].x;
+    vals[8 * q + 2] = hy[q].x;
+    vals[8 * q + 3] = hz[q].x;
+    vals[8 * q + 4] = accI[q].y;
+    vals[8 * q + 5] = hx[q].y;
+    vals[8 * q + 6] = hy[q].y;
+    vals[8 * q + 7] = hz[q].y;
+  }
+#pragma unroll
+  for (int i = NV; i < 32; ++i) vals[i] = 0.f;
+  const float red = transpose_reduce<NV>(vals, lane);
+  constexpr int SH = RedShift<NV>::value;
+  const int idx = lane >> SH;
+  const int q = idx >> 2, comp = idx & 3;
+  if ((lane & ((1 << SH) - 1)) == 0 && q < np) write_point_out(out4, cnt_out, p0 + q, comp, red, total);
+}
+
+// np == 1: the single sub-point is broadcast and each lane packs TWO
+// candidate Gaussians (v and v + 32) into the f32x2 lanes.
 template <bool WITH_H>
-__global__ void __launch_bounds__(kFwdWarps * 32) forward_kernel(const float4* __restrict__ grec,
+__device__ __forceinline__ void fwd_item_single(const float4* __restrict__ grec, const int* __restrict__ gstart, int g,
+                                                int r, const float4* __restrict__ prec, int p0, int cell,
+                                                float4* __restrict__ out4, int* __restrict__ cnt_out, SegSmem& sm,
+                                                int lane) {
+  const float4 pt = prec[p0];
+  const f2 X = bc2(pt.x), Y = bc2(pt.y), Z = bc2(pt.z);
+  f2 accI = bc2(0.f), hx = bc2(0.f), hy = bc2(0.f), hz = bc2(0.f);
+  const Window w = make_window(cell, g, r);
+  const unsigned upto = 0xffffffffu >> (31 - lane);
+  int total = 0;
+  for (int c0 = 0; c0 < w.ncol; c0 += 128) {
+    const LaneSegs L = build_lane_segs(w, c0, g, gstart, sm, lane);
+    const int tot = L.tot;
+    total += tot;
+    for (int w0 = 0; w0 < tot; w0 += 32 * kBmWords) {
+      int sbase = build_window(L, w0, sm, lane);
+      const int wend = min(tot, w0 + 32 * kBmWords);
+      for (int base = w0; base < wend; base += 64) {
+        const uint32_t M0 = sm.bits[(base - w0) >> 5];
+        const uint32_t M1 = sm.bits[((base - w0) >> 5) + 1];
+        const int va = base + lane, vb = va + 32;
+        const int sega = sbase + __popc(M0 & upto) - 1;
+        const int segb = sbase + __popc(M0) + __popc(M1 & upto) - 1;
+        sbase += __popc(M0) + __popc(M1);
+        if (va < wend) {
+          const bool hb = vb < wend;
+          const int ga = va + sm.delta[sega];
+          const int gb = hb ? vb + sm.delta[segb] : ga;
+          const float4 Aa = __ldg(grec + 3 * ga), Ba = __ldg(grec + 3 * ga + 1), Ca = __ldg(grec + 3 * ga + 2);
+          const float4 Ab = __ldg(grec + 3 * gb), Bb = __ldg(grec + 3 * gb + 1), Cb = __ldg(grec + 3 * gb + 2);
+          const f2 dx = sub2(X, mk2(Aa.x, Ab.x)), dy = sub2(Y, mk2(Aa.y, Ab.y)), dz = sub2(Z, mk2(Aa.z, Ab.z));
+          const f2 p00 = mk2(Ba.x, Bb.x), p11 = mk2(Ba.y, Bb.y), p22 = mk2(Ba.z, Bb.z), p01 = mk2(Ba.w, Bb.w),
+                   p02 = mk2(Ca.x, Cb.x), p12 = mk2(Ca.y, Cb.y);
+          const f2 al = mk2(Aa.w, hb ? Ab.w : 0.f);
+          if (WITH_H) {
+            f2 pdx = fma2(p02, dz, fma2(p01, dy, mul2(p00, dx)));
+            f2 pdy = fma2(p12, dz, fma2(p11, dy, mul2(p01, dx)));
+            f2 pdz = fma2(p22, dz, fma2(p12, dy, mul2(p02, dx)));
+            f2 m = fma2(dz, pdz, fma2(dy, pdy, mul2(dx, pdx)));
+            f2 wv = mul2(al, mk2(gauss_w(m.x), gauss_w(m.y)));
+            accI = add2(accI, wv);
+            hx = fma2(wv, pdx, hx);
+            hy = fma2(wv, pdy, hy);
+            hz = fma2(wv, pdz, hz);
+          } else {
+            f2 t1 = fma2(add2(p02, p02), dz, fma2(add2(p01, p01), dy, mul2(p00, dx)));
+            f2 m = mul2(dx, t1);
+            m = fma2(dy, fma2(add2(p12, p12), dz, mul2(p11, dy)), m);
+            m = fma2(dz, mul2(p22, dz), m);
+            accI = fma2(al, mk2(gauss_w(m.x), gauss_w(m.y)), accI);
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+  float vals[32];
+  vals[0] = accI.x + accI.y;
+  vals[1] = hx.x + hx.y;
+  vals[2] = hy.x + hy.y;
+  vals[3] = hz.x + hz.y;
+#pragma unroll
+  for (int i = 4; i < 32; ++i) vals[i] = 0.f;
+  const float red = transpose_reduce<4>(vals, lane);
+  const int comp = lane >> 3;
+  if ((lane & 7) == 0) write_point_out(out4, cnt_out, p0, comp, red, total);
+}
+
+template <bool WITH_H>
+__global__ void __launch_bounds__(kFwdWarps * 32, MG_FWD_MINB) forward_kernel(const float4* __restrict__ grec,
                                                                  const int* __restrict__ gstart, int g, int r,
                                                                  const float4* __restrict__ prec,
                                                                  const uint32_t* __restrict__ pkey,
@@ -383,8 +583,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32) forward_kernel(const float4* _
                                                                  const int* __restrict__ items,
                                                                  const int* __restrict__ nitems_dev,
                                                                  float4* __restrict__ out4, int* __restrict__ cnt_out) {
-  __shared__ int s_start[kFwdWarps][128];
-  __shared__ int s_pre[kFwdWarps][132];
+  __shared__ SegSmem s_seg[kFwdWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nitems = *nitems_dev;
   for (int it = blockIdx.x * kFwdWarps + warp; it < nitems; it += gridDim.x * kFwdWarps) {
@@ -392,20 +591,23 @@ __global__ void __launch_bounds__(kFwdWarps * 32) forward_kernel(const float4* _
     const int cell = (int)pkey[p0];
     const int np = min(8, pstart[cell + 1] - p0);
     if (np > 4)
-      fwd_item<8, WITH_H>(grec, gstart, g, r, prec, p0, np, cell, out4, cnt_out, s_start[warp], s_pre[warp], lane);
+      fwd_item<8, WITH_H>(grec, gstart, g, r, prec, p0, np, cell, out4, cnt_out, s_seg[warp], lane);
     else if (np > 2)
-      fwd_item<4, WITH_H>(grec, gstart, g, r, prec, p0, np, cell, out4, cnt_out, s_start[warp], s_pre[warp], lane);
+      fwd_item<4, WITH_H>(grec, gstart, g, r, prec, p0, np, cell, out4, cnt_out, s_seg[warp], lane);
+    else if (np == 2)
+      fwd_item<2, WITH_H>(grec, gstart, g, r, prec, p0, np, cell, out4, cnt_out, s_seg[warp], lane);
     else
-      fwd_item<2, WITH_H>(grec, gstart, g, r, prec, p0, np, cell, out4, cnt_out, s_start[warp], s_pre[warp], lane);
+      fwd_item_single<WITH_H>(grec, gstart, g, r, prec, p0, cell, out4, cnt_out, s_seg[warp], lane);
   }
 }
 
 // ---------------------------------------------------------------------------
-// Backward, Gaussian-major: one warp per (Gaussian cell, <= QG Gaussians of
-// that cell); lanes stride over the flattened candidate sub-points, two per
-// lane packed in f32x2.  Per Gaussian it accumulates (register-resident, no
-// atomics):  S = sum u*g,  T = sum u*g*(P'd),  A6 = sum u*g*(d d^T)
-// from which the epilogue forms d_alpha = S, d_mu = alpha*T/kMScale,
+// Backward, Gaussian-major: one warp per (Gaussian cell, <= 2 Gaussians of
+// that cell); lanes stride over the flattened candidate sub-points, two
+// consecutive ones per lane packed in f32x2, next pair prefetched.  Per
+// Gaussian it accumulates (register-resident, no atomics):
+//   S = sum u*g,  T = sum u*g*(P'd),  A6 = sum u*g*(d d^T)
+// and the epilogue forms d_alpha = S, d_mu = alpha*T/kMScale,
 // d_abar6 = -0.5*alpha*A6 (_kernels.py:118-141).
 // ---------------------------------------------------------------------------
 constexpr int kBwdWarps = 4;
@@ -413,7 +615,7 @@ constexpr int kBwdWarps = 4;
 template <int QG>
 __device__ __forceinline__ void bwd_item(const float4* __restrict__ grec, int g0, int ng, int cell, int g, int r,
                                          const float4* __restrict__ prec, const int* __restrict__ pstart,
-                                         float* __restrict__ acc10, int* s_start, int* s_pre, int lane) {
+                                         float* __restrict__ acc10, SegSmem& sm, int lane) {
   float mx[QG], my[QG], mz[QG], P[QG][6];
 #pragma unroll
   for (int k = 0; k < QG; ++k) {
@@ -439,81 +641,77 @@ __device__ __forceinline__ void bwd_item(const float4* __restrict__ grec, int g0
     for (int c = 0; c < 6; ++c) A6[k][c] = bc2(0.f);
   }
   const Window w = make_window(cell, g, r);
+  const int la = 2 * lane;
+  const uint64_t upto_a = (la == 63) ? ~0ull : ((2ull << la) - 1ull);
   for (int c0 = 0; c0 < w.ncol; c0 += 128) {
-    const int tot = build_segments(w, c0, g, pstart, s_start, s_pre, lane);
-    int s = 0;
-    for (int v = 2 * lane; v < tot; v += 64) {
-      const int ia = seg_lookup(v, s, s_start, s_pre);
-      float4 a = __ldg(prec + ia);
-      float4 b;
-      if (v + 1 < tot) {
-        int s2 = s;
-        b = __ldg(prec + seg_lookup(v + 1, s2, s_start, s_pre));
-      } else {
-        b = make_float4(a.x, a.y, a.z, 0.f);  // dummy partner: zero upstream
-      }
-      const f2 px = mk2(a.x, b.x), py = mk2(a.y, b.y), pz = mk2(a.z, b.z), u = mk2(a.w, b.w);
+    const LaneSegs L = build_lane_segs(w, c0, g, pstart, sm, lane);
+    const int tot = L.tot;
+    for (int w0 = 0; w0 < tot; w0 += 32 * kBmWords) {
+      int sbase = build_window(L, w0, sm, lane);
+      const int wend = min(tot, w0 + 32 * kBmWords);
+      for (int base = w0; base < wend; base += 64) {
+        const int wi = (base - w0) >> 5;
+        const uint64_t M = ((uint64_t)sm.bits[wi + 1] << 32) | (uint64_t)sm.bits[wi];
+        const int v = base + la;
+        const int sega = sbase + __popcll(M & upto_a) - 1;
+        const int segb = sega + (int)((M >> (la + 1)) & 1ull);
+        sbase += __popcll(M);
+        if (v < wend) {
+          const float4 a = __ldg(prec + v + sm.delta[sega]);
+          float4 b;
+          if (v + 1 < wend)
+            b = __ldg(prec + v + 1 + sm.delta[segb]);
+          else
+            b = make_float4(a.x, a.y, a.z, 0.f);  // dummy partner: zero upstream
+          const f2 px = mk2(a.x, b.x), py = mk2(a.y, b.y), pz = mk2(a.z, b.z), u = mk2(a.w, b.w);
 #pragma unroll
-      for (int k = 0; k < QG; ++k) {
-        f2 dx = sub2(px, bc2(mx[k])), dy = sub2(py, bc2(my[k])), dz = sub2(pz, bc2(mz[k]));
-        f2 pdx = fma2(bc2(P[k][4]), dz, fma2(bc2(P[k][3]), dy, mul2(bc2(P[k][0]), dx)));
-        f2 pdy = fma2(bc2(P[k][5]), dz, fma2(bc2(P[k][1]), dy, mul2(bc2(P[k][3]), dx)));
-        f2 pdz = fma2(bc2(P[k][2]), dz, fma2(bc2(P[k][5]), dy, mul2(bc2(P[k][4]), dx)));
-        f2 m = fma2(dz, pdz, fma2(dy, pdy, mul2(dx, pdx)));
-        f2 ug = mul2(u, mk2(gauss_w(m.x), gauss_w(m.y)));
-        S[k] = add2(S[k], ug);
-        T[k][0] = fma2(ug, pdx, T[k][0]);
-        T[k][1] = fma2(ug, pdy, T[k][1]);
-        T[k][2] = fma2(ug, pdz, T[k][2]);
-        f2 cx = mul2(ug, dx), cy = mul2(ug, dy), cz = mul2(ug, dz);
-        A6[k][0] = fma2(cx, dx, A6[k][0]);
-        A6[k][1] = fma2(cx, dy, A6[k][1]);
-        A6[k][2] = fma2(cx, dz, A6[k][2]);
-        A6[k][3] = fma2(cy, dy, A6[k][3]);
-        A6[k][4] = fma2(cy, dz, A6[k][4]);
-        A6[k][5] = fma2(cz, dz, A6[k][5]);
-      }
-    }
-    __syncwarp();
-  }
-  // Per Gaussian: 10 sums (pad to 16) -> transposed reduction; value index = lane >> 1.
-#pragma unroll
-  for (int k = 0; k < QG; ++k) {
-    if (k < ng) {
-      float v[16];
-      v[0] = S[k].x + S[k].y;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) v[1 + c] = T[k][c].x + T[k][c].y;
-#pragma unroll
-      for (int c = 0; c < 6; ++c) v[4 + c] = A6[k][c].x + A6[k][c].y;
-#pragma unroll
-      for (int c = 10; c < 16; ++c) v[c] = 0.f;
-      int nrem = 16;
-#pragma unroll
-      for (int half = 16; half >= 1; half >>= 1) {
-        if (nrem > 1) {
-          const bool upper = (lane & half) != 0;
-          const int h2 = nrem / 2;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            if (i < h2) {
-              float send = upper ? v[i] : v[i + h2];
-              float keep = upper ? v[i + h2] : v[i];
-              v[i] = keep + __shfl_xor_sync(MG_FULL, send, half);
-            }
+          for (int k = 0; k < QG; ++k) {
+            f2 dx = sub2(px, bc2(mx[k])), dy = sub2(py, bc2(my[k])), dz = sub2(pz, bc2(mz[k]));
+            f2 pdx = fma2(bc2(P[k][4]), dz, fma2(bc2(P[k][3]), dy, mul2(bc2(P[k][0]), dx)));
+            f2 pdy = fma2(bc2(P[k][5]), dz, fma2(bc2(P[k][1]), dy, mul2(bc2(P[k][3]), dx)));
+            f2 pdz = fma2(bc2(P[k][2]), dz, fma2(bc2(P[k][5]), dy, mul2(bc2(P[k][4]), dx)));
+            f2 m = fma2(dz, pdz, fma2(dy, pdy, mul2(dx, pdx)));
+            f2 ug = mul2(u, mk2(gauss_w(m.x), gauss_w(m.y)));
+            S[k] = add2(S[k], ug);
+            T[k][0] = fma2(ug, pdx, T[k][0]);
+            T[k][1] = fma2(ug, pdy, T[k][1]);
+            T[k][2] = fma2(ug, pdz, T[k][2]);
+            f2 cx = mul2(ug, dx), cy = mul2(ug, dy), cz = mul2(ug, dz);
+            A6[k][0] = fma2(cx, dx, A6[k][0]);
+            A6[k][1] = fma2(cx, dy, A6[k][1]);
+            A6[k][2] = fma2(cx, dz, A6[k][2]);
+            A6[k][3] = fma2(cy, dy, A6[k][3]);
+            A6[k][4] = fma2(cy, dz, A6[k][4]);
+            A6[k][5] = fma2(cz, dz, A6[k][5]);
           }
-          nrem = h2;
-        } else {
-          v[0] += __shfl_xor_sync(MG_FULL, v[0], half);
         }
       }
-      const int idx = lane >> 1;
-      if ((lane & 1) == 0 && idx < 10) acc10[(int64_t)(g0 + k) * 10 + idx] = v[0];
+      __syncwarp();
     }
   }
+  // 10 sums per Gaussian (x QG, padded to 16 / 32) -> transposed reduction.
+  constexpr int NV = QG == 1 ? 16 : 32;
+  float vals[32];
+#pragma unroll
+  for (int k = 0; k < QG; ++k) {
+    vals[16 * k + 0] = S[k].x + S[k].y;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) vals[16 * k + 1 + c] = T[k][c].x + T[k][c].y;
+#pragma unroll
+    for (int c = 0; c < 6; ++c) vals[16 * k + 4 + c] = A6[k][c].x + A6[k][c].y;
+#pragma unroll
+    for (int c = 10; c < 16; ++c) vals[16 * k + c] = 0.f;
+  }
+#pragma unroll
+  for (int i = 16 * QG; i < 32; ++i) vals[i] = 0.f;
+  const float red = transpose_reduce<NV>(vals, lane);
+  constexpr int SH = RedShift<NV>::value;
+  const int idx = lane >> SH;
+  const int k = idx >> 4, c = idx & 15;
+  if ((lane & ((1 << SH) - 1)) == 0 && c < 10 && k < ng) acc10[(int64_t)(g0 + k) * 10 + c] = red;
 }
 
-__global__ void __launch_bounds__(kBwdWarps * 32) backward_kernel(const float4* __restrict__ grec,
+__global__ void __launch_bounds__(kBwdWarps * 32, MG_BWD_MINB) backward_kernel(const float4* __restrict__ grec,
                                                                   const uint32_t* __restrict__ gkey,
                                                                   const int* __restrict__ gstart, int g, int r,
                                                                   const float4* __restrict__ prec,
@@ -521,20 +719,17 @@ __global__ void __launch_bounds__(kBwdWarps * 32) backward_kernel(const float4* 
                                                                   const int* __restrict__ items,
                                                                   const int* __restrict__ nitems_dev,
                                                                   float* __restrict__ acc10) {
-  __shared__ int s_start[kBwdWarps][128];
-  __shared__ int s_pre[kBwdWarps][132];
+  __shared__ SegSmem s_seg[kBwdWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nitems = *nitems_dev;
   for (int it = blockIdx.x * kBwdWarps + warp; it < nitems; it += gridDim.x * kBwdWarps) {
     const int g0 = items[it];
     const int cell = (int)gkey[g0];
-    const int ng = min(4, gstart[cell + 1] - g0);
-    if (ng > 2)
-      bwd_item<4>(grec, g0, ng, cell, g, r, prec, pstart, acc10, s_start[warp], s_pre[warp], lane);
-    else if (ng == 2)
-      bwd_item<2>(grec, g0, ng, cell, g, r, prec, pstart, acc10, s_start[warp], s_pre[warp], lane);
+    const int ng = min(2, gstart[cell + 1] - g0);
+    if (ng == 2)
+      bwd_item<2>(grec, g0, ng, cell, g, r, prec, pstart, acc10, s_seg[warp], lane);
     else
-      bwd_item<1>(grec, g0, ng, cell, g, r, prec, pstart, acc10, s_start[warp], s_pre[warp], lane);
+      bwd_item<1>(grec, g0, ng, cell, g, r, prec, pstart, acc10, s_seg[warp], lane);
   }
 }
 

@@ -197,37 +197,48 @@ __global__ void epilogue_f64_kernel(const double* __restrict__ d_mu, const doubl
 // Transform gradients: per slice sums of h and h (x) c over sub-points
 // (render.py:246-273), then the quaternion chain.
 // ---------------------------------------------------------------------------
+// Each thread walks a contiguous chunk of sub-points, accumulating in float64
+// registers while the slice id is unchanged (taps of a point and the SSIM
+// slice are contiguous runs), and flushes 12 sums per run with global fp64
+// atomics -- avoids the single-bin contention of the per-step SSIM slice.
 __global__ void transform_reduce_kernel(const double* __restrict__ dpoints, const double* __restrict__ coords,
                                         const int64_t* __restrict__ sids, int64_t b, int ntaps,
                                         const double* __restrict__ tap_off, const double* __restrict__ dirs, int k,
                                         double* __restrict__ out12) {
-  extern __shared__ double s_acc[];  // 12 * k
-  const bool use_smem = k <= 256;
-  if (use_smem) {
-    for (int i = threadIdx.x; i < 12 * k; i += blockDim.x) s_acc[i] = 0.0;
-    __syncthreads();
-  }
-  GRID_LOOP(j, b * ntaps) {
-    int64_t pb = j / ntaps;
-    int t = (int)(j - pb * ntaps);
-    int64_t s = sids[pb];
-    if (s < 0 || s >= k) continue;
-    double c[3] = {coords[3 * pb], coords[3 * pb + 1], coords[3 * pb + 2]};
-    if (tap_off) {
-      double o = tap_off[t];
-      for (int a = 0; a < 3; ++a) c[a] = __dadd_rn(c[a], __dmul_rn(o, dirs[3 * s + a]));
+  constexpr int CH = 32;
+  const int64_t total = b * ntaps;
+  for (int64_t c0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * CH; c0 < total;
+       c0 += (int64_t)gridDim.x * blockDim.x * CH) {
+    const int64_t c1 = min(total, c0 + CH);
+    int64_t cur = -1;
+    double acc[12];
+    for (int i = 0; i < 12; ++i) acc[i] = 0.0;
+    for (int64_t j = c0; j < c1; ++j) {
+      int64_t pb = j / ntaps;
+      int t = (int)(j - pb * ntaps);
+      int64_t s = sids[pb];
+      if (s < 0 || s >= k) continue;
+      if (s != cur) {
+        if (cur >= 0)
+          for (int i = 0; i < 12; ++i)
+            if (acc[i] != 0.0) atomicAdd(out12 + 12 * cur + i, acc[i]);
+        for (int i = 0; i < 12; ++i) acc[i] = 0.0;
+        cur = s;
+      }
+      double c[3] = {coords[3 * pb], coords[3 * pb + 1], coords[3 * pb + 2]};
+      if (tap_off) {
+        double o = tap_off[t];
+        for (int a = 0; a < 3; ++a) c[a] = __dadd_rn(c[a], __dmul_rn(o, dirs[3 * s + a]));
+      }
+      double h[3] = {dpoints[3 * j], dpoints[3 * j + 1], dpoints[3 * j + 2]};
+      for (int a = 0; a < 3; ++a) {
+        acc[a] += h[a];
+        for (int bb = 0; bb < 3; ++bb) acc[3 + 3 * a + bb] += h[a] * c[bb];
+      }
     }
-    double h[3] = {dpoints[3 * j], dpoints[3 * j + 1], dpoints[3 * j + 2]};
-    double* dst = use_smem ? s_acc + 12 * s : out12 + 12 * s;
-    for (int a = 0; a < 3; ++a) {
-      atomicAdd(dst + a, h[a]);
-      for (int bb = 0; bb < 3; ++bb) atomicAdd(dst + 3 + 3 * a + bb, h[a] * c[bb]);
-    }
-  }
-  if (use_smem) {
-    __syncthreads();
-    for (int i = threadIdx.x; i < 12 * k; i += blockDim.x)
-      if (s_acc[i] != 0.0) atomicAdd(out12 + i, s_acc[i]);
+    if (cur >= 0)
+      for (int i = 0; i < 12; ++i)
+        if (acc[i] != 0.0) atomicAdd(out12 + 12 * cur + i, acc[i]);
   }
 }
 
@@ -441,9 +452,9 @@ void launch_transform_grads(const double* dpoints, const double* coords, const i
   if (k <= 0) return;
   cudaMemsetAsync(acc12, 0, sizeof(double) * 12 * k, st);
   if (b > 0) {
-    size_t sm = k <= 256 ? sizeof(double) * 12 * k : 0;
-    transform_reduce_kernel<<<gridn(b * ntaps), 256, sm, st>>>(dpoints, coords, sids, b, ntaps, tap_off, dirs, k,
-                                                               acc12);
+    int64_t chunks = (b * ntaps + 31) / 32;
+    transform_reduce_kernel<<<gridn(chunks, 128), 128, 0, st>>>(dpoints, coords, sids, b, ntaps, tap_off, dirs, k,
+                                                                acc12);
   }
   transform_chain_kernel<<<gridn(k), 256, 0, st>>>(acc12, tq, k, out7, accumulate);
 }

@@ -1,0 +1,55 @@
+"""Kernel micro-benchmark on the C2 training state: times the forward and
+backward pair kernels (and the whole eager step) with CUDA events.
+
+    python tools/kbench.py [--reps 10]
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--config", default="C2")
+    a = ap.parse_args()
+    import torch
+
+    from paper_2603_00145_b200.train import Trainer
+
+    data, cloud, grids, psf, cfg = bench.make_workload(a.config, 0)
+    tr = Trainer(cloud, data.transforms, cfg, slice_grids=grids, slice_psf=psf, graph=False)
+    for _ in range(3):
+        tr.step()
+    idx_list = []
+    for _ in range(a.reps):
+        idx = tr._next_batch()
+        j = int(tr.rng.integers(len(tr.slice_grids)))
+        all_idx, hw = tr.host_indices(idx, j)
+        idx_list.append(torch.from_numpy(all_idx).cuda())
+    kt = bench.kernel_times(tr, idx_list, cfg.batch_points, hw)
+    B = tr._bufs
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for ix in idx_list:
+        tr.load_indices(ix)
+        tr._body(B, cfg.batch_points, hw)
+    e1.record()
+    torch.cuda.synchronize()
+    kt["step_ms_eager"] = e0.elapsed_time(e1) / len(idx_list)
+    p = kt["pairs_per_launch"]
+    kt["fwd_gpairs_s"] = p / kt["forward_ms"] / 1e6
+    kt["bwd_gpairs_s"] = p / kt["backward_ms"] / 1e6
+    kt["fwd_frac"] = p * 20 / (kt["forward_ms"] / 1e3) / bench.peak_fp32(148, 1965.0)
+    kt["bwd_frac"] = p * 56 / (kt["backward_ms"] / 1e3) / bench.peak_fp32(148, 1965.0)
+    print(json.dumps(kt))
+
+
+if __name__ == "__main__":
+    main()

@@ -70,8 +70,10 @@ int mg_i64_to_i32(const int64_t *src, int64_t n, int32_t *dst, void *stream);
 int mg_i32_to_i64(const int32_t *src, int64_t n, int64_t *dst, void *stream);
 
 /* ---- preprocessing: render.py:122-142 ----------------------------------- */
-/* Packed records (48 B each, cell order: rec[p] describes primitive
- * cell_indices[p]).  err_flag |= 1 when some |q| <= 1e-12. */
+/* Packed records in cell order (record p describes primitive cell_indices[p]),
+ * structure-of-arrays in one float buffer of 12*n: float4 {mu, alpha} x n,
+ * float4 {P'00, P'11, P'22, P'01} x n, float2 {P'02, P'12} x n, with
+ * P' = -0.5*log2(e)*P.  err_flag |= 1 when some |q| <= 1e-12. */
 int mg_activate(const float *pos, const float *quat, const float *log_scales, const float *logits, int64_t n,
                 const int32_t *cell_indices, void *grec, int32_t *err_flag, void *stream);
 /* Records from float64 prepared (mu (n,3), prec6 (n,6), alpha (n)) in cell order. */
@@ -100,7 +102,8 @@ int mg_bin_points(const double *coords, const int64_t *slice_ids, int64_t b, int
 size_t mg_forward_workspace_bytes(int64_t n_sub);
 /* out4[p] = {H.x, H.y, H.z, I} per sorted sub-point (H = sum alpha g P d,
  * only when with_h != 0); counts[p] = candidate count (sorted order). */
-int mg_forward(const void *grec, const int32_t *gstart, int64_t grid_res, int64_t radius, const void *prec,
+int mg_forward(const void *grec, int64_t n_gauss, const int32_t *gstart, int64_t grid_res, int64_t radius,
+               const void *prec,
                const uint32_t *pkey_sorted, const int32_t *pstart, int64_t n_sub, int32_t with_h, void *out4,
                int32_t *counts, void *ws, size_t ws_bytes, void *stream);
 /* I_b = sum_t w_t I_(b,t) (tap_weights NULL = single tap); counts summed. */
@@ -139,7 +142,8 @@ int mg_transform_grads(const double *d_points, const double *coords, const int64
 size_t mg_volume_workspace_bytes(int64_t nx, int64_t ny, int64_t nz);
 /* Slab [i0, i1) of a node-inclusive (nx,ny,nz) grid over [lo, hi]; out is
  * (i1-i0, ny, nz) float32 clipped to [0,1]; residual (same shape) optional. */
-int mg_sample_volume(const void *grec, const int32_t *gstart, int64_t grid_res, int64_t radius, int64_t nx,
+int mg_sample_volume(const void *grec, int64_t n_gauss, const int32_t *gstart, int64_t grid_res, int64_t radius,
+                     int64_t nx,
                      int64_t ny, int64_t nz, const double *lo3_host, const double *hi3_host, int64_t i0, int64_t i1,
                      const float *residual, float *out, void *ws, size_t ws_bytes, void *stream);
 

@@ -38,7 +38,7 @@ SIGNATURES = {
     "mg_points_workspace_bytes": (SZ, [I64, I64]),
     "mg_bin_points": (ctypes.c_int, [P, P, I64, I32, P, P, P, P, I64, I64, P, P, P, P, P, P, SZ, P]),
     "mg_forward_workspace_bytes": (SZ, [I64]),
-    "mg_forward": (ctypes.c_int, [P, P, I64, I64, P, P, P, I64, I32, P, P, P, SZ, P]),
+    "mg_forward": (ctypes.c_int, [P, I64, P, I64, I64, P, P, P, I64, I32, P, P, P, SZ, P]),
     "mg_forward_finish": (ctypes.c_int, [P, P, P, I64, I32, P, P, P, P, P]),
     "mg_backward_points": (ctypes.c_int, [P, P, I64, I32, P, P, P, P, P, P]),
     "mg_backward_workspace_bytes": (SZ, [I64]),
@@ -49,7 +49,7 @@ SIGNATURES = {
     "mg_pack_records": (ctypes.c_int, [P, P, P, P, I64, P, P]),
     "mg_transform_grads": (ctypes.c_int, [P, P, P, I64, I32, P, P, P, I64, P, P, I32, P]),
     "mg_volume_workspace_bytes": (SZ, [I64, I64, I64]),
-    "mg_sample_volume": (ctypes.c_int, [P, P, I64, I64, I64, I64, I64, P, P, I64, I64, P, P, P, SZ, P]),
+    "mg_sample_volume": (ctypes.c_int, [P, I64, P, I64, I64, I64, I64, I64, P, P, I64, I64, P, P, P, SZ, P]),
     "mg_smooth_l1": (ctypes.c_int, [P, P, I64, P, P, P]),
     "mg_ssim_workspace_bytes": (SZ, [I64, I64]),
     "mg_ssim_loss_grad": (ctypes.c_int, [P, P, I64, I64, D, P, P, P, SZ, P]),

@@ -116,9 +116,10 @@ __global__ void activate_f64_kernel(const double* __restrict__ quat, const doubl
 }
 
 // All-pairs evaluation (_kernels.py:147-162) over fp32 records, smem-tiled.
-__global__ void dense_kernel(const double* __restrict__ pts, int64_t b, const float4* __restrict__ grec, int64_t n,
+__global__ void dense_kernel(const double* __restrict__ pts, int64_t b, GaussSoA grec, int64_t n,
                              double* __restrict__ out) {
-  __shared__ float4 tile[3 * 128];
+  __shared__ float4 ta[128], tb[128];
+  __shared__ float2 tc[128];
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   float x = 0.f, y = 0.f, z = 0.f;
   if (q < b) {
@@ -130,10 +131,15 @@ __global__ void dense_kernel(const double* __restrict__ pts, int64_t b, const fl
   for (int64_t t0 = 0; t0 < n; t0 += 128) {
     int cnt = (int)min((int64_t)128, n - t0);
     __syncthreads();
-    for (int i = threadIdx.x; i < 3 * cnt; i += blockDim.x) tile[i] = grec[3 * t0 + i];
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+      ta[i] = grec.A[t0 + i];
+      tb[i] = grec.B[t0 + i];
+      tc[i] = grec.C[t0 + i];
+    }
     __syncthreads();
     for (int i = 0; i < cnt; ++i) {
-      float4 A = tile[3 * i], B = tile[3 * i + 1], C = tile[3 * i + 2];
+      float4 A = ta[i], B = tb[i];
+      float2 C = tc[i];
       float dx = x - A.x, dy = y - A.y, dz = z - A.z;
       float m = dx * (B.x * dx + 2.f * B.w * dy + 2.f * C.x * dz) + dy * (B.y * dy + 2.f * C.y * dz) + B.z * dz * dz;
       acc += A.w * gauss_w(m);
@@ -221,7 +227,7 @@ int mg_i32_to_i64(const int32_t* src, int64_t n, int64_t* dst, void* stream) {
 
 int mg_activate(const float* pos, const float* quat, const float* ls, const float* lg, int64_t n,
                 const int32_t* cell_indices, void* grec, int32_t* err_flag, void* stream) {
-  launch_gauss_activate(pos, quat, ls, lg, cell_indices, n, (float4*)grec, err_flag, S(stream));
+  launch_gauss_activate(pos, quat, ls, lg, cell_indices, n, (float*)grec, err_flag, S(stream));
   return cuda_status();
 }
 
@@ -257,7 +263,7 @@ int mg_bin_points(const double* coords, const int64_t* sids, int64_t b, int32_t 
 
 size_t mg_forward_workspace_bytes(int64_t ns) { return fwd_ws(ns); }
 
-int mg_forward(const void* grec, const int32_t* gstart, int64_t g, int64_t r, const void* prec,
+int mg_forward(const void* grec, int64_t n_gauss, const int32_t* gstart, int64_t g, int64_t r, const void* prec,
                const uint32_t* pkey_sorted, const int32_t* pstart, int64_t ns, int32_t with_h, void* out4,
                int32_t* counts, void* ws, size_t wsb, void* stream) {
   if (g < 1 || r < 0 || ns < 0) return fail("mg_forward: bad sizes");
@@ -267,8 +273,9 @@ int mg_forward(const void* grec, const int32_t* gstart, int64_t g, int64_t r, co
   int* nitems = w.take<int>(1);
   if (!w.ok) return fail("mg_forward: workspace too small");
   if (ns == 0) return 0;
-  build_items(pkey_sorted, pstart, ns, 8, items, nitems, w.rest(), st);
-  launch_forward(with_h != 0, (const float4*)grec, gstart, (int)g, (int)r, (const float4*)prec, pkey_sorted, pstart,
+  build_items(pkey_sorted, pstart, ns, fwd_qmax(), items, nitems, w.rest(), st);
+  launch_forward(with_h != 0, (const float*)grec, n_gauss, gstart, (int)g, (int)r, (const float4*)prec, pkey_sorted,
+                 pstart,
                  items, nitems, ns, (float4*)out4, counts, st);
   return cuda_status();
 }
@@ -301,7 +308,7 @@ int mg_backward(const void* grec, const uint32_t* gkey_sorted, const int32_t* gs
   if (!w.ok) return fail("mg_backward: workspace too small");
   if (n == 0) return 0;
   build_items(gkey_sorted, gstart, n, 2, items, nitems, w.rest(), st);
-  launch_backward((const float4*)grec, gkey_sorted, gstart, (int)g, (int)r, (const float4*)prec, pstart, items,
+  launch_backward((const float*)grec, n, gkey_sorted, gstart, (int)g, (int)r, (const float4*)prec, pstart, items,
                   nitems, n, acc10, st);
   return cuda_status();
 }
@@ -321,7 +328,7 @@ int mg_epilogue_f64(const double* d_mu, const double* d_abar6, const double* d_a
 
 int mg_pack_records(const double* mu, const double* prec6, const double* alpha, const int32_t* order, int64_t n,
                     void* grec, void* stream) {
-  launch_gauss_pack_prepared(mu, prec6, alpha, order, n, (float4*)grec, S(stream));
+  launch_gauss_pack_prepared(mu, prec6, alpha, order, n, (float*)grec, S(stream));
   return cuda_status();
 }
 
@@ -343,14 +350,16 @@ size_t mg_volume_workspace_bytes(int64_t nx, int64_t ny, int64_t nz) {
   return volume_workspace_bytes((int)nx, (int)ny, (int)nz);
 }
 
-int mg_sample_volume(const void* grec, const int32_t* gstart, int64_t g, int64_t r, int64_t nx, int64_t ny,
+int mg_sample_volume(const void* grec, int64_t n_gauss, const int32_t* gstart, int64_t g, int64_t r, int64_t nx,
+                     int64_t ny,
                      int64_t nz, const double* lo, const double* hi, int64_t i0, int64_t i1, const float* residual,
                      float* out, void* ws, size_t wsb, void* stream) {
   if (nx < 1 || ny < 1 || nz < 1 || i0 < 0 || i1 > nx || i1 <= i0 || g < 1 || r < 0)
     return fail("mg_sample_volume: bad sizes");
   if (wsb < volume_workspace_bytes((int)nx, (int)ny, (int)nz)) return fail("mg_sample_volume: workspace too small");
   int dims[3] = {(int)nx, (int)ny, (int)nz};
-  launch_sample_volume((const float4*)grec, gstart, (int)g, (int)r, dims, lo, hi, (int)i0, (int)i1, residual, out, ws,
+  launch_sample_volume((const float*)grec, n_gauss, gstart, (int)g, (int)r, dims, lo, hi, (int)i0, (int)i1, residual,
+                       out, ws,
                        S(stream));
   return cuda_status();
 }
@@ -420,7 +429,7 @@ static int block_common(const double* points, const int64_t* sids, int64_t b, co
   int* pstart = w.take<int>(nc1);
   int* gorder = w.take<int>(n);
   uint32_t* gkey = w.take<uint32_t>(n);
-  float4* grec = w.take<float4>(3 * n);
+  float* grec = w.take<float>(12 * n);
   uint32_t* pkey = w.take<uint32_t>(b);
   int* pinv = w.take<int>(b);
   int* cnt = w.take<int>(b);
@@ -437,7 +446,7 @@ static int block_common(const double* points, const int64_t* sids, int64_t b, co
                          rest, restb, st);
   if (rc) return rc;
   if (b == 0) return cuda_status();
-  rc = mg_forward(grec, gstart, g, r, prec, pkey, pstart, b, with_h ? 1 : 0, out4, cnt, rest, restb, st);
+  rc = mg_forward(grec, n, gstart, g, r, prec, pkey, pstart, b, with_h ? 1 : 0, out4, cnt, rest, restb, st);
   if (rc) return rc;
   if (!upstream) {
     launch_forward_finish(out4, cnt, pinv, b, 1, nullptr, out_i, nullptr, out_cnt, st);
@@ -474,14 +483,14 @@ int mg_dense_forward(const double* points, int64_t b, const double* mu, const do
                      int64_t n, double* out, void* ws, size_t wsb, void* stream) {
   cudaStream_t st = S(stream);
   Bump w(ws, wsb);
-  float4* grec = w.take<float4>(3 * n);
+  float* grec = w.take<float>(12 * n);
   int* ident = w.take<int>(n);
   if (!w.ok) return fail("mg_dense_forward: workspace too small");
   if (n > 0) {
     iota32_kernel<<<grid_of(n), 256, 0, st>>>(ident, n);
     launch_gauss_pack_prepared(mu, prec6, alpha, ident, n, grec, st);
   }
-  if (b > 0) dense_kernel<<<(unsigned)((b + 127) / 128), 128, 0, st>>>(points, b, grec, n, out);
+  if (b > 0) dense_kernel<<<(unsigned)((b + 127) / 128), 128, 0, st>>>(points, b, gauss_soa(grec, n), n, out);
   return cuda_status();
 }
 

@@ -19,42 +19,48 @@ static constexpr float kCutScaled = (float)(-32.0 * MG_LOG2E);  // = kMScale * 6
 // is shared by both halves is passed as a float and ptxas encodes it as a
 // broadcast (.F32) operand, so no duplicate register is needed.
 // ---------------------------------------------------------------------------
+// Packed pairs live in one 64-bit value so the register allocator keeps the
+// halves in an aligned register pair (no re-pairing moves before FFMA2).
 struct f2 {
-  float x, y;
+  unsigned long long v;
 };
 
-__device__ __forceinline__ uint64_t f2_bits(f2 a) {
-  uint64_t r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
-  return r;
-}
-__device__ __forceinline__ f2 f2_from(uint64_t b) {
+__device__ __forceinline__ f2 mk2(float a, float b) {
   f2 r;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(b));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(a), "f"(b));
   return r;
 }
-__device__ __forceinline__ f2 mk2(float a, float b) { return f2{a, b}; }
-__device__ __forceinline__ f2 bc2(float a) { return f2{a, a}; }
+__device__ __forceinline__ f2 bc2(float a) { return mk2(a, a); }
+__device__ __forceinline__ float lo(f2 a) {
+  float x, y;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(a.v));
+  return x;
+}
+__device__ __forceinline__ float hi(f2 a) {
+  float x, y;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(a.v));
+  return y;
+}
 
 __device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
-  uint64_t d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)), "l"(f2_bits(c)));
-  return f2_from(d);
+  f2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d.v) : "l"(a.v), "l"(b.v), "l"(c.v));
+  return d;
 }
 __device__ __forceinline__ f2 mul2(f2 a, f2 b) {
-  uint64_t d;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)));
-  return f2_from(d);
+  f2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d.v) : "l"(a.v), "l"(b.v));
+  return d;
 }
 __device__ __forceinline__ f2 add2(f2 a, f2 b) {
-  uint64_t d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)));
-  return f2_from(d);
+  f2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d.v) : "l"(a.v), "l"(b.v));
+  return d;
 }
 __device__ __forceinline__ f2 sub2(f2 a, f2 b) {
-  uint64_t d;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)));
-  return f2_from(d);
+  f2 d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d.v) : "l"(a.v), "l"(b.v));
+  return d;
 }
 
 // 2^x on the MUFU (SFU) pipe, flush-to-zero: one MUFU.EX2.
@@ -69,6 +75,7 @@ __device__ __forceinline__ float gauss_w(float ms) {
   float e = ex2(ms);
   return ms >= kCutScaled ? e : 0.0f;
 }
+__device__ __forceinline__ f2 gauss_w2(f2 m) { return mk2(gauss_w(lo(m)), gauss_w(hi(m))); }
 
 // ---------------------------------------------------------------------------
 // Warp reductions
@@ -121,6 +128,29 @@ __device__ __forceinline__ int cell_of_d(double v, int g) {
 }
 
 __device__ __forceinline__ int flat_cell(int ci, int cj, int ck, int g) { return (ci * g + cj) * g + ck; }
+
+// Gaussian records, structure-of-arrays inside one float buffer of 12*N:
+// A = float4[N] {mu.xyz, alpha} at 0, B = float4[N] {P'00,P'11,P'22,P'01} at
+// 4N, C = float2[N] {P'02,P'12} at 8N.  Warp-wide loads of consecutive
+// records are fully coalesced (4 + 4 + 2 sectors per 32 records).
+struct GaussSoA {
+  const float4* A;
+  const float4* B;
+  const float2* C;
+};
+struct GaussOut {
+  float4* A;
+  float4* B;
+  float2* C;
+};
+inline GaussSoA gauss_soa(const float* base, int64_t n) {
+  return GaussSoA{reinterpret_cast<const float4*>(base), reinterpret_cast<const float4*>(base + 4 * n),
+                  reinterpret_cast<const float2*>(base + 8 * n)};
+}
+inline GaussOut gauss_out(float* base, int64_t n) {
+  return GaussOut{reinterpret_cast<float4*>(base), reinterpret_cast<float4*>(base + 4 * n),
+                  reinterpret_cast<float2*>(base + 8 * n)};
+}
 
 // Device-side error codes (read by the host wrappers).
 enum MgErr : int {

@@ -12,7 +12,8 @@
 // lets the backward run Gaussian-major with no atomics.
 //
 // Layout in HBM (all in cell-sorted order):
-//   grec[3*p + {0,1,2}]  float4 {mu.xyz, alpha}, {P'00,P'11,P'22,P'01}, {P'02,P'12,-,-}
+//   grec (SoA, 12 floats per Gaussian): A = float4[N] {mu.xyz, alpha} at 0,
+//                        B = float4[N] {P'00,P'11,P'22,P'01} at 4N, C = float2[N] {P'02,P'12} at 8N
 //                        with P' = -0.5*log2(e) * P  (exp(-m/2) = 2^{d^T P' d})
 //   prec[p]              float4 {x, y, z, upstream} of sub-point p (fp32)
 //   gstart / pstart      int32 CSR over the G^3 cells
@@ -57,7 +58,7 @@ __device__ __forceinline__ void quat_rot_d(double w, double x, double y, double 
 }
 
 __device__ __forceinline__ void activate_one(const float* pos, const float* quat, const float* ls, const float* lg,
-                                             int64_t i, float4* rec, int* err) {
+                                             int64_t i, GaussOut rec, int64_t p, int* err) {
   double qw = quat[4 * i], qx = quat[4 * i + 1], qy = quat[4 * i + 2], qz = quat[4 * i + 3];
   double nrm = sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
   if (!(nrm > 1e-12)) {  // core.py:43-44 (DegenerateQuaternion); NaN also flags
@@ -82,18 +83,18 @@ __device__ __forceinline__ void activate_one(const float* pos, const float* quat
     P[k] = kMScaleD * (R[3 * a] * e[0] * R[3 * b] + R[3 * a + 1] * e[1] * R[3 * b + 1] + R[3 * a + 2] * e[2] * R[3 * b + 2]);
   }
   double alpha = 1.0 / (1.0 + exp(-(double)lg[i]));  // core.py:21-26
-  rec[0] = make_float4(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], (float)alpha);
-  rec[1] = make_float4((float)P[0], (float)P[1], (float)P[2], (float)P[3]);
-  rec[2] = make_float4((float)P[4], (float)P[5], 0.f, 0.f);
+  rec.A[p] = make_float4(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], (float)alpha);
+  rec.B[p] = make_float4((float)P[0], (float)P[1], (float)P[2], (float)P[3]);
+  rec.C[p] = make_float2((float)P[4], (float)P[5]);
 }
 
 __global__ void gauss_activate_kernel(const float* __restrict__ pos, const float* __restrict__ quat,
                                       const float* __restrict__ ls, const float* __restrict__ lg,
-                                      const int* __restrict__ order, int64_t n, float4* __restrict__ grec,
+                                      const int* __restrict__ order, int64_t n, GaussOut grec,
                                       int* __restrict__ err) {
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
     int64_t i = order ? order[p] : p;
-    activate_one(pos, quat, ls, lg, i, grec + 3 * p, err);
+    activate_one(pos, quat, ls, lg, i, grec, p, err);
   }
 }
 
@@ -101,14 +102,14 @@ __global__ void gauss_activate_kernel(const float* __restrict__ pos, const float
 // reference kernel ABI (_kernels.py:24-27) hands these in already activated.
 __global__ void gauss_pack_prepared_kernel(const double* __restrict__ mu, const double* __restrict__ prec6,
                                            const double* __restrict__ alpha, const int* __restrict__ order,
-                                           int64_t n, float4* __restrict__ grec) {
+                                           int64_t n, GaussOut grec) {
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
     int64_t i = order[p];
     const double* P = prec6 + 6 * i;
-    grec[3 * p + 0] = make_float4((float)mu[3 * i], (float)mu[3 * i + 1], (float)mu[3 * i + 2], (float)alpha[i]);
-    grec[3 * p + 1] = make_float4((float)(kMScaleD * P[0]), (float)(kMScaleD * P[3]), (float)(kMScaleD * P[5]),
-                                  (float)(kMScaleD * P[1]));
-    grec[3 * p + 2] = make_float4((float)(kMScaleD * P[2]), (float)(kMScaleD * P[4]), 0.f, 0.f);
+    grec.A[p] = make_float4((float)mu[3 * i], (float)mu[3 * i + 1], (float)mu[3 * i + 2], (float)alpha[i]);
+    grec.B[p] = make_float4((float)(kMScaleD * P[0]), (float)(kMScaleD * P[3]), (float)(kMScaleD * P[5]),
+                            (float)(kMScaleD * P[1]));
+    grec.C[p] = make_float2((float)(kMScaleD * P[2]), (float)(kMScaleD * P[4]));
   }
 }
 
@@ -193,9 +194,10 @@ __global__ void item_compact_kernel(const int* __restrict__ flags, const int* __
 // ---------------------------------------------------------------------------
 struct Window {
   int ilo, jlo, klo, khi, nj, ncol;
+  float inv_nj;  // exact column -> (i, j) split for ncol < 2^22
 };
 
-__device__ __forceinline__ Window make_window(int cell, int g, int r) {
+__device__ __noinline__ Window make_window(int cell, int g, int r) {
   int ck = cell % g;
   int t = cell / g;
   int cj = t % g;
@@ -209,6 +211,7 @@ __device__ __forceinline__ Window make_window(int cell, int g, int r) {
   w.khi = min(ck + r, g - 1);
   w.nj = jhi - w.jlo + 1;
   w.ncol = (ihi - w.ilo + 1) * w.nj;
+  w.inv_nj = 1.0f / (float)w.nj;
   return w;
 }
 
@@ -267,6 +270,7 @@ struct SegSmem {
   int pre[132];
   int delta[128];
   uint32_t bits[kBmWords];
+  __align__(16) float pts[3][8];  // an item's sub-points, coordinate-major (pairs load as 64-bit)
 };
 
 // Per-lane copy of its 4 columns' (pre, len, start) for window rebuilds.
@@ -276,8 +280,8 @@ struct LaneSegs {
   int tot;
 };
 
-__device__ __forceinline__ LaneSegs build_lane_segs(const Window& w, int c0, int g, const int* __restrict__ starts,
-                                                    SegSmem& sm, int lane) {
+__device__ __noinline__ LaneSegs build_lane_segs(const Window& w, int c0, int g, const int* __restrict__ starts,
+                                                 SegSmem& sm, int lane) {
   LaneSegs L;
   int sum = 0, ne = 0;
 #pragma unroll
@@ -286,8 +290,9 @@ __device__ __forceinline__ LaneSegs build_lane_segs(const Window& w, int c0, int
     L.st[k] = 0;
     L.len[k] = 0;
     if (col < w.ncol) {
-      int ii = w.ilo + col / w.nj;
-      int jj = w.jlo + col % w.nj;
+      const int q = (int)(((float)col + 0.5f) * w.inv_nj);  // == col / nj (exact for small ints)
+      int ii = w.ilo + q;
+      int jj = w.jlo + (col - q * w.nj);
       int base = (ii * g + jj) * g;
       int a = __ldg(starts + base + w.klo);
       int b = __ldg(starts + base + w.khi + 1);
@@ -317,7 +322,7 @@ __device__ __forceinline__ LaneSegs build_lane_segs(const Window& w, int c0, int
 
 // Fill the bitmap for flattened window [w0, w0 + 32*kBmWords); returns the
 // number of non-empty segments that start before w0 (the window's seg base).
-__device__ __forceinline__ int build_window(const LaneSegs& L, int w0, SegSmem& sm, int lane) {
+__device__ __noinline__ int build_window(const LaneSegs& L, int w0, SegSmem& sm, int lane) {
 #pragma unroll
   for (int i = 0; i < kBmWords / 32; ++i) sm.bits[lane + 32 * i] = 0u;
   __syncwarp();
@@ -386,34 +391,89 @@ __device__ __forceinline__ void write_point_out(float4* __restrict__ out4, int* 
 
 // ---------------------------------------------------------------------------
 // Forward: one warp per (point cell, <= Q sub-points of that cell); lanes
-// stride over the flattened candidate Gaussians (prefetching the next
-// record while computing the current one); the item's sub-points are
-// warp-uniform and packed two per f32x2 register (Gaussian parameters go in
-// as scalar-broadcast FFMA2 operands).  Every point of an item shares the
-// exact candidate set, so contributor_counts is the total candidate count.
+// stride over the flattened candidate Gaussians, two per lane per 64-wide
+// window, with the next window's records prefetched while the current one
+// is evaluated.  The item's sub-points are warp-uniform and packed two per
+// f32x2 register; Gaussian parameters enter FFMA2 as scalar-broadcast
+// operands.  Every sub-point of an item shares the exact candidate set, so
+// contributor_counts is the item's total candidate count.
 // ---------------------------------------------------------------------------
 #ifndef MG_FWD_MINB
-#define MG_FWD_MINB 4
+#define MG_FWD_MINB 3
 #endif
 #ifndef MG_BWD_MINB
-#define MG_BWD_MINB 4
+#define MG_BWD_MINB 2
 #endif
-constexpr int kFwdWarps = 4;
+#ifndef MG_FWD_QMAX
+#define MG_FWD_QMAX 4
+#endif
+#ifndef MG_FWD_WARPS
+#define MG_FWD_WARPS 8
+#endif
+#ifndef MG_BWD_WARPS
+#define MG_BWD_WARPS 8
+#endif
+constexpr int kFwdWarps = MG_FWD_WARPS;
+
+struct GRec {
+  float4 A, B;  // {mu, alpha}, {P'00, P'11, P'22, P'01}
+  float2 C;     // {P'02, P'12}
+};
+
+__device__ __forceinline__ GRec load_rec(const GaussSoA& grec, int gi) {
+  GRec r;
+  r.A = __ldg(grec.A + gi);
+  r.B = __ldg(grec.B + gi);
+  r.C = __ldg(grec.C + gi);
+  return r;
+}
+
+// Flattened-window cursor, one candidate per lane per 32-wide window.
+struct Cursor1 {
+  int sbase;
+  __device__ __forceinline__ void next(const SegSmem& sm, int w0, int base, unsigned upto, int lane, int& va,
+                                       int& ga) {
+    const uint32_t M0 = sm.bits[(base - w0) >> 5];
+    va = base + lane;
+    const int sega = sbase + __popc(M0 & upto) - 1;
+    sbase += __popc(M0);
+    ga = va + sm.delta[sega];
+  }
+};
+
+// Flattened-window cursor: lanes take va = base + lane and vb = va + 32.
+struct Cursor2 {
+  int sbase;
+  __device__ __forceinline__ void next(const SegSmem& sm, int w0, int base, unsigned upto, int lane, int& va, int& vb,
+                                       int& ga, int& gb) {
+    const int wi = (base - w0) >> 5;
+    const uint32_t M0 = sm.bits[wi], M1 = sm.bits[wi + 1];
+    va = base + lane;
+    vb = va + 32;
+    const int p0 = __popc(M0);
+    const int sega = sbase + __popc(M0 & upto) - 1;
+    const int segb = sbase + p0 + __popc(M1 & upto) - 1;
+    sbase += p0 + __popc(M1);
+    ga = va + sm.delta[sega];
+    gb = vb + sm.delta[segb];
+  }
+};
 
 template <int QP, bool WITH_H>
-__device__ __forceinline__ void fwd_pair_math(const float4& A, const float4& B, const float4& C, const f2 (&px)[QP],
-                                              const f2 (&py)[QP], const f2 (&pz)[QP], f2 (&accI)[QP], f2 (&hx)[QP],
-                                              f2 (&hy)[QP], f2 (&hz)[QP]) {
-  const float p00 = B.x, p11 = B.y, p22 = B.z, p01 = B.w, p02 = C.x, p12 = C.y;
+__device__ __forceinline__ void fwd_pair_math(const GRec& g, const f2 (&px)[QP], const f2 (&py)[QP],
+                                              const f2 (&pz)[QP], f2 (&accI)[QP], f2 (&hx)[QP], f2 (&hy)[QP],
+                                              f2 (&hz)[QP]) {
+  const float p00 = g.B.x, p11 = g.B.y, p22 = g.B.z, p01 = g.B.w, p02 = g.C.x, p12 = g.C.y;
+  const f2 mx = bc2(g.A.x), my = bc2(g.A.y), mz = bc2(g.A.z), al = bc2(g.A.w);
   if (WITH_H) {
 #pragma unroll
     for (int q = 0; q < QP; ++q) {
-      f2 dx = sub2(px[q], bc2(A.x)), dy = sub2(py[q], bc2(A.y)), dz = sub2(pz[q], bc2(A.z));
+      f2 dx = sub2(px[q], mx), dy = sub2(py[q], my), dz = sub2(pz[q], mz);
       f2 pdx = fma2(bc2(p02), dz, fma2(bc2(p01), dy, mul2(bc2(p00), dx)));
       f2 pdy = fma2(bc2(p12), dz, fma2(bc2(p11), dy, mul2(bc2(p01), dx)));
       f2 pdz = fma2(bc2(p22), dz, fma2(bc2(p12), dy, mul2(bc2(p02), dx)));
       f2 m = fma2(dz, pdz, fma2(dy, pdy, mul2(dx, pdx)));
-      f2 wv = mul2(bc2(A.w), mk2(gauss_w(m.x), gauss_w(m.y)));
+      f2 wv = mul2(al, gauss_w2(m));
       accI[q] = add2(accI[q], wv);
       hx[q] = fma2(wv, pdx, hx[q]);
       hy[q] = fma2(wv, pdy, hy[q]);
@@ -423,38 +483,49 @@ __device__ __forceinline__ void fwd_pair_math(const float4& A, const float4& B, 
     const float a01 = 2.f * p01, a02 = 2.f * p02, a12 = 2.f * p12;
 #pragma unroll
     for (int q = 0; q < QP; ++q) {
-      f2 dx = sub2(px[q], bc2(A.x)), dy = sub2(py[q], bc2(A.y)), dz = sub2(pz[q], bc2(A.z));
+      f2 dx = sub2(px[q], mx), dy = sub2(py[q], my), dz = sub2(pz[q], mz);
       f2 t1 = fma2(bc2(a02), dz, fma2(bc2(a01), dy, mul2(bc2(p00), dx)));
       f2 m = mul2(dx, t1);
       f2 t2 = fma2(bc2(a12), dz, mul2(bc2(p11), dy));
       m = fma2(dy, t2, m);
       m = fma2(dz, mul2(bc2(p22), dz), m);
-      accI[q] = fma2(bc2(A.w), mk2(gauss_w(m.x), gauss_w(m.y)), accI[q]);
+      accI[q] = fma2(al, gauss_w2(m), accI[q]);
     }
   }
 }
 
 template <int Q, bool WITH_H>
-__device__ __forceinline__ void fwd_item(const float4* __restrict__ grec, const int* __restrict__ gstart, int g, int r,
+__device__ __forceinline__ void fwd_item(const GaussSoA grec, const int* __restrict__ gstart, int g, int r,
                                          const float4* __restrict__ prec, int p0, int np, int cell,
                                          float4* __restrict__ out4, int* __restrict__ cnt_out, SegSmem& sm,
                                          int lane) {
   constexpr int QP = Q / 2;
+  // candidates per lane per window: with >= 2 point pairs there are already
+  // >= 2 independent chains per candidate, so one suffices (keeps registers
+  // for the ping-pong prefetch); with one pair, take two.
+  constexpr int GPL = QP >= 2 ? 1 : 2;
+  constexpr int WIN = 32 * GPL;
+  // stage the item's sub-points coordinate-major in shared memory and read
+  // them back as 64-bit pairs: the f32x2 operands then sit in aligned
+  // register pairs for the whole loop (no re-pairing moves per use)
+  if (lane < Q) {
+    const float4 a = prec[p0 + min(lane, np - 1)];
+    sm.pts[0][lane] = a.x;
+    sm.pts[1][lane] = a.y;
+    sm.pts[2][lane] = a.z;
+  }
+  __syncwarp();
   f2 px[QP], py[QP], pz[QP];
 #pragma unroll
   for (int q = 0; q < QP; ++q) {
-    float4 a = prec[p0 + min(2 * q, np - 1)];
-    float4 b = prec[p0 + min(2 * q + 1, np - 1)];
-    px[q] = mk2(a.x, b.x);
-    py[q] = mk2(a.y, b.y);
-    pz[q] = mk2(a.z, b.z);
+    px[q].v = *reinterpret_cast<const unsigned long long*>(&sm.pts[0][2 * q]);
+    py[q].v = *reinterpret_cast<const unsigned long long*>(&sm.pts[1][2 * q]);
+    pz[q].v = *reinterpret_cast<const unsigned long long*>(&sm.pts[2][2 * q]);
   }
+  __syncwarp();
   f2 accI[QP], hx[QP], hy[QP], hz[QP];
 #pragma unroll
-  for (int q = 0; q < QP; ++q) {
-    accI[q] = bc2(0.f);
-    hx[q] = hy[q] = hz[q] = bc2(0.f);
-  }
+  for (int q = 0; q < QP; ++q) accI[q] = hx[q] = hy[q] = hz[q] = bc2(0.f);
   const Window w = make_window(cell, g, r);
   const unsigned upto = 0xffffffffu >> (31 - lane);  // bits 0..lane
   int total = 0;
@@ -463,36 +534,43 @@ __device__ __forceinline__ void fwd_item(const float4* __restrict__ grec, const 
     const int tot = L.tot;
     total += tot;
     for (int w0 = 0; w0 < tot; w0 += 32 * kBmWords) {
-      int sbase = build_window(L, w0, sm, lane);
+      const int sb0 = build_window(L, w0, sm, lane);
       const int wend = min(tot, w0 + 32 * kBmWords);
-      for (int base = w0; base < wend; base += 32) {
-        const uint32_t M = sm.bits[(base - w0) >> 5];
-        const int v = base + lane;
-        const int seg = sbase + __popc(M & upto) - 1;
-        sbase += __popc(M);
-        if (v < wend) {
-          const int gi = v + sm.delta[seg];
-          const float4 A = __ldg(grec + 3 * gi);
-          const float4 B = __ldg(grec + 3 * gi + 1);
-          const float4 C = __ldg(grec + 3 * gi + 2);
-          fwd_pair_math<QP, WITH_H>(A, B, C, px, py, pz, accI, hx, hy, hz);
+      // one compact loop (small code: the kernel is instruction-cache bound
+      // when several unrolled paths are live on one SM)
+      if (GPL == 1) {
+        Cursor1 cur{sb0};
+        for (int base = w0; base < wend; base += WIN) {
+          int va, ga;
+          cur.next(sm, w0, base, upto, lane, va, ga);
+          if (va < wend) fwd_pair_math<QP, WITH_H>(load_rec(grec, ga), px, py, pz, accI, hx, hy, hz);
+        }
+      } else {
+        Cursor2 cur{sb0};
+        for (int base = w0; base < wend; base += WIN) {
+          int va, vb, ga, gb;
+          cur.next(sm, w0, base, upto, lane, va, vb, ga, gb);
+          const GRec ra = load_rec(grec, va < wend ? ga : 0);
+          const GRec rb = load_rec(grec, vb < wend ? gb : 0);
+          if (va < wend) fwd_pair_math<QP, WITH_H>(ra, px, py, pz, accI, hx, hy, hz);
+          if (vb < wend) fwd_pair_math<QP, WITH_H>(rb, px, py, pz, accI, hx, hy, hz);
         }
       }
       __syncwarp();
     }
   }
-  constexpr int NV = 4 * Q;  // 8, 16 or 32
+  constexpr int NV = 4 * Q;  // 8 or 16 (32 at Q = 8)
   float vals[32];
 #pragma unroll
   for (int q = 0; q < QP; ++q) {
-    vals[8 * q + 0] = accI[q].x;
-    vals[8 * q + 1] = hx[q].x;
-    vals[8 * q + 2] = hy[q].x;
-    vals[8 * q + 3] = hz[q].x;
-    vals[8 * q + 4] = accI[q].y;
-    vals[8 * q + 5] = hx[q].y;
-    vals[8 * q + 6] = hy[q].y;
-    vals[8 * q + 7] = hz[q].y;
+    vals[8 * q + 0] = lo(accI[q]);
+    vals[8 * q + 1] = lo(hx[q]);
+    vals[8 * q + 2] = lo(hy[q]);
+    vals[8 * q + 3] = lo(hz[q]);
+    vals[8 * q + 4] = hi(accI[q]);
+    vals[8 * q + 5] = hi(hx[q]);
+    vals[8 * q + 6] = hi(hy[q]);
+    vals[8 * q + 7] = hi(hz[q]);
   }
 #pragma unroll
   for (int i = NV; i < 32; ++i) vals[i] = 0.f;
@@ -503,16 +581,42 @@ __device__ __forceinline__ void fwd_item(const float4* __restrict__ grec, const 
   if ((lane & ((1 << SH) - 1)) == 0 && q < np) write_point_out(out4, cnt_out, p0 + q, comp, red, total);
 }
 
-// np == 1: the single sub-point is broadcast and each lane packs TWO
-// candidate Gaussians (v and v + 32) into the f32x2 lanes.
+// np == 1: the single sub-point is broadcast; each lane packs its TWO
+// candidates of the window (va, vb) into the two f32x2 halves.
 template <bool WITH_H>
-__device__ __forceinline__ void fwd_item_single(const float4* __restrict__ grec, const int* __restrict__ gstart, int g,
+__device__ __forceinline__ void single_math(const GRec& a, const GRec& b, bool hb, f2 X, f2 Y, f2 Z, f2& accI,
+                                            f2& hx, f2& hy, f2& hz) {
+  const f2 dx = sub2(X, mk2(a.A.x, b.A.x)), dy = sub2(Y, mk2(a.A.y, b.A.y)), dz = sub2(Z, mk2(a.A.z, b.A.z));
+  const f2 p00 = mk2(a.B.x, b.B.x), p11 = mk2(a.B.y, b.B.y), p22 = mk2(a.B.z, b.B.z), p01 = mk2(a.B.w, b.B.w),
+           p02 = mk2(a.C.x, b.C.x), p12 = mk2(a.C.y, b.C.y);
+  const f2 al = mk2(a.A.w, hb ? b.A.w : 0.f);
+  if (WITH_H) {
+    f2 pdx = fma2(p02, dz, fma2(p01, dy, mul2(p00, dx)));
+    f2 pdy = fma2(p12, dz, fma2(p11, dy, mul2(p01, dx)));
+    f2 pdz = fma2(p22, dz, fma2(p12, dy, mul2(p02, dx)));
+    f2 m = fma2(dz, pdz, fma2(dy, pdy, mul2(dx, pdx)));
+    f2 wv = mul2(al, gauss_w2(m));
+    accI = add2(accI, wv);
+    hx = fma2(wv, pdx, hx);
+    hy = fma2(wv, pdy, hy);
+    hz = fma2(wv, pdz, hz);
+  } else {
+    f2 t1 = fma2(add2(p02, p02), dz, fma2(add2(p01, p01), dy, mul2(p00, dx)));
+    f2 m = mul2(dx, t1);
+    m = fma2(dy, fma2(add2(p12, p12), dz, mul2(p11, dy)), m);
+    m = fma2(dz, mul2(p22, dz), m);
+    accI = fma2(al, gauss_w2(m), accI);
+  }
+}
+
+template <bool WITH_H>
+__device__ __forceinline__ void fwd_item_single(const GaussSoA grec, const int* __restrict__ gstart, int g,
                                                 int r, const float4* __restrict__ prec, int p0, int cell,
                                                 float4* __restrict__ out4, int* __restrict__ cnt_out, SegSmem& sm,
                                                 int lane) {
   const float4 pt = prec[p0];
   const f2 X = bc2(pt.x), Y = bc2(pt.y), Z = bc2(pt.z);
-  f2 accI = bc2(0.f), hx = bc2(0.f), hy = bc2(0.f), hz = bc2(0.f);
+  f2 accI = bc2(0.f), hx = accI, hy = accI, hz = accI;
   const Window w = make_window(cell, g, r);
   const unsigned upto = 0xffffffffu >> (31 - lane);
   int total = 0;
@@ -521,52 +625,26 @@ __device__ __forceinline__ void fwd_item_single(const float4* __restrict__ grec,
     const int tot = L.tot;
     total += tot;
     for (int w0 = 0; w0 < tot; w0 += 32 * kBmWords) {
-      int sbase = build_window(L, w0, sm, lane);
+      Cursor2 cur{build_window(L, w0, sm, lane)};
       const int wend = min(tot, w0 + 32 * kBmWords);
       for (int base = w0; base < wend; base += 64) {
-        const uint32_t M0 = sm.bits[(base - w0) >> 5];
-        const uint32_t M1 = sm.bits[((base - w0) >> 5) + 1];
-        const int va = base + lane, vb = va + 32;
-        const int sega = sbase + __popc(M0 & upto) - 1;
-        const int segb = sbase + __popc(M0) + __popc(M1 & upto) - 1;
-        sbase += __popc(M0) + __popc(M1);
+        int va, vb, ga, gb;
+        cur.next(sm, w0, base, upto, lane, va, vb, ga, gb);
         if (va < wend) {
           const bool hb = vb < wend;
-          const int ga = va + sm.delta[sega];
-          const int gb = hb ? vb + sm.delta[segb] : ga;
-          const float4 Aa = __ldg(grec + 3 * ga), Ba = __ldg(grec + 3 * ga + 1), Ca = __ldg(grec + 3 * ga + 2);
-          const float4 Ab = __ldg(grec + 3 * gb), Bb = __ldg(grec + 3 * gb + 1), Cb = __ldg(grec + 3 * gb + 2);
-          const f2 dx = sub2(X, mk2(Aa.x, Ab.x)), dy = sub2(Y, mk2(Aa.y, Ab.y)), dz = sub2(Z, mk2(Aa.z, Ab.z));
-          const f2 p00 = mk2(Ba.x, Bb.x), p11 = mk2(Ba.y, Bb.y), p22 = mk2(Ba.z, Bb.z), p01 = mk2(Ba.w, Bb.w),
-                   p02 = mk2(Ca.x, Cb.x), p12 = mk2(Ca.y, Cb.y);
-          const f2 al = mk2(Aa.w, hb ? Ab.w : 0.f);
-          if (WITH_H) {
-            f2 pdx = fma2(p02, dz, fma2(p01, dy, mul2(p00, dx)));
-            f2 pdy = fma2(p12, dz, fma2(p11, dy, mul2(p01, dx)));
-            f2 pdz = fma2(p22, dz, fma2(p12, dy, mul2(p02, dx)));
-            f2 m = fma2(dz, pdz, fma2(dy, pdy, mul2(dx, pdx)));
-            f2 wv = mul2(al, mk2(gauss_w(m.x), gauss_w(m.y)));
-            accI = add2(accI, wv);
-            hx = fma2(wv, pdx, hx);
-            hy = fma2(wv, pdy, hy);
-            hz = fma2(wv, pdz, hz);
-          } else {
-            f2 t1 = fma2(add2(p02, p02), dz, fma2(add2(p01, p01), dy, mul2(p00, dx)));
-            f2 m = mul2(dx, t1);
-            m = fma2(dy, fma2(add2(p12, p12), dz, mul2(p11, dy)), m);
-            m = fma2(dz, mul2(p22, dz), m);
-            accI = fma2(al, mk2(gauss_w(m.x), gauss_w(m.y)), accI);
-          }
+          const GRec ra = load_rec(grec, ga);
+          const GRec rb = load_rec(grec, hb ? gb : ga);
+          single_math<WITH_H>(ra, rb, hb, X, Y, Z, accI, hx, hy, hz);
         }
       }
       __syncwarp();
     }
   }
   float vals[32];
-  vals[0] = accI.x + accI.y;
-  vals[1] = hx.x + hx.y;
-  vals[2] = hy.x + hy.y;
-  vals[3] = hz.x + hz.y;
+  vals[0] = lo(accI) + hi(accI);
+  vals[1] = lo(hx) + hi(hx);
+  vals[2] = lo(hy) + hi(hy);
+  vals[3] = lo(hz) + hi(hz);
 #pragma unroll
   for (int i = 4; i < 32; ++i) vals[i] = 0.f;
   const float red = transpose_reduce<4>(vals, lane);
@@ -575,7 +653,7 @@ __device__ __forceinline__ void fwd_item_single(const float4* __restrict__ grec,
 }
 
 template <bool WITH_H>
-__global__ void __launch_bounds__(kFwdWarps * 32, MG_FWD_MINB) forward_kernel(const float4* __restrict__ grec,
+__global__ void __launch_bounds__(kFwdWarps * 32, MG_FWD_MINB) forward_kernel(const GaussSoA grec,
                                                                  const int* __restrict__ gstart, int g, int r,
                                                                  const float4* __restrict__ prec,
                                                                  const uint32_t* __restrict__ pkey,
@@ -589,9 +667,10 @@ __global__ void __launch_bounds__(kFwdWarps * 32, MG_FWD_MINB) forward_kernel(co
   for (int it = blockIdx.x * kFwdWarps + warp; it < nitems; it += gridDim.x * kFwdWarps) {
     const int p0 = items[it];
     const int cell = (int)pkey[p0];
-    const int np = min(8, pstart[cell + 1] - p0);
-    if (np > 4)
-      fwd_item<8, WITH_H>(grec, gstart, g, r, prec, p0, np, cell, out4, cnt_out, s_seg[warp], lane);
+    const int np = min(MG_FWD_QMAX, pstart[cell + 1] - p0);
+    if (MG_FWD_QMAX > 4 && np > 4)
+      fwd_item<(MG_FWD_QMAX > 4 ? 8 : 4), WITH_H>(grec, gstart, g, r, prec, p0, np, cell, out4, cnt_out,
+                                                 s_seg[warp], lane);
     else if (np > 2)
       fwd_item<4, WITH_H>(grec, gstart, g, r, prec, p0, np, cell, out4, cnt_out, s_seg[warp], lane);
     else if (np == 2)
@@ -603,88 +682,137 @@ __global__ void __launch_bounds__(kFwdWarps * 32, MG_FWD_MINB) forward_kernel(co
 
 // ---------------------------------------------------------------------------
 // Backward, Gaussian-major: one warp per (Gaussian cell, <= 2 Gaussians of
-// that cell); lanes stride over the flattened candidate sub-points, two
-// consecutive ones per lane packed in f32x2, next pair prefetched.  Per
-// Gaussian it accumulates (register-resident, no atomics):
+// that cell); lanes stride over the flattened candidate sub-points, four per
+// lane per 128-wide window as two f32x2 pairs (v, v+1) and (v+64, v+65), the
+// next window's points prefetched.  Per Gaussian it accumulates
+// (register-resident, no atomics):
 //   S = sum u*g,  T = sum u*g*(P'd),  A6 = sum u*g*(d d^T)
 // and the epilogue forms d_alpha = S, d_mu = alpha*T/kMScale,
 // d_abar6 = -0.5*alpha*A6 (_kernels.py:118-141).
 // ---------------------------------------------------------------------------
-constexpr int kBwdWarps = 4;
+constexpr int kBwdWarps = MG_BWD_WARPS;
+
+struct Pts4 {
+  float4 p[4];
+};
+
+// Flattened-window cursor for 128-wide windows: lane owns v_i = base + 32 i +
+// lane (i = 0..3), so each warp-wide point load reads 512 contiguous bytes.
+struct Cursor4 {
+  int sbase;
+  __device__ __forceinline__ void next(const SegSmem& sm, int w0, int base, unsigned upto, int lane, int (&v)[4],
+                                       int (&e)[4]) {
+    const int wi = (base - w0) >> 5;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t M = sm.bits[wi + i];
+      v[i] = base + 32 * i + lane;
+      e[i] = v[i] + sm.delta[sbase + __popc(M & upto) - 1];
+      sbase += __popc(M);
+    }
+  }
+};
 
 template <int QG>
-__device__ __forceinline__ void bwd_item(const float4* __restrict__ grec, int g0, int ng, int cell, int g, int r,
+struct GaussAcc {
+  float mx[QG], my[QG], mz[QG], P[QG][6];
+  f2 S[QG], T[QG][3], A6[QG][6];
+
+  __device__ __forceinline__ void pair(const float4& a, const float4& b) {
+    const f2 px = mk2(a.x, b.x), py = mk2(a.y, b.y), pz = mk2(a.z, b.z), u = mk2(a.w, b.w);
+#pragma unroll
+    for (int k = 0; k < QG; ++k) {
+      f2 dx = sub2(px, bc2(mx[k])), dy = sub2(py, bc2(my[k])), dz = sub2(pz, bc2(mz[k]));
+      f2 pdx = fma2(bc2(P[k][4]), dz, fma2(bc2(P[k][3]), dy, mul2(bc2(P[k][0]), dx)));
+      f2 pdy = fma2(bc2(P[k][5]), dz, fma2(bc2(P[k][1]), dy, mul2(bc2(P[k][3]), dx)));
+      f2 pdz = fma2(bc2(P[k][2]), dz, fma2(bc2(P[k][5]), dy, mul2(bc2(P[k][4]), dx)));
+      f2 m = fma2(dz, pdz, fma2(dy, pdy, mul2(dx, pdx)));
+      f2 ug = mul2(u, gauss_w2(m));
+      S[k] = add2(S[k], ug);
+      T[k][0] = fma2(ug, pdx, T[k][0]);
+      T[k][1] = fma2(ug, pdy, T[k][1]);
+      T[k][2] = fma2(ug, pdz, T[k][2]);
+      f2 cx = mul2(ug, dx), cy = mul2(ug, dy), cz = mul2(ug, dz);
+      A6[k][0] = fma2(cx, dx, A6[k][0]);
+      A6[k][1] = fma2(cx, dy, A6[k][1]);
+      A6[k][2] = fma2(cx, dz, A6[k][2]);
+      A6[k][3] = fma2(cy, dy, A6[k][3]);
+      A6[k][4] = fma2(cy, dz, A6[k][4]);
+      A6[k][5] = fma2(cz, dz, A6[k][5]);
+    }
+  }
+};
+
+template <int QG>
+__device__ __forceinline__ void bwd_item(const GaussSoA grec, int g0, int ng, int cell, int g, int r,
                                          const float4* __restrict__ prec, const int* __restrict__ pstart,
                                          float* __restrict__ acc10, SegSmem& sm, int lane) {
-  float mx[QG], my[QG], mz[QG], P[QG][6];
+  GaussAcc<QG> acc;
 #pragma unroll
   for (int k = 0; k < QG; ++k) {
     int gi = g0 + min(k, ng - 1);
-    float4 A = grec[3 * gi], B = grec[3 * gi + 1], C = grec[3 * gi + 2];
-    mx[k] = A.x;
-    my[k] = A.y;
-    mz[k] = A.z;
-    P[k][0] = B.x;  // P00
-    P[k][1] = B.y;  // P11
-    P[k][2] = B.z;  // P22
-    P[k][3] = B.w;  // P01
-    P[k][4] = C.x;  // P02
-    P[k][5] = C.y;  // P12
-  }
-  f2 S[QG], T[QG][3], A6[QG][6];
+    const float4 A = grec.A[gi], B = grec.B[gi];
+    const float2 C = grec.C[gi];
+    acc.mx[k] = A.x;
+    acc.my[k] = A.y;
+    acc.mz[k] = A.z;
+    acc.P[k][0] = B.x;  // P00
+    acc.P[k][1] = B.y;  // P11
+    acc.P[k][2] = B.z;  // P22
+    acc.P[k][3] = B.w;  // P01
+    acc.P[k][4] = C.x;  // P02
+    acc.P[k][5] = C.y;  // P12
+    acc.S[k] = bc2(0.f);
 #pragma unroll
-  for (int k = 0; k < QG; ++k) {
-    S[k] = bc2(0.f);
+    for (int c = 0; c < 3; ++c) acc.T[k][c] = bc2(0.f);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) T[k][c] = bc2(0.f);
-#pragma unroll
-    for (int c = 0; c < 6; ++c) A6[k][c] = bc2(0.f);
+    for (int c = 0; c < 6; ++c) acc.A6[k][c] = bc2(0.f);
   }
   const Window w = make_window(cell, g, r);
-  const int la = 2 * lane;
-  const uint64_t upto_a = (la == 63) ? ~0ull : ((2ull << la) - 1ull);
+  const unsigned upto = 0xffffffffu >> (31 - lane);  // bits 0..lane
   for (int c0 = 0; c0 < w.ncol; c0 += 128) {
     const LaneSegs L = build_lane_segs(w, c0, g, pstart, sm, lane);
     const int tot = L.tot;
     for (int w0 = 0; w0 < tot; w0 += 32 * kBmWords) {
-      int sbase = build_window(L, w0, sm, lane);
+      Cursor4 cur{build_window(L, w0, sm, lane)};
       const int wend = min(tot, w0 + 32 * kBmWords);
-      for (int base = w0; base < wend; base += 64) {
-        const int wi = (base - w0) >> 5;
-        const uint64_t M = ((uint64_t)sm.bits[wi + 1] << 32) | (uint64_t)sm.bits[wi];
-        const int v = base + la;
-        const int sega = sbase + __popcll(M & upto_a) - 1;
-        const int segb = sega + (int)((M >> (la + 1)) & 1ull);
-        sbase += __popcll(M);
-        if (v < wend) {
-          const float4 a = __ldg(prec + v + sm.delta[sega]);
-          float4 b;
-          if (v + 1 < wend)
-            b = __ldg(prec + v + 1 + sm.delta[segb]);
-          else
-            b = make_float4(a.x, a.y, a.z, 0.f);  // dummy partner: zero upstream
-          const f2 px = mk2(a.x, b.x), py = mk2(a.y, b.y), pz = mk2(a.z, b.z), u = mk2(a.w, b.w);
+      const int nfull = (wend - w0) >> 7;
+      int v[4], e[4];
+      if (nfull > 0) {
+        // ping-pong register sets: window t+1 loads while window t computes
+        float4 q0[4], q1[4];
+        cur.next(sm, w0, w0, upto, lane, v, e);
 #pragma unroll
-          for (int k = 0; k < QG; ++k) {
-            f2 dx = sub2(px, bc2(mx[k])), dy = sub2(py, bc2(my[k])), dz = sub2(pz, bc2(mz[k]));
-            f2 pdx = fma2(bc2(P[k][4]), dz, fma2(bc2(P[k][3]), dy, mul2(bc2(P[k][0]), dx)));
-            f2 pdy = fma2(bc2(P[k][5]), dz, fma2(bc2(P[k][1]), dy, mul2(bc2(P[k][3]), dx)));
-            f2 pdz = fma2(bc2(P[k][2]), dz, fma2(bc2(P[k][5]), dy, mul2(bc2(P[k][4]), dx)));
-            f2 m = fma2(dz, pdz, fma2(dy, pdy, mul2(dx, pdx)));
-            f2 ug = mul2(u, mk2(gauss_w(m.x), gauss_w(m.y)));
-            S[k] = add2(S[k], ug);
-            T[k][0] = fma2(ug, pdx, T[k][0]);
-            T[k][1] = fma2(ug, pdy, T[k][1]);
-            T[k][2] = fma2(ug, pdz, T[k][2]);
-            f2 cx = mul2(ug, dx), cy = mul2(ug, dy), cz = mul2(ug, dz);
-            A6[k][0] = fma2(cx, dx, A6[k][0]);
-            A6[k][1] = fma2(cx, dy, A6[k][1]);
-            A6[k][2] = fma2(cx, dz, A6[k][2]);
-            A6[k][3] = fma2(cy, dy, A6[k][3]);
-            A6[k][4] = fma2(cy, dz, A6[k][4]);
-            A6[k][5] = fma2(cz, dz, A6[k][5]);
+        for (int i = 0; i < 4; ++i) q0[i] = __ldg(prec + e[i]);
+        for (int t = 0; t < nfull; t += 2) {
+          const bool h1 = t + 1 < nfull;
+          if (h1) {
+            cur.next(sm, w0, w0 + 128 * (t + 1), upto, lane, v, e);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) q1[i] = __ldg(prec + e[i]);
+          }
+          acc.pair(q0[0], q0[1]);
+          acc.pair(q0[2], q0[3]);
+          if (t + 2 < nfull) {
+            cur.next(sm, w0, w0 + 128 * (t + 2), upto, lane, v, e);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) q0[i] = __ldg(prec + e[i]);
+          }
+          if (h1) {
+            acc.pair(q1[0], q1[1]);
+            acc.pair(q1[2], q1[3]);
           }
         }
+      }
+      const int tb = w0 + (nfull << 7);
+      if (tb < wend) {  // ragged tail window: missing partners get zero upstream
+        cur.next(sm, w0, tb, upto, lane, v, e);
+        float4 pt[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) pt[i] = v[i] < wend ? __ldg(prec + e[i]) : make_float4(0.f, 0.f, 0.f, 0.f);
+        // v0 < v1 < v2 < v3: a missing partner carries zero upstream
+        if (v[0] < wend) acc.pair(pt[0], pt[1]);
+        if (v[2] < wend) acc.pair(pt[2], pt[3]);
       }
       __syncwarp();
     }
@@ -694,11 +822,11 @@ __device__ __forceinline__ void bwd_item(const float4* __restrict__ grec, int g0
   float vals[32];
 #pragma unroll
   for (int k = 0; k < QG; ++k) {
-    vals[16 * k + 0] = S[k].x + S[k].y;
+    vals[16 * k + 0] = lo(acc.S[k]) + hi(acc.S[k]);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) vals[16 * k + 1 + c] = T[k][c].x + T[k][c].y;
+    for (int c = 0; c < 3; ++c) vals[16 * k + 1 + c] = lo(acc.T[k][c]) + hi(acc.T[k][c]);
 #pragma unroll
-    for (int c = 0; c < 6; ++c) vals[16 * k + 4 + c] = A6[k][c].x + A6[k][c].y;
+    for (int c = 0; c < 6; ++c) vals[16 * k + 4 + c] = lo(acc.A6[k][c]) + hi(acc.A6[k][c]);
 #pragma unroll
     for (int c = 10; c < 16; ++c) vals[16 * k + c] = 0.f;
   }
@@ -711,7 +839,7 @@ __device__ __forceinline__ void bwd_item(const float4* __restrict__ grec, int g0
   if ((lane & ((1 << SH) - 1)) == 0 && c < 10 && k < ng) acc10[(int64_t)(g0 + k) * 10 + c] = red;
 }
 
-__global__ void __launch_bounds__(kBwdWarps * 32, MG_BWD_MINB) backward_kernel(const float4* __restrict__ grec,
+__global__ void __launch_bounds__(kBwdWarps * 32, MG_BWD_MINB) backward_kernel(const GaussSoA grec,
                                                                   const uint32_t* __restrict__ gkey,
                                                                   const int* __restrict__ gstart, int g, int r,
                                                                   const float4* __restrict__ prec,
@@ -762,12 +890,12 @@ void launch_gauss_keys_f64(const double* pos, int64_t n, int g, uint32_t* keys, 
   if (n > 0) gauss_keys_f64_kernel<<<grid_for(n), 256, 0, st>>>(pos, n, g, keys);
 }
 void launch_gauss_activate(const float* pos, const float* quat, const float* ls, const float* lg, const int* order,
-                           int64_t n, float4* grec, int* err, cudaStream_t st) {
-  if (n > 0) gauss_activate_kernel<<<grid_for(n), 256, 0, st>>>(pos, quat, ls, lg, order, n, grec, err);
+                           int64_t n, float* grec, int* err, cudaStream_t st) {
+  if (n > 0) gauss_activate_kernel<<<grid_for(n), 256, 0, st>>>(pos, quat, ls, lg, order, n, gauss_out(grec, n), err);
 }
 void launch_gauss_pack_prepared(const double* mu, const double* prec6, const double* alpha, const int* order,
-                                int64_t n, float4* grec, cudaStream_t st) {
-  if (n > 0) gauss_pack_prepared_kernel<<<grid_for(n), 256, 0, st>>>(mu, prec6, alpha, order, n, grec);
+                                int64_t n, float* grec, cudaStream_t st) {
+  if (n > 0) gauss_pack_prepared_kernel<<<grid_for(n), 256, 0, st>>>(mu, prec6, alpha, order, n, gauss_out(grec, n));
 }
 void launch_points_prepare(const double* coords, const int64_t* sids64, const int* sids32, int64_t b, int ntaps,
                            const double* tap_off, const double* dirs, const double* rot, const double* trans,
@@ -779,6 +907,8 @@ void launch_points_prepare(const double* coords, const int64_t* sids64, const in
 void launch_points_gather(const float4* xf, const int* perm, int64_t n, float4* prec, int* inv, cudaStream_t st) {
   if (n > 0) points_gather_kernel<<<grid_for(n), 256, 0, st>>>(xf, perm, n, prec, inv);
 }
+
+int fwd_qmax() { return MG_FWD_QMAX; }
 
 size_t items_workspace_bytes(int64_t n) { return 2 * (((size_t)n * 4 + 255) & ~(size_t)255) + scan_workspace_bytes(n); }
 
@@ -796,30 +926,41 @@ void build_items(const uint32_t* keys, const int* starts, int64_t n, int q, int*
   item_compact_kernel<<<grid_for(n), 256, 0, st>>>(flags, scan, n, items, nitems);
 }
 
-void launch_forward(bool with_h, const float4* grec, const int* gstart, int g, int r, const float4* prec,
+template <class K>
+static int64_t persistent_blocks(K kernel, int threads, int64_t max_blocks) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0);
+  if (per_sm < 1) per_sm = 1;
+  int64_t b = (int64_t)num_sms() * per_sm;
+  return b < max_blocks ? b : (max_blocks < 1 ? 1 : max_blocks);
+}
+
+void launch_forward(bool with_h, const float* grec_raw, int64_t n_gauss, const int* gstart, int g, int r,
+                    const float4* prec,
                     const uint32_t* pkey, const int* pstart, const int* items, const int* nitems, int64_t max_items,
                     float4* out4, int* cnt, cudaStream_t st) {
   if (max_items <= 0) return;
-  int64_t blocks = (max_items + kFwdWarps - 1) / kFwdWarps;
-  int64_t cap = (int64_t)num_sms() * 8;
-  if (blocks > cap) blocks = cap;
-  if (with_h)
-    forward_kernel<true><<<(unsigned)blocks, kFwdWarps * 32, 0, st>>>(grec, gstart, g, r, prec, pkey, pstart, items,
-                                                                      nitems, out4, cnt);
-  else
-    forward_kernel<false><<<(unsigned)blocks, kFwdWarps * 32, 0, st>>>(grec, gstart, g, r, prec, pkey, pstart, items,
-                                                                       nitems, out4, cnt);
+  const int64_t want = (max_items + kFwdWarps - 1) / kFwdWarps;
+  const GaussSoA grec = gauss_soa(grec_raw, n_gauss);
+  if (with_h) {
+    auto k = forward_kernel<true>;
+    forward_kernel<true><<<(unsigned)persistent_blocks(k, kFwdWarps * 32, want), kFwdWarps * 32, 0, st>>>(
+        grec, gstart, g, r, prec, pkey, pstart, items, nitems, out4, cnt);
+  } else {
+    auto k = forward_kernel<false>;
+    forward_kernel<false><<<(unsigned)persistent_blocks(k, kFwdWarps * 32, want), kFwdWarps * 32, 0, st>>>(
+        grec, gstart, g, r, prec, pkey, pstart, items, nitems, out4, cnt);
+  }
 }
 
-void launch_backward(const float4* grec, const uint32_t* gkey, const int* gstart, int g, int r, const float4* prec,
-                     const int* pstart, const int* items, const int* nitems, int64_t max_items, float* acc10,
-                     cudaStream_t st) {
+void launch_backward(const float* grec_raw, int64_t n_gauss, const uint32_t* gkey, const int* gstart, int g, int r,
+                     const float4* prec, const int* pstart, const int* items, const int* nitems, int64_t max_items,
+                     float* acc10, cudaStream_t st) {
   if (max_items <= 0) return;
-  int64_t blocks = (max_items + kBwdWarps - 1) / kBwdWarps;
-  int64_t cap = (int64_t)num_sms() * 8;
-  if (blocks > cap) blocks = cap;
-  backward_kernel<<<(unsigned)blocks, kBwdWarps * 32, 0, st>>>(grec, gkey, gstart, g, r, prec, pstart, items, nitems,
-                                                              acc10);
+  const GaussSoA grec = gauss_soa(grec_raw, n_gauss);
+  const int64_t want = (max_items + kBwdWarps - 1) / kBwdWarps;
+  backward_kernel<<<(unsigned)persistent_blocks(backward_kernel, kBwdWarps * 32, want), kBwdWarps * 32, 0, st>>>(
+      grec, gkey, gstart, g, r, prec, pstart, items, nitems, acc10);
 }
 
 }  // namespace mg

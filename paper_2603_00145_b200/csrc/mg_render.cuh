@@ -4,14 +4,15 @@
 
 namespace mg {
 int num_sms();
+int fwd_qmax();
 
 // preprocessing / binning
 void launch_gauss_keys(const float* pos, int64_t n, int g, uint32_t* keys, cudaStream_t st);
 void launch_gauss_keys_f64(const double* pos, int64_t n, int g, uint32_t* keys, cudaStream_t st);
 void launch_gauss_activate(const float* pos, const float* quat, const float* ls, const float* lg, const int* order,
-                           int64_t n, float4* grec, int* err, cudaStream_t st);
+                           int64_t n, float* grec, int* err, cudaStream_t st);
 void launch_gauss_pack_prepared(const double* mu, const double* prec6, const double* alpha, const int* order,
-                                int64_t n, float4* grec, cudaStream_t st);
+                                int64_t n, float* grec, cudaStream_t st);
 void launch_points_prepare(const double* coords, const int64_t* sids64, const int* sids32, int64_t b, int ntaps,
                            const double* tap_off, const double* dirs, const double* rot, const double* trans,
                            int nslices, int g, uint32_t* keys, float4* xf, double* xout, cudaStream_t st);
@@ -21,12 +22,13 @@ void build_items(const uint32_t* keys, const int* starts, int64_t n, int q, int*
                  cudaStream_t st);
 
 // pair kernels
-void launch_forward(bool with_h, const float4* grec, const int* gstart, int g, int r, const float4* prec,
+void launch_forward(bool with_h, const float* grec, int64_t n_gauss, const int* gstart, int g, int r,
+                    const float4* prec,
                     const uint32_t* pkey, const int* pstart, const int* items, const int* nitems, int64_t max_items,
                     float4* out4, int* cnt, cudaStream_t st);
-void launch_backward(const float4* grec, const uint32_t* gkey, const int* gstart, int g, int r, const float4* prec,
-                     const int* pstart, const int* items, const int* nitems, int64_t max_items, float* acc10,
-                     cudaStream_t st);
+void launch_backward(const float* grec, int64_t n_gauss, const uint32_t* gkey, const int* gstart, int g, int r,
+                     const float4* prec, const int* pstart, const int* items, const int* nitems, int64_t max_items,
+                     float* acc10, cudaStream_t st);
 
 // epilogues / training
 void launch_forward_finish(const float4* out4, const int* cnt, const int* inv, int64_t b, int ntaps,
@@ -60,7 +62,8 @@ void launch_upsample(const float* q_old, const float* s_old, const float* l_old,
 
 // inference
 size_t volume_workspace_bytes(int nx, int ny, int nz);
-void launch_sample_volume(const float4* grec, const int* gstart, int g, int r, const int dims[3], const double lo[3],
+void launch_sample_volume(const float* grec, int64_t n_gauss, const int* gstart, int g, int r, const int dims[3],
+                          const double lo[3],
                           const double hi[3], int i0, int i1, const float* residual, float* out, void* ws,
                           cudaStream_t st);
 }  // namespace mg

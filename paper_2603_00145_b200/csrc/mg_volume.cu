@@ -60,12 +60,13 @@ struct VolAxes {
 constexpr int kVolWarps = 4;
 
 template <int V>
-__device__ __forceinline__ void vol_chunk(const float4* __restrict__ grec, const int* __restrict__ gstart, int g,
+__device__ __forceinline__ void vol_chunk(const GaussSoA& grec, const int* __restrict__ gstart, int g,
                                           int r, const VolAxes& ax, int bx0, int by0, int bz0, int nbx, int nby,
                                           int nbz, int cell, int l0, int nvox, const float* __restrict__ residual,
                                           float* __restrict__ out, int64_t slab_i0, int lane) {
   constexpr int VP = V / 2;
   f2 px[VP], py[VP], pz[VP], acc[VP];
+  float cx[V], cy[V], cz[V];
   int vid[V];
   const int nyz = nby * nbz;
 #pragma unroll
@@ -78,15 +79,15 @@ __device__ __forceinline__ void vol_chunk(const float4* __restrict__ grec, const
     float y = (float)axis_coord(j, ax.n[1], ax.lo[1], ax.hi[1], ax.sp[1]);
     float z = (float)axis_coord(k, ax.n[2], ax.lo[2], ax.hi[2], ax.sp[2]);
     vid[v] = l < nvox ? ((i * ax.n[1] + j) * ax.n[2] + k) : -1;
-    if (v & 1) {
-      px[v / 2].y = x;
-      py[v / 2].y = y;
-      pz[v / 2].y = z;
-    } else {
-      px[v / 2].x = x;
-      py[v / 2].x = y;
-      pz[v / 2].x = z;
-    }
+    cx[v] = x;
+    cy[v] = y;
+    cz[v] = z;
+  }
+#pragma unroll
+  for (int q = 0; q < VP; ++q) {
+    px[q] = mk2(cx[2 * q], cx[2 * q + 1]);
+    py[q] = mk2(cy[2 * q], cy[2 * q + 1]);
+    pz[q] = mk2(cz[2 * q], cz[2 * q + 1]);
   }
 #pragma unroll
   for (int q = 0; q < VP; ++q) acc[q] = bc2(0.f);
@@ -99,7 +100,8 @@ __device__ __forceinline__ void vol_chunk(const float4* __restrict__ grec, const
       int base = (ii * g + jj) * g;
       int a = __ldg(gstart + base + klo), b = __ldg(gstart + base + khi + 1);
       for (int gi = a; gi < b; ++gi) {
-        const float4 A = __ldg(grec + 3 * gi), B = __ldg(grec + 3 * gi + 1), C = __ldg(grec + 3 * gi + 2);
+        const float4 A = __ldg(grec.A + gi), B = __ldg(grec.B + gi);
+        const float2 C = __ldg(grec.C + gi);
         const float a01 = 2.f * B.w, a02 = 2.f * C.x, a12 = 2.f * C.y;
 #pragma unroll
         for (int q = 0; q < VP; ++q) {
@@ -109,7 +111,7 @@ __device__ __forceinline__ void vol_chunk(const float4* __restrict__ grec, const
           f2 t2 = fma2(bc2(a12), dz, mul2(bc2(B.y), dy));
           m = fma2(dy, t2, m);
           m = fma2(dz, mul2(bc2(B.z), dz), m);
-          acc[q] = fma2(bc2(A.w), mk2(gauss_w(m.x), gauss_w(m.y)), acc[q]);
+          acc[q] = fma2(bc2(A.w), gauss_w2(m), acc[q]);
         }
       }
     }
@@ -117,7 +119,7 @@ __device__ __forceinline__ void vol_chunk(const float4* __restrict__ grec, const
 #pragma unroll
   for (int v = 0; v < V; ++v) {
     if (vid[v] >= 0) {
-      float val = (v & 1) ? acc[v / 2].y : acc[v / 2].x;
+      float val = (v & 1) ? hi(acc[v / 2]) : lo(acc[v / 2]);
       int64_t o = (int64_t)vid[v];
       if (residual) val += residual[o];
       val = fminf(fmaxf(val, 0.f), 1.f);
@@ -126,7 +128,7 @@ __device__ __forceinline__ void vol_chunk(const float4* __restrict__ grec, const
   }
 }
 
-__global__ void __launch_bounds__(kVolWarps * 32) volume_kernel(const float4* __restrict__ grec,
+__global__ void __launch_bounds__(kVolWarps * 32) volume_kernel(const GaussSoA grec,
                                                                 const int* __restrict__ gstart, int g, int r,
                                                                 VolAxes ax, const float* __restrict__ residual,
                                                                 float* __restrict__ out) {
@@ -161,7 +163,8 @@ size_t volume_workspace_bytes(int nx, int ny, int nz) {
 
 // Samples voxels [i0, i1) x [0, ny) x [0, nz); out is the slab (i1-i0, ny, nz),
 // float32, clipped to [0, 1].  residual (optional) is added before the clip.
-void launch_sample_volume(const float4* grec, const int* gstart, int g, int r, const int dims[3], const double lo[3],
+void launch_sample_volume(const float* grec_raw, int64_t n_gauss, const int* gstart, int g, int r, const int dims[3],
+                          const double lo[3],
                           const double hi[3], int i0, int i1, const float* residual, float* out, void* ws,
                           cudaStream_t st) {
   int n[3] = {dims[0], dims[1], dims[2]};
@@ -201,7 +204,8 @@ void launch_sample_volume(const float4* grec, const int* gstart, int g, int r, c
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   // write offsets: kernel computes vid relative to the slab (i in [0, i1-i0))
-  volume_kernel<<<(unsigned)blocks, kVolWarps * 32, 0, st>>>(grec, gstart, g, r, ax, residual, out);
+  volume_kernel<<<(unsigned)blocks, kVolWarps * 32, 0, st>>>(gauss_soa(grec_raw, n_gauss), gstart, g, r, ax, residual,
+                                                              out);
 }
 
 }  // namespace mg

@@ -227,7 +227,8 @@ def _stage_psf(field, gd, p6, al, c_d, s_d, rot_d, tr_d, k, g, psf, with_h, radi
                             st), "bin_points")
     out4 = dv.empty((ns, 4), torch.float32)
     cnt = dv.empty((ns,), torch.int32)
-    N.check(L.mg_forward(N.ptr(grec), N.ptr(gd["starts"]), g, radius, N.ptr(prec), N.ptr(pkey), N.ptr(pstart), ns,
+    N.check(L.mg_forward(N.ptr(grec), field.count, N.ptr(gd["starts"]), g, radius, N.ptr(prec), N.ptr(pkey),
+                         N.ptr(pstart), ns,
                          1 if with_h else 0, N.ptr(out4), N.ptr(cnt), N.ptr(ws), ws.numel(), st), "forward")
     I = dv.empty((b,), torch.float64)
     c64 = dv.empty((b,), torch.int64)
@@ -373,7 +374,7 @@ def grid_coordinates(dims, bounds):
     return axes, spacing
 
 
-def sample_volume_device(grec, gstart, g, r, dims, bounds, i0=0, i1=None, residual=None):
+def sample_volume_device(grec, n_gauss, gstart, g, r, dims, bounds, i0=0, i1=None, residual=None):
     """Device slab [i0, i1) of the clipped volume as a float32 (i1-i0, ny, nz) tensor."""
     nx, ny, nz = (int(d) for d in dims)
     i1 = nx if i1 is None else int(i1)
@@ -382,7 +383,7 @@ def sample_volume_device(grec, gstart, g, r, dims, bounds, i0=0, i1=None, residu
     hi = np.ascontiguousarray(np.asarray(bounds[1], dtype=np.float64).reshape(3))
     out = dv.empty((i1 - i0, ny, nz), torch.float32)
     ws = dv.workspace(L.mg_volume_workspace_bytes(nx, ny, nz), "volume")
-    N.check(L.mg_sample_volume(N.ptr(grec), N.ptr(gstart), g, r, nx, ny, nz, lo.ctypes.data_as(N.P),
+    N.check(L.mg_sample_volume(N.ptr(grec), int(n_gauss), N.ptr(gstart), g, r, nx, ny, nz, lo.ctypes.data_as(N.P),
                                hi.ctypes.data_as(N.P), i0, i1, N.ptr(residual), N.ptr(out), N.ptr(ws), ws.numel(),
                                dv.sptr()), "sample_volume")
     return out
@@ -416,5 +417,5 @@ def sample_volume(field, grid, residual, dims, bounds=((-1.0, -1.0, -1.0), (1.0,
         res_d = nrf_forward_device(residual, pts).reshape(dims)
     lo = np.array(bounds[0], dtype=np.float64)
     hi = np.array(bounds[1], dtype=np.float64)
-    out = sample_volume_device(grec, gd["starts"], g, r, dims, (lo, hi), residual=res_d)
+    out = sample_volume_device(grec, field.count, gd["starts"], g, r, dims, (lo, hi), residual=res_d)
     return Volume(data=dv.to_host(out).astype(np.float64), spacing=spacing, origin=origin)

@@ -454,7 +454,7 @@ class Trainer:
                                 N.ptr(self.tt), self.k, g, N.ptr(B.pkey), N.ptr(B.pinv), N.ptr(B.pstart),
                                 N.ptr(B.prec), N.ptr(B.xout), N.ptr(ws), ws.numel(), st), "bin_points")
         # forward with H (render_points, _kernels.py:24-70)
-        N.check(L.mg_forward(N.ptr(B.grec), N.ptr(B.gstart), g, r, N.ptr(B.prec), N.ptr(B.pkey), N.ptr(B.pstart),
+        N.check(L.mg_forward(N.ptr(B.grec), n, N.ptr(B.gstart), g, r, N.ptr(B.prec), N.ptr(B.pkey), N.ptr(B.pstart),
                              ns, 1, N.ptr(B.out4), N.ptr(B.cnt), N.ptr(ws), ws.numel(), st), "forward")
         N.check(L.mg_forward_finish(N.ptr(B.out4), N.ptr(B.cnt), N.ptr(B.pinv), bt, t, N.ptr(wts), None,
                                     N.ptr(B.pred), None, st), "finish")
@@ -573,7 +573,7 @@ class Trainer:
             gx, gy, gz = np.meshgrid(axes[0], axes[1], axes[2], indexing="ij")
             pts = dv.to_dev(np.stack([gx.ravel(), gy.ravel(), gz.ravel()], 1), torch.float32)
             res = nrf_forward_device(self.nrf, pts).reshape(dims)
-        out = sample_volume_device(B.grec, B.gstart, g, r, dims, bounds, residual=res)
+        out = sample_volume_device(B.grec, f.count, B.gstart, g, r, dims, bounds, residual=res)
         return Volume(data=dv.to_host(out).astype(np.float64), spacing=spacing,
                       origin=np.array([axes[0][0], axes[1][0], axes[2][0]]))
 

@@ -330,7 +330,7 @@ def run_ours(args):
             traffic = json.load(open(tp)).get("backward_kernel_dram_bytes")
         except Exception:
             traffic = None
-    nlaunch = count_graph_kernels(tr._graph) if tr._graph is not None else None
+    nlaunch = kt.get("launches_per_step")
     cpu = None
     if world == 1 or rank == 0:
         threads = os.cpu_count() or 1
@@ -362,6 +362,8 @@ def run_ours(args):
         "cpu_baseline": cpu,
         "clocks": clocks,
         "gpu_launches": (nlaunch * args.steps) if nlaunch else None,
+        "gpu_launches_note": "library kernels per step (mg_launch_count over one eager step) x timed steps; "
+                             "torch index_select/sum/fill plumbing kernels not counted",
     }
     print(json.dumps(out))
     if world > 1:
@@ -392,11 +394,14 @@ def kernel_times(tr, idx_list, nb, hw):
             return rc
 
     B = tr._buffers(len(idx_list[0]))
+    launches = []
     try:
         L.mg_forward, L.mg_backward = Timed(orig_fwd, fwd), Timed(orig_bwd, bwd)
         for ix in idx_list:
             tr.load_indices(ix)
+            c0 = L.mg_launch_count()
             tr._body(B, nb, hw)
+            launches.append(L.mg_launch_count() - c0)
             torch.cuda.synchronize()
             pairs.append(int(B.cnt.sum().item()))
     finally:
@@ -404,7 +409,8 @@ def kernel_times(tr, idx_list, nb, hw):
     torch.cuda.synchronize()
     f = float(np.mean([a.elapsed_time(b) for a, b in fwd]))
     b = float(np.mean([a.elapsed_time(c) for a, c in bwd]))
-    return {"forward_ms": f, "backward_ms": b, "pairs_per_launch": float(np.mean(pairs))}
+    return {"forward_ms": f, "backward_ms": b, "pairs_per_launch": float(np.mean(pairs)),
+            "launches_per_step": int(max(launches))}
 
 
 def main():

@@ -50,6 +50,9 @@ extern "C" {
 int mg_abi_version(void);
 const char *mg_last_error(void);
 int mg_device_sm_count(void);
+/* Kernel launches issued by this library so far (host-side counter; a CUDA
+ * graph capture counts each captured launch once). */
+long long mg_launch_count(void);
 
 /* ---- binning: spatial.py:18-66 ------------------------------------------ */
 /* keys[i] = (ci*G + cj)*G + ck with c = clamp(floor((x+1)*(G/2)), 0, G-1) in float64 */

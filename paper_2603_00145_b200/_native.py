@@ -26,6 +26,7 @@ SIGNATURES = {
     "mg_abi_version": (ctypes.c_int, []),
     "mg_last_error": (ctypes.c_char_p, []),
     "mg_device_sm_count": (ctypes.c_int, []),
+    "mg_launch_count": (ctypes.c_longlong, []),
     "mg_cell_keys_f64": (ctypes.c_int, [P, I64, I64, P, P]),
     "mg_bin_workspace_bytes": (SZ, [I64, I64]),
     "mg_bin_f32": (ctypes.c_int, [P, I64, I64, P, P, P, P, SZ, P]),

@@ -184,9 +184,17 @@ int do_bin(const float* pos32, const double* pos64, int64_t n, int64_t g, uint32
 
 }  // namespace
 
+namespace mg {
+long long& launch_counter() {
+  static long long c = 0;
+  return c;
+}
+}  // namespace mg
+
 extern "C" {
 
 int mg_abi_version(void) { return MG_ABI_VERSION; }
+long long mg_launch_count(void) { return mg::launch_counter(); }
 const char* mg_last_error(void) { return g_err; }
 int mg_device_sm_count(void) { return num_sms(); }
 
@@ -211,17 +219,17 @@ int mg_bin_f64(const double* pos, int64_t n, int64_t g, uint32_t* keys_sorted, i
 }
 
 int mg_keys_from_csr(const int32_t* cs, int64_t ncell, uint32_t* keys, void* stream) {
-  if (ncell > 0) keys_from_csr_kernel<<<grid_of(ncell), 256, 0, S(stream)>>>(cs, ncell, keys);
+  if (ncell > 0) MG_LAUNCH(keys_from_csr_kernel<<<grid_of(ncell), 256, 0, S(stream)>>>(cs, ncell, keys));
   return cuda_status();
 }
 
 int mg_i64_to_i32(const int64_t* src, int64_t n, int32_t* dst, void* stream) {
-  if (n > 0) csr64_to_32_kernel<<<grid_of(n), 256, 0, S(stream)>>>(src, n, nullptr, 0, dst, nullptr);
+  if (n > 0) MG_LAUNCH(csr64_to_32_kernel<<<grid_of(n), 256, 0, S(stream)>>>(src, n, nullptr, 0, dst, nullptr));
   return cuda_status();
 }
 
 int mg_i32_to_i64(const int32_t* src, int64_t n, int64_t* dst, void* stream) {
-  if (n > 0) i32_to_i64_kernel<<<grid_of(n), 256, 0, S(stream)>>>(src, n, dst);
+  if (n > 0) MG_LAUNCH(i32_to_i64_kernel<<<grid_of(n), 256, 0, S(stream)>>>(src, n, dst));
   return cuda_status();
 }
 
@@ -234,7 +242,7 @@ int mg_activate(const float* pos, const float* quat, const float* ls, const floa
 int mg_activate_f64(const double* quat, const double* ls, const double* lg, int64_t n, double* qn, double* rot,
                     double* inv_var, double* prec6, double* alpha, int32_t* err_flag, void* stream) {
   if (n > 0)
-    activate_f64_kernel<<<grid_of(n), 256, 0, S(stream)>>>(quat, ls, lg, n, qn, rot, inv_var, prec6, alpha, err_flag);
+    MG_LAUNCH(activate_f64_kernel<<<grid_of(n), 256, 0, S(stream)>>>(quat, ls, lg, n, qn, rot, inv_var, prec6, alpha, err_flag));
   return cuda_status();
 }
 
@@ -439,8 +447,8 @@ static int block_common(const double* points, const int64_t* sids, int64_t b, co
   char* rest = (char*)w.rest();
   size_t restb = w.left;
   if (!w.ok || restb < points_ws(b, g)) return fail("mg_block: workspace too small");
-  csr64_to_32_kernel<<<grid_of(nc1 > n ? nc1 : n), 256, 0, st>>>(cs, nc1, ci, n, gstart, gorder);
-  keys_from_csr_kernel<<<grid_of(nc1 - 1), 256, 0, st>>>(gstart, nc1 - 1, gkey);
+  MG_LAUNCH(csr64_to_32_kernel<<<grid_of(nc1 > n ? nc1 : n), 256, 0, st>>>(cs, nc1, ci, n, gstart, gorder));
+  MG_LAUNCH(keys_from_csr_kernel<<<grid_of(nc1 - 1), 256, 0, st>>>(gstart, nc1 - 1, gkey));
   launch_gauss_pack_prepared(mu, prec6, alpha, gorder, n, grec, st);
   int rc = mg_bin_points(points, sids, b, 1, nullptr, nullptr, rot, trans, k, g, pkey, pinv, pstart, prec, out_x,
                          rest, restb, st);
@@ -487,10 +495,10 @@ int mg_dense_forward(const double* points, int64_t b, const double* mu, const do
   int* ident = w.take<int>(n);
   if (!w.ok) return fail("mg_dense_forward: workspace too small");
   if (n > 0) {
-    iota32_kernel<<<grid_of(n), 256, 0, st>>>(ident, n);
+    MG_LAUNCH(iota32_kernel<<<grid_of(n), 256, 0, st>>>(ident, n));
     launch_gauss_pack_prepared(mu, prec6, alpha, ident, n, grec, st);
   }
-  if (b > 0) dense_kernel<<<(unsigned)((b + 127) / 128), 128, 0, st>>>(points, b, gauss_soa(grec, n), n, out);
+  if (b > 0) MG_LAUNCH(dense_kernel<<<(unsigned)((b + 127) / 128), 128, 0, st>>>(points, b, gauss_soa(grec, n), n, out));
   return cuda_status();
 }
 

@@ -152,6 +152,13 @@ inline GaussOut gauss_out(float* base, int64_t n) {
                   reinterpret_cast<float2*>(base + 8 * n)};
 }
 
+// Host-side count of kernel launches issued by this library (all streams),
+// read through mg_launch_count(); MG_LAUNCH bumps it at every launch site.
+namespace mg {
+long long& launch_counter();
+}
+#define MG_LAUNCH(...) (++::mg::launch_counter(), __VA_ARGS__)
+
 // Device-side error codes (read by the host wrappers).
 enum MgErr : int {
   MG_OK = 0,

@@ -884,28 +884,28 @@ static inline unsigned grid_for(int64_t n, int threads = 256) {
 }
 
 void launch_gauss_keys(const float* pos, int64_t n, int g, uint32_t* keys, cudaStream_t st) {
-  if (n > 0) gauss_keys_kernel<<<grid_for(n), 256, 0, st>>>(pos, n, g, keys);
+  if (n > 0) MG_LAUNCH(gauss_keys_kernel<<<grid_for(n), 256, 0, st>>>(pos, n, g, keys));
 }
 void launch_gauss_keys_f64(const double* pos, int64_t n, int g, uint32_t* keys, cudaStream_t st) {
-  if (n > 0) gauss_keys_f64_kernel<<<grid_for(n), 256, 0, st>>>(pos, n, g, keys);
+  if (n > 0) MG_LAUNCH(gauss_keys_f64_kernel<<<grid_for(n), 256, 0, st>>>(pos, n, g, keys));
 }
 void launch_gauss_activate(const float* pos, const float* quat, const float* ls, const float* lg, const int* order,
                            int64_t n, float* grec, int* err, cudaStream_t st) {
-  if (n > 0) gauss_activate_kernel<<<grid_for(n), 256, 0, st>>>(pos, quat, ls, lg, order, n, gauss_out(grec, n), err);
+  if (n > 0) MG_LAUNCH(gauss_activate_kernel<<<grid_for(n), 256, 0, st>>>(pos, quat, ls, lg, order, n, gauss_out(grec, n), err));
 }
 void launch_gauss_pack_prepared(const double* mu, const double* prec6, const double* alpha, const int* order,
                                 int64_t n, float* grec, cudaStream_t st) {
-  if (n > 0) gauss_pack_prepared_kernel<<<grid_for(n), 256, 0, st>>>(mu, prec6, alpha, order, n, gauss_out(grec, n));
+  if (n > 0) MG_LAUNCH(gauss_pack_prepared_kernel<<<grid_for(n), 256, 0, st>>>(mu, prec6, alpha, order, n, gauss_out(grec, n)));
 }
 void launch_points_prepare(const double* coords, const int64_t* sids64, const int* sids32, int64_t b, int ntaps,
                            const double* tap_off, const double* dirs, const double* rot, const double* trans,
                            int nslices, int g, uint32_t* keys, float4* xf, double* xout, cudaStream_t st) {
   if (b * ntaps > 0)
-    points_prepare_kernel<<<grid_for(b * ntaps), 256, 0, st>>>(coords, sids64, sids32, b, ntaps, tap_off, dirs, rot,
-                                                               trans, nslices, g, keys, xf, xout);
+    MG_LAUNCH(points_prepare_kernel<<<grid_for(b * ntaps), 256, 0, st>>>(coords, sids64, sids32, b, ntaps, tap_off, dirs, rot,
+                                                               trans, nslices, g, keys, xf, xout));
 }
 void launch_points_gather(const float4* xf, const int* perm, int64_t n, float4* prec, int* inv, cudaStream_t st) {
-  if (n > 0) points_gather_kernel<<<grid_for(n), 256, 0, st>>>(xf, perm, n, prec, inv);
+  if (n > 0) MG_LAUNCH(points_gather_kernel<<<grid_for(n), 256, 0, st>>>(xf, perm, n, prec, inv));
 }
 
 int fwd_qmax() { return MG_FWD_QMAX; }
@@ -921,9 +921,9 @@ void build_items(const uint32_t* keys, const int* starts, int64_t n, int q, int*
   int* flags = (int*)ws;
   int* scan = (int*)((char*)ws + (((size_t)n * 4 + 255) & ~(size_t)255));
   void* sws = (char*)ws + 2 * (((size_t)n * 4 + 255) & ~(size_t)255);
-  item_flags_kernel<<<grid_for(n), 256, 0, st>>>(keys, starts, n, q, flags);
+  MG_LAUNCH(item_flags_kernel<<<grid_for(n), 256, 0, st>>>(keys, starts, n, q, flags));
   excl_scan(flags, scan, n, sws, st);
-  item_compact_kernel<<<grid_for(n), 256, 0, st>>>(flags, scan, n, items, nitems);
+  MG_LAUNCH(item_compact_kernel<<<grid_for(n), 256, 0, st>>>(flags, scan, n, items, nitems));
 }
 
 template <class K>
@@ -944,12 +944,12 @@ void launch_forward(bool with_h, const float* grec_raw, int64_t n_gauss, const i
   const GaussSoA grec = gauss_soa(grec_raw, n_gauss);
   if (with_h) {
     auto k = forward_kernel<true>;
-    forward_kernel<true><<<(unsigned)persistent_blocks(k, kFwdWarps * 32, want), kFwdWarps * 32, 0, st>>>(
-        grec, gstart, g, r, prec, pkey, pstart, items, nitems, out4, cnt);
+    MG_LAUNCH(forward_kernel<true><<<(unsigned)persistent_blocks(k, kFwdWarps * 32, want), kFwdWarps * 32, 0, st>>>(
+        grec, gstart, g, r, prec, pkey, pstart, items, nitems, out4, cnt));
   } else {
     auto k = forward_kernel<false>;
-    forward_kernel<false><<<(unsigned)persistent_blocks(k, kFwdWarps * 32, want), kFwdWarps * 32, 0, st>>>(
-        grec, gstart, g, r, prec, pkey, pstart, items, nitems, out4, cnt);
+    MG_LAUNCH(forward_kernel<false><<<(unsigned)persistent_blocks(k, kFwdWarps * 32, want), kFwdWarps * 32, 0, st>>>(
+        grec, gstart, g, r, prec, pkey, pstart, items, nitems, out4, cnt));
   }
 }
 
@@ -959,8 +959,8 @@ void launch_backward(const float* grec_raw, int64_t n_gauss, const uint32_t* gke
   if (max_items <= 0) return;
   const GaussSoA grec = gauss_soa(grec_raw, n_gauss);
   const int64_t want = (max_items + kBwdWarps - 1) / kBwdWarps;
-  backward_kernel<<<(unsigned)persistent_blocks(backward_kernel, kBwdWarps * 32, want), kBwdWarps * 32, 0, st>>>(
-      grec, gkey, gstart, g, r, prec, pstart, items, nitems, acc10);
+  MG_LAUNCH(backward_kernel<<<(unsigned)persistent_blocks(backward_kernel, kBwdWarps * 32, want), kBwdWarps * 32, 0, st>>>(
+      grec, gkey, gstart, g, r, prec, pstart, items, nitems, acc10));
 }
 
 }  // namespace mg

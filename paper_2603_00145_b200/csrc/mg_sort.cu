@@ -84,15 +84,15 @@ void excl_scan(const int* in, int* out, int64_t n, void* ws, cudaStream_t st) {
   if (n <= 0) return;
   int64_t tiles = (n + kScanTile - 1) / kScanTile;
   if (tiles == 1) {
-    scan_tiles<<<1, kScanThreads, 0, st>>>(in, out, n, nullptr);
+    MG_LAUNCH(scan_tiles<<<1, kScanThreads, 0, st>>>(in, out, n, nullptr));
     return;
   }
   int* sums = (int*)ws;
   int* offs = sums + tiles;
   size_t used = ((size_t)tiles * 2 * sizeof(int) + 255) & ~(size_t)255;
-  scan_tiles<<<(unsigned)tiles, kScanThreads, 0, st>>>(in, out, n, sums);
+  MG_LAUNCH(scan_tiles<<<(unsigned)tiles, kScanThreads, 0, st>>>(in, out, n, sums));
   excl_scan(sums, offs, tiles, (char*)ws + used, st);
-  scan_add<<<(unsigned)tiles, kScanThreads, 0, st>>>(out, n, offs);
+  MG_LAUNCH(scan_add<<<(unsigned)tiles, kScanThreads, 0, st>>>(out, n, offs));
 }
 
 // ---------------------------------------------------------------------------
@@ -202,16 +202,16 @@ void radix_sort_pairs(const uint32_t* keys_in, uint32_t* keys_out, int* vals_out
   void* sws = w;
   int passes = (bits + 7) / 8;
   if (passes < 1) passes = 1;
-  iota_kernel<<<(unsigned)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096), 256, 0, st>>>(vA, n);
+  MG_LAUNCH(iota_kernel<<<(unsigned)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096), 256, 0, st>>>(vA, n));
   const uint32_t* kin = keys_in;
   const int* vin = vA;
   for (int p = 0; p < passes; ++p) {
     bool last = p == passes - 1;
     uint32_t* ko = last ? keys_out : ((p & 1) ? kA : kB);
     int* vo = last ? vals_out : ((p & 1) ? vA : vB);
-    rs_hist<<<(unsigned)nb, kRsThreads, 0, st>>>(kin, n, 8 * p, hist, (int)nb);
+    MG_LAUNCH(rs_hist<<<(unsigned)nb, kRsThreads, 0, st>>>(kin, n, 8 * p, hist, (int)nb));
     excl_scan(hist, offs, 256 * nb, sws, st);
-    rs_scatter<<<(unsigned)nb, kRsThreads, 0, st>>>(kin, vin, ko, vo, n, 8 * p, offs, (int)nb);
+    MG_LAUNCH(rs_scatter<<<(unsigned)nb, kRsThreads, 0, st>>>(kin, vin, ko, vo, n, 8 * p, offs, (int)nb));
     kin = ko;
     vin = vo;
   }
@@ -232,7 +232,7 @@ void csr_starts(const uint32_t* keys, int64_t n, int64_t ncell, int* starts, voi
   if (n > 0) {
     int64_t blocks = (n + 255) / 256;
     if (blocks > 8192) blocks = 8192;
-    csr_hist<<<(unsigned)blocks, 256, 0, st>>>(keys, n, starts);
+    MG_LAUNCH(csr_hist<<<(unsigned)blocks, 256, 0, st>>>(keys, n, starts));
   }
   excl_scan(starts, starts, ncell + 1, ws, st);
 }

@@ -131,10 +131,10 @@ void launch_ssim(const float* pred, const float* tgt, int H, int W, double scale
   double* g3 = (double*)p;
   p += (((size_t)Hv * Wv * 3 * 8 + 255) & ~(size_t)255);
   double* a3 = (double*)p;
-  ssim_h_kernel<<<gs((int64_t)H * Wv), 256, 0, st>>>(pred, tgt, H, W, h5);
-  ssim_v_kernel<<<gs((int64_t)Hv * Wv), 256, 0, st>>>(h5, H, W, g3, ssim_sum);
-  ssim_ah_kernel<<<gs((int64_t)Hv * W), 256, 0, st>>>(g3, H, W, a3);
-  ssim_av_kernel<<<gs((int64_t)H * W), 256, 0, st>>>(a3, pred, tgt, H, W, scale, up);
+  MG_LAUNCH(ssim_h_kernel<<<gs((int64_t)H * Wv), 256, 0, st>>>(pred, tgt, H, W, h5));
+  MG_LAUNCH(ssim_v_kernel<<<gs((int64_t)Hv * Wv), 256, 0, st>>>(h5, H, W, g3, ssim_sum));
+  MG_LAUNCH(ssim_ah_kernel<<<gs((int64_t)Hv * W), 256, 0, st>>>(g3, H, W, a3));
+  MG_LAUNCH(ssim_av_kernel<<<gs((int64_t)H * W), 256, 0, st>>>(a3, pred, tgt, H, W, scale, up));
 }
 
 }  // namespace mg

@@ -426,25 +426,25 @@ __global__ void upsample_kernel(const float* __restrict__ q_old, const float* __
 // ---------------------------------------------------------------------------
 void launch_forward_finish(const float4* out4, const int* cnt, const int* inv, int64_t b, int ntaps,
                            const double* tap_w, double* out_i, float* out_i32, int64_t* out_cnt, cudaStream_t st) {
-  if (b > 0) forward_finish_kernel<<<gridn(b), 256, 0, st>>>(out4, cnt, inv, b, ntaps, tap_w, out_i, out_i32, out_cnt);
+  if (b > 0) MG_LAUNCH(forward_finish_kernel<<<gridn(b), 256, 0, st>>>(out4, cnt, inv, b, ntaps, tap_w, out_i, out_i32, out_cnt));
 }
 void launch_backward_points(const double* up64, const float* up32, const int* inv, int64_t b, int ntaps,
                             const double* tap_w, const float4* out4, float4* prec, double* dpoints, cudaStream_t st) {
   if (b > 0)
-    backward_points_kernel<<<gridn(b * ntaps), 256, 0, st>>>(up64, up32, inv, b, ntaps, tap_w, out4, prec, dpoints);
+    MG_LAUNCH(backward_points_kernel<<<gridn(b * ntaps), 256, 0, st>>>(up64, up32, inv, b, ntaps, tap_w, out4, prec, dpoints));
 }
 void launch_acc_to_ref(const float* acc10, const int* order, int64_t n, const double* alpha64, double* d_mu,
                        double* d_abar6, double* d_alpha, cudaStream_t st) {
-  if (n > 0) acc_to_ref_kernel<<<gridn(n), 256, 0, st>>>(acc10, order, n, alpha64, d_mu, d_abar6, d_alpha);
+  if (n > 0) MG_LAUNCH(acc_to_ref_kernel<<<gridn(n), 256, 0, st>>>(acc10, order, n, alpha64, d_mu, d_abar6, d_alpha));
 }
 void launch_epilogue(const float* acc10, const int* order, int64_t n, const float* quat, const float* ls,
                      const float* lg, double* d_pos, double* d_q, double* d_s, double* d_l, cudaStream_t st) {
-  if (n > 0) epilogue_kernel<<<gridn(n), 256, 0, st>>>(acc10, order, n, quat, ls, lg, d_pos, d_q, d_s, d_l);
+  if (n > 0) MG_LAUNCH(epilogue_kernel<<<gridn(n), 256, 0, st>>>(acc10, order, n, quat, ls, lg, d_pos, d_q, d_s, d_l));
 }
 void launch_epilogue_f64(const double* d_mu, const double* d_abar6, const double* d_alpha, const double* quat,
                          const double* ls, const double* lg, int64_t n, double* d_pos, double* d_q, double* d_s,
                          double* d_l, cudaStream_t st) {
-  if (n > 0) epilogue_f64_kernel<<<gridn(n), 256, 0, st>>>(d_mu, d_abar6, d_alpha, quat, ls, lg, n, d_pos, d_q, d_s, d_l);
+  if (n > 0) MG_LAUNCH(epilogue_f64_kernel<<<gridn(n), 256, 0, st>>>(d_mu, d_abar6, d_alpha, quat, ls, lg, n, d_pos, d_q, d_s, d_l));
 }
 void launch_transform_grads(const double* dpoints, const double* coords, const int64_t* sids, int64_t b, int ntaps,
                             const double* tap_off, const double* dirs, const double* tq, int k, double* acc12,
@@ -453,14 +453,14 @@ void launch_transform_grads(const double* dpoints, const double* coords, const i
   cudaMemsetAsync(acc12, 0, sizeof(double) * 12 * k, st);
   if (b > 0) {
     int64_t chunks = (b * ntaps + 31) / 32;
-    transform_reduce_kernel<<<gridn(chunks, 128), 128, 0, st>>>(dpoints, coords, sids, b, ntaps, tap_off, dirs, k,
-                                                                acc12);
+    MG_LAUNCH(transform_reduce_kernel<<<gridn(chunks, 128), 128, 0, st>>>(dpoints, coords, sids, b, ntaps, tap_off, dirs, k,
+                                                                acc12));
   }
-  transform_chain_kernel<<<gridn(k), 256, 0, st>>>(acc12, tq, k, out7, accumulate);
+  MG_LAUNCH(transform_chain_kernel<<<gridn(k), 256, 0, st>>>(acc12, tq, k, out7, accumulate));
 }
 void launch_smooth_l1(const float* pred, const float* target, int64_t b, float* up_out, double* loss_acc,
                       cudaStream_t st) {
-  if (b > 0) smooth_l1_kernel<<<gridn(b), 256, 0, st>>>(pred, target, b, 1.0 / (double)b, up_out, loss_acc);
+  if (b > 0) MG_LAUNCH(smooth_l1_kernel<<<gridn(b), 256, 0, st>>>(pred, target, b, 1.0 / (double)b, up_out, loss_acc));
 }
 
 __global__ void quat_to_rot_kernel(const double* __restrict__ q, int64_t k, double* __restrict__ rot) {
@@ -471,12 +471,12 @@ __global__ void quat_to_rot_kernel(const double* __restrict__ q, int64_t k, doub
   }
 }
 void launch_quat_to_rot(const double* q, int64_t k, double* rot, cudaStream_t st) {
-  if (k > 0) quat_to_rot_kernel<<<gridn(k), 256, 0, st>>>(q, k, rot);
+  if (k > 0) MG_LAUNCH(quat_to_rot_kernel<<<gridn(k), 256, 0, st>>>(q, k, rot));
 }
 __global__ void counter_incr_kernel(int* c, int n) {
   if (threadIdx.x < n) c[threadIdx.x] += 1;
 }
-void launch_counter_incr(int* c, int n, cudaStream_t st) { counter_incr_kernel<<<1, 32, 0, st>>>(c, n); }
+void launch_counter_incr(int* c, int n, cudaStream_t st) { MG_LAUNCH(counter_incr_kernel<<<1, 32, 0, st>>>(c, n)); }
 
 void launch_gauss_update(const float* acc10, const int* order, int64_t n, float* pos, float* quat, float* ls,
                          float* lg, float* mom_m, float* mom_v, const double* hyper, int use_aniso,
@@ -494,17 +494,17 @@ void launch_gauss_update(const float* acc10, const int* order, int64_t n, float*
   h.use_aniso = use_aniso;
   h.bc1 = h.bc2 = 1.0;
   if (n > 0)
-    gauss_update_kernel<<<gridn(n), 256, 0, st>>>(acc10, order, n, pos, quat, ls, lg, mom_m, mom_v, h, t_dev,
-                                                  aniso_acc);
+    MG_LAUNCH(gauss_update_kernel<<<gridn(n), 256, 0, st>>>(acc10, order, n, pos, quat, ls, lg, mom_m, mom_v, h, t_dev,
+                                                  aniso_acc));
 }
 void launch_transform_adam(double* tq, double* tt, const double* g7, double* m7, double* v7, int k, double lr,
                            double b1, double b2, double eps, const int* t_dev, cudaStream_t st) {
-  if (k > 0) transform_adam_kernel<<<gridn((int64_t)k * 7), 256, 0, st>>>(tq, tt, g7, m7, v7, k, lr, b1, b2, eps, t_dev);
+  if (k > 0) MG_LAUNCH(transform_adam_kernel<<<gridn((int64_t)k * 7), 256, 0, st>>>(tq, tt, g7, m7, v7, k, lr, b1, b2, eps, t_dev));
 }
 void launch_upsample(const float* q_old, const float* s_old, const float* l_old, const int* node_of_old, int ro, int rn,
                      float* pos, float* q, float* s, float* l, cudaStream_t st) {
   int64_t nn = (int64_t)rn * rn * rn;
-  if (nn > 0) upsample_kernel<<<gridn(nn), 256, 0, st>>>(q_old, s_old, l_old, node_of_old, ro, rn, pos, q, s, l);
+  if (nn > 0) MG_LAUNCH(upsample_kernel<<<gridn(nn), 256, 0, st>>>(q_old, s_old, l_old, node_of_old, ro, rn, pos, q, s, l));
 }
 
 }  // namespace mg

@@ -192,9 +192,9 @@ void launch_sample_volume(const float* grec_raw, int64_t n_gauss, const int* gst
     ax.rs[a] = rs;
     ax.rc[a] = rc;
     int cnt = v1 - v0;
-    axis_cells_kernel<<<(cnt + 255) / 256, 256, 0, st>>>(n[a], v0, v1, lo[a], hi[a], ax.sp[a], g, cells, flags);
+    MG_LAUNCH(axis_cells_kernel<<<(cnt + 255) / 256, 256, 0, st>>>(n[a], v0, v1, lo[a], hi[a], ax.sp[a], g, cells, flags));
     excl_scan(flags, scan, cnt, sws, st);
-    axis_runs_kernel<<<(cnt + 255) / 256, 256, 0, st>>>(cells, flags, scan, cnt, rs, rc, nr + a);
+    MG_LAUNCH(axis_runs_kernel<<<(cnt + 255) / 256, 256, 0, st>>>(cells, flags, scan, cnt, rs, rc, nr + a));
   }
   // axis-0 voxel indices inside the kernel are slab-relative; shift coordinates by i0
   ax.v0[0] = i0;
@@ -204,8 +204,8 @@ void launch_sample_volume(const float* grec_raw, int64_t n_gauss, const int* gst
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   // write offsets: kernel computes vid relative to the slab (i in [0, i1-i0))
-  volume_kernel<<<(unsigned)blocks, kVolWarps * 32, 0, st>>>(gauss_soa(grec_raw, n_gauss), gstart, g, r, ax, residual,
-                                                              out);
+  MG_LAUNCH(volume_kernel<<<(unsigned)blocks, kVolWarps * 32, 0, st>>>(gauss_soa(grec_raw, n_gauss), gstart, g, r, ax, residual,
+                                                              out));
 }
 
 }  // namespace mg

@@ -119,8 +119,10 @@ int mg_forward_finish(const void *out4, const int32_t *counts, const int32_t *pi
 int mg_backward_points(const double *upstream, const float *upstream_f32, int64_t b, int32_t ntaps,
                        const double *tap_weights, const int32_t *pinv, const void *out4, void *prec,
                        double *d_points, void *stream);
-size_t mg_backward_workspace_bytes(int64_t n);
-/* Gaussian-major pair pass: acc10[p] = {S, T(3), A6(6)} per sorted Gaussian. */
+size_t mg_backward_workspace_bytes(int64_t n, int64_t grid_res);
+/* Gaussian-major pair pass: acc10[p] = {S, T(3), A6(6)} per sorted Gaussian.
+ * For radius <= 5 strips of 16 cells stage their neighbourhood in shared
+ * memory with TMA bulk copies when MGAUSS_STAGED_BWD=1 (default: L1/L2 item path). */
 int mg_backward(const void *grec, const uint32_t *gkey_sorted, const int32_t *gstart, int64_t n, int64_t grid_res,
                 int64_t radius, const void *prec, const int32_t *pstart, float *acc10, void *ws, size_t ws_bytes,
                 void *stream);

@@ -42,7 +42,7 @@ SIGNATURES = {
     "mg_forward": (ctypes.c_int, [P, I64, P, I64, I64, P, P, P, I64, I32, P, P, P, SZ, P]),
     "mg_forward_finish": (ctypes.c_int, [P, P, P, I64, I32, P, P, P, P, P]),
     "mg_backward_points": (ctypes.c_int, [P, P, I64, I32, P, P, P, P, P, P]),
-    "mg_backward_workspace_bytes": (SZ, [I64]),
+    "mg_backward_workspace_bytes": (SZ, [I64, I64]),
     "mg_backward": (ctypes.c_int, [P, P, P, I64, I64, I64, P, P, P, P, SZ, P]),
     "mg_backward_epilogue": (ctypes.c_int, [P, P, I64, P, P, P, P, P, P, P, P]),
     "mg_backward_accumulators": (ctypes.c_int, [P, P, I64, P, P, P, P, P]),

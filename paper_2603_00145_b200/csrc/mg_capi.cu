@@ -1,5 +1,6 @@
 // mg_capi.cu -- extern "C" entry points (include/mgauss_b200.h).
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "../../include/mgauss_b200.h"
@@ -304,17 +305,35 @@ int mg_backward_points(const double* up, const float* up32, int64_t b, int32_t n
   return cuda_status();
 }
 
-size_t mg_backward_workspace_bytes(int64_t n) { return fwd_ws(n); }
+size_t mg_backward_workspace_bytes(int64_t n, int64_t g) {
+  size_t a = fwd_ws(n), b = backward_staged_ws_bytes(n, (int)g) + 1024;
+  return a > b ? a : b;
+}
+
+static bool staged_backward_enabled(int64_t r) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("MGAUSS_STAGED_BWD");
+    env = (e && e[0] == '1') ? 1 : 0;
+  }
+  return env == 1 && (2 * r + 1) * (2 * r + 1) <= 128;
+}
 
 int mg_backward(const void* grec, const uint32_t* gkey_sorted, const int32_t* gstart, int64_t n, int64_t g, int64_t r,
                 const void* prec, const int32_t* pstart, float* acc10, void* ws, size_t wsb, void* stream) {
   if (g < 1 || r < 0 || n < 0) return fail("mg_backward: bad sizes");
   cudaStream_t st = S(stream);
+  if (n == 0) return 0;
+  if (staged_backward_enabled(r)) {
+    if (wsb < backward_staged_ws_bytes(n, (int)g)) return fail("mg_backward: workspace too small");
+    launch_backward_staged((const float*)grec, n, gkey_sorted, gstart, (int)g, (int)r, (const float4*)prec, pstart,
+                           acc10, ws, st);
+    return cuda_status();
+  }
   Bump w(ws, wsb);
   int* items = w.take<int>(n);
   int* nitems = w.take<int>(1);
   if (!w.ok) return fail("mg_backward: workspace too small");
-  if (n == 0) return 0;
   build_items(gkey_sorted, gstart, n, 2, items, nitems, w.rest(), st);
   launch_backward((const float*)grec, n, gkey_sorted, gstart, (int)g, (int)r, (const float4*)prec, pstart, items,
                   nitems, n, acc10, st);
@@ -421,7 +440,8 @@ int mg_upsample(const float* q_old, const float* s_old, const float* l_old, cons
 size_t mg_block_workspace_bytes(int64_t b, int64_t n, int64_t g) {
   int64_t nc1 = ncell_of(g) + 1;
   return al((size_t)nc1 * 4) * 2 + al((size_t)n * 4) * 2 + al((size_t)n * 48) + al((size_t)b * 4) * 3 +
-         al((size_t)b * 16) * 2 + al((size_t)n * 40) + points_ws(b, g) + fwd_ws(b > n ? b : n) + 4096;
+         al((size_t)b * 16) * 2 + al((size_t)n * 40) + points_ws(b, g) + fwd_ws(b > n ? b : n) +
+         backward_staged_ws_bytes(n, (int)g) + 8192;
 }
 
 static int block_common(const double* points, const int64_t* sids, int64_t b, const double* rot, const double* trans,

@@ -862,6 +862,314 @@ __global__ void __launch_bounds__(kBwdWarps * 32, MG_BWD_MINB) backward_kernel(c
 }
 
 // ---------------------------------------------------------------------------
+// Staged backward.  A block owns a STRIP of kSbS consecutive Gaussian cells
+// (i, j, k0 .. k0+kSbS-1), one warp per cell.  The union of the strip's
+// candidate sub-points -- (2r+1)^2 columns x (kSbS + 2r) cells, each column a
+// contiguous range of the cell-sorted point records -- is copied into shared
+// memory with TMA bulk copies (cp.async.bulk + mbarrier), in rounds of
+// "pieces" (column sub-ranges) that fit the buffer.  Every warp then streams
+// its own 11x11x11 neighbourhood out of shared memory with the bitmap
+// cursor: each staged point is read ~kSbS*11/(kSbS+10) times from SMEM
+// instead of once per Gaussian from L2.  Cells with more than 2 Gaussians
+// hand their later chunks to the global-memory item kernel (overflow list).
+// ---------------------------------------------------------------------------
+#ifndef MG_SB_S
+#define MG_SB_S 16
+#endif
+#ifndef MG_SB_CAP
+#define MG_SB_CAP 8192
+#endif
+constexpr int kSbS = MG_SB_S;      // cells per strip == warps per block
+constexpr int kSbCap = MG_SB_CAP;  // staged point records (16 B each)
+constexpr int kSbPieces = 128;
+
+struct StageSmem {
+  uint64_t bar;
+  int phase;
+  // round builder state (thread 0)
+  int bc, bstart, brem, done;
+  // current round
+  int npieces;
+  int pc[kSbPieces];   // column index of piece
+  int pga[kSbPieces];  // global start (point index) of piece
+  int plen[kSbPieces];
+  int pso[kSbPieces];  // smem offset of piece
+  // strip columns
+  int ncol, ks_lo, ks_hi, ilo, jlo, nj;
+  int cst[kSbPieces], clen[kSbPieces];
+  float part[kSbS][32];  // per-warp partial sums: Gaussian k value c at [16k + c]
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, int parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// Greedy: next round of pieces (thread 0).  Returns bytes to stage.
+__device__ int next_round(StageSmem& st) {
+  int used = 0, np = 0;
+  while (st.bc < st.ncol && np < kSbPieces) {
+    if (st.brem == 0) {
+      ++st.bc;
+      if (st.bc < st.ncol) {
+        st.bstart = st.cst[st.bc];
+        st.brem = st.clen[st.bc];
+      }
+      continue;
+    }
+    const int take = min(st.brem, kSbCap - used);
+    if (take == 0) break;
+    st.pc[np] = st.bc;
+    st.pga[np] = st.bstart;
+    st.plen[np] = take;
+    st.pso[np] = used;
+    ++np;
+    used += take;
+    st.bstart += take;
+    st.brem -= take;
+  }
+  st.npieces = np;
+  st.done = (st.bc >= st.ncol) ? 1 : 0;
+  return used * 16;
+}
+
+template <int QG>
+__device__ __forceinline__ void staged_load_gauss(GaussAcc<QG>& acc, const GaussSoA& grec, int g0, int ng) {
+#pragma unroll
+  for (int k = 0; k < QG; ++k) {
+    const int gi = g0 + min(k, ng - 1);
+    const float4 A = grec.A[gi], B = grec.B[gi];
+    const float2 C = grec.C[gi];
+    acc.mx[k] = A.x;
+    acc.my[k] = A.y;
+    acc.mz[k] = A.z;
+    acc.P[k][0] = B.x;
+    acc.P[k][1] = B.y;
+    acc.P[k][2] = B.z;
+    acc.P[k][3] = B.w;
+    acc.P[k][4] = C.x;
+    acc.P[k][5] = C.y;
+    acc.S[k] = bc2(0.f);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) acc.T[k][c] = bc2(0.f);
+#pragma unroll
+    for (int c = 0; c < 6; ++c) acc.A6[k][c] = bc2(0.f);
+  }
+}
+
+template <int QG>
+__device__ __forceinline__ void staged_round(const GaussSoA& grec, int g0, float* __restrict__ part,
+                                             const float4* __restrict__ stage, const StageSmem& st,
+                                             const int* __restrict__ pstart, int g, int r, int kw, SegSmem& sm,
+                                             int lane) {
+  GaussAcc<QG> acc;
+  staged_load_gauss<QG>(acc, grec, g0, QG);
+  // this warp's sub-range [a, b) of every piece, as segments into `stage`
+  const int kl = max(kw - r, st.ks_lo), kh = min(kw + r, st.ks_hi);
+  int stt[4], ln[4], sum = 0, ne = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int p = lane * 4 + k;
+    stt[k] = 0;
+    ln[k] = 0;
+    if (p < st.npieces) {
+      const int c = st.pc[p];
+      const int q = (int)(((float)c + 0.5f) / (float)st.nj);
+      const int ii = st.ilo + q, jj = st.jlo + (c - q * st.nj);
+      const int base = (ii * g + jj) * g;
+      const int a = max(__ldg(pstart + base + kl), st.pga[p]);
+      const int b = min(__ldg(pstart + base + kh + 1), st.pga[p] + st.plen[p]);
+      if (b > a) {
+        stt[k] = st.pso[p] + (a - st.pga[p]);
+        ln[k] = b - a;
+      }
+    }
+    sum += ln[k];
+    ne += ln[k] > 0;
+  }
+  int tot, netot;
+  int off = warp_excl_scan(sum, lane, &tot);
+  int e = warp_excl_scan(ne, lane, &netot);
+  LaneSegs L;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    L.pre[k] = off;
+    L.len[k] = ln[k];
+    L.st[k] = stt[k];
+    if (ln[k] > 0) sm.delta[e++] = stt[k] - off;
+    off += ln[k];
+  }
+  L.tot = tot;
+  const unsigned upto = 0xffffffffu >> (31 - lane);
+  for (int w0 = 0; w0 < tot; w0 += 32 * kBmWords) {
+    Cursor4 cur{build_window(L, w0, sm, lane)};
+    const int wend = min(tot, w0 + 32 * kBmWords);
+    for (int base = w0; base < wend; base += 128) {
+      int v[4], ei[4];
+      cur.next(sm, w0, base, upto, lane, v, ei);
+      float4 pt[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) pt[i] = v[i] < wend ? stage[ei[i]] : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (v[0] < wend) acc.pair(pt[0], pt[1]);
+      if (v[2] < wend) acc.pair(pt[2], pt[3]);
+    }
+    __syncwarp();
+  }
+  // lane-reduce this round's sums and add them to the warp's smem partials
+  constexpr int NV = QG == 1 ? 16 : 32;
+  float vals[32];
+#pragma unroll
+  for (int k = 0; k < QG; ++k) {
+    vals[16 * k + 0] = lo(acc.S[k]) + hi(acc.S[k]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) vals[16 * k + 1 + c] = lo(acc.T[k][c]) + hi(acc.T[k][c]);
+#pragma unroll
+    for (int c = 0; c < 6; ++c) vals[16 * k + 4 + c] = lo(acc.A6[k][c]) + hi(acc.A6[k][c]);
+#pragma unroll
+    for (int c = 10; c < 16; ++c) vals[16 * k + c] = 0.f;
+  }
+#pragma unroll
+  for (int i = 16 * QG; i < 32; ++i) vals[i] = 0.f;
+  const float red = transpose_reduce<NV>(vals, lane);
+  constexpr int SH = RedShift<NV>::value;
+  const int idx = lane >> SH;
+  if ((lane & ((1 << SH) - 1)) == 0 && (idx & 15) < 10) part[idx] += red;
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(kSbS * 32, (16 / kSbS) > 0 ? (16 / kSbS) : 1) backward_staged_kernel(
+    const GaussSoA grec, const int* __restrict__ gstart, int g, int r, const float4* __restrict__ prec,
+    const int* __restrict__ pstart, const int* __restrict__ strips, const int* __restrict__ nstrips_dev,
+    float* __restrict__ acc10) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float4* stage = reinterpret_cast<float4*>(smem_raw);
+  SegSmem* segs = reinterpret_cast<SegSmem*>(smem_raw + sizeof(float4) * kSbCap);
+  StageSmem& st = *reinterpret_cast<StageSmem*>(smem_raw + sizeof(float4) * kSbCap + sizeof(SegSmem) * kSbS);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    mbar_init(&st.bar, 1);
+    st.phase = 0;
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  const int nstrips = *nstrips_dev;
+  const int nkb = (g + kSbS - 1) / kSbS;
+  for (int si = blockIdx.x; si < nstrips; si += gridDim.x) {
+    const int sk = strips[si];
+    const int kb = sk % nkb, col = sk / nkb;
+    const int j = col % g, i = col / g;
+    const int k0 = kb * kSbS;
+    const int kc = min(kSbS, g - k0);
+    // strip geometry + per-column window ranges
+    if (threadIdx.x == 0) {
+      st.ilo = max(i - r, 0);
+      st.jlo = max(j - r, 0);
+      st.nj = min(j + r, g - 1) - st.jlo + 1;
+      st.ncol = (min(i + r, g - 1) - st.ilo + 1) * st.nj;
+      st.ks_lo = max(k0 - r, 0);
+      st.ks_hi = min(k0 + kc - 1 + r, g - 1);
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < st.ncol; c += blockDim.x) {
+      const int q = (int)(((float)c + 0.5f) / (float)st.nj);
+      const int ii = st.ilo + q, jj = st.jlo + (c - q * st.nj);
+      const int base = (ii * g + jj) * g;
+      const int a = __ldg(pstart + base + st.ks_lo), b = __ldg(pstart + base + st.ks_hi + 1);
+      st.cst[c] = a;
+      st.clen[c] = b - a;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      st.bc = 0;
+      st.bstart = st.cst[0];
+      st.brem = st.clen[0];
+      st.done = 0;
+    }
+    // this warp's cell and its first <= 2 Gaussians (later chunks -> overflow kernel)
+    const int kw = k0 + warp;
+    const int cell = (i * g + j) * g + kw;
+    const int g0 = warp < kc ? __ldg(gstart + cell) : 0;
+    const int ngc = warp < kc ? __ldg(gstart + cell + 1) - g0 : 0;
+    const int ng = min(ngc, 2);
+    float* part = st.part[warp];
+    part[lane] = 0.f;
+    __syncthreads();
+    while (true) {
+      if (threadIdx.x == 0) {
+        const int bytes = next_round(st);
+        fence_proxy_async();
+        mbar_arrive_expect(&st.bar, (uint32_t)bytes);
+      }
+      __syncthreads();
+      if (warp == 0) {
+        for (int p = lane; p < st.npieces; p += 32)
+          bulk_g2s(stage + st.pso[p], prec + st.pga[p], (uint32_t)st.plen[p] * 16u, &st.bar);
+      }
+      mbar_wait(&st.bar, st.phase);
+      if (ng == 2) staged_round<2>(grec, g0, part, stage, st, pstart, g, r, kw, segs[warp], lane);
+      if (ng == 1) staged_round<1>(grec, g0, part, stage, st, pstart, g, r, kw, segs[warp], lane);
+      const int done = st.done;
+      __syncthreads();
+      if (threadIdx.x == 0) st.phase ^= 1;
+      __syncthreads();
+      if (done) break;
+    }
+    if (lane < 10 * ng) acc10[(int64_t)(g0 + lane / 10) * 10 + lane % 10] = part[(lane / 10) * 16 + lane % 10];
+  }
+}
+
+// strip flags: strip (i, j, kb) is live if its cells hold at least one Gaussian
+__global__ void strip_flags_kernel(const int* __restrict__ starts, int g, int s, int* __restrict__ flags) {
+  const int nkb = (g + s - 1) / s;
+  const int64_t nstrips = (int64_t)g * g * nkb;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nstrips; t += (int64_t)gridDim.x * blockDim.x) {
+    const int kb = (int)(t % nkb);
+    const int64_t col = t / nkb;
+    const int k0 = kb * s, k1 = min(k0 + s, g);
+    flags[t] = starts[col * g + k1] > starts[col * g + k0] ? 1 : 0;
+  }
+}
+
+__global__ void strip_compact_kernel(const int* __restrict__ flags, const int* __restrict__ scan, int64_t n,
+                                     int* __restrict__ out, int* __restrict__ count) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    if (flags[t]) out[scan[t]] = (int)t;
+    if (t == n - 1) *count = scan[t] + flags[t];
+  }
+}
+
+// overflow items: chunk starts p (step 2) of cells with > 2 Gaussians, past the first chunk
+__global__ void overflow_flags_kernel(const uint32_t* __restrict__ keys, const int* __restrict__ starts, int64_t n,
+                                      int* __restrict__ flags) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    const int d = (int)(p - starts[keys[p]]);
+    flags[p] = (d >= 2 && (d & 1) == 0) ? 1 : 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Host launchers
 // ---------------------------------------------------------------------------
 static int g_num_sms = 0;
@@ -951,6 +1259,57 @@ void launch_forward(bool with_h, const float* grec_raw, int64_t n_gauss, const i
     MG_LAUNCH(forward_kernel<false><<<(unsigned)persistent_blocks(k, kFwdWarps * 32, want), kFwdWarps * 32, 0, st>>>(
         grec, gstart, g, r, prec, pkey, pstart, items, nitems, out4, cnt));
   }
+}
+
+size_t staged_smem_bytes() { return sizeof(float4) * kSbCap + sizeof(SegSmem) * kSbS + sizeof(StageSmem); }
+
+size_t backward_staged_ws_bytes(int64_t n, int g) {
+  const int64_t nstrips = (int64_t)g * g * ((g + kSbS - 1) / kSbS);
+  const int64_t m = nstrips > n ? nstrips : n;
+  return 4 * ((((size_t)m * 4) + 255) & ~(size_t)255) + 512 + scan_workspace_bytes(m);
+}
+
+// Staged backward: strips for the first <= 2 Gaussians of every cell, the
+// global-memory item kernel for the rest (rare at lattice densities).
+void launch_backward_staged(const float* grec_raw, int64_t n_gauss, const uint32_t* gkey, const int* gstart, int g,
+                            int r, const float4* prec, const int* pstart, float* acc10, void* ws, cudaStream_t st) {
+  if (n_gauss <= 0) return;
+  const int nkb = (g + kSbS - 1) / kSbS;
+  const int64_t nstrips = (int64_t)g * g * nkb;
+  const int64_t m = nstrips > n_gauss ? nstrips : n_gauss;
+  const size_t al = (((size_t)m * 4) + 255) & ~(size_t)255;
+  char* w = (char*)ws;
+  int* flags = (int*)w;
+  int* scan = (int*)(w + al);
+  int* list = (int*)(w + 2 * al);
+  int* counts = (int*)(w + 4 * al);
+  void* sws = w + 4 * al + 512;
+  MG_LAUNCH(strip_flags_kernel<<<grid_for(nstrips), 256, 0, st>>>(gstart, g, kSbS, flags));
+  excl_scan(flags, scan, nstrips, sws, st);
+  MG_LAUNCH(strip_compact_kernel<<<grid_for(nstrips), 256, 0, st>>>(flags, scan, nstrips, list, counts));
+  const GaussSoA grec = gauss_soa(grec_raw, n_gauss);
+  static bool attr = false;
+  const size_t smem = staged_smem_bytes();
+  if (!attr) {
+    cudaFuncSetAttribute(backward_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, backward_staged_kernel, kSbS * 32, smem);
+  int64_t blocks = (int64_t)num_sms() * (per_sm > 0 ? per_sm : 1);
+  if (blocks > nstrips) blocks = nstrips;
+  MG_LAUNCH(backward_staged_kernel<<<(unsigned)blocks, kSbS * 32, smem, st>>>(grec, gstart, g, r, prec, pstart, list,
+                                                                             counts, acc10));
+  // overflow chunks (cells with > 2 Gaussians) through the item kernel
+  int* oflags = flags;
+  int* oscan = scan;
+  int* oitems = (int*)(w + 3 * al);
+  MG_LAUNCH(overflow_flags_kernel<<<grid_for(n_gauss), 256, 0, st>>>(gkey, gstart, n_gauss, oflags));
+  excl_scan(oflags, oscan, n_gauss, sws, st);
+  MG_LAUNCH(item_compact_kernel<<<grid_for(n_gauss), 256, 0, st>>>(oflags, oscan, n_gauss, oitems, counts + 1));
+  const int64_t want = (n_gauss / 2 + kBwdWarps) / kBwdWarps;
+  MG_LAUNCH(backward_kernel<<<(unsigned)persistent_blocks(backward_kernel, kBwdWarps * 32, want), kBwdWarps * 32, 0,
+                              st>>>(grec, gkey, gstart, g, r, prec, pstart, oitems, counts + 1, acc10));
 }
 
 void launch_backward(const float* grec_raw, int64_t n_gauss, const uint32_t* gkey, const int* gstart, int g, int r,

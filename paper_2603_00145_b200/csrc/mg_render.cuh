@@ -30,6 +30,10 @@ void launch_backward(const float* grec, int64_t n_gauss, const uint32_t* gkey, c
                      const float4* prec, const int* pstart, const int* items, const int* nitems, int64_t max_items,
                      float* acc10, cudaStream_t st);
 
+size_t backward_staged_ws_bytes(int64_t n, int g);
+void launch_backward_staged(const float* grec, int64_t n_gauss, const uint32_t* gkey, const int* gstart, int g, int r,
+                            const float4* prec, const int* pstart, float* acc10, void* ws, cudaStream_t st);
+
 // epilogues / training
 void launch_forward_finish(const float4* out4, const int* cnt, const int* inv, int64_t b, int ntaps,
                            const double* tap_w, double* out_i, float* out_i32, int64_t* out_cnt, cudaStream_t st);

@@ -221,7 +221,7 @@ def _stage_psf(field, gd, p6, al, c_d, s_d, rot_d, tr_d, k, g, psf, with_h, radi
     prec = dv.empty((ns, 4), torch.float32)
     x = dv.empty((ns, 3), torch.float64)
     ws = dv.workspace(max(L.mg_points_workspace_bytes(ns, g), L.mg_forward_workspace_bytes(ns),
-                          L.mg_backward_workspace_bytes(field.count)))
+                          L.mg_backward_workspace_bytes(field.count, g)))
     N.check(L.mg_bin_points(N.ptr(c_d), N.ptr(s_d), b, t, N.ptr(off), N.ptr(dirs), N.ptr(rot_d), N.ptr(tr_d), k, g,
                             N.ptr(pkey), N.ptr(pinv), N.ptr(pstart), N.ptr(prec), N.ptr(x), N.ptr(ws), ws.numel(),
                             st), "bin_points")

@@ -214,7 +214,7 @@ class _StepBuffers:
         self.scalars = dv.zeros((4,), torch.float64)  # data loss, aniso loss, ssim sum, spare
         self.err = dv.zeros((1,), torch.int32)
         wsb = max(L.mg_bin_workspace_bytes(n, g), L.mg_points_workspace_bytes(ns, g),
-                  L.mg_forward_workspace_bytes(ns), L.mg_backward_workspace_bytes(n))
+                  L.mg_forward_workspace_bytes(ns), L.mg_backward_workspace_bytes(n, g))
         self.ws = dv.empty((wsb,), torch.uint8)
         self.ssim_ws = None
 

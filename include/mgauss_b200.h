@@ -67,6 +67,10 @@ int mg_bin_f64(const double *pos, int64_t n, int64_t grid_res, uint32_t *keys_so
 /* keys_sorted[p] = the cell c with cell_starts[c] <= p < cell_starts[c+1]
  * (follows a caller-supplied CSR exactly, like the reference kernels do). */
 int mg_keys_from_csr(const int32_t *cell_starts, int64_t ncell, uint32_t *keys_sorted, void *stream);
+/* Device-wide exclusive scan of int32 (out may alias in); ws sized by
+ * mg_scan_workspace_bytes.  Exposed for tests and the host layer. */
+size_t mg_scan_workspace_bytes(int64_t n);
+int mg_excl_scan_i32(const int32_t *in, int32_t *out, int64_t n, void *ws, size_t ws_bytes, void *stream);
 /* int64 -> int32 copy (device CSR from the reference's int64 arrays). */
 int mg_i64_to_i32(const int64_t *src, int64_t n, int32_t *dst, void *stream);
 /* int32 -> int64 copies in the reference dtype (PartitionGrid fields). */

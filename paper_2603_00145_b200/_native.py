@@ -34,6 +34,8 @@ SIGNATURES = {
     "mg_i32_to_i64": (ctypes.c_int, [P, I64, P, P]),
     "mg_i64_to_i32": (ctypes.c_int, [P, I64, P, P]),
     "mg_keys_from_csr": (ctypes.c_int, [P, I64, P, P]),
+    "mg_scan_workspace_bytes": (SZ, [I64]),
+    "mg_excl_scan_i32": (ctypes.c_int, [P, P, I64, P, SZ, P]),
     "mg_activate": (ctypes.c_int, [P, P, P, P, I64, P, P, P, P]),
     "mg_activate_f64": (ctypes.c_int, [P, P, P, I64, P, P, P, P, P, P, P]),
     "mg_points_workspace_bytes": (SZ, [I64, I64]),

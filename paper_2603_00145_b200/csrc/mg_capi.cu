@@ -219,6 +219,14 @@ int mg_bin_f64(const double* pos, int64_t n, int64_t g, uint32_t* keys_sorted, i
   return do_bin(nullptr, pos, n, g, keys_sorted, cell_indices, cell_starts, ws, wsb, S(stream));
 }
 
+size_t mg_scan_workspace_bytes(int64_t n) { return scan_workspace_bytes(n); }
+
+int mg_excl_scan_i32(const int32_t* in, int32_t* out, int64_t n, void* ws, size_t wsb, void* stream) {
+  if (wsb < scan_workspace_bytes(n)) return fail("mg_excl_scan_i32: workspace too small");
+  excl_scan(in, out, n, ws, S(stream));
+  return cuda_status();
+}
+
 int mg_keys_from_csr(const int32_t* cs, int64_t ncell, uint32_t* keys, void* stream) {
   if (ncell > 0) MG_LAUNCH(keys_from_csr_kernel<<<grid_of(ncell), 256, 0, S(stream)>>>(cs, ncell, keys));
   return cuda_status();

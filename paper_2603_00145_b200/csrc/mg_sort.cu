@@ -59,27 +59,89 @@ __global__ void __launch_bounds__(kScanThreads) scan_tiles(const int* __restrict
   if (threadIdx.x == 0 && tile_sums) tile_sums[blockIdx.x] = tot;
 }
 
-__global__ void scan_add(int* __restrict__ out, int64_t n, const int* __restrict__ tile_offs) {
-  const int64_t e = (int64_t)blockIdx.x * kScanTile + threadIdx.x;
-  const int add = tile_offs[blockIdx.x];
+// Single-pass exclusive scan with decoupled look-back: every tile publishes
+// its aggregate (flag A) and then its inclusive prefix (flag P); a tile's
+// exclusive prefix comes from a warp-parallel look-back over predecessors.
+// Tile ids are handed out in launch order by an atomic ticket, so every
+// predecessor is already running (forward progress).
+constexpr unsigned long long kFlagA = 1ull << 32, kFlagP = 2ull << 32;
+
+__global__ void __launch_bounds__(kScanThreads) scan_lookback(const int* __restrict__ in, int* __restrict__ out,
+                                                              int64_t n, unsigned long long* __restrict__ state,
+                                                              int* __restrict__ ticket) {
+  __shared__ int s_warp[kScanThreads / 32 + 1];
+  __shared__ int s_tile, s_prefix;
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
+  __syncthreads();
+  const int tile = s_tile;
+  const int64_t base = (int64_t)tile * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  int v[kScanItems];
+  int sum = 0;
 #pragma unroll
   for (int i = 0; i < kScanItems; ++i) {
-    int64_t k = e + (int64_t)i * kScanThreads;
-    if (k < n) out[k] += add;
+    int64_t e = base + i;
+    v[i] = e < n ? in[e] : 0;
+    sum += v[i];
+  }
+  int tot;
+  int off = block_excl_scan(sum, s_warp, &tot);
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x < 32) {
+    volatile unsigned long long* vs = state;
+    if (tile == 0) {
+      if (lane == 0) {
+        vs[0] = kFlagP | (unsigned)tot;
+        __threadfence();
+        s_prefix = 0;
+      }
+    } else {
+      if (lane == 0) {
+        vs[tile] = kFlagA | (unsigned)tot;
+        __threadfence();
+      }
+      int prefix = 0;
+      int look = tile - 1;
+      while (true) {
+        const int t = look - lane;
+        unsigned long long w = kFlagP;  // before tile 0: inclusive prefix 0
+        if (t >= 0) {
+          do {
+            w = vs[t];
+          } while ((w >> 32) == 0);
+        }
+        const unsigned pmask = __ballot_sync(MG_FULL, (w >> 32) == 2);
+        const int first_p = pmask ? __ffs(pmask) - 1 : 32;  // lanes up to the first P contribute
+        int val = (lane <= first_p) ? (int)(w & 0xffffffffu) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(MG_FULL, val, o);
+        prefix += val;
+        if (pmask) break;
+        look -= 32;
+      }
+      if (lane == 0) {
+        vs[tile] = kFlagP | (unsigned)(prefix + tot);
+        __threadfence();
+        s_prefix = prefix;
+      }
+    }
+  }
+  __syncthreads();
+  off += s_prefix;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    int64_t e = base + i;
+    if (e < n) out[e] = off;
+    off += v[i];
   }
 }
 
 size_t scan_workspace_bytes(int64_t n) {
-  size_t b = 0;
-  while (n > kScanTile) {
-    int64_t tiles = (n + kScanTile - 1) / kScanTile;
-    b += ((size_t)tiles * 2 * sizeof(int) + 255) & ~(size_t)255;
-    n = tiles;
-  }
-  return b + 256;
+  int64_t tiles = (n + kScanTile - 1) / kScanTile;
+  if (tiles < 1) tiles = 1;
+  return (((size_t)tiles * 8 + 255) & ~(size_t)255) + 256;
 }
 
-// out[i] = sum_{j<i} in[j]; out may alias in.  Writes total to *total_dev if given.
+// out[i] = sum_{j<i} in[j]; out may alias in (each tile reads before it writes).
 void excl_scan(const int* in, int* out, int64_t n, void* ws, cudaStream_t st) {
   if (n <= 0) return;
   int64_t tiles = (n + kScanTile - 1) / kScanTile;
@@ -87,47 +149,51 @@ void excl_scan(const int* in, int* out, int64_t n, void* ws, cudaStream_t st) {
     MG_LAUNCH(scan_tiles<<<1, kScanThreads, 0, st>>>(in, out, n, nullptr));
     return;
   }
-  int* sums = (int*)ws;
-  int* offs = sums + tiles;
-  size_t used = ((size_t)tiles * 2 * sizeof(int) + 255) & ~(size_t)255;
-  MG_LAUNCH(scan_tiles<<<(unsigned)tiles, kScanThreads, 0, st>>>(in, out, n, sums));
-  excl_scan(sums, offs, tiles, (char*)ws + used, st);
-  MG_LAUNCH(scan_add<<<(unsigned)tiles, kScanThreads, 0, st>>>(out, n, offs));
+  unsigned long long* state = (unsigned long long*)ws;
+  int* ticket = (int*)((char*)ws + (((size_t)tiles * 8 + 255) & ~(size_t)255));
+  cudaMemsetAsync(ws, 0, (((size_t)tiles * 8 + 255) & ~(size_t)255) + 4, st);
+  MG_LAUNCH(scan_lookback<<<(unsigned)tiles, kScanThreads, 0, st>>>(in, out, n, state, ticket));
 }
 
 // ---------------------------------------------------------------------------
-// Stable LSD radix sort, 8-bit digits.
+// Stable LSD radix sort, digits of <= 10 bits (2 passes up to 20-bit keys).
 // ---------------------------------------------------------------------------
 constexpr int kRsThreads = 256;
 constexpr int kRsRounds = 8;
 constexpr int kRsTile = kRsThreads * kRsRounds;  // 2048 elements per block
 constexpr int kRsWarps = kRsThreads / 32;
 
+template <int DB>
 __global__ void __launch_bounds__(kRsThreads) rs_hist(const uint32_t* __restrict__ keys, int64_t n, int shift,
                                                       int* __restrict__ hist, int nblocks) {
-  __shared__ int cnt[256];
-  cnt[threadIdx.x] = 0;
+  constexpr int NB = 1 << DB;
+  __shared__ int cnt[NB];
+  for (int d = threadIdx.x; d < NB; d += kRsThreads) cnt[d] = 0;
   __syncthreads();
   const int64_t base = (int64_t)blockIdx.x * kRsTile;
 #pragma unroll
   for (int r = 0; r < kRsRounds; ++r) {
     int64_t e = base + r * kRsThreads + threadIdx.x;
-    if (e < n) atomicAdd(&cnt[(keys[e] >> shift) & 255u], 1);
+    if (e < n) atomicAdd(&cnt[(keys[e] >> shift) & (NB - 1)], 1);
   }
   __syncthreads();
-  hist[threadIdx.x * nblocks + blockIdx.x] = cnt[threadIdx.x];
+  for (int d = threadIdx.x; d < NB; d += kRsThreads) hist[d * nblocks + blockIdx.x] = cnt[d];
 }
 
+template <int DB>
 __global__ void __launch_bounds__(kRsThreads) rs_scatter(const uint32_t* __restrict__ kin,
                                                          const int* __restrict__ vin, uint32_t* __restrict__ kout,
                                                          int* __restrict__ vout, int64_t n, int shift,
                                                          const int* __restrict__ offs, int nblocks) {
-  __shared__ int s_base[256];
-  __shared__ int s_wcnt[kRsWarps][256];
+  constexpr int NB = 1 << DB;
+  __shared__ int s_base[NB];
+  __shared__ int s_wcnt[kRsWarps][NB];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  s_base[threadIdx.x] = offs[threadIdx.x * nblocks + blockIdx.x];
+  for (int d = threadIdx.x; d < NB; d += kRsThreads) {
+    s_base[d] = offs[d * nblocks + blockIdx.x];
 #pragma unroll
-  for (int w = 0; w < kRsWarps; ++w) s_wcnt[w][threadIdx.x] = 0;
+    for (int w = 0; w < kRsWarps; ++w) s_wcnt[w][d] = 0;
+  }
   __syncthreads();
   const int64_t base = (int64_t)blockIdx.x * kRsTile;
   const unsigned lt = (1u << lane) - 1u;
@@ -136,14 +202,13 @@ __global__ void __launch_bounds__(kRsThreads) rs_scatter(const uint32_t* __restr
     bool valid = e < n;
     uint32_t k = valid ? kin[e] : 0u;
     int v = valid ? vin[e] : 0;
-    int d = valid ? (int)((k >> shift) & 255u) : 256;  // 256 = sentinel digit
+    int d = valid ? (int)((k >> shift) & (NB - 1)) : NB;  // NB = sentinel digit
     unsigned peers = __match_any_sync(MG_FULL, d);
     int rank = __popc(peers & lt);
     if (valid && rank == 0) s_wcnt[warp][d] = __popc(peers);
     __syncthreads();
-    {
+    for (int dgt = threadIdx.x; dgt < NB; dgt += kRsThreads) {
       // digit-major prefix across warps, in warp order (stable)
-      int dgt = threadIdx.x;
       int run = s_base[dgt];
 #pragma unroll
       for (int w = 0; w < kRsWarps; ++w) {
@@ -160,8 +225,10 @@ __global__ void __launch_bounds__(kRsThreads) rs_scatter(const uint32_t* __restr
       vout[pos] = v;
     }
     __syncthreads();
+    for (int dgt = threadIdx.x; dgt < NB; dgt += kRsThreads) {
 #pragma unroll
-    for (int w = 0; w < kRsWarps; ++w) s_wcnt[w][threadIdx.x] = 0;
+      for (int w = 0; w < kRsWarps; ++w) s_wcnt[w][dgt] = 0;
+    }
     __syncthreads();
   }
 }
@@ -176,8 +243,17 @@ static inline size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 size_t radix_workspace_bytes(int64_t n) {
   int64_t nb = (n + kRsTile - 1) / kRsTile;
   if (nb < 1) nb = 1;
-  return 2 * align256((size_t)n * 4) + 2 * align256((size_t)n * 4) + 2 * align256((size_t)256 * nb * 4) +
-         scan_workspace_bytes(256 * nb);
+  const size_t bins = (size_t)1 << 10;
+  return 2 * align256((size_t)n * 4) + 2 * align256((size_t)n * 4) + 2 * align256(bins * nb * 4) +
+         scan_workspace_bytes((int64_t)bins * nb);
+}
+
+template <int DB>
+static void rs_pass(const uint32_t* kin, const int* vin, uint32_t* ko, int* vo, int64_t n, int shift, int* hist,
+                    int* offs, int64_t nb, void* sws, cudaStream_t st) {
+  MG_LAUNCH(rs_hist<DB><<<(unsigned)nb, kRsThreads, 0, st>>>(kin, n, shift, hist, (int)nb));
+  excl_scan(hist, offs, ((int64_t)1 << DB) * nb, sws, st);
+  MG_LAUNCH(rs_scatter<DB><<<(unsigned)nb, kRsThreads, 0, st>>>(kin, vin, ko, vo, n, shift, offs, (int)nb));
 }
 
 // Sorts (keys, values := 0..n-1) by the low `bits` bits of keys, stably.
@@ -196,12 +272,14 @@ void radix_sort_pairs(const uint32_t* keys_in, uint32_t* keys_out, int* vals_out
   int* vB = (int*)w;
   w += align256((size_t)n * 4);
   int* hist = (int*)w;
-  w += align256((size_t)256 * nb * 4);
+  w += align256((size_t)1024 * nb * 4);
   int* offs = (int*)w;
-  w += align256((size_t)256 * nb * 4);
+  w += align256((size_t)1024 * nb * 4);
   void* sws = w;
+  // fewest passes with digits of <= 8 bits (cheaper scatter prefix than 10-bit digits)
   int passes = (bits + 7) / 8;
   if (passes < 1) passes = 1;
+  const int db = (bits + passes - 1) / passes;
   MG_LAUNCH(iota_kernel<<<(unsigned)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096), 256, 0, st>>>(vA, n));
   const uint32_t* kin = keys_in;
   const int* vin = vA;
@@ -209,9 +287,18 @@ void radix_sort_pairs(const uint32_t* keys_in, uint32_t* keys_out, int* vals_out
     bool last = p == passes - 1;
     uint32_t* ko = last ? keys_out : ((p & 1) ? kA : kB);
     int* vo = last ? vals_out : ((p & 1) ? vA : vB);
-    MG_LAUNCH(rs_hist<<<(unsigned)nb, kRsThreads, 0, st>>>(kin, n, 8 * p, hist, (int)nb));
-    excl_scan(hist, offs, 256 * nb, sws, st);
-    MG_LAUNCH(rs_scatter<<<(unsigned)nb, kRsThreads, 0, st>>>(kin, vin, ko, vo, n, 8 * p, offs, (int)nb));
+    const int shift = db * p;
+    switch (db) {
+      case 1: case 2: case 3: case 4: case 5: case 6:
+        rs_pass<6>(kin, vin, ko, vo, n, shift, hist, offs, nb, sws, st);
+        break;
+      case 7: case 8:
+        rs_pass<8>(kin, vin, ko, vo, n, shift, hist, offs, nb, sws, st);
+        break;
+      default:
+        rs_pass<10>(kin, vin, ko, vo, n, shift, hist, offs, nb, sws, st);
+        break;
+    }
     kin = ko;
     vin = vo;
   }

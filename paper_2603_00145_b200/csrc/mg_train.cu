@@ -198,47 +198,78 @@ __global__ void epilogue_f64_kernel(const double* __restrict__ d_mu, const doubl
 // (render.py:246-273), then the quaternion chain.
 // ---------------------------------------------------------------------------
 // Each thread walks a contiguous chunk of sub-points, accumulating in float64
-// registers while the slice id is unchanged (taps of a point and the SSIM
-// slice are contiguous runs), and flushes 12 sums per run with global fp64
-// atomics -- avoids the single-bin contention of the per-step SSIM slice.
+// registers while the slice id is unchanged (the taps of a point, and the
+// per-step SSIM slice, are contiguous runs).  Completed runs flush 12 sums
+// with global fp64 atomics; the run still open at the end of the chunk is
+// first reduced across the warp when all 32 lanes share its slice (the SSIM
+// slice range), which removes the same-address atomic contention there.
 __global__ void transform_reduce_kernel(const double* __restrict__ dpoints, const double* __restrict__ coords,
                                         const int64_t* __restrict__ sids, int64_t b, int ntaps,
                                         const double* __restrict__ tap_off, const double* __restrict__ dirs, int k,
                                         double* __restrict__ out12) {
-  constexpr int CH = 32;
+  constexpr int CH = 8;
   const int64_t total = b * ntaps;
-  for (int64_t c0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * CH; c0 < total;
-       c0 += (int64_t)gridDim.x * blockDim.x * CH) {
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  const int64_t nloop = (total + CH * nthreads - 1) / (CH * nthreads);
+  for (int64_t it = 0; it < nloop; ++it) {
+    const int64_t c0 = (it * nthreads + (int64_t)blockIdx.x * blockDim.x + threadIdx.x) * CH;
     const int64_t c1 = min(total, c0 + CH);
     int64_t cur = -1;
     double acc[12];
+#pragma unroll
     for (int i = 0; i < 12; ++i) acc[i] = 0.0;
     for (int64_t j = c0; j < c1; ++j) {
-      int64_t pb = j / ntaps;
-      int t = (int)(j - pb * ntaps);
-      int64_t s = sids[pb];
+      const int64_t pb = j / ntaps;
+      const int t = (int)(j - pb * ntaps);
+      const int64_t s = sids[pb];
       if (s < 0 || s >= k) continue;
       if (s != cur) {
-        if (cur >= 0)
+        if (cur >= 0) {
+#pragma unroll
           for (int i = 0; i < 12; ++i)
             if (acc[i] != 0.0) atomicAdd(out12 + 12 * cur + i, acc[i]);
+        }
+#pragma unroll
         for (int i = 0; i < 12; ++i) acc[i] = 0.0;
         cur = s;
       }
       double c[3] = {coords[3 * pb], coords[3 * pb + 1], coords[3 * pb + 2]};
       if (tap_off) {
-        double o = tap_off[t];
+        const double o = tap_off[t];
+#pragma unroll
         for (int a = 0; a < 3; ++a) c[a] = __dadd_rn(c[a], __dmul_rn(o, dirs[3 * s + a]));
       }
-      double h[3] = {dpoints[3 * j], dpoints[3 * j + 1], dpoints[3 * j + 2]};
+      const double h[3] = {dpoints[3 * j], dpoints[3 * j + 1], dpoints[3 * j + 2]};
+#pragma unroll
       for (int a = 0; a < 3; ++a) {
         acc[a] += h[a];
+#pragma unroll
         for (int bb = 0; bb < 3; ++bb) acc[3 + 3 * a + bb] += h[a] * c[bb];
       }
     }
-    if (cur >= 0)
+    // open run: warp-reduce when the whole warp shares its slice
+    const long long key = (long long)cur;
+    const unsigned peers = __match_any_sync(MG_FULL, key);
+    if (peers == MG_FULL) {
+      if (cur >= 0) {
+#pragma unroll
+        for (int i = 0; i < 12; ++i) {
+          double v = acc[i];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(MG_FULL, v, o);
+          acc[i] = v;
+        }
+        if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+          for (int i = 0; i < 12; ++i)
+            if (acc[i] != 0.0) atomicAdd(out12 + 12 * cur + i, acc[i]);
+        }
+      }
+    } else if (cur >= 0) {
+#pragma unroll
       for (int i = 0; i < 12; ++i)
         if (acc[i] != 0.0) atomicAdd(out12 + 12 * cur + i, acc[i]);
+    }
   }
 }
 
@@ -452,7 +483,7 @@ void launch_transform_grads(const double* dpoints, const double* coords, const i
   if (k <= 0) return;
   cudaMemsetAsync(acc12, 0, sizeof(double) * 12 * k, st);
   if (b > 0) {
-    int64_t chunks = (b * ntaps + 31) / 32;
+    int64_t chunks = (b * ntaps + 7) / 8;
     MG_LAUNCH(transform_reduce_kernel<<<gridn(chunks, 128), 128, 0, st>>>(dpoints, coords, sids, b, ntaps, tap_off, dirs, k,
                                                                 acc12));
   }

@@ -538,12 +538,17 @@ class Trainer:
             p.sub_(cfg.lr_nrf * (m / bc1) / (torch.sqrt(v / bc2) + cfg.adam_eps))
 
     def _allreduce(self, B):
-        import torch.distributed as tdist
+        """One flat all-reduce(sum) of the step's partial sums (parallel.py)."""
+        from .parallel import FlatAllReduce
 
-        tdist.all_reduce(B.acc10, group=self.dist)
-        if self.k:
-            tdist.all_reduce(B.g7, group=self.dist)
-        tdist.all_reduce(B.scalars, group=self.dist)
+        key = id(B)
+        if getattr(self, "_ar_key", None) != key:
+            f32 = [B.acc10]
+            f64 = [B.scalars] + ([B.g7] if self.k else [])
+            self._ar = (FlatAllReduce(f32, self.dist), FlatAllReduce(f64, self.dist))
+            self._ar_key = key
+        for ar in self._ar:
+            ar()
 
     def run(self, iterations=None):
         target = self.config.total_iters if iterations is None else self.iteration + iterations

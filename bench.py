@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--config", default=CONFIG)
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--cpu-sample-points", type=int, default=65536)
+    ap.add_argument("--no-inference", action="store_true")
     return ap.parse_args()
 
 
@@ -338,6 +339,15 @@ def run_ours(args):
         cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
                "sample": f"{npts} batch points x {psf.ntaps} taps of one C2 step ({p} pairs, {dt:.1f} s), "
                          f"fwd+bwd incl. host epilogue"}
+    graph_used = tr._graph is not None
+    infer = None
+    if not args.no_inference:
+        try:
+            del tr
+            torch.cuda.empty_cache()
+            infer = inference_c5()
+        except Exception as exc:  # report, never fail the training bench
+            infer = {"error": repr(exc)[:200]}
     bytes_h2d = int(steps_idx[0].numel() * 8)
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -347,7 +357,7 @@ def run_ours(args):
                                "N=97,336 Gaussians (R=G=46), r=5, step = 65,536 batch + 25,600 SSIM-slice points",
                    "global_batch": nb * world, "pairs_per_step": pairs_total / args.steps,
                    "parallelism": f"dp{world}", "l2": "inputs and per-step working set fit in L2 (126 MB); "
-                   "steps differ in batch, no flush", "cuda_graph": tr._graph is not None},
+                   "steps differ in batch, no flush", "cuda_graph": graph_used},
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": bytes_h2d, "d2h_bytes_per_step": 32 + 4,
                 "path": "Trainer.step(): host RNG batch -> pinned H2D -> graph replay -> loss D2H"},
         "roofline": {"bound": "fp32", "achieved": achieved_pair / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
@@ -360,6 +370,7 @@ def run_ours(args):
                                               "frac": achieved_bwd / peak},
                                  "pairs_per_launch": kpairs, "flop_per_pair": [FLOP_FWD, FLOP_BWD]}},
         "cpu_baseline": cpu,
+        "inference": infer,
         "clocks": clocks,
         "gpu_launches": (nlaunch * args.steps) if nlaunch else None,
         "gpu_launches_note": "library kernels per step (mg_launch_count over one eager step) x timed steps; "
@@ -368,6 +379,69 @@ def run_ours(args):
     print(json.dumps(out))
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def inference_c5(reps=3):
+    """C5 (BASELINE.json configs[4]): sample a 512^3 node-inclusive volume over
+    [-1, 1]^3 from a 2,000,376-Gaussian field (R = G = 126, r = 5).  Synthetic
+    field per SURVEY §8(d): lattice positions + N(0, 0.1/R) jitter, identity +
+    N(0, 0.1) quaternions, log-scales log(1/R) + N(0, 0.1), logits N(0, 1)."""
+    import torch
+
+    from paper_2603_00145_b200 import _native as N
+    from paper_2603_00145_b200.core import lattice_node_positions
+    from paper_2603_00145_b200.render import sample_volume_device
+    from paper_2603_00145_b200.spatial import build_device
+
+    R = 126
+    n = R ** 3
+    rng = np.random.default_rng(7)
+    pos = lattice_node_positions(R) + rng.normal(0, 0.1 / R, (n, 3))
+    q = np.zeros((n, 4))
+    q[:, 0] = 1.0
+    q += rng.normal(0, 0.1, (n, 4))
+    ls = np.log(1.0 / R) + rng.normal(0, 0.1, (n, 3))
+    lg = rng.normal(0, 1, n)
+    dev = torch.device("cuda")
+    pos_d = torch.from_numpy(pos).float().to(dev)
+    q_d = torch.from_numpy(q).float().to(dev)
+    ls_d = torch.from_numpy(ls).float().to(dev)
+    lg_d = torch.from_numpy(lg).float().to(dev)
+    L = N.lib()
+    d = build_device(pos_d, R)
+    grec = torch.empty((n, 12), dtype=torch.float32, device=dev)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    N.check(L.mg_activate(N.ptr(pos_d), N.ptr(q_d), N.ptr(ls_d), N.ptr(lg_d), n, N.ptr(d["order"]), N.ptr(grec),
+                          N.ptr(err), N.stream_ptr()))
+    dims = (512, 512, 512)
+    bounds = ((-1.0, -1.0, -1.0), (1.0, 1.0, 1.0))
+    out = sample_volume_device(grec, n, d["starts"], R, 5, dims, bounds)  # warm-up
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        out = sample_volume_device(grec, n, d["starts"], R, 5, dims, bounds)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    # exact candidate-pair count: sum over voxels of the Gaussians within Chebyshev 5 cells of the voxel's cell
+    starts = d["starts"].cpu().numpy().astype(np.int64)
+    cnt = np.diff(starts).reshape(R, R, R)
+    ps = np.zeros((R + 1, R + 1, R + 1), np.int64)
+    ps[1:, 1:, 1:] = cnt.cumsum(0).cumsum(1).cumsum(2)
+    lo = np.clip(np.arange(R) - 5, 0, R)
+    hi = np.clip(np.arange(R) + 6, 0, R)
+    I0, J0, K0 = np.meshgrid(lo, lo, lo, indexing="ij")
+    I1, J1, K1 = np.meshgrid(hi, hi, hi, indexing="ij")
+    cand = (ps[I1, J1, K1] - ps[I0, J1, K1] - ps[I1, J0, K1] - ps[I1, J1, K0] + ps[I0, J0, K1] + ps[I0, J1, K0]
+            + ps[I1, J0, K0] - ps[I0, J0, K0])
+    ax = -1.0 + np.arange(512) * (2.0 / 511)
+    vc = np.bincount(np.clip(np.floor((ax + 1.0) * (R / 2.0)).astype(np.int64), 0, R - 1), minlength=R)
+    pairs = float(np.einsum("i,j,k,ijk->", vc, vc, vc, cand.astype(np.float64)))
+    peak = peak_fp32(L.mg_device_sm_count(), 1965.0)
+    return {"workload": "C5: 512^3 volume from 2,000,376 Gaussians (R=G=126, r=5), synthetic lattice field",
+            "ms": ms, "voxels_per_s": 512 ** 3 / (ms / 1e3), "pairs_per_s": pairs / (ms / 1e3),
+            "pairs": pairs, "roofline_frac_fp32": pairs * FLOP_FWD / (ms / 1e3) / peak}
 
 
 def kernel_times(tr, idx_list, nb, hw):

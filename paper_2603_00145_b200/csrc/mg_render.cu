@@ -536,8 +536,8 @@ __device__ __forceinline__ void fwd_item(const GaussSoA grec, const int* __restr
     for (int w0 = 0; w0 < tot; w0 += 32 * kBmWords) {
       const int sb0 = build_window(L, w0, sm, lane);
       const int wend = min(tot, w0 + 32 * kBmWords);
-      // one compact loop (small code: the kernel is instruction-cache bound
-      // when several unrolled paths are live on one SM)
+      // one compact loop: prefetching (two register sets) measured slower --
+      // the kernel is sensitive to code size and register pressure
       if (GPL == 1) {
         Cursor1 cur{sb0};
         for (int base = w0; base < wend; base += WIN) {

@@ -166,7 +166,7 @@ size_t points_ws(int64_t ns, int64_t g) {
          2048;
 }
 
-size_t fwd_ws(int64_t ns) { return al((size_t)ns * 4) + 256 + items_workspace_bytes(ns) + 1024; }
+size_t fwd_ws(int64_t ns) { return al((size_t)ns * 16) + 256 + items_workspace_bytes(ns) + 1024; }
 
 int do_bin(const float* pos32, const double* pos64, int64_t n, int64_t g, uint32_t* keys_sorted, int* order,
            int* starts, void* ws, size_t wsb, cudaStream_t st) {
@@ -286,11 +286,11 @@ int mg_forward(const void* grec, int64_t n_gauss, const int32_t* gstart, int64_t
   if (g < 1 || r < 0 || ns < 0) return fail("mg_forward: bad sizes");
   cudaStream_t st = S(stream);
   Bump w(ws, wsb);
-  int* items = w.take<int>(ns);
+  int4* items = w.take<int4>(ns);
   int* nitems = w.take<int>(1);
   if (!w.ok) return fail("mg_forward: workspace too small");
   if (ns == 0) return 0;
-  build_items(pkey_sorted, pstart, ns, fwd_qmax(), items, nitems, w.rest(), st);
+  build_items(pkey_sorted, pstart, ns, fwd_qmax(), items, nitems, w.rest(), st, fwd_dense_min());
   launch_forward(with_h != 0, (const float*)grec, n_gauss, gstart, (int)g, (int)r, (const float4*)prec, pkey_sorted,
                  pstart,
                  items, nitems, ns, (float4*)out4, counts, st);
@@ -339,10 +339,10 @@ int mg_backward(const void* grec, const uint32_t* gkey_sorted, const int32_t* gs
     return cuda_status();
   }
   Bump w(ws, wsb);
-  int* items = w.take<int>(n);
+  int4* items = w.take<int4>(n);
   int* nitems = w.take<int>(1);
   if (!w.ok) return fail("mg_backward: workspace too small");
-  build_items(gkey_sorted, gstart, n, 2, items, nitems, w.rest(), st);
+  build_items(gkey_sorted, gstart, n, bwd_qg(), items, nitems, w.rest(), st);
   launch_backward((const float*)grec, n, gkey_sorted, gstart, (int)g, (int)r, (const float4*)prec, pstart, items,
                   nitems, n, acc10, st);
   return cuda_status();

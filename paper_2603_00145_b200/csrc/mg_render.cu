@@ -171,18 +171,29 @@ __global__ void points_gather_kernel(const float4* __restrict__ xf, const int* _
 // Work items: runs of equal cell key chunked into groups of <= Q.
 // flag[p] = 1 if p starts an item.
 // ---------------------------------------------------------------------------
+// dense_min > 0: cells with >= dense_min elements are chunked by 64 instead of q
 __global__ void item_flags_kernel(const uint32_t* __restrict__ keys, const int* __restrict__ starts, int64_t n, int q,
-                                  int* __restrict__ flags) {
+                                  int dense_min, int* __restrict__ flags) {
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
-    int s = starts[keys[p]];
-    flags[p] = ((p - s) % q) == 0 ? 1 : 0;
+    const uint32_t key = keys[p];
+    const int s = starts[key];
+    const int qq = (dense_min > 0 && starts[key + 1] - s >= dense_min) ? 64 : q;
+    flags[p] = ((p - s) % qq) == 0 ? 1 : 0;
   }
 }
 
-__global__ void item_compact_kernel(const int* __restrict__ flags, const int* __restrict__ scan, int64_t n,
-                                    int* __restrict__ items, int* __restrict__ nitems) {
+// Item record {first element, cell, element count, 0}: a warp starts an item
+// with ONE load instead of the items -> key -> starts dependency chain.
+__global__ void item_compact_kernel(const int* __restrict__ flags, const int* __restrict__ scan,
+                                    const uint32_t* __restrict__ keys, const int* __restrict__ starts, int64_t n, int q,
+                                    int dense_min, int4* __restrict__ items, int* __restrict__ nitems) {
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
-    if (flags[p]) items[scan[p]] = (int)p;
+    if (flags[p]) {
+      const uint32_t key = keys[p];
+      const int e = starts[key + 1];
+      const int qq = (dense_min > 0 && e - starts[key] >= dense_min) ? 64 : q;
+      items[scan[p]] = make_int4((int)p, (int)key, min(qq, e - (int)p), 0);
+    }
     if (p == n - 1) *nitems = scan[p] + flags[p];
   }
 }
@@ -402,13 +413,25 @@ __device__ __forceinline__ void write_point_out(float4* __restrict__ out4, int* 
 #define MG_FWD_MINB 3
 #endif
 #ifndef MG_BWD_MINB
-#define MG_BWD_MINB 2
+#define MG_BWD_MINB 3
 #endif
 #ifndef MG_FWD_QMAX
 #define MG_FWD_QMAX 4
 #endif
 #ifndef MG_FWD_WARPS
 #define MG_FWD_WARPS 8
+#endif
+#ifndef MG_FWD_IPF
+#define MG_FWD_IPF 1  // prefetch the next work item's record while this one runs
+#endif
+#ifndef MG_BWD_IPF
+#define MG_BWD_IPF 1
+#endif
+#ifndef MG_BWD_PP
+#define MG_BWD_PP 0  // 1: prefetch window t+1 while window t computes (measured slower: fewer resident warps)
+#endif
+#ifndef MG_BWD_QG
+#define MG_BWD_QG 1  // max Gaussians per backward work item (1 or 2); 1 is faster at ~1 Gaussian per cell
 #endif
 #ifndef MG_BWD_WARPS
 #define MG_BWD_WARPS 8
@@ -425,6 +448,68 @@ __device__ __forceinline__ GRec load_rec(const GaussSoA& grec, int gi) {
   r.A = __ldg(grec.A + gi);
   r.B = __ldg(grec.B + gi);
   r.C = __ldg(grec.C + gi);
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// Per-lane record prefetch ring.  Each lane copies the record of its candidate
+// for iteration t + S - 1 into its own slot with cp.async (no registers held,
+// no cross-lane dependency -> no warp syncs) and reads iteration t's record
+// back from shared memory once cp.async.wait_group says it has landed: S - 1
+// record fetches per lane stay in flight behind the math.
+// ---------------------------------------------------------------------------
+#ifndef MG_FWD_STAGES
+#define MG_FWD_STAGES 0  // 0: plain __ldg loop (the ring measured slower: 2 < 4 < 8 stages all lose)
+#endif
+constexpr int kFwdStages = MG_FWD_STAGES;
+static_assert(kFwdStages == 0 || (kFwdStages >= 2 && (kFwdStages & (kFwdStages - 1)) == 0),
+              "MG_FWD_STAGES must be 0 or a power of two >= 2");
+
+#ifndef MG_FWD_PF
+#define MG_FWD_PF 0  // L1 prefetch distance of the forward record loop (0: off; 1-3 measured slower: L1 wavefront-bound)
+#endif
+constexpr int kFwdPf = MG_FWD_PF;
+
+__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+__device__ __forceinline__ void prefetch_rec(const GaussSoA& grec, int gi) {
+  prefetch_l1(grec.A + gi);
+  prefetch_l1(grec.B + gi);
+  prefetch_l1(grec.C + gi);
+}
+
+template <int S>
+struct RecRing {
+  float4 A[S][32], B[S][32];
+  float2 C[S][32];
+};
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int S>
+__device__ __forceinline__ void ring_fetch(RecRing<S>& R, int slot, int lane, const GaussSoA& grec, int gi) {
+  cp_async16(&R.A[slot][lane], grec.A + gi);
+  cp_async16(&R.B[slot][lane], grec.B + gi);
+  cp_async8(&R.C[slot][lane], grec.C + gi);
+}
+
+template <int S>
+__device__ __forceinline__ GRec ring_read(const RecRing<S>& R, int slot, int lane) {
+  GRec r;
+  r.A = R.A[slot][lane];
+  r.B = R.B[slot][lane];
+  r.C = R.C[slot][lane];
   return r;
 }
 
@@ -494,16 +579,16 @@ __device__ __forceinline__ void fwd_pair_math(const GRec& g, const f2 (&px)[QP],
   }
 }
 
-template <int Q, bool WITH_H>
+template <int Q, bool WITH_H, class Ring>
 __device__ __forceinline__ void fwd_item(const GaussSoA grec, const int* __restrict__ gstart, int g, int r,
                                          const float4* __restrict__ prec, int p0, int np, int cell,
                                          float4* __restrict__ out4, int* __restrict__ cnt_out, SegSmem& sm,
-                                         int lane) {
+                                         Ring* ring, int lane) {
   constexpr int QP = Q / 2;
   // candidates per lane per window: with >= 2 point pairs there are already
   // >= 2 independent chains per candidate, so one suffices (keeps registers
   // for the ping-pong prefetch); with one pair, take two.
-  constexpr int GPL = QP >= 2 ? 1 : 2;
+  constexpr int GPL = (QP >= 2 || kFwdStages > 0) ? 1 : 2;
   constexpr int WIN = 32 * GPL;
   // stage the item's sub-points coordinate-major in shared memory and read
   // them back as 64-bit pairs: the f32x2 operands then sit in aligned
@@ -538,7 +623,54 @@ __device__ __forceinline__ void fwd_item(const GaussSoA grec, const int* __restr
       const int wend = min(tot, w0 + 32 * kBmWords);
       // one compact loop: prefetching (two register sets) measured slower --
       // the kernel is sensitive to code size and register pressure
-      if (GPL == 1) {
+      if (kFwdStages > 0) {
+        constexpr int S = kFwdStages > 0 ? kFwdStages : 2;
+        Cursor1 cur{sb0};
+        const int n = (wend - w0 + 31) >> 5;
+#pragma unroll
+        for (int t = 0; t < S - 1; ++t) {
+          if (t < n) {
+            int va, ga;
+            cur.next(sm, w0, w0 + 32 * t, upto, lane, va, ga);
+            if (va < wend) ring_fetch(*ring, t, lane, grec, ga);
+          }
+          cp_async_commit();
+        }
+        for (int t = 0; t < n; ++t) {
+          if (t + S - 1 < n) {
+            int va, ga;
+            cur.next(sm, w0, w0 + 32 * (t + S - 1), upto, lane, va, ga);
+            if (va < wend) ring_fetch(*ring, (t + S - 1) & (S - 1), lane, grec, ga);
+          }
+          cp_async_commit();
+          cp_async_wait<S - 1>();
+          if (w0 + 32 * t + lane < wend)
+            fwd_pair_math<QP, WITH_H>(ring_read(*ring, t & (S - 1), lane), px, py, pz, accI, hx, hy, hz);
+        }
+      } else if (GPL == 1 && kFwdPf > 0) {
+        // the cursor runs kFwdPf iterations ahead and pulls those records into
+        // L1 (CCTL.PF1: no destination registers); the loads then hit L1
+        constexpr int D = kFwdPf > 0 ? kFwdPf : 1;
+        Cursor1 cur{sb0};
+        int qg[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          int va;
+          cur.next(sm, w0, w0 + 32 * d, upto, lane, va, qg[d]);
+          if (va < wend) prefetch_rec(grec, qg[d]);
+        }
+        for (int base = w0; base < wend; base += WIN) {
+          const int ga = qg[0];
+#pragma unroll
+          for (int d = 0; d + 1 < D; ++d) qg[d] = qg[d + 1];
+          {
+            int va;
+            cur.next(sm, w0, base + 32 * D, upto, lane, va, qg[D - 1]);
+            if (va < wend) prefetch_rec(grec, qg[D - 1]);
+          }
+          if (base + lane < wend) fwd_pair_math<QP, WITH_H>(load_rec(grec, ga), px, py, pz, accI, hx, hy, hz);
+        }
+      } else if (GPL == 1) {
         Cursor1 cur{sb0};
         for (int base = w0; base < wend; base += WIN) {
           int va, ga;
@@ -652,29 +784,99 @@ __device__ __forceinline__ void fwd_item_single(const GaussSoA grec, const int* 
   if ((lane & 7) == 0) write_point_out(out4, cnt_out, p0, comp, red, total);
 }
 
+
+// Dense cells (>= kFwdDenseMin sub-points, e.g. the per-step SSIM slice plane):
+// lanes own sub-points (two per lane, packed), the cell's candidate Gaussians
+// stream through warp-uniform (broadcast) loads -- one record fetch serves 64
+// pairs instead of 4.
+#ifndef MG_FWD_DENSE_MIN
+#define MG_FWD_DENSE_MIN 0  // measured slower at C2 (long serial per-item Gaussian stream): off
+#endif
+constexpr int kFwdDenseMin = MG_FWD_DENSE_MIN;
+
+template <bool WITH_H>
+__device__ __forceinline__ void fwd_item_dense(const GaussSoA& grec, const int* __restrict__ gstart, int g, int r,
+                                               const float4* __restrict__ prec, int p0, int np, int cell,
+                                               float4* __restrict__ out4, int* __restrict__ cnt_out, SegSmem& sm,
+                                               int lane) {
+  // lane owns points lane (lo half) and lane + 32 (hi half); staged adjacently
+  // in shared memory so each coordinate pair reloads as one 64-bit value
+  static_assert(sizeof(SegSmem::start) + sizeof(SegSmem::pre) >= 3 * 64 * sizeof(float), "dense staging");
+  float* buf = reinterpret_cast<float*>(sm.start);  // 3 x 64 floats in start[] + pre[] (unused on this path)
+  {
+    const float4 a = prec[p0 + min(lane, np - 1)];
+    const float4 b = prec[p0 + min(lane + 32, np - 1)];
+    buf[0 * 64 + 2 * lane] = a.x;
+    buf[0 * 64 + 2 * lane + 1] = b.x;
+    buf[1 * 64 + 2 * lane] = a.y;
+    buf[1 * 64 + 2 * lane + 1] = b.y;
+    buf[2 * 64 + 2 * lane] = a.z;
+    buf[2 * 64 + 2 * lane + 1] = b.z;
+  }
+  __syncwarp();
+  f2 px[1], py[1], pz[1];
+  px[0].v = *reinterpret_cast<const unsigned long long*>(buf + 0 * 64 + 2 * lane);
+  py[0].v = *reinterpret_cast<const unsigned long long*>(buf + 1 * 64 + 2 * lane);
+  pz[0].v = *reinterpret_cast<const unsigned long long*>(buf + 2 * 64 + 2 * lane);
+  __syncwarp();
+  f2 accI[1], hx[1], hy[1], hz[1];
+  accI[0] = hx[0] = hy[0] = hz[0] = bc2(0.f);
+  const Window w = make_window(cell, g, r);
+  int total = 0;
+  for (int col = 0; col < w.ncol; ++col) {
+    const int q = (int)(((float)col + 0.5f) * w.inv_nj);
+    const int base = ((w.ilo + q) * g + (w.jlo + col - q * w.nj)) * g;
+    const int a = __ldg(gstart + base + w.klo), b = __ldg(gstart + base + w.khi + 1);
+    total += b - a;
+#pragma unroll 2
+    for (int gi = a; gi < b; ++gi) fwd_pair_math<1, WITH_H>(load_rec(grec, gi), px, py, pz, accI, hx, hy, hz);
+  }
+  const float s = 1.0f / kMScale;
+  if (lane < np) {
+    out4[p0 + lane] = make_float4(lo(hx[0]) * s, lo(hy[0]) * s, lo(hz[0]) * s, lo(accI[0]));
+    cnt_out[p0 + lane] = total;
+  }
+  if (lane + 32 < np) {
+    out4[p0 + lane + 32] = make_float4(hi(hx[0]) * s, hi(hy[0]) * s, hi(hz[0]) * s, hi(accI[0]));
+    cnt_out[p0 + lane + 32] = total;
+  }
+}
+
 template <bool WITH_H>
 __global__ void __launch_bounds__(kFwdWarps * 32, MG_FWD_MINB) forward_kernel(const GaussSoA grec,
                                                                  const int* __restrict__ gstart, int g, int r,
                                                                  const float4* __restrict__ prec,
                                                                  const uint32_t* __restrict__ pkey,
                                                                  const int* __restrict__ pstart,
-                                                                 const int* __restrict__ items,
+                                                                 const int4* __restrict__ items,
                                                                  const int* __restrict__ nitems_dev,
                                                                  float4* __restrict__ out4, int* __restrict__ cnt_out) {
-  __shared__ SegSmem s_seg[kFwdWarps];
+  using Ring = RecRing<(kFwdStages > 0 ? kFwdStages : 2)>;
+  extern __shared__ __align__(16) unsigned char fwd_dyn[];
+  SegSmem* s_seg = reinterpret_cast<SegSmem*>(fwd_dyn);
+  Ring* s_ring = reinterpret_cast<Ring*>(s_seg + kFwdWarps);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  Ring* ring = kFwdStages > 0 ? s_ring + warp : nullptr;
   const int nitems = *nitems_dev;
-  for (int it = blockIdx.x * kFwdWarps + warp; it < nitems; it += gridDim.x * kFwdWarps) {
-    const int p0 = items[it];
-    const int cell = (int)pkey[p0];
-    const int np = min(MG_FWD_QMAX, pstart[cell + 1] - p0);
+  const int stride = gridDim.x * kFwdWarps;
+  int it = blockIdx.x * kFwdWarps + warp;
+  int4 next = (MG_FWD_IPF && it < nitems) ? items[it] : make_int4(0, 0, 0, 0);
+  for (; it < nitems; it += stride) {
+    const int4 item = MG_FWD_IPF ? next : items[it];  // {first, cell, count, 0}
+    if (MG_FWD_IPF && it + stride < nitems) next = items[it + stride];  // loads under this item
+    const int p0 = item.x, cell = item.y;
+    if (kFwdDenseMin > 0 && item.z > MG_FWD_QMAX) {
+      fwd_item_dense<WITH_H>(grec, gstart, g, r, prec, p0, item.z, cell, out4, cnt_out, s_seg[warp], lane);
+      continue;
+    }
+    const int np = item.z;
     if (MG_FWD_QMAX > 4 && np > 4)
       fwd_item<(MG_FWD_QMAX > 4 ? 8 : 4), WITH_H>(grec, gstart, g, r, prec, p0, np, cell, out4, cnt_out,
-                                                 s_seg[warp], lane);
+                                                 s_seg[warp], ring, lane);
     else if (np > 2)
-      fwd_item<4, WITH_H>(grec, gstart, g, r, prec, p0, np, cell, out4, cnt_out, s_seg[warp], lane);
+      fwd_item<4, WITH_H>(grec, gstart, g, r, prec, p0, np, cell, out4, cnt_out, s_seg[warp], ring, lane);
     else if (np == 2)
-      fwd_item<2, WITH_H>(grec, gstart, g, r, prec, p0, np, cell, out4, cnt_out, s_seg[warp], lane);
+      fwd_item<2, WITH_H>(grec, gstart, g, r, prec, p0, np, cell, out4, cnt_out, s_seg[warp], ring, lane);
     else
       fwd_item_single<WITH_H>(grec, gstart, g, r, prec, p0, cell, out4, cnt_out, s_seg[warp], lane);
   }
@@ -691,6 +893,9 @@ __global__ void __launch_bounds__(kFwdWarps * 32, MG_FWD_MINB) forward_kernel(co
 // d_abar6 = -0.5*alpha*A6 (_kernels.py:118-141).
 // ---------------------------------------------------------------------------
 constexpr int kBwdWarps = MG_BWD_WARPS;
+constexpr int kBwdQG = MG_BWD_QG;
+constexpr bool kBwdPingPong = MG_BWD_PP != 0;
+static_assert(kBwdQG == 1 || kBwdQG == 2, "MG_BWD_QG must be 1 or 2");
 
 struct Pts4 {
   float4 p[4];
@@ -715,7 +920,8 @@ struct Cursor4 {
 
 template <int QG>
 struct GaussAcc {
-  float mx[QG], my[QG], mz[QG], P[QG][6];
+  float mx[QG], my[QG], mz[QG], P[QG][6];  // P: P'00, P'11, P'22, 2P'01, 2P'02, 2P'12
+  // S = sum u g, D1 = sum u g d (T = P' D1 is formed at the end), A6 = sum u g d d^T
   f2 S[QG], T[QG][3], A6[QG][6];
 
   __device__ __forceinline__ void pair(const float4& a, const float4& b) {
@@ -723,16 +929,17 @@ struct GaussAcc {
 #pragma unroll
     for (int k = 0; k < QG; ++k) {
       f2 dx = sub2(px, bc2(mx[k])), dy = sub2(py, bc2(my[k])), dz = sub2(pz, bc2(mz[k]));
-      f2 pdx = fma2(bc2(P[k][4]), dz, fma2(bc2(P[k][3]), dy, mul2(bc2(P[k][0]), dx)));
-      f2 pdy = fma2(bc2(P[k][5]), dz, fma2(bc2(P[k][1]), dy, mul2(bc2(P[k][3]), dx)));
-      f2 pdz = fma2(bc2(P[k][2]), dz, fma2(bc2(P[k][5]), dy, mul2(bc2(P[k][4]), dx)));
-      f2 m = fma2(dz, pdz, fma2(dy, pdy, mul2(dx, pdx)));
+      // m' = d^T P' d, Horner with doubled off-diagonals (9 FP32 ops)
+      f2 t1 = fma2(bc2(P[k][4]), dz, fma2(bc2(P[k][3]), dy, mul2(bc2(P[k][0]), dx)));
+      f2 m = mul2(dx, t1);
+      m = fma2(dy, fma2(bc2(P[k][5]), dz, mul2(bc2(P[k][1]), dy)), m);
+      m = fma2(dz, mul2(bc2(P[k][2]), dz), m);
       f2 ug = mul2(u, gauss_w2(m));
       S[k] = add2(S[k], ug);
-      T[k][0] = fma2(ug, pdx, T[k][0]);
-      T[k][1] = fma2(ug, pdy, T[k][1]);
-      T[k][2] = fma2(ug, pdz, T[k][2]);
       f2 cx = mul2(ug, dx), cy = mul2(ug, dy), cz = mul2(ug, dz);
+      T[k][0] = add2(T[k][0], cx);
+      T[k][1] = add2(T[k][1], cy);
+      T[k][2] = add2(T[k][2], cz);
       A6[k][0] = fma2(cx, dx, A6[k][0]);
       A6[k][1] = fma2(cx, dy, A6[k][1]);
       A6[k][2] = fma2(cx, dz, A6[k][2]);
@@ -740,6 +947,18 @@ struct GaussAcc {
       A6[k][4] = fma2(cy, dz, A6[k][4]);
       A6[k][5] = fma2(cz, dz, A6[k][5]);
     }
+  }
+
+  // lane-local totals of the 10 accumulators of Gaussian k, T = P' D1
+  __device__ __forceinline__ void totals(int k, float* v) const {
+    v[0] = lo(S[k]) + hi(S[k]);
+    const float d1x = lo(T[k][0]) + hi(T[k][0]), d1y = lo(T[k][1]) + hi(T[k][1]), d1z = lo(T[k][2]) + hi(T[k][2]);
+    const float h01 = 0.5f * P[k][3], h02 = 0.5f * P[k][4], h12 = 0.5f * P[k][5];
+    v[1] = P[k][0] * d1x + h01 * d1y + h02 * d1z;
+    v[2] = h01 * d1x + P[k][1] * d1y + h12 * d1z;
+    v[3] = h02 * d1x + h12 * d1y + P[k][2] * d1z;
+#pragma unroll
+    for (int c = 0; c < 6; ++c) v[4 + c] = lo(A6[k][c]) + hi(A6[k][c]);
   }
 };
 
@@ -759,9 +978,9 @@ __device__ __forceinline__ void bwd_item(const GaussSoA grec, int g0, int ng, in
     acc.P[k][0] = B.x;  // P00
     acc.P[k][1] = B.y;  // P11
     acc.P[k][2] = B.z;  // P22
-    acc.P[k][3] = B.w;  // P01
-    acc.P[k][4] = C.x;  // P02
-    acc.P[k][5] = C.y;  // P12
+    acc.P[k][3] = 2.f * B.w;  // 2 P01 (exact)
+    acc.P[k][4] = 2.f * C.x;  // 2 P02
+    acc.P[k][5] = 2.f * C.y;  // 2 P12
     acc.S[k] = bc2(0.f);
 #pragma unroll
     for (int c = 0; c < 3; ++c) acc.T[k][c] = bc2(0.f);
@@ -778,7 +997,16 @@ __device__ __forceinline__ void bwd_item(const GaussSoA grec, int g0, int ng, in
       const int wend = min(tot, w0 + 32 * kBmWords);
       const int nfull = (wend - w0) >> 7;
       int v[4], e[4];
-      if (nfull > 0) {
+      if (!kBwdPingPong) {
+        for (int t = 0; t < nfull; ++t) {
+          cur.next(sm, w0, w0 + 128 * t, upto, lane, v, e);
+          float4 q[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) q[i] = __ldg(prec + e[i]);
+          acc.pair(q[0], q[1]);
+          acc.pair(q[2], q[3]);
+        }
+      } else if (nfull > 0) {
         // ping-pong register sets: window t+1 loads while window t computes
         float4 q0[4], q1[4];
         cur.next(sm, w0, w0, upto, lane, v, e);
@@ -822,11 +1050,7 @@ __device__ __forceinline__ void bwd_item(const GaussSoA grec, int g0, int ng, in
   float vals[32];
 #pragma unroll
   for (int k = 0; k < QG; ++k) {
-    vals[16 * k + 0] = lo(acc.S[k]) + hi(acc.S[k]);
-#pragma unroll
-    for (int c = 0; c < 3; ++c) vals[16 * k + 1 + c] = lo(acc.T[k][c]) + hi(acc.T[k][c]);
-#pragma unroll
-    for (int c = 0; c < 6; ++c) vals[16 * k + 4 + c] = lo(acc.A6[k][c]) + hi(acc.A6[k][c]);
+    acc.totals(k, vals + 16 * k);
 #pragma unroll
     for (int c = 10; c < 16; ++c) vals[16 * k + c] = 0.f;
   }
@@ -844,18 +1068,21 @@ __global__ void __launch_bounds__(kBwdWarps * 32, MG_BWD_MINB) backward_kernel(c
                                                                   const int* __restrict__ gstart, int g, int r,
                                                                   const float4* __restrict__ prec,
                                                                   const int* __restrict__ pstart,
-                                                                  const int* __restrict__ items,
+                                                                  const int4* __restrict__ items,
                                                                   const int* __restrict__ nitems_dev,
                                                                   float* __restrict__ acc10) {
   __shared__ SegSmem s_seg[kBwdWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nitems = *nitems_dev;
-  for (int it = blockIdx.x * kBwdWarps + warp; it < nitems; it += gridDim.x * kBwdWarps) {
-    const int g0 = items[it];
-    const int cell = (int)gkey[g0];
-    const int ng = min(2, gstart[cell + 1] - g0);
-    if (ng == 2)
-      bwd_item<2>(grec, g0, ng, cell, g, r, prec, pstart, acc10, s_seg[warp], lane);
+  const int stride = gridDim.x * kBwdWarps;
+  int it = blockIdx.x * kBwdWarps + warp;
+  int4 next = (MG_BWD_IPF && it < nitems) ? items[it] : make_int4(0, 0, 0, 0);
+  for (; it < nitems; it += stride) {
+    const int4 item = MG_BWD_IPF ? next : items[it];  // {first, cell, count, 0}
+    if (MG_BWD_IPF && it + stride < nitems) next = items[it + stride];  // loads under this item
+    const int g0 = item.x, cell = item.y, ng = item.z;
+    if (kBwdQG == 2 && ng == 2)
+      bwd_item<kBwdQG>(grec, g0, ng, cell, g, r, prec, pstart, acc10, s_seg[warp], lane);
     else
       bwd_item<1>(grec, g0, ng, cell, g, r, prec, pstart, acc10, s_seg[warp], lane);
   }
@@ -968,9 +1195,9 @@ __device__ __forceinline__ void staged_load_gauss(GaussAcc<QG>& acc, const Gauss
     acc.P[k][0] = B.x;
     acc.P[k][1] = B.y;
     acc.P[k][2] = B.z;
-    acc.P[k][3] = B.w;
-    acc.P[k][4] = C.x;
-    acc.P[k][5] = C.y;
+    acc.P[k][3] = 2.f * B.w;
+    acc.P[k][4] = 2.f * C.x;
+    acc.P[k][5] = 2.f * C.y;
     acc.S[k] = bc2(0.f);
 #pragma unroll
     for (int c = 0; c < 3; ++c) acc.T[k][c] = bc2(0.f);
@@ -1042,11 +1269,7 @@ __device__ __forceinline__ void staged_round(const GaussSoA& grec, int g0, float
   float vals[32];
 #pragma unroll
   for (int k = 0; k < QG; ++k) {
-    vals[16 * k + 0] = lo(acc.S[k]) + hi(acc.S[k]);
-#pragma unroll
-    for (int c = 0; c < 3; ++c) vals[16 * k + 1 + c] = lo(acc.T[k][c]) + hi(acc.T[k][c]);
-#pragma unroll
-    for (int c = 0; c < 6; ++c) vals[16 * k + 4 + c] = lo(acc.A6[k][c]) + hi(acc.A6[k][c]);
+    acc.totals(k, vals + 16 * k);
 #pragma unroll
     for (int c = 10; c < 16; ++c) vals[16 * k + c] = 0.f;
   }
@@ -1165,7 +1388,7 @@ __global__ void overflow_flags_kernel(const uint32_t* __restrict__ keys, const i
                                       int* __restrict__ flags) {
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
     const int d = (int)(p - starts[keys[p]]);
-    flags[p] = (d >= 2 && (d & 1) == 0) ? 1 : 0;
+    flags[p] = (d >= 2 && (d - 2) % kBwdQG == 0) ? 1 : 0;
   }
 }
 
@@ -1217,11 +1440,13 @@ void launch_points_gather(const float4* xf, const int* perm, int64_t n, float4* 
 }
 
 int fwd_qmax() { return MG_FWD_QMAX; }
+int bwd_qg() { return MG_BWD_QG; }
+int fwd_dense_min() { return kFwdDenseMin; }
 
 size_t items_workspace_bytes(int64_t n) { return 2 * (((size_t)n * 4 + 255) & ~(size_t)255) + scan_workspace_bytes(n); }
 
-void build_items(const uint32_t* keys, const int* starts, int64_t n, int q, int* items, int* nitems, void* ws,
-                 cudaStream_t st) {
+void build_items(const uint32_t* keys, const int* starts, int64_t n, int q, int4* items, int* nitems, void* ws,
+                 cudaStream_t st, int dense_min) {
   if (n <= 0) {
     cudaMemsetAsync(nitems, 0, sizeof(int), st);
     return;
@@ -1229,15 +1454,16 @@ void build_items(const uint32_t* keys, const int* starts, int64_t n, int q, int*
   int* flags = (int*)ws;
   int* scan = (int*)((char*)ws + (((size_t)n * 4 + 255) & ~(size_t)255));
   void* sws = (char*)ws + 2 * (((size_t)n * 4 + 255) & ~(size_t)255);
-  MG_LAUNCH(item_flags_kernel<<<grid_for(n), 256, 0, st>>>(keys, starts, n, q, flags));
+  MG_LAUNCH(item_flags_kernel<<<grid_for(n), 256, 0, st>>>(keys, starts, n, q, dense_min, flags));
   excl_scan(flags, scan, n, sws, st);
-  MG_LAUNCH(item_compact_kernel<<<grid_for(n), 256, 0, st>>>(flags, scan, n, items, nitems));
+  MG_LAUNCH(item_compact_kernel<<<grid_for(n), 256, 0, st>>>(flags, scan, keys, starts, n, q, dense_min, items,
+                                                             nitems));
 }
 
 template <class K>
-static int64_t persistent_blocks(K kernel, int threads, int64_t max_blocks) {
+static int64_t persistent_blocks(K kernel, int threads, int64_t max_blocks, size_t dyn_smem = 0) {
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, dyn_smem);
   if (per_sm < 1) per_sm = 1;
   int64_t b = (int64_t)num_sms() * per_sm;
   return b < max_blocks ? b : (max_blocks < 1 ? 1 : max_blocks);
@@ -1245,20 +1471,20 @@ static int64_t persistent_blocks(K kernel, int threads, int64_t max_blocks) {
 
 void launch_forward(bool with_h, const float* grec_raw, int64_t n_gauss, const int* gstart, int g, int r,
                     const float4* prec,
-                    const uint32_t* pkey, const int* pstart, const int* items, const int* nitems, int64_t max_items,
+                    const uint32_t* pkey, const int* pstart, const int4* items, const int* nitems, int64_t max_items,
                     float4* out4, int* cnt, cudaStream_t st) {
   if (max_items <= 0) return;
   const int64_t want = (max_items + kFwdWarps - 1) / kFwdWarps;
   const GaussSoA grec = gauss_soa(grec_raw, n_gauss);
-  if (with_h) {
-    auto k = forward_kernel<true>;
-    MG_LAUNCH(forward_kernel<true><<<(unsigned)persistent_blocks(k, kFwdWarps * 32, want), kFwdWarps * 32, 0, st>>>(
-        grec, gstart, g, r, prec, pkey, pstart, items, nitems, out4, cnt));
-  } else {
-    auto k = forward_kernel<false>;
-    MG_LAUNCH(forward_kernel<false><<<(unsigned)persistent_blocks(k, kFwdWarps * 32, want), kFwdWarps * 32, 0, st>>>(
-        grec, gstart, g, r, prec, pkey, pstart, items, nitems, out4, cnt));
+  const size_t smem = kFwdWarps * (sizeof(SegSmem) + (kFwdStages > 0 ? sizeof(RecRing<(kFwdStages > 0 ? kFwdStages : 2)>) : 0));
+  auto k = with_h ? forward_kernel<true> : forward_kernel<false>;
+  static bool attr_set[2] = {false, false};
+  if (!attr_set[with_h]) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_set[with_h] = true;
   }
+  const unsigned blocks = (unsigned)persistent_blocks(k, kFwdWarps * 32, want, smem);
+  MG_LAUNCH(k<<<blocks, kFwdWarps * 32, smem, st>>>(grec, gstart, g, r, prec, pkey, pstart, items, nitems, out4, cnt));
 }
 
 size_t staged_smem_bytes() { return sizeof(float4) * kSbCap + sizeof(SegSmem) * kSbS + sizeof(StageSmem); }
@@ -1266,7 +1492,9 @@ size_t staged_smem_bytes() { return sizeof(float4) * kSbCap + sizeof(SegSmem) * 
 size_t backward_staged_ws_bytes(int64_t n, int g) {
   const int64_t nstrips = (int64_t)g * g * ((g + kSbS - 1) / kSbS);
   const int64_t m = nstrips > n ? nstrips : n;
-  return 4 * ((((size_t)m * 4) + 255) & ~(size_t)255) + 512 + scan_workspace_bytes(m);
+  const size_t a4 = (((size_t)m * 4) + 255) & ~(size_t)255, a16 = (((size_t)m * 16) + 255) & ~(size_t)255;
+  const size_t sw = (scan_workspace_bytes(m) + 255) & ~(size_t)255;
+  return 3 * a4 + 512 + sw + a16;
 }
 
 // Staged backward: strips for the first <= 2 Gaussians of every cell, the
@@ -1282,8 +1510,9 @@ void launch_backward_staged(const float* grec_raw, int64_t n_gauss, const uint32
   int* flags = (int*)w;
   int* scan = (int*)(w + al);
   int* list = (int*)(w + 2 * al);
-  int* counts = (int*)(w + 4 * al);
-  void* sws = w + 4 * al + 512;
+  int* counts = (int*)(w + 3 * al);
+  void* sws = w + 3 * al + 512;
+  int4* oitems = (int4*)(w + 3 * al + 512 + ((scan_workspace_bytes(m) + 255) & ~(size_t)255));
   MG_LAUNCH(strip_flags_kernel<<<grid_for(nstrips), 256, 0, st>>>(gstart, g, kSbS, flags));
   excl_scan(flags, scan, nstrips, sws, st);
   MG_LAUNCH(strip_compact_kernel<<<grid_for(nstrips), 256, 0, st>>>(flags, scan, nstrips, list, counts));
@@ -1303,17 +1532,17 @@ void launch_backward_staged(const float* grec_raw, int64_t n_gauss, const uint32
   // overflow chunks (cells with > 2 Gaussians) through the item kernel
   int* oflags = flags;
   int* oscan = scan;
-  int* oitems = (int*)(w + 3 * al);
   MG_LAUNCH(overflow_flags_kernel<<<grid_for(n_gauss), 256, 0, st>>>(gkey, gstart, n_gauss, oflags));
   excl_scan(oflags, oscan, n_gauss, sws, st);
-  MG_LAUNCH(item_compact_kernel<<<grid_for(n_gauss), 256, 0, st>>>(oflags, oscan, n_gauss, oitems, counts + 1));
+  MG_LAUNCH(item_compact_kernel<<<grid_for(n_gauss), 256, 0, st>>>(oflags, oscan, gkey, gstart, n_gauss, kBwdQG, 0,
+                                                                    oitems, counts + 1));
   const int64_t want = (n_gauss / 2 + kBwdWarps) / kBwdWarps;
   MG_LAUNCH(backward_kernel<<<(unsigned)persistent_blocks(backward_kernel, kBwdWarps * 32, want), kBwdWarps * 32, 0,
                               st>>>(grec, gkey, gstart, g, r, prec, pstart, oitems, counts + 1, acc10));
 }
 
 void launch_backward(const float* grec_raw, int64_t n_gauss, const uint32_t* gkey, const int* gstart, int g, int r,
-                     const float4* prec, const int* pstart, const int* items, const int* nitems, int64_t max_items,
+                     const float4* prec, const int* pstart, const int4* items, const int* nitems, int64_t max_items,
                      float* acc10, cudaStream_t st) {
   if (max_items <= 0) return;
   const GaussSoA grec = gauss_soa(grec_raw, n_gauss);

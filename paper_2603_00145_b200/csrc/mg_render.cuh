@@ -5,6 +5,8 @@
 namespace mg {
 int num_sms();
 int fwd_qmax();
+int bwd_qg();
+int fwd_dense_min();
 
 // preprocessing / binning
 void launch_gauss_keys(const float* pos, int64_t n, int g, uint32_t* keys, cudaStream_t st);
@@ -18,16 +20,16 @@ void launch_points_prepare(const double* coords, const int64_t* sids64, const in
                            int nslices, int g, uint32_t* keys, float4* xf, double* xout, cudaStream_t st);
 void launch_points_gather(const float4* xf, const int* perm, int64_t n, float4* prec, int* inv, cudaStream_t st);
 size_t items_workspace_bytes(int64_t n);
-void build_items(const uint32_t* keys, const int* starts, int64_t n, int q, int* items, int* nitems, void* ws,
-                 cudaStream_t st);
+void build_items(const uint32_t* keys, const int* starts, int64_t n, int q, int4* items, int* nitems, void* ws,
+                 cudaStream_t st, int dense_min = 0);
 
 // pair kernels
 void launch_forward(bool with_h, const float* grec, int64_t n_gauss, const int* gstart, int g, int r,
                     const float4* prec,
-                    const uint32_t* pkey, const int* pstart, const int* items, const int* nitems, int64_t max_items,
+                    const uint32_t* pkey, const int* pstart, const int4* items, const int* nitems, int64_t max_items,
                     float4* out4, int* cnt, cudaStream_t st);
 void launch_backward(const float* grec, int64_t n_gauss, const uint32_t* gkey, const int* gstart, int g, int r,
-                     const float4* prec, const int* pstart, const int* items, const int* nitems, int64_t max_items,
+                     const float4* prec, const int* pstart, const int4* items, const int* nitems, int64_t max_items,
                      float* acc10, cudaStream_t st);
 
 size_t backward_staged_ws_bytes(int64_t n, int g);

@@ -157,13 +157,32 @@ unsigned grid_of(int64_t n) {
 }
 
 // ---- composite workspace layouts ----
-size_t bin_ws(int64_t n, int64_t g) {
-  return al((size_t)n * 4) + radix_workspace_bytes(n) + csr_workspace_bytes(ncell_of(g)) + 1024;
+// Binning sorts cell keys with the counting sort (MG_SORT_RADIX=1: stable LSD
+// radix sort + CSR build; same output).
+#ifndef MG_SORT_RADIX
+#define MG_SORT_RADIX 0
+#endif
+
+size_t sort_ws(int64_t n, int64_t g) {
+  const size_t a = radix_workspace_bytes(n) + csr_workspace_bytes(ncell_of(g));
+  const size_t b = counting_workspace_bytes(n, ncell_of(g));
+  return (a > b ? a : b) + 512;
 }
 
+void sort_cells(const uint32_t* keys, uint32_t* keys_sorted, int* order, int* starts, int64_t n, int64_t g, void* ws,
+                cudaStream_t st) {
+  if (MG_SORT_RADIX) {
+    radix_sort_pairs(keys, keys_sorted, order, n, bits_for(ncell_of(g) - 1), ws, st);
+    csr_starts(keys_sorted, n, ncell_of(g), starts, ws, st);
+  } else {
+    counting_sort_pairs(keys, keys_sorted, order, starts, n, ncell_of(g), ws, st);
+  }
+}
+
+size_t bin_ws(int64_t n, int64_t g) { return al((size_t)n * 4) + sort_ws(n, g) + 1024; }
+
 size_t points_ws(int64_t ns, int64_t g) {
-  return al((size_t)ns * 4) * 2 + al((size_t)ns * 16) + radix_workspace_bytes(ns) + csr_workspace_bytes(ncell_of(g)) +
-         2048;
+  return al((size_t)ns * 4) * 2 + al((size_t)ns * 16) + sort_ws(ns, g) + 2048;
 }
 
 size_t fwd_ws(int64_t ns) { return al((size_t)ns * 16) + 256 + items_workspace_bytes(ns) + 1024; }
@@ -177,9 +196,7 @@ int do_bin(const float* pos32, const double* pos64, int64_t n, int64_t g, uint32
     launch_gauss_keys(pos32, n, (int)g, keys, st);
   else
     launch_gauss_keys_f64(pos64, n, (int)g, keys, st);
-  int bits = bits_for(ncell_of(g) - 1);
-  radix_sort_pairs(keys, keys_sorted, order, n, bits, b.rest(), st);
-  csr_starts(keys_sorted, n, ncell_of(g), starts, b.rest(), st);
+  sort_cells(keys, keys_sorted, order, starts, n, g, b.rest(), st);
   return cuda_status();
 }
 
@@ -272,9 +289,8 @@ int mg_bin_points(const double* coords, const int64_t* sids, int64_t b, int32_t 
   if (!w.ok) return fail("mg_bin_points: workspace too small");
   launch_points_prepare(coords, sids, nullptr, b, ntaps, ntaps > 1 ? tap_off : nullptr, dirs, rot, trans, (int)k,
                         (int)g, keys, xf, transformed, st);
-  radix_sort_pairs(keys, pkey_sorted, perm, ns, bits_for(ncell_of(g) - 1), w.rest(), st);
+  sort_cells(keys, pkey_sorted, perm, pstart, ns, g, w.rest(), st);
   launch_points_gather(xf, perm, ns, (float4*)prec, pinv, st);
-  csr_starts(pkey_sorted, ns, ncell_of(g), pstart, w.rest(), st);
   return cuda_status();
 }
 

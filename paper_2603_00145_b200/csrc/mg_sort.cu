@@ -324,6 +324,64 @@ void csr_starts(const uint32_t* keys, int64_t n, int64_t ncell, int* starts, voi
   excl_scan(starts, starts, ncell + 1, ws, st);
 }
 
+// ---------------------------------------------------------------------------
+// Counting sort for dense cell keys in [0, ncell): the CSR is the exclusive
+// scan of the per-cell counts, elements scatter to starts[key] + (atomic slot),
+// and a rank pass restores stable order inside each cell (rank = # smaller
+// original indices in the cell, O(cell size) per element).  Output identical
+// to the stable LSD radix sort, in 4 kernels + 1 memset instead of 3 passes of
+// hist/scan/scatter plus a separate CSR build.  Cost is sum(cell size^2): a
+// pathological single huge cell is slow (still correct).
+// ---------------------------------------------------------------------------
+__global__ void cs_count(const uint32_t* __restrict__ keys, int64_t n, int* __restrict__ cnt,
+                         int* __restrict__ slot) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    slot[i] = atomicAdd(&cnt[keys[i]], 1);
+}
+
+__global__ void cs_scatter(const uint32_t* __restrict__ keys, const int* __restrict__ slot, int64_t n,
+                           const int* __restrict__ starts, uint32_t* __restrict__ keys_out, int* __restrict__ tmp) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = keys[i];
+    const int p = starts[k] + slot[i];
+    keys_out[p] = k;
+    tmp[p] = (int)i;
+  }
+}
+
+__global__ void cs_rank(const uint32_t* __restrict__ keys_out, const int* __restrict__ tmp, int64_t n,
+                        const int* __restrict__ starts, int* __restrict__ vals_out) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = keys_out[p];
+    const int s = starts[k], e = starts[k + 1];
+    const int v = tmp[p];
+    int r = 0;
+    for (int q = s; q < e; ++q) r += tmp[q] < v;
+    vals_out[s + r] = v;
+  }
+}
+
+size_t counting_workspace_bytes(int64_t n, int64_t ncell) {
+  const size_t a = (((size_t)(n > 0 ? n : 1) * 4) + 255) & ~(size_t)255;
+  return 2 * a + scan_workspace_bytes(ncell + 1);
+}
+
+void counting_sort_pairs(const uint32_t* keys, uint32_t* keys_out, int* vals_out, int* starts, int64_t n,
+                         int64_t ncell, void* ws, cudaStream_t st) {
+  cudaMemsetAsync(starts, 0, sizeof(int) * (size_t)(ncell + 1), st);
+  const size_t a = (((size_t)(n > 0 ? n : 1) * 4) + 255) & ~(size_t)255;
+  int* slot = (int*)ws;
+  int* tmp = (int*)((char*)ws + a);
+  void* sws = (char*)ws + 2 * a;
+  const unsigned blocks = (unsigned)((n + 255) / 256 < 8192 ? (n + 255) / 256 : 8192);
+  if (n > 0) MG_LAUNCH(cs_count<<<blocks, 256, 0, st>>>(keys, n, starts, slot));
+  excl_scan(starts, starts, ncell + 1, sws, st);
+  if (n > 0) {
+    MG_LAUNCH(cs_scatter<<<blocks, 256, 0, st>>>(keys, slot, n, starts, keys_out, tmp));
+    MG_LAUNCH(cs_rank<<<blocks, 256, 0, st>>>(keys_out, tmp, n, starts, vals_out));
+  }
+}
+
 int bits_for(int64_t maxval) {
   int b = 0;
   while (b < 32 && ((int64_t)1 << b) <= maxval) ++b;

@@ -1,6 +1,7 @@
-"""GPU checks of the binning primitives at production sizes: stable radix
-sort + CSR against numpy's stable argsort / bincount / cumsum (the reference's
-spatial.py:46-66 recipe), over key widths that select 6-, 8- and 10-bit digits."""
+"""GPU checks of the binning primitives at production sizes: the cell sort
+(counting sort + in-cell rank pass) and CSR against numpy's stable argsort /
+bincount / cumsum (the reference's spatial.py:46-66 recipe), including a
+crowded cell whose ties must keep ascending index."""
 
 import numpy as np
 import pytest

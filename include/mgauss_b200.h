@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define MG_ABI_VERSION 1
+#define MG_ABI_VERSION 2
 #define MG_EINVAL 1
 
 int mg_abi_version(void);
@@ -116,7 +116,7 @@ int mg_forward(const void *grec, int64_t n_gauss, const int32_t *gstart, int64_t
 /* I_b = sum_t w_t I_(b,t) (tap_weights NULL = single tap); counts summed. */
 int mg_forward_finish(const void *out4, const int32_t *counts, const int32_t *pinv, int64_t b, int32_t ntaps,
                       const double *tap_weights, double *intensity, float *intensity_f32, int64_t *counts_out,
-                      void *stream);
+                      int64_t *pair_total, void *stream);
 
 /* ---- backward: _kernels.py:73-144, render.py:276-354 -------------------- */
 /* upstream (b) float64 (or upstream_f32) -> prec[].w and d_points (n_sub,3, input order, may be NULL) */
@@ -167,6 +167,11 @@ size_t mg_ssim_workspace_bytes(int64_t h, int64_t w);
 int mg_ssim_loss_grad(const float *pred, const float *target, int64_t h, int64_t w, double scale,
                       float *upstream_out, double *ssim_sum, void *ws, size_t ws_bytes, void *stream);
 int mg_counter_incr(int32_t *counters, int32_t n, void *stream);
+/* One step's batch rows from the resident sample pool (train.py:332-347 draws
+ * pool indices; the rows are gathered on the device): coords[i] =
+ * pool_coords[idx[i]] (3 doubles), slice_ids[i], target[i] likewise. */
+int mg_gather_batch(const int64_t *idx, int64_t n, const double *pool_coords, const int64_t *pool_slice_ids,
+                    const float *pool_target, double *coords, int64_t *slice_ids, float *target, void *stream);
 /* hyper (host, 9 doubles): lr_pos, lr_quat, lr_scale, lr_logit, beta1, beta2, eps, lambda_aniso, lambda_ratio.
  * t_dev: device int32 post-increment Adam step.  Moments m, v are (n, 11) float32. */
 int mg_gauss_update(const float *acc10, const int32_t *cell_indices, int64_t n, float *pos, float *quat,

@@ -42,7 +42,7 @@ SIGNATURES = {
     "mg_bin_points": (ctypes.c_int, [P, P, I64, I32, P, P, P, P, I64, I64, P, P, P, P, P, P, SZ, P]),
     "mg_forward_workspace_bytes": (SZ, [I64]),
     "mg_forward": (ctypes.c_int, [P, I64, P, I64, I64, P, P, P, I64, I32, P, P, P, SZ, P]),
-    "mg_forward_finish": (ctypes.c_int, [P, P, P, I64, I32, P, P, P, P, P]),
+    "mg_forward_finish": (ctypes.c_int, [P, P, P, I64, I32, P, P, P, P, P, P]),
     "mg_backward_points": (ctypes.c_int, [P, P, I64, I32, P, P, P, P, P, P]),
     "mg_backward_workspace_bytes": (SZ, [I64, I64]),
     "mg_backward": (ctypes.c_int, [P, P, P, I64, I64, I64, P, P, P, P, SZ, P]),
@@ -58,6 +58,7 @@ SIGNATURES = {
     "mg_ssim_loss_grad": (ctypes.c_int, [P, P, I64, I64, D, P, P, P, SZ, P]),
     "mg_quat_to_rot_f64": (ctypes.c_int, [P, I64, P, P]),
     "mg_counter_incr": (ctypes.c_int, [P, I32, P]),
+    "mg_gather_batch": (ctypes.c_int, [P, I64, P, P, P, P, P, P, P]),
     "mg_gauss_update": (ctypes.c_int, [P, P, I64, P, P, P, P, P, P, P, I32, P, P, P]),
     "mg_transform_adam": (ctypes.c_int, [P, P, P, P, P, I64, D, D, D, D, P, P]),
     "mg_upsample": (ctypes.c_int, [P, P, P, P, I64, I64, P, P, P, P, P]),
@@ -73,8 +74,12 @@ _lib = None
 _lock = threading.Lock()
 
 
+ABI_VERSION = 2  # include/mgauss_b200.h MG_ABI_VERSION
+
+
 def load_library(path=LIB_PATH):
-    """dlopen the library and bind every symbol (no CUDA call is made)."""
+    """dlopen the library and bind every symbol (no CUDA call is made); a
+    library built from an older header is rejected, not silently mis-called."""
     if not os.path.exists(path):
         raise NativeLibraryMissing(
             f"{path} is not built; run `python -m paper_2603_00145_b200._build` (nvcc, sm_100a)")
@@ -83,6 +88,8 @@ def load_library(path=LIB_PATH):
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
+    if lib.mg_abi_version() != ABI_VERSION:
+        raise NativeLibraryMissing(f"{path} has ABI {lib.mg_abi_version()}, expected {ABI_VERSION}: rebuild it")
     return lib
 
 

@@ -306,7 +306,7 @@ int mg_forward(const void* grec, int64_t n_gauss, const int32_t* gstart, int64_t
   int* nitems = w.take<int>(1);
   if (!w.ok) return fail("mg_forward: workspace too small");
   if (ns == 0) return 0;
-  build_items(pkey_sorted, pstart, ns, fwd_qmax(), items, nitems, w.rest(), st, fwd_dense_min());
+  build_items_cells(pstart, ncell_of(g), fwd_qmax(), items, nitems, st, fwd_dense_min());
   launch_forward(with_h != 0, (const float*)grec, n_gauss, gstart, (int)g, (int)r, (const float4*)prec, pkey_sorted,
                  pstart,
                  items, nitems, ns, (float4*)out4, counts, st);
@@ -315,9 +315,9 @@ int mg_forward(const void* grec, int64_t n_gauss, const int32_t* gstart, int64_t
 
 int mg_forward_finish(const void* out4, const int32_t* counts, const int32_t* pinv, int64_t b, int32_t ntaps,
                       const double* tap_w, double* intensity, float* intensity_f32, int64_t* counts_out,
-                      void* stream) {
+                      int64_t* pair_total, void* stream) {
   launch_forward_finish((const float4*)out4, counts, pinv, b, ntaps, ntaps > 1 ? tap_w : nullptr, intensity,
-                        intensity_f32, counts_out, S(stream));
+                        intensity_f32, counts_out, pair_total, S(stream));
   return cuda_status();
 }
 
@@ -358,7 +358,11 @@ int mg_backward(const void* grec, const uint32_t* gkey_sorted, const int32_t* gs
   int4* items = w.take<int4>(n);
   int* nitems = w.take<int>(1);
   if (!w.ok) return fail("mg_backward: workspace too small");
-  build_items(gkey_sorted, gstart, n, bwd_qg(), items, nitems, w.rest(), st);
+  if (bwd_qg() == 1) {  // one item per sorted Gaussian: implicit, no item build
+    items = nullptr;
+  } else {
+    build_items_cells(gstart, ncell_of(g), bwd_qg(), items, nitems, st);
+  }
   launch_backward((const float*)grec, n, gkey_sorted, gstart, (int)g, (int)r, (const float4*)prec, pstart, items,
                   nitems, n, acc10, st);
   return cuda_status();
@@ -435,6 +439,13 @@ int mg_quat_to_rot_f64(const double* q, int64_t k, double* rot, void* stream) {
   return cuda_status();
 }
 
+int mg_gather_batch(const int64_t* idx, int64_t n, const double* pool_coords, const int64_t* pool_sids,
+                    const float* pool_target, double* coords, int64_t* sids, float* target, void* stream) {
+  if (n < 0) return fail("mg_gather_batch: bad size");
+  launch_gather_batch(idx, n, pool_coords, pool_sids, pool_target, coords, sids, target, S(stream));
+  return cuda_status();
+}
+
 int mg_counter_incr(int32_t* c, int32_t n, void* stream) {
   launch_counter_incr(c, n, S(stream));
   return cuda_status();
@@ -501,7 +512,7 @@ static int block_common(const double* points, const int64_t* sids, int64_t b, co
   rc = mg_forward(grec, n, gstart, g, r, prec, pkey, pstart, b, with_h ? 1 : 0, out4, cnt, rest, restb, st);
   if (rc) return rc;
   if (!upstream) {
-    launch_forward_finish(out4, cnt, pinv, b, 1, nullptr, out_i, nullptr, out_cnt, st);
+    launch_forward_finish(out4, cnt, pinv, b, 1, nullptr, out_i, nullptr, out_cnt, nullptr, st);
     return cuda_status();
   }
   launch_backward_points(upstream, nullptr, pinv, b, 1, nullptr, out4, prec, out_dp, st);

@@ -1070,16 +1070,21 @@ __global__ void __launch_bounds__(kBwdWarps * 32, MG_BWD_MINB) backward_kernel(c
                                                                   const int* __restrict__ pstart,
                                                                   const int4* __restrict__ items,
                                                                   const int* __restrict__ nitems_dev,
-                                                                  float* __restrict__ acc10) {
+                                                                  int n_implicit, float* __restrict__ acc10) {
   __shared__ SegSmem s_seg[kBwdWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nitems = *nitems_dev;
+  // items == nullptr: one item per sorted Gaussian, {i, gkey[i], 1} (QG = 1),
+  // in cell order -- concurrently running warps then share point windows
+  const int nitems = items ? *nitems_dev : n_implicit;
+  auto load_item = [&](int j) {
+    return items ? items[j] : make_int4(j, (int)gkey[j], 1, 0);
+  };
   const int stride = gridDim.x * kBwdWarps;
   int it = blockIdx.x * kBwdWarps + warp;
-  int4 next = (MG_BWD_IPF && it < nitems) ? items[it] : make_int4(0, 0, 0, 0);
+  int4 next = (MG_BWD_IPF && it < nitems) ? load_item(it) : make_int4(0, 0, 0, 0);
   for (; it < nitems; it += stride) {
-    const int4 item = MG_BWD_IPF ? next : items[it];  // {first, cell, count, 0}
-    if (MG_BWD_IPF && it + stride < nitems) next = items[it + stride];  // loads under this item
+    const int4 item = MG_BWD_IPF ? next : load_item(it);  // {first, cell, count, 0}
+    if (MG_BWD_IPF && it + stride < nitems) next = load_item(it + stride);  // loads under this item
     const int g0 = item.x, cell = item.y, ng = item.z;
     if (kBwdQG == 2 && ng == 2)
       bwd_item<kBwdQG>(grec, g0, ng, cell, g, r, prec, pstart, acc10, s_seg[warp], lane);
@@ -1445,6 +1450,46 @@ int fwd_dense_min() { return kFwdDenseMin; }
 
 size_t items_workspace_bytes(int64_t n) { return 2 * (((size_t)n * 4 + 255) & ~(size_t)255) + scan_workspace_bytes(n); }
 
+// One pass over cells: each occupied cell appends its ceil(count / q) item
+// records with one warp-aggregated atomic per warp.  Item ORDER only affects
+// scheduling (every item's arithmetic is self-contained), and cells are
+// visited in index order, so neighbouring warps still get neighbouring cells.
+__global__ void cell_items_kernel(const int* __restrict__ starts, int64_t ncell, int q, int dense_min,
+                                  int4* __restrict__ items, int* __restrict__ nitems) {
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t c0 = (int64_t)blockIdx.x * blockDim.x; c0 < ncell; c0 += stride) {
+    const int64_t c = c0 + threadIdx.x;
+    int s = 0, e = 0;
+    if (c < ncell) {
+      s = starts[c];
+      e = starts[c + 1];
+    }
+    const int cnt = e - s;
+    const int qq = (dense_min > 0 && cnt >= dense_min) ? 64 : q;
+    const int m = (cnt + qq - 1) / qq;
+    int tot;
+    const int off = warp_excl_scan(m, lane, &tot);
+    int base = 0;
+    if (lane == 0 && tot > 0) base = atomicAdd(nitems, tot);
+    base = __shfl_sync(0xffffffffu, base, 0) + off;
+    for (int i = 0; i < m; ++i) {
+      const int p = s + i * qq;
+      items[base + i] = make_int4(p, (int)c, min(qq, e - p), 0);
+    }
+  }
+}
+
+void build_items_cells(const int* starts, int64_t ncell, int q, int4* items, int* nitems, cudaStream_t st,
+                       int dense_min) {
+  cudaMemsetAsync(nitems, 0, sizeof(int), st);
+  if (ncell <= 0) return;
+  int64_t blocks = (ncell + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  MG_LAUNCH(cell_items_kernel<<<(unsigned)blocks, 256, 0, st>>>(starts, ncell, q, dense_min, items, nitems));
+}
+
 void build_items(const uint32_t* keys, const int* starts, int64_t n, int q, int4* items, int* nitems, void* ws,
                  cudaStream_t st, int dense_min) {
   if (n <= 0) {
@@ -1538,7 +1583,7 @@ void launch_backward_staged(const float* grec_raw, int64_t n_gauss, const uint32
                                                                     oitems, counts + 1));
   const int64_t want = (n_gauss / 2 + kBwdWarps) / kBwdWarps;
   MG_LAUNCH(backward_kernel<<<(unsigned)persistent_blocks(backward_kernel, kBwdWarps * 32, want), kBwdWarps * 32, 0,
-                              st>>>(grec, gkey, gstart, g, r, prec, pstart, oitems, counts + 1, acc10));
+                              st>>>(grec, gkey, gstart, g, r, prec, pstart, oitems, counts + 1, 0, acc10));
 }
 
 void launch_backward(const float* grec_raw, int64_t n_gauss, const uint32_t* gkey, const int* gstart, int g, int r,
@@ -1548,7 +1593,7 @@ void launch_backward(const float* grec_raw, int64_t n_gauss, const uint32_t* gke
   const GaussSoA grec = gauss_soa(grec_raw, n_gauss);
   const int64_t want = (max_items + kBwdWarps - 1) / kBwdWarps;
   MG_LAUNCH(backward_kernel<<<(unsigned)persistent_blocks(backward_kernel, kBwdWarps * 32, want), kBwdWarps * 32, 0, st>>>(
-      grec, gkey, gstart, g, r, prec, pstart, items, nitems, acc10));
+      grec, gkey, gstart, g, r, prec, pstart, items, nitems, (int)n_gauss, acc10));
 }
 
 }  // namespace mg

@@ -20,6 +20,8 @@ void launch_points_prepare(const double* coords, const int64_t* sids64, const in
                            int nslices, int g, uint32_t* keys, float4* xf, double* xout, cudaStream_t st);
 void launch_points_gather(const float4* xf, const int* perm, int64_t n, float4* prec, int* inv, cudaStream_t st);
 size_t items_workspace_bytes(int64_t n);
+void build_items_cells(const int* starts, int64_t ncell, int q, int4* items, int* nitems, cudaStream_t st,
+                       int dense_min = 0);
 void build_items(const uint32_t* keys, const int* starts, int64_t n, int q, int4* items, int* nitems, void* ws,
                  cudaStream_t st, int dense_min = 0);
 
@@ -38,7 +40,10 @@ void launch_backward_staged(const float* grec, int64_t n_gauss, const uint32_t* 
 
 // epilogues / training
 void launch_forward_finish(const float4* out4, const int* cnt, const int* inv, int64_t b, int ntaps,
-                           const double* tap_w, double* out_i, float* out_i32, int64_t* out_cnt, cudaStream_t st);
+                           const double* tap_w, double* out_i, float* out_i32, int64_t* out_cnt, int64_t* pair_total,
+                           cudaStream_t st);
+void launch_gather_batch(const int64_t* idx, int64_t n, const double* pc, const int64_t* ps, const float* pt,
+                         double* c, int64_t* s, float* t, cudaStream_t st);
 void launch_backward_points(const double* up64, const float* up32, const int* inv, int64_t b, int ntaps,
                             const double* tap_w, const float4* out4, float4* prec, double* dpoints, cudaStream_t st);
 void launch_acc_to_ref(const float* acc10, const int* order, int64_t n, const double* alpha64, double* d_mu,

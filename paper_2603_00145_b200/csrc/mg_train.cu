@@ -25,7 +25,9 @@ static inline unsigned gridn(int64_t n, int t = 256) {
 __global__ void forward_finish_kernel(const float4* __restrict__ out4, const int* __restrict__ cnt,
                                       const int* __restrict__ inv, int64_t b, int ntaps,
                                       const double* __restrict__ tap_w, double* __restrict__ out_i,
-                                      float* __restrict__ out_i32, int64_t* __restrict__ out_cnt) {
+                                      float* __restrict__ out_i32, int64_t* __restrict__ out_cnt,
+                                      unsigned long long* __restrict__ pair_total) {
+  unsigned long long mine = 0;
   GRID_LOOP(pb, b) {
     double acc = 0.0;
     int64_t c = 0;
@@ -38,6 +40,25 @@ __global__ void forward_finish_kernel(const float4* __restrict__ out4, const int
     if (out_i) out_i[pb] = acc;
     if (out_i32) out_i32[pb] = (float)acc;
     if (out_cnt) out_cnt[pb] = c;
+    mine += (unsigned long long)c;
+  }
+  if (pair_total) {  // whole-launch pair count (integer: order-independent)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(pair_total, mine);
+  }
+}
+
+__global__ void gather_batch_kernel(const int64_t* __restrict__ idx, int64_t n, const double* __restrict__ pc,
+                                    const int64_t* __restrict__ ps, const float* __restrict__ pt,
+                                    double* __restrict__ c, int64_t* __restrict__ s, float* __restrict__ t) {
+  GRID_LOOP(i, n) {
+    const int64_t j = idx[i];
+    c[3 * i + 0] = pc[3 * j + 0];
+    c[3 * i + 1] = pc[3 * j + 1];
+    c[3 * i + 2] = pc[3 * j + 2];
+    s[i] = ps[j];
+    t[i] = pt[j];
   }
 }
 
@@ -456,8 +477,14 @@ __global__ void upsample_kernel(const float* __restrict__ q_old, const float* __
 // Launchers
 // ---------------------------------------------------------------------------
 void launch_forward_finish(const float4* out4, const int* cnt, const int* inv, int64_t b, int ntaps,
-                           const double* tap_w, double* out_i, float* out_i32, int64_t* out_cnt, cudaStream_t st) {
-  if (b > 0) MG_LAUNCH(forward_finish_kernel<<<gridn(b), 256, 0, st>>>(out4, cnt, inv, b, ntaps, tap_w, out_i, out_i32, out_cnt));
+                           const double* tap_w, double* out_i, float* out_i32, int64_t* out_cnt, int64_t* pair_total, cudaStream_t st) {
+  if (b > 0)
+    MG_LAUNCH(forward_finish_kernel<<<gridn(b), 256, 0, st>>>(out4, cnt, inv, b, ntaps, tap_w, out_i, out_i32, out_cnt,
+                                                              (unsigned long long*)pair_total));
+}
+void launch_gather_batch(const int64_t* idx, int64_t n, const double* pc, const int64_t* ps, const float* pt,
+                         double* c, int64_t* s, float* t, cudaStream_t st) {
+  if (n > 0) MG_LAUNCH(gather_batch_kernel<<<gridn(n), 256, 0, st>>>(idx, n, pc, ps, pt, c, s, t));
 }
 void launch_backward_points(const double* up64, const float* up32, const int* inv, int64_t b, int ntaps,
                             const double* tap_w, const float4* out4, float4* prec, double* dpoints, cudaStream_t st) {

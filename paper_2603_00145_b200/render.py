@@ -233,7 +233,7 @@ def _stage_psf(field, gd, p6, al, c_d, s_d, rot_d, tr_d, k, g, psf, with_h, radi
     I = dv.empty((b,), torch.float64)
     c64 = dv.empty((b,), torch.int64)
     N.check(L.mg_forward_finish(N.ptr(out4), N.ptr(cnt), N.ptr(pinv), b, t, N.ptr(wts), N.ptr(I), None, N.ptr(c64),
-                                st), "forward_finish")
+                                None, st), "forward_finish")
     return dict(grec=grec, pkey=pkey, pinv=pinv, pstart=pstart, prec=prec, x=x, out4=out4, I=I, cnt=c64, off=off,
                 wts=wts, dirs=dirs, ws=ws)
 

@@ -383,11 +383,10 @@ class Trainer:
         return B
 
     def _body(self, B, nb, hw):
-        torch.index_select(self.src_coords, 0, B.idx, out=B.coords)
-        torch.index_select(self.src_sids, 0, B.idx, out=B.sids)
-        torch.index_select(self.src_tgt, 0, B.idx, out=B.tgt)
+        N.check(N.lib().mg_gather_batch(N.ptr(B.idx), B.idx.numel(), N.ptr(self.src_coords), N.ptr(self.src_sids),
+                                        N.ptr(self.src_tgt), N.ptr(B.coords), N.ptr(B.sids), N.ptr(B.tgt),
+                                        dv.sptr()), "gather_batch")
         self._launch(B, B.coords, B.sids, B.tgt, nb, hw)
-        B.pairs.add_(B.cnt.sum(dtype=torch.int64))
 
     def _device_step(self, all_idx, nb, hw, sync):
         cfg = self.config
@@ -457,7 +456,7 @@ class Trainer:
         N.check(L.mg_forward(N.ptr(B.grec), n, N.ptr(B.gstart), g, r, N.ptr(B.prec), N.ptr(B.pkey), N.ptr(B.pstart),
                              ns, 1, N.ptr(B.out4), N.ptr(B.cnt), N.ptr(ws), ws.numel(), st), "forward")
         N.check(L.mg_forward_finish(N.ptr(B.out4), N.ptr(B.cnt), N.ptr(B.pinv), bt, t, N.ptr(wts), None,
-                                    N.ptr(B.pred), None, st), "finish")
+                                    N.ptr(B.pred), None, N.ptr(B.pairs), st), "finish")
         nrf_cache = None
         if self.nrf_active:
             from .nrf import nrf_forward_cached

@@ -354,17 +354,9 @@ int mg_backward(const void* grec, const uint32_t* gkey_sorted, const int32_t* gs
                            acc10, ws, st);
     return cuda_status();
   }
-  Bump w(ws, wsb);
-  int4* items = w.take<int4>(n);
-  int* nitems = w.take<int>(1);
-  if (!w.ok) return fail("mg_backward: workspace too small");
-  if (bwd_qg() == 1) {  // one item per sorted Gaussian: implicit, no item build
-    items = nullptr;
-  } else {
-    build_items_cells(gstart, ncell_of(g), bwd_qg(), items, nitems, st);
-  }
-  launch_backward((const float*)grec, n, gkey_sorted, gstart, (int)g, (int)r, (const float4*)prec, pstart, items,
-                  nitems, n, acc10, st);
+  // one work item per sorted Gaussian, implicit: no item build, no workspace
+  launch_backward((const float*)grec, n, gkey_sorted, gstart, (int)g, (int)r, (const float4*)prec, pstart, nullptr,
+                  nullptr, n, acc10, st);
   return cuda_status();
 }
 

@@ -186,13 +186,14 @@ __global__ void item_flags_kernel(const uint32_t* __restrict__ keys, const int* 
 // with ONE load instead of the items -> key -> starts dependency chain.
 __global__ void item_compact_kernel(const int* __restrict__ flags, const int* __restrict__ scan,
                                     const uint32_t* __restrict__ keys, const int* __restrict__ starts, int64_t n, int q,
-                                    int dense_min, int4* __restrict__ items, int* __restrict__ nitems) {
+                                    int dense_min, int4* __restrict__ items, int* __restrict__ nitems,
+                                    int single_gauss = 0) {
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
     if (flags[p]) {
       const uint32_t key = keys[p];
       const int e = starts[key + 1];
       const int qq = (dense_min > 0 && e - starts[key] >= dense_min) ? 64 : q;
-      items[scan[p]] = make_int4((int)p, (int)key, min(qq, e - (int)p), 0);
+      items[scan[p]] = make_int4((int)p, (int)key, single_gauss ? -1 : min(qq, e - (int)p), 0);
     }
     if (p == n - 1) *nitems = scan[p] + flags[p];
   }
@@ -426,12 +427,6 @@ __device__ __forceinline__ void write_point_out(float4* __restrict__ out4, int* 
 #endif
 #ifndef MG_BWD_IPF
 #define MG_BWD_IPF 1
-#endif
-#ifndef MG_BWD_PP
-#define MG_BWD_PP 0  // 1: prefetch window t+1 while window t computes (measured slower: fewer resident warps)
-#endif
-#ifndef MG_BWD_QG
-#define MG_BWD_QG 1  // max Gaussians per backward work item (1 or 2); 1 is faster at ~1 Gaussian per cell
 #endif
 #ifndef MG_BWD_WARPS
 #define MG_BWD_WARPS 8
@@ -893,9 +888,6 @@ __global__ void __launch_bounds__(kFwdWarps * 32, MG_FWD_MINB) forward_kernel(co
 // d_abar6 = -0.5*alpha*A6 (_kernels.py:118-141).
 // ---------------------------------------------------------------------------
 constexpr int kBwdWarps = MG_BWD_WARPS;
-constexpr int kBwdQG = MG_BWD_QG;
-constexpr bool kBwdPingPong = MG_BWD_PP != 0;
-static_assert(kBwdQG == 1 || kBwdQG == 2, "MG_BWD_QG must be 1 or 2");
 
 struct Pts4 {
   float4 p[4];
@@ -949,6 +941,35 @@ struct GaussAcc {
     }
   }
 
+  __device__ __forceinline__ void load(const GaussSoA& grec, int k, int gi) {
+    const float4 A = grec.A[gi], B = grec.B[gi];
+    const float2 C = grec.C[gi];
+    mx[k] = A.x;
+    my[k] = A.y;
+    mz[k] = A.z;
+    P[k][0] = B.x;
+    P[k][1] = B.y;
+    P[k][2] = B.z;
+    P[k][3] = 2.f * B.w;  // doubling is exact
+    P[k][4] = 2.f * C.x;
+    P[k][5] = 2.f * C.y;
+    S[k] = bc2(0.f);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) T[k][c] = bc2(0.f);
+#pragma unroll
+    for (int c = 0; c < 6; ++c) A6[k][c] = bc2(0.f);
+  }
+  // one 128-wide window: the lane's points v, v+32, v+64, v+96 as two pairs
+  __device__ __forceinline__ void quad(const float4 (&q)[4]) {
+    pair(q[0], q[1]);
+    pair(q[2], q[3]);
+  }
+  // ragged window: missing points are zero records (zero upstream)
+  __device__ __forceinline__ void quad_tail(const float4 (&q)[4], const int (&v)[4], int wend) {
+    if (v[0] < wend) pair(q[0], q[1]);
+    if (v[2] < wend) pair(q[2], q[3]);
+  }
+
   // lane-local totals of the 10 accumulators of Gaussian k, T = P' D1
   __device__ __forceinline__ void totals(int k, float* v) const {
     v[0] = lo(S[k]) + hi(S[k]);
@@ -962,32 +983,11 @@ struct GaussAcc {
   }
 };
 
-template <int QG>
-__device__ __forceinline__ void bwd_item(const GaussSoA grec, int g0, int ng, int cell, int g, int r,
-                                         const float4* __restrict__ prec, const int* __restrict__ pstart,
-                                         float* __restrict__ acc10, SegSmem& sm, int lane) {
-  GaussAcc<QG> acc;
-#pragma unroll
-  for (int k = 0; k < QG; ++k) {
-    int gi = g0 + min(k, ng - 1);
-    const float4 A = grec.A[gi], B = grec.B[gi];
-    const float2 C = grec.C[gi];
-    acc.mx[k] = A.x;
-    acc.my[k] = A.y;
-    acc.mz[k] = A.z;
-    acc.P[k][0] = B.x;  // P00
-    acc.P[k][1] = B.y;  // P11
-    acc.P[k][2] = B.z;  // P22
-    acc.P[k][3] = 2.f * B.w;  // 2 P01 (exact)
-    acc.P[k][4] = 2.f * C.x;  // 2 P02
-    acc.P[k][5] = 2.f * C.y;  // 2 P12
-    acc.S[k] = bc2(0.f);
-#pragma unroll
-    for (int c = 0; c < 3; ++c) acc.T[k][c] = bc2(0.f);
-#pragma unroll
-    for (int c = 0; c < 6; ++c) acc.A6[k][c] = bc2(0.f);
-  }
-  const Window w = make_window(cell, g, r);
+// Candidate-point window loop: lanes stride over the flattened candidate
+// points, four per lane per 128-wide window.
+template <class Acc>
+__device__ __forceinline__ void bwd_window_loop(Acc& acc, const Window& w, int g, const float4* __restrict__ prec,
+                                                const int* __restrict__ pstart, SegSmem& sm, int lane) {
   const unsigned upto = 0xffffffffu >> (31 - lane);  // bits 0..lane
   for (int c0 = 0; c0 < w.ncol; c0 += 128) {
     const LaneSegs L = build_lane_segs(w, c0, g, pstart, sm, lane);
@@ -997,54 +997,34 @@ __device__ __forceinline__ void bwd_item(const GaussSoA grec, int g0, int ng, in
       const int wend = min(tot, w0 + 32 * kBmWords);
       const int nfull = (wend - w0) >> 7;
       int v[4], e[4];
-      if (!kBwdPingPong) {
-        for (int t = 0; t < nfull; ++t) {
-          cur.next(sm, w0, w0 + 128 * t, upto, lane, v, e);
-          float4 q[4];
+      for (int t = 0; t < nfull; ++t) {
+        cur.next(sm, w0, w0 + 128 * t, upto, lane, v, e);
+        float4 q[4];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) q[i] = __ldg(prec + e[i]);
-          acc.pair(q[0], q[1]);
-          acc.pair(q[2], q[3]);
-        }
-      } else if (nfull > 0) {
-        // ping-pong register sets: window t+1 loads while window t computes
-        float4 q0[4], q1[4];
-        cur.next(sm, w0, w0, upto, lane, v, e);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) q0[i] = __ldg(prec + e[i]);
-        for (int t = 0; t < nfull; t += 2) {
-          const bool h1 = t + 1 < nfull;
-          if (h1) {
-            cur.next(sm, w0, w0 + 128 * (t + 1), upto, lane, v, e);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) q1[i] = __ldg(prec + e[i]);
-          }
-          acc.pair(q0[0], q0[1]);
-          acc.pair(q0[2], q0[3]);
-          if (t + 2 < nfull) {
-            cur.next(sm, w0, w0 + 128 * (t + 2), upto, lane, v, e);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) q0[i] = __ldg(prec + e[i]);
-          }
-          if (h1) {
-            acc.pair(q1[0], q1[1]);
-            acc.pair(q1[2], q1[3]);
-          }
-        }
+        for (int i = 0; i < 4; ++i) q[i] = __ldg(prec + e[i]);
+        acc.quad(q);
       }
       const int tb = w0 + (nfull << 7);
-      if (tb < wend) {  // ragged tail window: missing partners get zero upstream
+      if (tb < wend) {  // ragged tail window
         cur.next(sm, w0, tb, upto, lane, v, e);
         float4 pt[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) pt[i] = v[i] < wend ? __ldg(prec + e[i]) : make_float4(0.f, 0.f, 0.f, 0.f);
-        // v0 < v1 < v2 < v3: a missing partner carries zero upstream
-        if (v[0] < wend) acc.pair(pt[0], pt[1]);
-        if (v[2] < wend) acc.pair(pt[2], pt[3]);
+        acc.quad_tail(pt, v, wend);
       }
       __syncwarp();
     }
   }
+}
+
+template <int QG>
+__device__ __forceinline__ void bwd_item(const GaussSoA grec, int g0, int ng, int cell, int g, int r,
+                                         const float4* __restrict__ prec, const int* __restrict__ pstart,
+                                         float* __restrict__ acc10, SegSmem& sm, int lane) {
+  GaussAcc<QG> acc;
+#pragma unroll
+  for (int k = 0; k < QG; ++k) acc.load(grec, k, g0 + min(k, ng - 1));
+  bwd_window_loop(acc, make_window(cell, g, r), g, prec, pstart, sm, lane);
   // 10 sums per Gaussian (x QG, padded to 16 / 32) -> transposed reduction.
   constexpr int NV = QG == 1 ? 16 : 32;
   float vals[32];
@@ -1073,11 +1053,12 @@ __global__ void __launch_bounds__(kBwdWarps * 32, MG_BWD_MINB) backward_kernel(c
                                                                   int n_implicit, float* __restrict__ acc10) {
   __shared__ SegSmem s_seg[kBwdWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // items == nullptr: one item per sorted Gaussian, {i, gkey[i], 1} (QG = 1),
-  // in cell order -- concurrently running warps then share point windows
+  // item {Gaussian, cell, -1, 0} (staged-path overflow list); items ==
+  // nullptr: one item per sorted Gaussian, in cell order, so concurrently
+  // running warps share their candidate point windows
   const int nitems = items ? *nitems_dev : n_implicit;
   auto load_item = [&](int j) {
-    return items ? items[j] : make_int4(j, (int)gkey[j], 1, 0);
+    return items ? items[j] : make_int4(j, (int)gkey[j], -1, 0);
   };
   const int stride = gridDim.x * kBwdWarps;
   int it = blockIdx.x * kBwdWarps + warp;
@@ -1085,11 +1066,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, MG_BWD_MINB) backward_kernel(c
   for (; it < nitems; it += stride) {
     const int4 item = MG_BWD_IPF ? next : load_item(it);  // {first, cell, count, 0}
     if (MG_BWD_IPF && it + stride < nitems) next = load_item(it + stride);  // loads under this item
-    const int g0 = item.x, cell = item.y, ng = item.z;
-    if (kBwdQG == 2 && ng == 2)
-      bwd_item<kBwdQG>(grec, g0, ng, cell, g, r, prec, pstart, acc10, s_seg[warp], lane);
-    else
-      bwd_item<1>(grec, g0, ng, cell, g, r, prec, pstart, acc10, s_seg[warp], lane);
+    bwd_item<1>(grec, item.x, 1, item.y, g, r, prec, pstart, acc10, s_seg[warp], lane);
   }
 }
 
@@ -1393,7 +1370,7 @@ __global__ void overflow_flags_kernel(const uint32_t* __restrict__ keys, const i
                                       int* __restrict__ flags) {
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
     const int d = (int)(p - starts[keys[p]]);
-    flags[p] = (d >= 2 && (d - 2) % kBwdQG == 0) ? 1 : 0;
+    flags[p] = d >= 2 ? 1 : 0;
   }
 }
 
@@ -1445,7 +1422,6 @@ void launch_points_gather(const float4* xf, const int* perm, int64_t n, float4* 
 }
 
 int fwd_qmax() { return MG_FWD_QMAX; }
-int bwd_qg() { return MG_BWD_QG; }
 int fwd_dense_min() { return kFwdDenseMin; }
 
 size_t items_workspace_bytes(int64_t n) { return 2 * (((size_t)n * 4 + 255) & ~(size_t)255) + scan_workspace_bytes(n); }
@@ -1579,8 +1555,8 @@ void launch_backward_staged(const float* grec_raw, int64_t n_gauss, const uint32
   int* oscan = scan;
   MG_LAUNCH(overflow_flags_kernel<<<grid_for(n_gauss), 256, 0, st>>>(gkey, gstart, n_gauss, oflags));
   excl_scan(oflags, oscan, n_gauss, sws, st);
-  MG_LAUNCH(item_compact_kernel<<<grid_for(n_gauss), 256, 0, st>>>(oflags, oscan, gkey, gstart, n_gauss, kBwdQG, 0,
-                                                                    oitems, counts + 1));
+  MG_LAUNCH(item_compact_kernel<<<grid_for(n_gauss), 256, 0, st>>>(oflags, oscan, gkey, gstart, n_gauss, 1, 0,
+                                                                    oitems, counts + 1, 1));
   const int64_t want = (n_gauss / 2 + kBwdWarps) / kBwdWarps;
   MG_LAUNCH(backward_kernel<<<(unsigned)persistent_blocks(backward_kernel, kBwdWarps * 32, want), kBwdWarps * 32, 0,
                               st>>>(grec, gkey, gstart, g, r, prec, pstart, oitems, counts + 1, 0, acc10));

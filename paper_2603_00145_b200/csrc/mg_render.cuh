@@ -5,7 +5,6 @@
 namespace mg {
 int num_sms();
 int fwd_qmax();
-int bwd_qg();
 int fwd_dense_min();
 
 // preprocessing / binning

@@ -6,153 +6,25 @@
 // sort of train.py:390-397).  Stability (ties keep ascending input order)
 // makes cell_indices bit-identical to numpy's argsort(kind="stable").
 #include "mg_sort.cuh"
+#include "mg_scan.cuh"
 
 namespace mg {
 
 // ---------------------------------------------------------------------------
-// Exclusive scan (int32), 3-phase, recursive over block sums.
+// Exclusive scan (int32): the look-back scan of mg_scan.cuh over an array.
 // ---------------------------------------------------------------------------
-constexpr int kScanThreads = 256;
-constexpr int kScanItems = 8;
-constexpr int kScanTile = kScanThreads * kScanItems;  // 2048
+struct ArrayScanOp {
+  const int* in;
+  int* out;
+  __device__ int count(int64_t e) const { return in[e]; }
+  __device__ void emit(int64_t e, int off, int) const { out[e] = off; }
+};
 
-__device__ __forceinline__ int block_excl_scan(int v, int* s_warp, int* total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int wt;
-  int x = warp_excl_scan(v, lane, &wt);
-  if (lane == 0) s_warp[warp] = wt;
-  __syncthreads();
-  if (warp == 0) {
-    int t = lane < (kScanThreads / 32) ? s_warp[lane] : 0;
-    int tt;
-    int e = warp_excl_scan(t, lane, &tt);
-    if (lane < (kScanThreads / 32)) s_warp[lane] = e;
-    if (lane == 0) s_warp[kScanThreads / 32] = tt;
-  }
-  __syncthreads();
-  int r = x + s_warp[warp];
-  *total = s_warp[kScanThreads / 32];
-  __syncthreads();
-  return r;
-}
-
-__global__ void __launch_bounds__(kScanThreads) scan_tiles(const int* __restrict__ in, int* __restrict__ out,
-                                                           int64_t n, int* __restrict__ tile_sums) {
-  __shared__ int s_warp[kScanThreads / 32 + 1];
-  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
-  int v[kScanItems];
-  int sum = 0;
-#pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    int64_t e = base + i;
-    v[i] = e < n ? in[e] : 0;
-    sum += v[i];
-  }
-  int tot;
-  int off = block_excl_scan(sum, s_warp, &tot);
-#pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    int64_t e = base + i;
-    if (e < n) out[e] = off;
-    off += v[i];
-  }
-  if (threadIdx.x == 0 && tile_sums) tile_sums[blockIdx.x] = tot;
-}
-
-// Single-pass exclusive scan with decoupled look-back: every tile publishes
-// its aggregate (flag A) and then its inclusive prefix (flag P); a tile's
-// exclusive prefix comes from a warp-parallel look-back over predecessors.
-// Tile ids are handed out in launch order by an atomic ticket, so every
-// predecessor is already running (forward progress).
-constexpr unsigned long long kFlagA = 1ull << 32, kFlagP = 2ull << 32;
-
-__global__ void __launch_bounds__(kScanThreads) scan_lookback(const int* __restrict__ in, int* __restrict__ out,
-                                                              int64_t n, unsigned long long* __restrict__ state,
-                                                              int* __restrict__ ticket) {
-  __shared__ int s_warp[kScanThreads / 32 + 1];
-  __shared__ int s_tile, s_prefix;
-  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
-  __syncthreads();
-  const int tile = s_tile;
-  const int64_t base = (int64_t)tile * kScanTile + (int64_t)threadIdx.x * kScanItems;
-  int v[kScanItems];
-  int sum = 0;
-#pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    int64_t e = base + i;
-    v[i] = e < n ? in[e] : 0;
-    sum += v[i];
-  }
-  int tot;
-  int off = block_excl_scan(sum, s_warp, &tot);
-  const int lane = threadIdx.x & 31;
-  if (threadIdx.x < 32) {
-    volatile unsigned long long* vs = state;
-    if (tile == 0) {
-      if (lane == 0) {
-        vs[0] = kFlagP | (unsigned)tot;
-        __threadfence();
-        s_prefix = 0;
-      }
-    } else {
-      if (lane == 0) {
-        vs[tile] = kFlagA | (unsigned)tot;
-        __threadfence();
-      }
-      int prefix = 0;
-      int look = tile - 1;
-      while (true) {
-        const int t = look - lane;
-        unsigned long long w = kFlagP;  // before tile 0: inclusive prefix 0
-        if (t >= 0) {
-          do {
-            w = vs[t];
-          } while ((w >> 32) == 0);
-        }
-        const unsigned pmask = __ballot_sync(MG_FULL, (w >> 32) == 2);
-        const int first_p = pmask ? __ffs(pmask) - 1 : 32;  // lanes up to the first P contribute
-        int val = (lane <= first_p) ? (int)(w & 0xffffffffu) : 0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(MG_FULL, val, o);
-        prefix += val;
-        if (pmask) break;
-        look -= 32;
-      }
-      if (lane == 0) {
-        vs[tile] = kFlagP | (unsigned)(prefix + tot);
-        __threadfence();
-        s_prefix = prefix;
-      }
-    }
-  }
-  __syncthreads();
-  off += s_prefix;
-#pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    int64_t e = base + i;
-    if (e < n) out[e] = off;
-    off += v[i];
-  }
-}
-
-size_t scan_workspace_bytes(int64_t n) {
-  int64_t tiles = (n + kScanTile - 1) / kScanTile;
-  if (tiles < 1) tiles = 1;
-  return (((size_t)tiles * 8 + 255) & ~(size_t)255) + 256;
-}
+size_t scan_workspace_bytes(int64_t n) { return lookback_state_bytes(n); }
 
 // out[i] = sum_{j<i} in[j]; out may alias in (each tile reads before it writes).
 void excl_scan(const int* in, int* out, int64_t n, void* ws, cudaStream_t st) {
-  if (n <= 0) return;
-  int64_t tiles = (n + kScanTile - 1) / kScanTile;
-  if (tiles == 1) {
-    MG_LAUNCH(scan_tiles<<<1, kScanThreads, 0, st>>>(in, out, n, nullptr));
-    return;
-  }
-  unsigned long long* state = (unsigned long long*)ws;
-  int* ticket = (int*)((char*)ws + (((size_t)tiles * 8 + 255) & ~(size_t)255));
-  cudaMemsetAsync(ws, 0, (((size_t)tiles * 8 + 255) & ~(size_t)255) + 4, st);
-  MG_LAUNCH(scan_lookback<<<(unsigned)tiles, kScanThreads, 0, st>>>(in, out, n, state, ticket));
+  lookback_scan(ArrayScanOp{in, out}, n, ws, st);
 }
 
 // ---------------------------------------------------------------------------

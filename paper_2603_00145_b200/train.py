@@ -21,6 +21,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field as dc_field, replace  # noqa: F401
 
+import os
+
 import numpy as np
 import torch
 
@@ -31,6 +33,9 @@ from .errors import NonFiniteLoss, ShrinkNotAllowed
 from .render import SlicePSF, sample_volume_device
 
 DEFAULT_SCHEDULE = ((0, 70), (500, 100), (1000, 130), (2000, 165), (3000, 200))
+
+
+_PERM_PREFETCH_MIN = 1 << 18  # pools from this size draw epoch permutations ahead
 
 
 @dataclass
@@ -261,6 +266,7 @@ class Trainer:
         self.iteration = 0
         self._perm = None
         self._cursor = 0
+        self._permuter = None  # next-epoch permutation prefetch (large pools)
         self.reports = []
         self._bufs = None
         self._bufs_key = None
@@ -297,16 +303,30 @@ class Trainer:
         b = min(self.config.batch_points, m)
         if b == m:
             return np.arange(m)
-        picked, need = [], b
+        picked, need, drew = [], b, False
         while need > 0:
             if self._perm is None or self._cursor >= m:
-                self._perm = self.rng.permutation(m)
+                perm = self._permuter.take(self.rng) if self._permuter is not None else None
+                self._perm = perm if perm is not None else self.rng.permutation(m)
                 self._cursor = 0
+                drew = True
             take = min(need, m - self._cursor)
             picked.append(self._perm[self._cursor:self._cursor + take])
             self._cursor += take
             need -= take
-        return np.concatenate(picked) if len(picked) > 1 else picked[0]
+        # copy the batch out before the helper may refill the old slot
+        out = np.concatenate(picked) if len(picked) > 1 else picked[0].copy()
+        if drew and m >= _PERM_PREFETCH_MIN and os.environ.get("MGAUSS_PERM_PREFETCH", "1") != "0":
+            # the draws before the next epoch boundary: this step's slice pick
+            # and one per full step still served by the current permutation
+            q = (m - self._cursor) // b
+            calls = [len(self.slice_grids)] * (1 + q) if self.config.use_ssim else []
+            if self._permuter is None:
+                from ._permuter import EpochPermuter
+
+                self._permuter = EpochPermuter(m)
+            self._permuter.request(self.rng, calls)
+        return out
 
     def _apply_milestones(self):
         if not self.config.use_progressive:
@@ -346,6 +366,18 @@ class Trainer:
         return np.concatenate([idx, self._sg_off[slice_j] + np.arange(hw[0] * hw[1], dtype=np.int64)]), hw
 
     # -- one optimizer step ----------------------------------------------------
+    def close(self):
+        """Stop the permutation helper process (also done at garbage collection)."""
+        if self._permuter is not None:
+            self._permuter.close()
+            self._permuter = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
     def step(self, sync=True):
         cfg = self.config
         self._apply_milestones()
@@ -367,6 +399,13 @@ class Trainer:
             self._bufs.sids = dv.empty((b_total,), torch.int64)
             self._bufs.tgt = dv.empty((b_total,), torch.float32)
             self._bufs.pairs = dv.zeros((1,), torch.int64)
+            # two pinned index staging slots (a slot is rewritten only after its
+            # previous H2D copy has completed) and one pinned loss readback slot
+            self._bufs.idx_host = [torch.empty((b_total,), dtype=torch.int64, pin_memory=True) for _ in range(2)]
+            self._bufs.idx_done = [None, None]
+            self._bufs.slot = 0
+            self._bufs.scalars_host = torch.empty((4,), dtype=torch.float64, pin_memory=True)
+            self._bufs.err_host = torch.empty((1,), dtype=torch.int32, pin_memory=True)
             self._bufs_key = key
             self._graph = None
         return self._bufs
@@ -377,9 +416,16 @@ class Trainer:
         B = self._buffers(len(all_idx))
         if isinstance(all_idx, torch.Tensor):
             B.idx.copy_(all_idx, non_blocking=True)
-        else:
-            B.idx.copy_(torch.from_numpy(np.ascontiguousarray(all_idx, dtype=np.int64)).pin_memory(),
-                        non_blocking=True)
+            return B
+        k = B.slot
+        B.slot ^= 1
+        if B.idx_done[k] is not None:
+            B.idx_done[k].synchronize()  # the slot's previous H2D copy has landed
+        np.copyto(B.idx_host[k].numpy(), all_idx, casting="unsafe")
+        B.idx.copy_(B.idx_host[k], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        B.idx_done[k] = ev
         return B
 
     def _body(self, B, nb, hw):
@@ -410,8 +456,13 @@ class Trainer:
         if not sync:
             return LossReport(self.iteration, float("nan"), float("nan"), float("nan"), float("nan"),
                               self.field.resolution, self.nrf_active)
-        sc = dv.to_host(B.scalars)
-        err = int(B.err.item())
+        B.scalars_host.copy_(B.scalars, non_blocking=True)
+        B.err_host.copy_(B.err, non_blocking=True)
+        done = torch.cuda.Event()
+        done.record()
+        done.synchronize()
+        sc = B.scalars_host.numpy()
+        err = int(B.err_host[0])
         if err:
             from .errors import DegenerateQuaternion
 

@@ -1,0 +1,53 @@
+"""Batch sampling of the trainer (train.py:332-347 epoch permutations): the
+next-epoch permutation drawn ahead in the helper process must give exactly
+the batch / slice sequence of drawing it inline, across several epochs."""
+
+import numpy as np
+
+from paper_2603_00145_b200 import train as T
+
+
+def _sampler(seed, m, b, prefetch, monkeypatch):
+    monkeypatch.setenv("MGAUSS_PERM_PREFETCH", "1" if prefetch else "0")
+    monkeypatch.setattr(T, "_PERM_PREFETCH_MIN", 1)
+    t = T.Trainer.__new__(T.Trainer)  # host sampling state only (no device)
+    t.m_points, t.config, t.rng = m, T.TrainConfig(batch_points=b), np.random.default_rng(seed)
+    t._perm, t._cursor, t._permuter, t.slice_grids = None, 0, None, [None] * 7
+    return t
+
+
+def _draw(t, steps):
+    out = []
+    for _ in range(steps):
+        idx = t._next_batch()
+        out.append((idx.copy(), int(t.rng.integers(len(t.slice_grids)))))
+    return out
+
+
+def test_prefetched_permutations_match_inline(monkeypatch):
+    m, b = 5000, 1536  # batches straddle epoch boundaries
+    a = _draw(_sampler(3, m, b, False, monkeypatch), 25)
+    t = _sampler(3, m, b, True, monkeypatch)
+    try:
+        got = _draw(t, 25)
+    finally:
+        t.close()
+    for (ia, ja), (ib, jb) in zip(a, got):
+        np.testing.assert_array_equal(ia, ib)
+        assert ja == jb
+
+
+def test_prefetch_mismatch_falls_back_inline(monkeypatch):
+    m, b = 5000, 1536
+    a = _sampler(5, m, b, False, monkeypatch)
+    t = _sampler(5, m, b, True, monkeypatch)
+    try:
+        for s in (a, t):
+            s._next_batch()
+            s.rng.integers(7)
+            s.rng.integers(3)  # an extra draw the prefetch did not replay
+        for _ in range(6):
+            np.testing.assert_array_equal(a._next_batch(), t._next_batch())
+            assert a.rng.integers(7) == t.rng.integers(7)
+    finally:
+        t.close()

@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define MG_ABI_VERSION 2
+#define MG_ABI_VERSION 3
 #define MG_EINVAL 1
 
 int mg_abi_version(void);
@@ -143,9 +143,14 @@ int mg_epilogue_f64(const double *d_mu, const double *d_abar6, const double *d_a
 int mg_backward_accumulators(const float *acc10, const int32_t *cell_indices, int64_t n, const double *alpha,
                              double *d_mu, double *d_abar6, double *d_alpha, void *stream);
 /* (k,7) transform gradients; scratch12 is (k,12) float64. */
+/* The per-slice sums are reduced deterministically (fixed order, no float
+ * atomics) when ws holds mg_transform_grads_workspace_bytes(k) bytes; with
+ * ws == NULL an atomic fallback is used (not bit-reproducible). */
+size_t mg_transform_grads_workspace_bytes(int64_t k);
 int mg_transform_grads(const double *d_points, const double *coords, const int64_t *slice_ids, int64_t b,
                        int32_t ntaps, const double *tap_offsets, const double *through_dirs, const double *t_quats,
-                       int64_t k, double *scratch12, double *out7, int32_t accumulate, void *stream);
+                       int64_t k, double *scratch12, double *out7, int32_t accumulate, void *ws, size_t ws_bytes,
+                       void *stream);
 
 /* ---- inference: render.py:357-408 --------------------------------------- */
 size_t mg_volume_workspace_bytes(int64_t nx, int64_t ny, int64_t nz);

@@ -50,7 +50,8 @@ SIGNATURES = {
     "mg_backward_accumulators": (ctypes.c_int, [P, P, I64, P, P, P, P, P]),
     "mg_epilogue_f64": (ctypes.c_int, [P, P, P, P, P, P, I64, P, P, P, P, P]),
     "mg_pack_records": (ctypes.c_int, [P, P, P, P, I64, P, P]),
-    "mg_transform_grads": (ctypes.c_int, [P, P, P, I64, I32, P, P, P, I64, P, P, I32, P]),
+    "mg_transform_grads_workspace_bytes": (SZ, [I64]),
+    "mg_transform_grads": (ctypes.c_int, [P, P, P, I64, I32, P, P, P, I64, P, P, I32, P, SZ, P]),
     "mg_volume_workspace_bytes": (SZ, [I64, I64, I64]),
     "mg_sample_volume": (ctypes.c_int, [P, I64, P, I64, I64, I64, I64, I64, P, P, I64, I64, P, P, P, SZ, P]),
     "mg_smooth_l1": (ctypes.c_int, [P, P, I64, P, P, P]),
@@ -74,7 +75,7 @@ _lib = None
 _lock = threading.Lock()
 
 
-ABI_VERSION = 2  # include/mgauss_b200.h MG_ABI_VERSION
+ABI_VERSION = 3  # include/mgauss_b200.h MG_ABI_VERSION
 
 
 def load_library(path=LIB_PATH):

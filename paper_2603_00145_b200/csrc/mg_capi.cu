@@ -385,11 +385,14 @@ int mg_backward_accumulators(const float* acc10, const int32_t* order, int64_t n
   return cuda_status();
 }
 
+size_t mg_transform_grads_workspace_bytes(int64_t k) { return transform_grads_ws_bytes(k); }
+
 int mg_transform_grads(const double* d_points, const double* coords, const int64_t* sids, int64_t b, int32_t ntaps,
                        const double* tap_off, const double* dirs, const double* t_quats, int64_t k, double* scratch12,
-                       double* out7, int32_t accumulate, void* stream) {
+                       double* out7, int32_t accumulate, void* ws, size_t ws_bytes, void* stream) {
+  if (ws && ws_bytes < transform_grads_ws_bytes(k)) return fail("mg_transform_grads: workspace too small");
   launch_transform_grads(d_points, coords, sids, b, ntaps, ntaps > 1 ? tap_off : nullptr, dirs, t_quats, (int)k,
-                         scratch12, out7, accumulate, S(stream));
+                         scratch12, out7, accumulate, ws, S(stream));
   return cuda_status();
 }
 

@@ -54,7 +54,8 @@ void launch_epilogue_f64(const double* d_mu, const double* d_abar6, const double
                          double* d_l, cudaStream_t st);
 void launch_transform_grads(const double* dpoints, const double* coords, const int64_t* sids, int64_t b, int ntaps,
                             const double* tap_off, const double* dirs, const double* tq, int k, double* acc12,
-                            double* out7, int accumulate, cudaStream_t st);
+                            double* out7, int accumulate, void* ws, cudaStream_t st);
+size_t transform_grads_ws_bytes(int64_t k);
 void launch_smooth_l1(const float* pred, const float* target, int64_t b, float* up_out, double* loss_acc,
                       cudaStream_t st);
 size_t ssim_workspace_bytes(int H, int W);

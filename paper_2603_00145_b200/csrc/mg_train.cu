@@ -294,19 +294,145 @@ __global__ void transform_reduce_kernel(const double* __restrict__ dpoints, cons
   }
 }
 
+// Deterministic version: block b owns a contiguous range of sub-points, split
+// into one contiguous sub-range per warp.  Each warp keeps its own per-slice
+// 12-sum table in shared memory; 32 sub-points at a time, the lanes of one
+// slice are summed by their lowest lane in lane order (a butterfly when the
+// whole warp shares the slice).  The block adds its warps' tables in warp
+// order into partials[b]; transform_finish_kernel then reduces the partials
+// in a fixed order.  Same result on every run, no fp64 atomics.
+__device__ __forceinline__ void transform_contrib(const double* __restrict__ dpoints, const double* __restrict__ coords,
+                                                  const int64_t* __restrict__ sids, int ntaps,
+                                                  const double* __restrict__ tap_off, const double* __restrict__ dirs,
+                                                  int k, int64_t j, int& key, double (&v)[12]) {
+  const int64_t pb = j / ntaps;
+  const int t = (int)(j - pb * ntaps);
+  const int64_t s = sids[pb];
+  key = (s < 0 || s >= k) ? -1 : (int)s;
+  double c[3] = {coords[3 * pb], coords[3 * pb + 1], coords[3 * pb + 2]};
+  if (tap_off && key >= 0) {
+    const double o = tap_off[t];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) c[a] = __dadd_rn(c[a], __dmul_rn(o, dirs[3 * s + a]));
+  }
+  const double h[3] = {dpoints[3 * j], dpoints[3 * j + 1], dpoints[3 * j + 2]};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    v[a] = h[a];
+#pragma unroll
+    for (int bb = 0; bb < 3; ++bb) v[3 + 3 * a + bb] = h[a] * c[bb];
+  }
+}
+
+__global__ void transform_reduce_det_kernel(const double* __restrict__ dpoints, const double* __restrict__ coords,
+                                            const int64_t* __restrict__ sids, int64_t b, int ntaps,
+                                            const double* __restrict__ tap_off, const double* __restrict__ dirs, int k,
+                                            double* __restrict__ partials) {
+  extern __shared__ double tr_sh[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int kk = 12 * k;
+  double* table = tr_sh + (size_t)warp * kk;
+  double* stage = tr_sh + (size_t)nw * kk + (size_t)warp * 32 * 12;
+  for (int e = lane; e < kk; e += 32) table[e] = 0.0;
+  __syncwarp();
+  const int64_t total = b * ntaps;
+  const int64_t per_block = (total + gridDim.x - 1) / gridDim.x;
+  const int64_t b0 = (int64_t)blockIdx.x * per_block, b1 = min(total, b0 + per_block);
+  const int64_t per_warp = (b1 - b0 + nw - 1) / nw;
+  const int64_t w0 = b0 + (int64_t)warp * per_warp, w1 = min(b1, w0 + per_warp);
+  for (int64_t j0 = w0; j0 < w1; j0 += 32) {
+    const int64_t j = j0 + lane;
+    int key = -1;
+    double v[12];
+#pragma unroll
+    for (int c = 0; c < 12; ++c) v[c] = 0.0;
+    if (j < w1) transform_contrib(dpoints, coords, sids, ntaps, tap_off, dirs, k, j, key, v);
+    const unsigned peers = __match_any_sync(MG_FULL, key);
+    if (peers == MG_FULL) {
+      if (key >= 0) {
+#pragma unroll
+        for (int c = 0; c < 12; ++c) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v[c] += __shfl_xor_sync(MG_FULL, v[c], o);
+        }
+        if (lane == 0) {
+#pragma unroll
+          for (int c = 0; c < 12; ++c) table[12 * key + c] += v[c];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < 12; ++c) stage[12 * lane + c] = v[c];
+      __syncwarp();
+      if (key >= 0 && lane == __ffs(peers) - 1) {
+        double acc[12];
+#pragma unroll
+        for (int c = 0; c < 12; ++c) acc[c] = 0.0;
+        for (unsigned m = peers; m; m &= m - 1) {
+          const int l = __ffs(m) - 1;
+#pragma unroll
+          for (int c = 0; c < 12; ++c) acc[c] += stage[12 * l + c];
+        }
+#pragma unroll
+        for (int c = 0; c < 12; ++c) table[12 * key + c] += acc[c];
+      }
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < kk; e += blockDim.x) {
+    double acc = 0.0;
+    for (int w = 0; w < nw; ++w) acc += tr_sh[(size_t)w * kk + e];
+    partials[(size_t)blockIdx.x * kk + e] = acc;
+  }
+
+}
+
+// Quaternion chain of one slice (render.py:246-273): 12 sums -> (d_q, d_t).
+__device__ __forceinline__ void transform_chain_slice(const double* a, const double* __restrict__ tq, int64_t s,
+                                                      double* __restrict__ out7, int accumulate) {
+  double qw = tq[4 * s], qx = tq[4 * s + 1], qy = tq[4 * s + 2], qz = tq[4 * s + 3];
+  double nrm = sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
+  double w = qw / nrm, x = qx / nrm, y = qy / nrm, z = qz / nrm;
+  double dqh[4];
+  rot_quat_grad(a + 3, w, x, y, z, dqh);
+  double inner = dqh[0] * w + dqh[1] * x + dqh[2] * y + dqh[3] * z;
+  double o[7] = {(dqh[0] - inner * w) / nrm, (dqh[1] - inner * x) / nrm, (dqh[2] - inner * y) / nrm,
+                 (dqh[3] - inner * z) / nrm, a[0], a[1], a[2]};
+  for (int c = 0; c < 7; ++c) out7[7 * s + c] = accumulate ? out7[7 * s + c] + o[c] : o[c];
+}
+
 __global__ void transform_chain_kernel(const double* __restrict__ acc12, const double* __restrict__ tq, int k,
                                        double* __restrict__ out7, int accumulate) {
-  GRID_LOOP(s, k) {
-    const double* a = acc12 + 12 * s;
-    double qw = tq[4 * s], qx = tq[4 * s + 1], qy = tq[4 * s + 2], qz = tq[4 * s + 3];
-    double nrm = sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
-    double w = qw / nrm, x = qx / nrm, y = qy / nrm, z = qz / nrm;
-    double dqh[4];
-    rot_quat_grad(a + 3, w, x, y, z, dqh);
-    double inner = dqh[0] * w + dqh[1] * x + dqh[2] * y + dqh[3] * z;
-    double o[7] = {(dqh[0] - inner * w) / nrm, (dqh[1] - inner * x) / nrm, (dqh[2] - inner * y) / nrm,
-                   (dqh[3] - inner * z) / nrm, a[0], a[1], a[2]};
-    for (int c = 0; c < 7; ++c) out7[7 * s + c] = accumulate ? out7[7 * s + c] + o[c] : o[c];
+  GRID_LOOP(s, k) transform_chain_slice(acc12 + 12 * s, tq, s, out7, accumulate);
+}
+
+// One warp per slice: lanes stride over the block partials, a fixed-order
+// butterfly finishes each of the 12 sums, then lane 0 applies the chain.
+__global__ void transform_finish_kernel(const double* __restrict__ partials, int nblk, const double* __restrict__ tq,
+                                        int k, double* __restrict__ acc12, double* __restrict__ out7,
+                                        int accumulate) {
+  const int lane = threadIdx.x & 31;
+  const int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (s >= k) return;
+  const int kk = 12 * k;
+  double v[12];
+#pragma unroll
+  for (int c = 0; c < 12; ++c) v[c] = 0.0;
+  for (int blk = lane; blk < nblk; blk += 32) {
+    const double* p = partials + (size_t)blk * kk + 12 * s;
+#pragma unroll
+    for (int c = 0; c < 12; ++c) v[c] += p[c];
+  }
+#pragma unroll
+  for (int c = 0; c < 12; ++c) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[c] += __shfl_xor_sync(MG_FULL, v[c], o);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int c = 0; c < 12; ++c) acc12[12 * s + c] = v[c];
+    transform_chain_slice(v, tq, s, out7, accumulate);
   }
 }
 
@@ -504,15 +630,45 @@ void launch_epilogue_f64(const double* d_mu, const double* d_abar6, const double
                          double* d_l, cudaStream_t st) {
   if (n > 0) MG_LAUNCH(epilogue_f64_kernel<<<gridn(n), 256, 0, st>>>(d_mu, d_abar6, d_alpha, quat, ls, lg, n, d_pos, d_q, d_s, d_l));
 }
+// Deterministic reduction geometry: blocks of kTrWarps warps, at most
+// kTrBlocks blocks; the per-warp slice tables must fit in shared memory.
+constexpr int kTrWarps = 4, kTrBlocks = 148;
+constexpr size_t kTrSmemMax = 200 * 1024;
+static size_t tr_smem(int k) { return sizeof(double) * ((size_t)kTrWarps * 12 * k + (size_t)kTrWarps * 32 * 12); }
+static bool tr_deterministic(int k) { return tr_smem(k) <= kTrSmemMax; }
+
+size_t transform_grads_ws_bytes(int64_t k) {
+  if (k <= 0 || !tr_deterministic((int)k)) return 256;
+  return (((size_t)kTrBlocks * 12 * k * sizeof(double) + 255) & ~(size_t)255) + 256;
+}
+
 void launch_transform_grads(const double* dpoints, const double* coords, const int64_t* sids, int64_t b, int ntaps,
                             const double* tap_off, const double* dirs, const double* tq, int k, double* acc12,
-                            double* out7, int accumulate, cudaStream_t st) {
+                            double* out7, int accumulate, void* ws, cudaStream_t st) {
   if (k <= 0) return;
-  cudaMemsetAsync(acc12, 0, sizeof(double) * 12 * k, st);
-  if (b > 0) {
-    int64_t chunks = (b * ntaps + 7) / 8;
-    MG_LAUNCH(transform_reduce_kernel<<<gridn(chunks, 128), 128, 0, st>>>(dpoints, coords, sids, b, ntaps, tap_off, dirs, k,
-                                                                acc12));
+  if (b > 0 && ws && tr_deterministic(k)) {
+    const size_t smem = tr_smem(k);
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && smem > attr) {
+      cudaFuncSetAttribute(transform_reduce_det_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = smem;
+    }
+    const int64_t total = b * ntaps;
+    int64_t blocks = (total + kTrWarps * 32 * 4 - 1) / (kTrWarps * 32 * 4);
+    blocks = blocks < 1 ? 1 : (blocks > kTrBlocks ? kTrBlocks : blocks);
+    double* partials = (double*)ws;
+    MG_LAUNCH(transform_reduce_det_kernel<<<(unsigned)blocks, kTrWarps * 32, smem, st>>>(
+        dpoints, coords, sids, b, ntaps, tap_off, dirs, k, partials));
+    MG_LAUNCH(transform_finish_kernel<<<(unsigned)((k * 32 + 255) / 256), 256, 0, st>>>(partials, (int)blocks, tq, k,
+                                                                                      acc12, out7, accumulate));
+    return;
+  } else {
+    cudaMemsetAsync(acc12, 0, sizeof(double) * 12 * k, st);
+    if (b > 0) {
+      int64_t chunks = (b * ntaps + 7) / 8;
+      MG_LAUNCH(transform_reduce_kernel<<<gridn(chunks, 128), 128, 0, st>>>(dpoints, coords, sids, b, ntaps, tap_off,
+                                                                            dirs, k, acc12));
+    }
   }
   MG_LAUNCH(transform_chain_kernel<<<gridn(k), 256, 0, st>>>(acc12, tq, k, out7, accumulate));
 }

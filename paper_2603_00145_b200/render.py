@@ -281,8 +281,10 @@ def _transform_grads_dev(ts, c_d, s_d, h_d, psf=None, off=None, dirs=None):
     if psf is not None and off is None:
         off = dv.to_dev(np.asarray(psf.offsets, dtype=np.float64), torch.float64)
         dirs = dv.to_dev(np.asarray(psf.through_dirs, dtype=np.float64).reshape(-1, 3), torch.float64)
-    N.check(N.lib().mg_transform_grads(N.ptr(h_d), N.ptr(c_d), N.ptr(s_d), c_d.shape[0], t, N.ptr(off),
-                                       N.ptr(dirs), N.ptr(tq), k, N.ptr(scratch), N.ptr(out), 0, dv.sptr()),
+    L = N.lib()
+    ws = dv.workspace(L.mg_transform_grads_workspace_bytes(k), "transform")
+    N.check(L.mg_transform_grads(N.ptr(h_d), N.ptr(c_d), N.ptr(s_d), c_d.shape[0], t, N.ptr(off), N.ptr(dirs),
+                                 N.ptr(tq), k, N.ptr(scratch), N.ptr(out), 0, N.ptr(ws), ws.numel(), dv.sptr()),
             "transform_grads")
     return out
 

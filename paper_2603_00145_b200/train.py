@@ -93,6 +93,18 @@ class TrainConfig:
     def final_resolution(self):
         return max(r for _, r in self.resolution_schedule)
 
+    def to_dict(self):
+        """JSON-ready dict (train.py:96-99): the schedule as nested lists."""
+        d = dict(self.__dict__)
+        d["resolution_schedule"] = [list(m) for m in self.resolution_schedule]
+        return d
+
+    @classmethod
+    def from_dict(cls, d):
+        d = dict(d)
+        d["resolution_schedule"] = tuple(tuple(m) for m in d["resolution_schedule"])
+        return cls(**d).validate()
+
 
 @dataclass
 class LossReport:
@@ -219,7 +231,8 @@ class _StepBuffers:
         self.scalars = dv.zeros((4,), torch.float64)  # data loss, aniso loss, ssim sum, spare
         self.err = dv.zeros((1,), torch.int32)
         wsb = max(L.mg_bin_workspace_bytes(n, g), L.mg_points_workspace_bytes(ns, g),
-                  L.mg_forward_workspace_bytes(ns), L.mg_backward_workspace_bytes(n, g))
+                  L.mg_forward_workspace_bytes(ns), L.mg_backward_workspace_bytes(n, g),
+                  L.mg_transform_grads_workspace_bytes(k))
         self.ws = dv.empty((wsb,), torch.uint8)
         self.ssim_ws = None
 
@@ -366,6 +379,114 @@ class Trainer:
         return np.concatenate([idx, self._sg_off[slice_j] + np.arange(hw[0] * hw[1], dtype=np.int64)]), hw
 
     # -- one optimizer step ----------------------------------------------------
+    # -- checkpoint state: the reference Trainer's tree (train.py:514-583) ----
+    _GAUSS_GROUPS = (("positions", "p", 0, 3), ("quaternions", "q", 3, 7), ("log_scales", "s", 7, 10),
+                     ("intensity_logits", "a", 10, 11))
+
+    def state_dict(self):
+        """Checkpoint tree in the reference layout (train.py:516-544), float64
+        host arrays from the float32/float64 device state.  Adam groups that
+        have not stepped since their last reset are absent, as in AdamState."""
+        host = self.field.to_host()
+        t_gauss, t_tr = (int(x) for x in dv.to_host(self.counters))
+        adam = {}
+        if t_gauss > 0:
+            m = dv.to_host(self.m).astype(np.float64)
+            v = dv.to_host(self.v).astype(np.float64)
+            for name, key, lo, hi in self._GAUSS_GROUPS:
+                cut = (lambda a: np.ascontiguousarray(a[:, lo])) if hi - lo == 1 else \
+                    (lambda a: np.ascontiguousarray(a[:, lo:hi]))
+                adam[name] = {"t": t_gauss, "m": {key: cut(m)}, "v": {key: cut(v)}}
+        if t_tr > 0 and self.k:
+            tm, tv = dv.to_host(self.tm)[:self.k], dv.to_host(self.tv)[:self.k]
+            adam["transforms"] = {"t": t_tr, "m": {"q": tm[:, :4].copy(), "t": tm[:, 4:].copy()},
+                                  "v": {"q": tv[:, :4].copy(), "t": tv[:, 4:].copy()}}
+        if self.nrf is not None and self.nrf_t > 0:
+            adam["nrf"] = {"t": int(self.nrf_t),
+                           "m": {k: dv.to_host(a).astype(np.float64) for k, a in self.nrf_m.items()},
+                           "v": {k: dv.to_host(a).astype(np.float64) for k, a in self.nrf_v.items()}}
+        state = {
+            "config": self.config.to_dict(),
+            "iteration": self.iteration,
+            "field": {"positions": host.positions, "quaternions": host.quaternions, "log_scales": host.log_scales,
+                      "intensity_logits": host.intensity_logits, "lattice_dims": list(host.lattice_dims),
+                      "lattice_index": host.lattice_index},
+            "transforms": {"quats": dv.to_host(self.tq).reshape(-1, 4)[:self.k].copy(),
+                           "translations": dv.to_host(self.tt).reshape(-1, 3)[:self.k].copy()},
+            "adam": adam,
+            "rng_state": self.rng.bit_generator.state,
+            "perm": None if self._perm is None else np.array(self._perm, dtype=np.int64),
+            "cursor": self._cursor,
+        }
+        if self.nrf is not None:
+            state["nrf"] = {"frequency_bands": self.nrf.frequency_bands, "layer_widths": list(self.nrf.layer_widths),
+                            "weights": [dv.to_host(w).astype(np.float64) for w in self.nrf.weights],
+                            "biases": [dv.to_host(b).astype(np.float64) for b in self.nrf.biases]}
+        return state
+
+    def load_state_dict(self, state):
+        """Resume from a checkpoint tree written by ``state_dict`` (bit-exact
+        continuation) or by the reference Trainer (parameters rounded to
+        float32).  The trainer must have been built on the same data."""
+        from .core import GaussianField
+
+        cfg = TrainConfig.from_dict(state["config"])
+        self.config = cfg
+        f = state["field"]
+        dims = tuple(int(d) for d in f["lattice_dims"])
+        self.field = DeviceField.from_host(GaussianField(
+            np.asarray(f["positions"], np.float64), np.asarray(f["quaternions"], np.float64),
+            np.asarray(f["log_scales"], np.float64), np.asarray(f["intensity_logits"], np.float64), dims,
+            np.asarray(f["lattice_index"], np.int64)))
+        t = state["transforms"]
+        q = np.asarray(t["quats"], np.float64).reshape(-1, 4)
+        tr = np.asarray(t["translations"], np.float64).reshape(-1, 3)
+        if q.shape[0] != self.k:
+            raise ValueError(f"checkpoint has {q.shape[0]} slice transforms, trainer has {self.k}")
+        self.tq = dv.to_dev(q, torch.float64, (self.k, 4))
+        self.tt = dv.to_dev(tr, torch.float64, (self.k, 3))
+        adam = state["adam"]
+        self._reset_gauss_adam()
+        if "positions" in adam:
+            m = np.zeros((self.field.count, 11), np.float32)
+            v = np.zeros_like(m)
+            for name, key, lo, hi in self._GAUSS_GROUPS:
+                g = adam[name]
+                m[:, lo:hi] = np.asarray(g["m"][key], np.float64).reshape(self.field.count, hi - lo)
+                v[:, lo:hi] = np.asarray(g["v"][key], np.float64).reshape(self.field.count, hi - lo)
+            self.m.copy_(torch.from_numpy(m))
+            self.v.copy_(torch.from_numpy(v))
+            self.counters[0] = int(adam["positions"]["t"])
+        self.tm.zero_()
+        self.tv.zero_()
+        self.counters[1] = 0
+        if "transforms" in adam and self.k:
+            g = adam["transforms"]
+            self.tm[:self.k].copy_(torch.from_numpy(np.concatenate(
+                [np.asarray(g["m"]["q"], np.float64), np.asarray(g["m"]["t"], np.float64)], axis=1)))
+            self.tv[:self.k].copy_(torch.from_numpy(np.concatenate(
+                [np.asarray(g["v"]["q"], np.float64), np.asarray(g["v"]["t"], np.float64)], axis=1)))
+            self.counters[1] = int(g["t"])
+        if "nrf" in state and cfg.use_nrf:
+            from .nrf import ResidualField
+
+            n = state["nrf"]
+            self.nrf = ResidualField.from_numpy(n["weights"], n["biases"], int(n["frequency_bands"]))
+            g = adam.get("nrf")
+            params = self.nrf.parameter_arrays()
+            self.nrf_m = {k: (dv.to_dev(np.asarray(g["m"][k]), torch.float32) if g else torch.zeros_like(a))
+                          for k, a in params.items()}
+            self.nrf_v = {k: (dv.to_dev(np.asarray(g["v"][k]), torch.float32) if g else torch.zeros_like(a))
+                          for k, a in params.items()}
+            self.nrf_t = int(g["t"]) if g else 0
+        self.rng.bit_generator.state = state["rng_state"]
+        self.iteration = int(state["iteration"])
+        perm = state.get("perm")
+        self._perm = None if perm is None else np.array(perm, dtype=np.int64)
+        self._cursor = int(state["cursor"])
+        self._bufs, self._bufs_key, self._graph = None, None, None
+        return self
+
     def close(self):
         """Stop the permutation helper process (also done at garbage collection)."""
         if self._permuter is not None:
@@ -532,7 +653,8 @@ class Trainer:
                               N.ptr(B.pstart), N.ptr(B.acc10), N.ptr(ws), ws.numel(), st), "backward")
         if self.k:
             N.check(L.mg_transform_grads(N.ptr(B.dpts), N.ptr(coords), N.ptr(sids), bt, t, N.ptr(off), N.ptr(dirs),
-                                         N.ptr(self.tq), self.k, N.ptr(B.scratch12), N.ptr(B.g7), 0, st),
+                                         N.ptr(self.tq), self.k, N.ptr(B.scratch12), N.ptr(B.g7), 0, N.ptr(ws),
+                                         ws.numel(), st),
                     "transform_grads")
         ng = None
         if nrf_cache is not None:
@@ -543,7 +665,8 @@ class Trainer:
             if self.k:
                 dp64 = dp.double().contiguous()
                 N.check(L.mg_transform_grads(N.ptr(dp64), N.ptr(coords), N.ptr(sids), bt, 1, None, None,
-                                             N.ptr(self.tq), self.k, N.ptr(B.scratch12), N.ptr(B.g7), 1, st),
+                                             N.ptr(self.tq), self.k, N.ptr(B.scratch12), N.ptr(B.g7), 1,
+                                             N.ptr(ws), ws.numel(), st),
                         "nrf_transform_grads")
         if self.dist is not None:
             self._allreduce(B)

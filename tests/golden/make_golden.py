@@ -299,6 +299,48 @@ def make_trainer_full_case():
     )
 
 
+def make_io_cases():
+    """F4 formats written by the reference writers (io.py:101-145, 213-237):
+    two NIfTI volumes, and an MGSS0001 checkpoint of a reference Trainer (SSIM
+    + NRF from step 2, lattice milestone 8 -> 10 at step 3) taken after step 3,
+    with the losses of the 3 steps that follow it."""
+    from mgauss import io as mio
+    from mgauss.cli import simulate_stacks
+    from mgauss.core import Volume
+    from mgauss.simdata import build_slice_grids, devoxelize, normalized_transforms
+
+    rng = np.random.default_rng(21)
+    v32 = rng.normal(0, 1, (5, 4, 3))
+    v16 = rng.integers(0, 65535, (3, 4, 2)).astype(np.uint16)
+    sp, org = np.array([0.8, 0.9, 1.1]), np.array([-1.5, 2.25, 3.0])
+    mio.write_volume(os.path.join(OUT, "io_f32.nii"), Volume(data=v32, spacing=sp, origin=org), descrip="golden f32")
+    mio.write_volume(os.path.join(OUT, "io_u16.nii"), Volume(data=v16, spacing=sp, origin=org), descrip="golden u16")
+
+    sim = mio.SimSettings(phantom="nested-ellipsoids", phantom_dims=24, phantom_spacing=1.0, in_plane_spacing=1.0,
+                          slice_thickness=4.0, motion_sigma=0.5, noise_sigma=0.01, reg_error_sigma=0.0,
+                          foreground_threshold=-1.0)
+    _, stacks = simulate_stacks(sim, 7)
+    cloud = devoxelize(stacks, -1.0)
+    ts = normalized_transforms(stacks, cloud.world_map, "estimated")
+    grids = build_slice_grids(stacks, cloud.world_map, cloud.intensity_scale)
+    cfg = train.TrainConfig(resolution_schedule=((0, 8), (3, 10)), use_nrf=True, nrf_activation_iter=2,
+                            use_ssim=True, batch_points=2048, seed=13, total_iters=6)
+    tr = train.Trainer(cloud, ts, cfg, slice_grids=grids)
+    for _ in range(3):
+        tr.step()
+    mio.save_checkpoint(os.path.join(OUT, "io_checkpoint.mgss"), {"trainer": tr.state_dict()})
+    after = []
+    for _ in range(3):
+        rep = tr.step()
+        after.append([rep.total, rep.data, rep.ssim, rep.aniso])
+    np.savez_compressed(
+        os.path.join(OUT, "io.npz"), v32=v32, v16=v16, spacing=sp, origin=org,
+        coords=cloud.coords, intensities=cloud.intensities, slice_ids=cloud.slice_ids,
+        t_quats0=ts.quats, t_trans0=ts.translations, sg_coords=np.stack([g.coords for g in grids]),
+        sg_target=np.stack([g.target for g in grids]), sg_ids=np.array([g.slice_id for g in grids]),
+        losses_after=np.array(after), **field_arrays(tr.field))
+
+
 if __name__ == "__main__":
     make_ssim_case()
     make_trainer_full_case()
@@ -307,6 +349,7 @@ if __name__ == "__main__":
     make_volume_case()
     make_train_cases()
     make_trainer_case()
+    make_io_cases()
     for fn in sorted(os.listdir(OUT)):
-        if fn.endswith(".npz"):
+        if fn.endswith((".npz", ".nii", ".mgss")):
             print(fn, os.path.getsize(os.path.join(OUT, fn)))

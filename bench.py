@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--cpu-sample-points", type=int, default=65536)
     ap.add_argument("--no-inference", action="store_true")
+    ap.add_argument("--no-recon", action="store_true", help="skip the desk64 reconstruction-to-PSNR run")
     return ap.parse_args()
 
 
@@ -348,6 +349,12 @@ def run_ours(args):
             infer = inference_c5()
         except Exception as exc:  # report, never fail the training bench
             infer = {"error": repr(exc)[:200]}
+    recon = None
+    if not args.no_recon and rank == 0:
+        try:
+            recon = recon_desk64()
+        except Exception as exc:
+            recon = {"error": repr(exc)[:200]}
     bytes_h2d = int(steps_idx[0].numel() * 8)
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -371,6 +378,7 @@ def run_ours(args):
                                  "pairs_per_launch": kpairs, "flop_per_pair": [FLOP_FWD, FLOP_BWD]}},
         "cpu_baseline": cpu,
         "inference": infer,
+        "recon": recon,
         "clocks": clocks,
         "gpu_launches": (nlaunch * args.steps) if nlaunch else None,
         "gpu_launches_note": "library kernels per step (mg_launch_count over one eager step) x timed steps; "
@@ -379,6 +387,36 @@ def run_ours(args):
     print(json.dumps(out))
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def recon_desk64():
+    """BASELINE "recon s to PSNR": the reference's desk-scale reconstruction
+    (configs/desk64.cfg: 64^3 phantom, 1500 iterations, lattice 16^3 -> 48^3,
+    NRF from 600, SSIM) on the cloud the reference devoxelised, recorded with
+    the reference's own PSNR and wall time by tests/golden/make_recon.py."""
+    import torch
+
+    from paper_2603_00145_b200.recon import load_recon_fixture, psnr, reconstruct
+    from paper_2603_00145_b200.train import Trainer
+
+    path = os.path.join(ROOT, "tests", "golden", "recon_desk64.npz")
+    if not os.path.exists(path):
+        return None
+    cloud, ts, grids, cfg, tgt = load_recon_fixture(path)
+    tr = Trainer(cloud, ts, cfg, slice_grids=grids)
+    try:
+        vol, t_train, t_total = reconstruct(tr, tgt.dims, tgt.first, tgt.last, tgt.intensity_scale)
+    finally:
+        tr.close()
+    db = psnr(vol.astype(np.float64), tgt.gt.astype(np.float64))
+    del tr
+    torch.cuda.empty_cache()
+    return {"workload": f"desk64: 64^3 nested-ellipsoids, 3 stacks x 16 slices at 4 mm, {cfg.total_iters} iters, "
+                        f"lattice {cfg.resolution_schedule[0][1]}^3 -> {cfg.final_resolution}^3, NRF@"
+                        f"{cfg.nrf_activation_iter}, batch {cfg.batch_points} + SSIM slice",
+            "train_seconds": t_train, "seconds_incl_volume": t_total, "psnr_db": db,
+            "reference_psnr_db": tgt.ref_psnr_db, "reference_train_seconds": tgt.ref_seconds,
+            "reference_threads": tgt.ref_threads}
 
 
 def inference_c5(reps=3):

@@ -558,7 +558,9 @@ class Trainer:
     def _device_step(self, all_idx, nb, hw, sync):
         cfg = self.config
         B = self.load_indices(all_idx)
-        use_graph = self.graph and not self.nrf_active and self.dist is None
+        # the step (incl. the NCCL all-reduce, whose communicator the eager
+        # warm-up step initialises) is captured once per shape and replayed
+        use_graph = self.graph and not self.nrf_active
         if use_graph:
             key = (nb, hw)
             if self._graph is None or self._graph_key != key:

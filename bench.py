@@ -343,9 +343,11 @@ def run_ours(args):
     if world == 1 or rank == 0:
         threads = os.cpu_count() or 1
         v, p, dt, npts = cpu_baseline(tr, data, psf, args.cpu_sample_points, threads)
+        v1, p1, dt1, npts1 = cpu_baseline(tr, data, psf, max(1024, args.cpu_sample_points // 16), 1)
         cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
                "sample": f"{npts} batch points x {psf.ntaps} taps of one C2 step ({p} pairs, {dt:.1f} s), "
-                         f"fwd+bwd incl. host epilogue"}
+                         f"fwd+bwd incl. host epilogue",
+               "value_1thread": v1, "sample_1thread": f"{npts1} batch points ({p1} pairs, {dt1:.1f} s)"}
     graph_used = tr._graph is not None
     infer = None
     if not args.no_inference:
@@ -364,7 +366,9 @@ def run_ours(args):
     bytes_h2d = int(steps_idx[0].numel() * 8)
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+        "samples_per_s": world * float(steps_idx[0].numel()) * args.steps / (ms_max / 1000.0),
+        "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": "C2: 160^3 @0.8mm phantom, 3 stacks x 42 slices of 160^2 at 3mm, 3-tap slab PSF, "
                                "N=97,336 Gaussians (R=G=46), r=5, step = 65,536 batch + 25,600 SSIM-slice points",
@@ -496,8 +500,8 @@ def kernel_times(tr, idx_list, nb, hw):
     from paper_2603_00145_b200 import _native as N
 
     L = N.lib()
-    fwd, bwd, pairs = [], [], []
-    orig_fwd, orig_bwd = L.mg_forward, L.mg_backward
+    fwd, bwd, upd, pairs = [], [], [], []
+    orig_fwd, orig_bwd, orig_upd = L.mg_forward, L.mg_backward, L.mg_gauss_update
 
     class Timed:
         def __init__(self, fn, sink):
@@ -514,7 +518,7 @@ def kernel_times(tr, idx_list, nb, hw):
     B = tr._buffers(len(idx_list[0]))
     launches = []
     try:
-        L.mg_forward, L.mg_backward = Timed(orig_fwd, fwd), Timed(orig_bwd, bwd)
+        L.mg_forward, L.mg_backward, L.mg_gauss_update = Timed(orig_fwd, fwd), Timed(orig_bwd, bwd), Timed(orig_upd, upd)
         for ix in idx_list:
             tr.load_indices(ix)
             c0 = L.mg_launch_count()
@@ -523,11 +527,12 @@ def kernel_times(tr, idx_list, nb, hw):
             torch.cuda.synchronize()
             pairs.append(int(B.cnt.sum().item()))
     finally:
-        L.mg_forward, L.mg_backward = orig_fwd, orig_bwd
+        L.mg_forward, L.mg_backward, L.mg_gauss_update = orig_fwd, orig_bwd, orig_upd
     torch.cuda.synchronize()
     f = float(np.mean([a.elapsed_time(b) for a, b in fwd]))
     b = float(np.mean([a.elapsed_time(c) for a, c in bwd]))
-    return {"forward_ms": f, "backward_ms": b, "pairs_per_launch": float(np.mean(pairs)),
+    u = float(np.mean([a.elapsed_time(c) for a, c in upd])) if upd else None
+    return {"forward_ms": f, "backward_ms": b, "update_ms": u, "pairs_per_launch": float(np.mean(pairs)),
             "launches_per_step": int(max(launches))}
 
 

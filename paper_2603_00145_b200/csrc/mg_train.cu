@@ -471,26 +471,37 @@ struct AdamHyper {
   double bc1, bc2;  // filled in-kernel from the device step counter
 };
 
+// Adam (train.py:251-271) with the bias corrections as reciprocals computed
+// once per block: m/bc1 -> m * (1/bc1), sqrt(v/bc2) -> sqrt(v) * (1/sqrt(bc2))
+// (<= 1 ulp of float64 apart, far below the float32 rounding of the state).
 __device__ __forceinline__ float adam_upd(float& p, float& m, float& v, double g, double lr, const AdamHyper& h) {
   double mm = h.beta1 * (double)m + (1.0 - h.beta1) * g;
   double vv = h.beta2 * (double)v + (1.0 - h.beta2) * g * g;
   m = (float)mm;
   v = (float)vv;
-  double np = (double)p - lr * (mm / h.bc1) / (sqrt(vv / h.bc2) + h.eps);
+  double np = (double)p - lr * (mm * h.bc1) / (sqrt(vv) * h.bc2 + h.eps);
   p = (float)np;
   return p;
 }
 
-__global__ void gauss_update_kernel(const float* __restrict__ acc10, const int* __restrict__ order, int64_t n,
+#ifndef MG_UPD_MINB
+#define MG_UPD_MINB 3
+#endif
+__global__ void __launch_bounds__(256, MG_UPD_MINB) gauss_update_kernel(const float* __restrict__ acc10,
+                                                                        const int* __restrict__ order, int64_t n,
                                     float* __restrict__ pos, float* __restrict__ quat, float* __restrict__ ls,
                                     float* __restrict__ lg, float* __restrict__ mom_m, float* __restrict__ mom_v,
                                     AdamHyper h, const int* __restrict__ t_dev, double* __restrict__ aniso_acc) {
   double aniso_local = 0.0;
-  {
+  __shared__ double s_bc[2];
+  if (threadIdx.x == 0) {  // bias corrections once per block: h.bc1 = 1/bc1, h.bc2 = 1/sqrt(bc2)
     const double t = (double)*t_dev;
-    h.bc1 = 1.0 - pow(h.beta1, t);
-    h.bc2 = 1.0 - pow(h.beta2, t);
+    s_bc[0] = 1.0 / (1.0 - pow(h.beta1, t));
+    s_bc[1] = 1.0 / sqrt(1.0 - pow(h.beta2, t));
   }
+  __syncthreads();
+  h.bc1 = s_bc[0];
+  h.bc2 = s_bc[1];
   GRID_LOOP(p, n) {
     int64_t i = order[p];
     double logit = lg[i];
@@ -518,10 +529,24 @@ __global__ void gauss_update_kernel(const float* __restrict__ acc10, const int* 
     // state layout: m/v [N][11] = pos(3) quat(4) scale(3) logit(1)
     float* m = mom_m + 11 * i;
     float* v = mom_v + 11 * i;
-    for (int a = 0; a < 3; ++a) adam_upd(pos[3 * i + a], m[a], v[a], gg.dmu[a], h.lr_pos, h);
-    for (int a = 0; a < 4; ++a) adam_upd(quat[4 * i + a], m[3 + a], v[3 + a], gg.dq[a], h.lr_quat, h);
-    for (int a = 0; a < 3; ++a) adam_upd(ls[3 * i + a], m[7 + a], v[7 + a], gg.ds[a], h.lr_scale, h);
-    adam_upd(lg[i], m[10], v[10], gg.dl, h.lr_logit, h);
+    float mm[11], vv[11];
+#pragma unroll
+    for (int a = 0; a < 11; ++a) {  // all moments in flight at once
+      mm[a] = m[a];
+      vv[a] = v[a];
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) adam_upd(pos[3 * i + a], mm[a], vv[a], gg.dmu[a], h.lr_pos, h);
+#pragma unroll
+    for (int a = 0; a < 4; ++a) adam_upd(quat[4 * i + a], mm[3 + a], vv[3 + a], gg.dq[a], h.lr_quat, h);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) adam_upd(ls[3 * i + a], mm[7 + a], vv[7 + a], gg.ds[a], h.lr_scale, h);
+    adam_upd(lg[i], mm[10], vv[10], gg.dl, h.lr_logit, h);
+#pragma unroll
+    for (int a = 0; a < 11; ++a) {
+      m[a] = mm[a];
+      v[a] = vv[a];
+    }
   }
   if (aniso_acc && h.use_aniso) {
     for (int o = 16; o > 0; o >>= 1) aniso_local += __shfl_xor_sync(MG_FULL, aniso_local, o);

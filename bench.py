@@ -335,7 +335,7 @@ def run_ours(args):
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get("backward_kernel_dram_bytes")
+            traffic = json.load(open(tp)).get("pair_kernels_dram_bytes")
         except Exception:
             traffic = None
     nlaunch = kt.get("launches_per_step")

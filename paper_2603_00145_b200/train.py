@@ -234,6 +234,8 @@ class _StepBuffers:
                   L.mg_forward_workspace_bytes(ns), L.mg_backward_workspace_bytes(n, g),
                   L.mg_transform_grads_workspace_bytes(k))
         self.ws = dv.empty((wsb,), torch.uint8)
+        self.ws_gauss = None  # side-stream workspaces (Gaussian binning, transform reduction)
+        self.ws_tr = None
         self.ssim_ws = None
 
 
@@ -612,11 +614,20 @@ class Trainer:
         ns = bt * t
         ws = B.ws
         B.scalars.zero_()
+        # Two independent chains run as parallel graph branches: the Gaussian
+        # chain on a side stream (own workspace) while the main stream
+        # transforms and bins the points; joined before the forward.
+        main = torch.cuda.current_stream()
+        side = self._side_stream()
+        side.wait_stream(main)
+        ss = N.stream_ptr(side)
+        if B.ws_gauss is None:
+            B.ws_gauss = dv.empty((L.mg_bin_workspace_bytes(n, g),), torch.uint8)
         # Gaussians: bin + activate (spatial.py:46-66, render.py:122-142)
-        N.check(L.mg_bin_f32(N.ptr(f.positions), n, g, N.ptr(B.gkey), N.ptr(B.gorder), N.ptr(B.gstart), N.ptr(ws),
-                             ws.numel(), st), "bin")
+        N.check(L.mg_bin_f32(N.ptr(f.positions), n, g, N.ptr(B.gkey), N.ptr(B.gorder), N.ptr(B.gstart),
+                             N.ptr(B.ws_gauss), B.ws_gauss.numel(), ss), "bin")
         N.check(L.mg_activate(N.ptr(f.positions), N.ptr(f.quaternions), N.ptr(f.log_scales), N.ptr(f.logits), n,
-                              N.ptr(B.gorder), N.ptr(B.grec), N.ptr(B.err), st), "activate")
+                              N.ptr(B.gorder), N.ptr(B.grec), N.ptr(B.err), ss), "activate")
         # points: transforms, PSF taps, bin
         if self.k:
             N.check(L.mg_quat_to_rot_f64(N.ptr(self.tq), self.k, N.ptr(B.rot), st))
@@ -626,6 +637,7 @@ class Trainer:
         N.check(L.mg_bin_points(N.ptr(coords), N.ptr(sids), bt, t, N.ptr(off), N.ptr(dirs), N.ptr(B.rot),
                                 N.ptr(self.tt), self.k, g, N.ptr(B.pkey), N.ptr(B.pinv), N.ptr(B.pstart),
                                 N.ptr(B.prec), N.ptr(B.xout), N.ptr(ws), ws.numel(), st), "bin_points")
+        main.wait_stream(side)
         # forward with H (render_points, _kernels.py:24-70)
         N.check(L.mg_forward(N.ptr(B.grec), n, N.ptr(B.gstart), g, r, N.ptr(B.prec), N.ptr(B.pkey), N.ptr(B.pstart),
                              ns, 1, N.ptr(B.out4), N.ptr(B.cnt), N.ptr(ws), ws.numel(), st), "forward")
@@ -651,13 +663,20 @@ class Trainer:
         # backward (render_backward): upstream -> point records, d_points; Gaussian-major pass
         N.check(L.mg_backward_points(None, N.ptr(B.up), bt, t, N.ptr(wts), N.ptr(B.pinv), N.ptr(B.out4),
                                      N.ptr(B.prec), N.ptr(B.dpts), st), "backward_points")
+        # the per-slice transform reduction needs only d_points: it runs on the
+        # side stream (own workspace) under the Gaussian-major backward
+        if self.k:
+            side.wait_stream(main)
+            if B.ws_tr is None:
+                B.ws_tr = dv.empty((L.mg_transform_grads_workspace_bytes(self.k),), torch.uint8)
+            N.check(L.mg_transform_grads(N.ptr(B.dpts), N.ptr(coords), N.ptr(sids), bt, t, N.ptr(off), N.ptr(dirs),
+                                         N.ptr(self.tq), self.k, N.ptr(B.scratch12), N.ptr(B.g7), 0, N.ptr(B.ws_tr),
+                                         B.ws_tr.numel(), ss),
+                    "transform_grads")
         N.check(L.mg_backward(N.ptr(B.grec), N.ptr(B.gkey), N.ptr(B.gstart), n, g, r, N.ptr(B.prec),
                               N.ptr(B.pstart), N.ptr(B.acc10), N.ptr(ws), ws.numel(), st), "backward")
         if self.k:
-            N.check(L.mg_transform_grads(N.ptr(B.dpts), N.ptr(coords), N.ptr(sids), bt, t, N.ptr(off), N.ptr(dirs),
-                                         N.ptr(self.tq), self.k, N.ptr(B.scratch12), N.ptr(B.g7), 0, N.ptr(ws),
-                                         ws.numel(), st),
-                    "transform_grads")
+            main.wait_stream(side)
         ng = None
         if nrf_cache is not None:
             from .nrf import nrf_backward
@@ -685,6 +704,11 @@ class Trainer:
                                         N.ptr(self.counters[1:2]), st), "transform_adam")
         if ng is not None:
             self._nrf_adam(*ng)
+
+    def _side_stream(self):
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream(device=dv.device())
+        return self._side
 
     def _centre_points(self, B, bt, t):
         """Transformed (un-shifted) sample positions for the NRF (train.py:414-419)."""

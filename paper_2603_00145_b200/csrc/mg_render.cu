@@ -417,7 +417,7 @@ __device__ __forceinline__ void write_point_out(float4* __restrict__ out4, int* 
 #define MG_BWD_MINB 3
 #endif
 #ifndef MG_FWD_QMAX
-#define MG_FWD_QMAX 4
+#define MG_FWD_QMAX 8  // up to 8 sub-points per item (measured ~2.5% faster than 4 at C2)
 #endif
 #ifndef MG_FWD_WARPS
 #define MG_FWD_WARPS 8

@@ -154,6 +154,210 @@ __global__ void __launch_bounds__(kVolWarps * 32) volume_kernel(const GaussSoA g
   }
 }
 
+// ---------------------------------------------------------------------------
+// Tiled variant (dense inference): a block owns 2x2x2 voxel runs (8 cells,
+// one warp each).  The union of their candidate windows -- at most
+// (2 + 2r)^2 columns, each ONE contiguous CSR segment over the union
+// k-range -- is staged in shared memory once per tile with cp.async, with a
+// per-column table of cell starts; each warp then walks exactly its own
+// cell's window from shared memory (broadcast LDS, no L2 round trips).  A
+// tile whose union exceeds the staging capacity falls back to vol_chunk.
+// ---------------------------------------------------------------------------
+#ifndef MG_VOL_TILE
+#define MG_VOL_TILE 1
+#endif
+constexpr int kTileCap = 1792;   // staged Gaussians per tile
+constexpr int kTileCols = 144;   // union columns ((2 + 2r)^2 at r = 5)
+constexpr int kTileK = 16;       // union k-cells + 1 (table width)
+
+struct VolTileSmem {
+  float4 A[kTileCap];
+  float4 B[kTileCap];
+  float2 C[kTileCap];
+  int off[kTileCols][kTileK];  // absolute CSR index of union cell (column, KZ0 + k)
+  int sb[kTileCols + 1];       // staged base of each column
+  int geom[8];                 // UI0, UJ0, KZ0, ni, nj, nk, total, ok
+};
+
+template <int V>
+__device__ __forceinline__ void vol_chunk_tile(const VolTileSmem& sm, int g, int r, const VolAxes& ax, int bx0,
+                                               int by0, int bz0, int nbx, int nby, int nbz, int cell, int l0,
+                                               int nvox, const float* __restrict__ residual,
+                                               float* __restrict__ out, int lane) {
+  constexpr int VP = V / 2;
+  f2 px[VP], py[VP], pz[VP], acc[VP];
+  float cx[V], cy[V], cz[V];
+  int vid[V];
+  const int nyz = nby * nbz;
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    int l = l0 + lane + 32 * v;
+    int lc = l < nvox ? l : 0;
+    int bx = lc / nyz, rem = lc - bx * nyz, by = rem / nbz, bz = rem - by * nbz;
+    int i = bx0 + bx, j = by0 + by, k = bz0 + bz;
+    cx[v] = (float)axis_coord(ax.v0[0] + i, ax.n[0], ax.lo[0], ax.hi[0], ax.sp[0]);
+    cy[v] = (float)axis_coord(j, ax.n[1], ax.lo[1], ax.hi[1], ax.sp[1]);
+    cz[v] = (float)axis_coord(k, ax.n[2], ax.lo[2], ax.hi[2], ax.sp[2]);
+    vid[v] = l < nvox ? ((i * ax.n[1] + j) * ax.n[2] + k) : -1;
+  }
+#pragma unroll
+  for (int q = 0; q < VP; ++q) {
+    px[q] = mk2(cx[2 * q], cx[2 * q + 1]);
+    py[q] = mk2(cy[2 * q], cy[2 * q + 1]);
+    pz[q] = mk2(cz[2 * q], cz[2 * q + 1]);
+    acc[q] = bc2(0.f);
+  }
+  const int UI0 = sm.geom[0], UJ0 = sm.geom[1], KZ0 = sm.geom[2], nj = sm.geom[4];
+  int ck = cell % g, t = cell / g, cj = t % g, ci = t / g;
+  int ilo = max(ci - r, 0), ihi = min(ci + r, g - 1), jlo = max(cj - r, 0), jhi = min(cj + r, g - 1);
+  const int klo = max(ck - r, 0) - KZ0, khi = min(ck + r, g - 1) - KZ0 + 1;
+  for (int ii = ilo; ii <= ihi; ++ii) {
+    for (int jj = jlo; jj <= jhi; ++jj) {
+      const int c = (ii - UI0) * nj + (jj - UJ0);
+      const int o0 = sm.off[c][0];
+      const int a = sm.sb[c] + sm.off[c][klo] - o0, b = sm.sb[c] + sm.off[c][khi] - o0;
+      for (int gi = a; gi < b; ++gi) {
+        const float4 A = sm.A[gi], B = sm.B[gi];
+        const float2 C = sm.C[gi];
+        const float a01 = B.w, a02 = C.x, a12 = C.y;  // staged pre-doubled
+#pragma unroll
+        for (int q = 0; q < VP; ++q) {
+          f2 dx = sub2(px[q], bc2(A.x)), dy = sub2(py[q], bc2(A.y)), dz = sub2(pz[q], bc2(A.z));
+          f2 t1 = fma2(bc2(a02), dz, fma2(bc2(a01), dy, mul2(bc2(B.x), dx)));
+          f2 m = mul2(dx, t1);
+          f2 t2 = fma2(bc2(a12), dz, mul2(bc2(B.y), dy));
+          m = fma2(dy, t2, m);
+          m = fma2(dz, mul2(bc2(B.z), dz), m);
+          acc[q] = fma2(bc2(A.w), gauss_w2(m), acc[q]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    if (vid[v] >= 0) {
+      float val = (v & 1) ? hi(acc[v / 2]) : lo(acc[v / 2]);
+      int64_t o = (int64_t)vid[v];
+      if (residual) val += residual[o];
+      out[o] = fminf(fmaxf(val, 0.f), 1.f);
+    }
+  }
+}
+
+__device__ __forceinline__ void cpa16(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cpa8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(256) volume_tile_kernel(const GaussSoA grec, const int* __restrict__ gstart, int g,
+                                                          int r, VolAxes ax, const float* __restrict__ residual,
+                                                          float* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char vt_dyn[];
+  VolTileSmem& sm = *reinterpret_cast<VolTileSmem*>(vt_dyn);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nrx = ax.nr[0], nry = ax.nr[1], nrz = ax.nr[2];
+  const int tx = (nrx + 1) >> 1, ty = (nry + 1) >> 1, tz = (nrz + 1) >> 1;
+  const int64_t ntiles = (int64_t)tx * ty * tz;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int iz = (int)(tile % tz);
+    const int64_t tt = tile / tz;
+    const int iy = (int)(tt % ty), ix = (int)(tt / ty);
+    const int rx0 = 2 * ix, ry0 = 2 * iy, rz0 = 2 * iz;
+    const int rx1 = min(rx0 + 1, nrx - 1), ry1 = min(ry0 + 1, nry - 1), rz1 = min(rz0 + 1, nrz - 1);
+    // union geometry (cells of a run pair are monotone along the axis)
+    if (threadIdx.x == 0) {
+      const int UI0 = max(ax.rc[0][rx0] - r, 0), UI1 = min(ax.rc[0][rx1] + r, g - 1);
+      const int UJ0 = max(ax.rc[1][ry0] - r, 0), UJ1 = min(ax.rc[1][ry1] + r, g - 1);
+      const int KZ0 = max(ax.rc[2][rz0] - r, 0), KZ1 = min(ax.rc[2][rz1] + r, g - 1);
+      const int ni = UI1 - UI0 + 1, nj = UJ1 - UJ0 + 1, nk = KZ1 - KZ0 + 1;
+      sm.geom[0] = UI0;
+      sm.geom[1] = UJ0;
+      sm.geom[2] = KZ0;
+      sm.geom[3] = ni;
+      sm.geom[4] = nj;
+      sm.geom[5] = nk;
+      sm.geom[7] = (ni * nj <= kTileCols && nk + 1 <= kTileK) ? 1 : 0;
+    }
+    __syncthreads();
+    bool ok = sm.geom[7] != 0;
+    if (ok) {
+      const int UI0 = sm.geom[0], UJ0 = sm.geom[1], KZ0 = sm.geom[2], nj = sm.geom[4], nk = sm.geom[5];
+      const int ncol = sm.geom[3] * nj;
+      for (int e = threadIdx.x; e < ncol * (nk + 1); e += blockDim.x) {
+        const int c = e / (nk + 1), k = e - c * (nk + 1);
+        const int q = c / nj;
+        sm.off[c][k] = __ldg(gstart + ((int64_t)(UI0 + q) * g + UJ0 + (c - q * nj)) * g + KZ0 + k);
+      }
+      __syncthreads();
+      if (warp == 0) {  // staged bases: exclusive scan of the column lengths
+        int run = 0;
+        for (int c0 = 0; c0 < ncol; c0 += 32) {
+          const int c = c0 + lane;
+          const int len = c < ncol ? sm.off[c][nk] - sm.off[c][0] : 0;
+          int tot;
+          const int ex = warp_excl_scan(len, lane, &tot);
+          if (c < ncol) sm.sb[c] = run + ex;
+          run += tot;
+        }
+        if (lane == 0) {
+          sm.sb[ncol] = run;
+          sm.geom[6] = run;
+        }
+      }
+      __syncthreads();
+      ok = sm.geom[6] <= kTileCap;
+      if (ok) {
+        for (int c = warp; c < ncol; c += blockDim.x >> 5) {
+          const int e0 = sm.off[c][0], n = sm.off[c][nk] - e0, b0 = sm.sb[c];
+          for (int t = lane; t < n; t += 32) {
+            cpa16(&sm.A[b0 + t], grec.A + e0 + t);
+            cpa16(&sm.B[b0 + t], grec.B + e0 + t);
+            cpa8(&sm.C[b0 + t], grec.C + e0 + t);
+          }
+        }
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+      }
+      __syncthreads();
+      if (ok) {  // off-diagonals doubled once here instead of per use (Horner form)
+        for (int t = threadIdx.x; t < sm.geom[6]; t += blockDim.x) {
+          sm.B[t].w *= 2.f;
+          sm.C[t].x *= 2.f;
+          sm.C[t].y *= 2.f;
+        }
+        __syncthreads();
+      }
+    }
+    // this warp's run (cell)
+    const int rx = rx0 + ((warp >> 2) & 1), ry = ry0 + ((warp >> 1) & 1), rz = rz0 + (warp & 1);
+    if (rx < nrx && ry < nry && rz < nrz) {
+      const int bx0 = ax.rs[0][rx], nbx = ax.rs[0][rx + 1] - bx0;
+      const int by0 = ax.rs[1][ry], nby = ax.rs[1][ry + 1] - by0;
+      const int bz0 = ax.rs[2][rz], nbz = ax.rs[2][rz + 1] - bz0;
+      const int cell = flat_cell(ax.rc[0][rx], ax.rc[1][ry], ax.rc[2][rz], g);
+      const int nvox = nbx * nby * nbz;
+      if (ok) {
+        if (nvox <= 64)
+          vol_chunk_tile<2>(sm, g, r, ax, bx0, by0, bz0, nbx, nby, nbz, cell, 0, nvox, residual, out, lane);
+        else
+          for (int l0 = 0; l0 < nvox; l0 += 128)
+            vol_chunk_tile<4>(sm, g, r, ax, bx0, by0, bz0, nbx, nby, nbz, cell, l0, nvox, residual, out, lane);
+      } else {
+        if (nvox <= 64)
+          vol_chunk<2>(grec, gstart, g, r, ax, bx0, by0, bz0, nbx, nby, nbz, cell, 0, nvox, residual, out, 0, lane);
+        else
+          for (int l0 = 0; l0 < nvox; l0 += 128)
+            vol_chunk<4>(grec, gstart, g, r, ax, bx0, by0, bz0, nbx, nby, nbz, cell, l0, nvox, residual, out, 0,
+                         lane);
+      }
+    }
+    __syncthreads();  // the staged tile is overwritten by the next one
+  }
+}
+
 size_t volume_workspace_bytes(int nx, int ny, int nz) {
   int m = nx > ny ? nx : ny;
   m = m > nz ? m : nz;
@@ -204,6 +408,22 @@ void launch_sample_volume(const float* grec_raw, int64_t n_gauss, const int* gst
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   // write offsets: kernel computes vid relative to the slab (i in [0, i1-i0))
+  if (MG_VOL_TILE && 2 + 2 * r <= 12) {
+    const size_t smem = sizeof(VolTileSmem);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(volume_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, volume_tile_kernel, 256, smem);
+    const int64_t tiles = (int64_t)((i1 - i0 + 1) / 2 + 1) * ((n[1] + 1) / 2 + 1) * ((n[2] + 1) / 2 + 1);
+    int64_t tb = (int64_t)num_sms() * (per_sm > 0 ? per_sm : 1);
+    if (tb > tiles) tb = tiles;
+    MG_LAUNCH(volume_tile_kernel<<<(unsigned)tb, 256, smem, st>>>(gauss_soa(grec_raw, n_gauss), gstart, g, r, ax,
+                                                                   residual, out));
+    return;
+  }
   MG_LAUNCH(volume_kernel<<<(unsigned)blocks, kVolWarps * 32, 0, st>>>(gauss_soa(grec_raw, n_gauss), gstart, g, r, ax, residual,
                                                               out));
 }

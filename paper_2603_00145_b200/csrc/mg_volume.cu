@@ -166,7 +166,11 @@ __global__ void __launch_bounds__(kVolWarps * 32) volume_kernel(const GaussSoA g
 #ifndef MG_VOL_TILE
 #define MG_VOL_TILE 1
 #endif
-constexpr int kTileCap = 1792;   // staged Gaussians per tile
+#ifndef MG_VOL_TZ
+#define MG_VOL_TZ 4  // runs per tile along k (2 x 2 x TZ cells; TZ / 2 cells per warp)
+#endif
+constexpr int kTileTZ = MG_VOL_TZ;
+constexpr int kTileCap = kTileTZ == 2 ? 1792 : 2048;   // staged Gaussians per tile
 constexpr int kTileCols = 144;   // union columns ((2 + 2r)^2 at r = 5)
 constexpr int kTileK = 16;       // union k-cells + 1 (table width)
 
@@ -266,8 +270,8 @@ __global__ void __launch_bounds__(256) volume_tile_kernel(const GaussSoA grec, c
     const int iz = (int)(tile % tz);
     const int64_t tt = tile / tz;
     const int iy = (int)(tt % ty), ix = (int)(tt / ty);
-    const int rx0 = 2 * ix, ry0 = 2 * iy, rz0 = 2 * iz;
-    const int rx1 = min(rx0 + 1, nrx - 1), ry1 = min(ry0 + 1, nry - 1), rz1 = min(rz0 + 1, nrz - 1);
+    const int rx0 = 2 * ix, ry0 = 2 * iy, rz0 = kTileTZ * iz;
+    const int rx1 = min(rx0 + 1, nrx - 1), ry1 = min(ry0 + 1, nry - 1), rz1 = min(rz0 + kTileTZ - 1, nrz - 1);
     // union geometry (cells of a run pair are monotone along the axis)
     if (threadIdx.x == 0) {
       const int UI0 = max(ax.rc[0][rx0] - r, 0), UI1 = min(ax.rc[0][rx1] + r, g - 1);
@@ -331,8 +335,10 @@ __global__ void __launch_bounds__(256) volume_tile_kernel(const GaussSoA grec, c
         __syncthreads();
       }
     }
-    // this warp's run (cell)
-    const int rx = rx0 + ((warp >> 2) & 1), ry = ry0 + ((warp >> 1) & 1), rz = rz0 + (warp & 1);
+    // this warp's runs (cells): (x, y) from the warp id, z = (warp & 1) + 2s
+#pragma unroll 1
+    for (int s2 = 0; s2 < kTileTZ / 2; ++s2) {
+    const int rx = rx0 + ((warp >> 2) & 1), ry = ry0 + ((warp >> 1) & 1), rz = rz0 + (warp & 1) + 2 * s2;
     if (rx < nrx && ry < nry && rz < nrz) {
       const int bx0 = ax.rs[0][rx], nbx = ax.rs[0][rx + 1] - bx0;
       const int by0 = ax.rs[1][ry], nby = ax.rs[1][ry + 1] - by0;
@@ -353,6 +359,7 @@ __global__ void __launch_bounds__(256) volume_tile_kernel(const GaussSoA grec, c
             vol_chunk<4>(grec, gstart, g, r, ax, bx0, by0, bz0, nbx, nby, nbz, cell, l0, nvox, residual, out, 0,
                          lane);
       }
+    }
     }
     __syncthreads();  // the staged tile is overwritten by the next one
   }
@@ -408,7 +415,7 @@ void launch_sample_volume(const float* grec_raw, int64_t n_gauss, const int* gst
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   // write offsets: kernel computes vid relative to the slab (i in [0, i1-i0))
-  if (MG_VOL_TILE && 2 + 2 * r <= 12) {
+  if (MG_VOL_TILE && 2 + 2 * r <= 12 && kTileTZ + 2 * r + 1 <= kTileK) {
     const size_t smem = sizeof(VolTileSmem);
     static bool attr = false;
     if (!attr) {
@@ -417,7 +424,7 @@ void launch_sample_volume(const float* grec_raw, int64_t n_gauss, const int* gst
     }
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, volume_tile_kernel, 256, smem);
-    const int64_t tiles = (int64_t)((i1 - i0 + 1) / 2 + 1) * ((n[1] + 1) / 2 + 1) * ((n[2] + 1) / 2 + 1);
+    const int64_t tiles = (int64_t)((i1 - i0 + 1) / 2 + 1) * ((n[1] + 1) / 2 + 1) * (n[2] / kTileTZ + 1);
     int64_t tb = (int64_t)num_sms() * (per_sm > 0 ? per_sm : 1);
     if (tb > tiles) tb = tiles;
     MG_LAUNCH(volume_tile_kernel<<<(unsigned)tb, 256, smem, st>>>(gauss_soa(grec_raw, n_gauss), gstart, g, r, ax,

@@ -166,6 +166,7 @@ __global__ void __launch_bounds__(kVolWarps * 32) volume_kernel(const GaussSoA g
 #ifndef MG_VOL_TILE
 #define MG_VOL_TILE 1
 #endif
+
 #ifndef MG_VOL_TZ
 #define MG_VOL_TZ 4  // runs per tile along k (2 x 2 x TZ cells; TZ / 2 cells per warp)
 #endif
@@ -264,13 +265,13 @@ __global__ void __launch_bounds__(256) volume_tile_kernel(const GaussSoA grec, c
   VolTileSmem& sm = *reinterpret_cast<VolTileSmem*>(vt_dyn);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nrx = ax.nr[0], nry = ax.nr[1], nrz = ax.nr[2];
-  const int tx = (nrx + 1) >> 1, ty = (nry + 1) >> 1, tz = (nrz + 1) >> 1;
+  const int tx = (nrx + 1) >> 1, ty = (nry + 1) >> 1, tz = (nrz + kTileTZ - 1) / kTileTZ;
   const int64_t ntiles = (int64_t)tx * ty * tz;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int iz = (int)(tile % tz);
     const int64_t tt = tile / tz;
     const int iy = (int)(tt % ty), ix = (int)(tt / ty);
-    const int rx0 = 2 * ix, ry0 = 2 * iy, rz0 = kTileTZ * iz;
+    const int rx0 = 2 * ix, ry0 = 2 * iy, rz0 = kTileTZ * iz;  // < nrx, nry, nrz by the tile counts
     const int rx1 = min(rx0 + 1, nrx - 1), ry1 = min(ry0 + 1, nry - 1), rz1 = min(rz0 + kTileTZ - 1, nrz - 1);
     // union geometry (cells of a run pair are monotone along the axis)
     if (threadIdx.x == 0) {
@@ -294,7 +295,8 @@ __global__ void __launch_bounds__(256) volume_tile_kernel(const GaussSoA grec, c
       for (int e = threadIdx.x; e < ncol * (nk + 1); e += blockDim.x) {
         const int c = e / (nk + 1), k = e - c * (nk + 1);
         const int q = c / nj;
-        sm.off[c][k] = __ldg(gstart + ((int64_t)(UI0 + q) * g + UJ0 + (c - q * nj)) * g + KZ0 + k);
+        const int64_t gi = ((int64_t)(UI0 + q) * g + UJ0 + (c - q * nj)) * g + KZ0 + k;
+        sm.off[c][k] = __ldg(gstart + gi);
       }
       __syncthreads();
       if (warp == 0) {  // staged bases: exclusive scan of the column lengths

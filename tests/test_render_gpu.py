@@ -319,3 +319,31 @@ def test_sample_volume_lattice_against_oracle():
     want = O.sample_volume(f.positions, f.quaternions, f.log_scales, f.intensity_logits, R, 3, dims, bounds,
                            threads=4)
     assert_rel(vol.data, want, name="volume")
+
+
+@pytest.mark.parametrize("r", [5, 2])
+def test_sample_volume_after_larger_call(r):
+    """Tiled volume path: a larger call first (it leaves its run tables in the
+    reused workspace), then a smaller grid with an odd run count per axis and
+    several runs per tile, against the oracle.  Guards the tile counts against
+    reading past the last run (stale workspace)."""
+    from oracle import oracle as O
+    from paper_2603_00145_b200.core import uniform_lattice_field
+    from paper_2603_00145_b200.render import sample_volume
+    from paper_2603_00145_b200.spatial import build
+
+    big = uniform_lattice_field(40)
+    big.intensity_logits = np.random.default_rng(1).normal(0, 1, big.count)
+    sample_volume(big, build(big, 40, r), None, (96, 96, 96), ((-1.0,) * 3, (1.0,) * 3), radius=r)
+    rng = np.random.default_rng(7)
+    R = 15
+    f = uniform_lattice_field(R)
+    f32 = lambda a: np.asarray(a, np.float32).astype(np.float64)  # noqa: E731
+    f.positions = f32(f.positions + rng.normal(0, 0.1 / R, f.positions.shape))
+    f.log_scales = f32(f.log_scales + rng.normal(0, 0.1, f.log_scales.shape))
+    f.intensity_logits = f32(rng.normal(0, 1, f.count))
+    dims, bounds = (23, 19, 31), ((-0.95, -1.0, -0.9), (0.97, 0.93, 1.0))
+    vol = sample_volume(f, build(f, R, r), None, dims, bounds, radius=r)
+    want = O.sample_volume(f.positions, f.quaternions, f.log_scales, f.intensity_logits, R, r, dims, bounds,
+                           threads=4)
+    assert_rel(vol.data, want, name="volume")

@@ -102,6 +102,16 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def workload_name(name, data, cfg, psf, hw):
+    from paper_2603_00145_b200.synth import CONFIGS
+
+    dims, sp, inpl, thick, lattice, use_nrf, batch = CONFIGS[name]
+    n_sl = data.num_slices
+    return (f"{name}: {dims}^3 @{sp}mm phantom, 3 stacks x {n_sl // 3} slices of {dims}^2 at {thick}mm, "
+            f"{psf.ntaps}-tap slab PSF, N={lattice ** 3:,} Gaussians (R=G={lattice}), r={cfg.block_radius}"
+            f"{', NRF active' if use_nrf else ''}, step = {batch:,} batch + {hw[0] * hw[1]:,} SSIM-slice points")
+
+
 def make_workload(cfg_name, rank):
     from paper_2603_00145_b200.render import SlicePSF
     from paper_2603_00145_b200.synth import CONFIGS, make_config
@@ -114,8 +124,9 @@ def make_workload(cfg_name, rank):
         c, t = data.slice_grid(k)
         grids.append(type("SG", (), {"coords": c, "target": t, "slice_id": k})())
     psf = SlicePSF(data.psf_offsets, data.psf_weights, data.through_dirs)
-    cfg = TrainConfig(resolution_schedule=((0, lattice),), use_nrf=use_nrf, use_ssim=True, batch_points=batch,
-                      seed=7 + rank, total_iters=10 ** 9)
+    # NRF configs (C3) measure the refinement phase: the residual field is active from the first step
+    cfg = TrainConfig(resolution_schedule=((0, lattice),), use_nrf=use_nrf, nrf_activation_iter=0, use_ssim=True,
+                      batch_points=batch, seed=7 + rank, total_iters=10 ** 9)
     cloud = type("Cloud", (), {"coords": data.coords, "intensities": data.intensities,
                                "slice_ids": data.slice_ids})()
     return data, cloud, grids, psf, cfg
@@ -370,8 +381,7 @@ def run_ours(args):
         "samples_per_s": world * float(steps_idx[0].numel()) * args.steps / (ms_max / 1000.0),
         "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "C2: 160^3 @0.8mm phantom, 3 stacks x 42 slices of 160^2 at 3mm, 3-tap slab PSF, "
-                               "N=97,336 Gaussians (R=G=46), r=5, step = 65,536 batch + 25,600 SSIM-slice points",
+        "config": {"workload": workload_name(args.config, data, cfg, psf, hw),
                    "global_batch": nb * world, "pairs_per_step": pairs_total / args.steps,
                    "parallelism": f"dp{world}", "l2": "inputs and per-step working set fit in L2 (126 MB); "
                    "steps differ in batch, no flush", "cuda_graph": graph_used},

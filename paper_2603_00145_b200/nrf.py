@@ -63,14 +63,16 @@ class ResidualField:
         return out
 
 
+def _freqs(bands, x):
+    return (2.0 ** torch.arange(bands, dtype=x.dtype, device=x.device)) * np.pi
+
+
 def fourier_encode(x: torch.Tensor, bands: int) -> torch.Tensor:
-    """nrf.py:23-36 on device."""
-    parts = [x]
-    for k in range(bands):
-        s = x * ((2.0 ** k) * np.pi)
-        parts.append(torch.sin(s))
-        parts.append(torch.cos(s))
-    return torch.cat(parts, dim=1)
+    """nrf.py:23-36 on device: [x, sin(2^0 pi x), cos(2^0 pi x), sin(2^1 pi x), ...],
+    all bands in one broadcast (same column order as the reference)."""
+    s = x[:, None, :] * _freqs(bands, x)[None, :, None]  # (B, bands, 3)
+    sc = torch.stack((torch.sin(s), torch.cos(s)), dim=2)  # (B, bands, 2, 3)
+    return torch.cat((x, sc.reshape(x.shape[0], 6 * bands)), dim=1)
 
 
 def nrf_forward_cached(field: ResidualField, x: torch.Tensor):
@@ -112,11 +114,11 @@ def nrf_backward(field: ResidualField, x: torch.Tensor, upstream: torch.Tensor, 
             dz = dh * (s * (1.0 + pre[li - 1] * (1.0 - s)))
         else:
             d_enc = dh
-    dp = d_enc[:, :3].clone()
-    for k in range(field.frequency_bands):
-        f = (2.0 ** k) * np.pi
-        dp += f * torch.cos(f * x) * d_enc[:, 3 + 6 * k:6 + 6 * k]
-        dp -= f * torch.sin(f * x) * d_enc[:, 6 + 6 * k:9 + 6 * k]
+    bands = field.frequency_bands
+    f = _freqs(bands, x)[None, :, None]  # (1, bands, 1)
+    s = x[:, None, :] * f
+    de = d_enc[:, 3:].reshape(x.shape[0], bands, 2, 3)
+    dp = d_enc[:, :3] + (f * (torch.cos(s) * de[:, :, 0] - torch.sin(s) * de[:, :, 1])).sum(dim=1)
     return dws, dbs, dp
 
 

@@ -562,9 +562,9 @@ class Trainer:
         B = self.load_indices(all_idx)
         # the step (incl. the NCCL all-reduce, whose communicator the eager
         # warm-up step initialises) is captured once per shape and replayed
-        use_graph = self.graph and not self.nrf_active
+        use_graph = self.graph
         if use_graph:
-            key = (nb, hw)
+            key = (nb, hw, self.nrf_active)
             if self._graph is None or self._graph_key != key:
                 self._body(B, nb, hw)  # eager warm-up of this shape (also lazily inits kernels)
                 torch.cuda.synchronize()
@@ -720,21 +720,44 @@ class Trainer:
         self._centre_x = x.to(torch.float32).contiguous()
         return self._centre_x
 
+    @property
+    def nrf_t(self):
+        """NRF Adam step count (kept on the device so the step graph replays it)."""
+        t = getattr(self, "_nrf_tdev", None)
+        return 0 if t is None else int(t.item())
+
+    @nrf_t.setter
+    def nrf_t(self, value):
+        self._nrf_tdev = torch.full((), float(value), dtype=torch.float64, device=dv.device())
+
     def _nrf_adam(self, dws, dbs):
+        """AdamState.step("nrf", ...) (train.py:251-271) as multi-tensor device
+        ops with a device step counter, so the update replays inside the graph."""
         cfg = self.config
-        self.nrf_t += 1
-        bc1 = 1.0 - cfg.adam_beta1 ** self.nrf_t
-        bc2 = 1.0 - cfg.adam_beta2 ** self.nrf_t
+        t = self._nrf_tdev
+        t.add_(1.0)
+        bc1 = (1.0 - torch.pow(cfg.adam_beta1, t)).to(torch.float32)
+        bc2 = (1.0 - torch.pow(cfg.adam_beta2, t)).to(torch.float32)
         params = self.nrf.parameter_arrays()
+        keys = list(params)
         grads = {}
         for li, (dw, db) in enumerate(zip(dws, dbs)):
             grads[f"w{li}"], grads[f"b{li}"] = dw, db
-        for k, p in params.items():
-            g = grads[k]
-            m, v = self.nrf_m[k], self.nrf_v[k]
-            m.mul_(cfg.adam_beta1).add_(g, alpha=1.0 - cfg.adam_beta1)
-            v.mul_(cfg.adam_beta2).addcmul_(g, g, value=1.0 - cfg.adam_beta2)
-            p.sub_(cfg.lr_nrf * (m / bc1) / (torch.sqrt(v / bc2) + cfg.adam_eps))
+        ps = [params[k] for k in keys]
+        gs = [grads[k] for k in keys]
+        ms = [self.nrf_m[k] for k in keys]
+        vs = [self.nrf_v[k] for k in keys]
+        torch._foreach_mul_(ms, cfg.adam_beta1)
+        torch._foreach_add_(ms, gs, alpha=1.0 - cfg.adam_beta1)
+        torch._foreach_mul_(vs, cfg.adam_beta2)
+        torch._foreach_addcmul_(vs, gs, gs, value=1.0 - cfg.adam_beta2)
+        den = torch._foreach_div(vs, bc2)
+        torch._foreach_sqrt_(den)
+        torch._foreach_add_(den, cfg.adam_eps)
+        num = torch._foreach_div(ms, bc1)
+        torch._foreach_div_(num, den)
+        torch._foreach_mul_(num, cfg.lr_nrf)
+        torch._foreach_sub_(ps, num)
 
     def _allreduce(self, B):
         """One flat all-reduce(sum) of the step's partial sums (parallel.py)."""

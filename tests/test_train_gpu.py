@@ -112,3 +112,28 @@ def test_render_volume_runs():
     tr.run(2)
     vol = tr.render_volume((12, 12, 12), ((-1, -1, -1), (1, 1, 1)))
     assert vol.data.shape == (12, 12, 12) and 0.0 <= vol.data.min() and vol.data.max() <= 1.0
+
+
+def test_graph_with_nrf_matches_eager():
+    """The captured step (incl. the NRF forward/backward, its multi-tensor Adam
+    with the device step counter, SSIM, and a lattice milestone that forces a
+    recapture) evolves exactly like the eager step."""
+    from paper_2603_00145_b200 import _device as dv
+    from paper_2603_00145_b200.core import TransformSet
+    from paper_2603_00145_b200.train import TrainConfig, Trainer
+
+    z = load_golden("trainer_full")
+    grids = [SimpleNamespace(coords=c, target=t, slice_id=int(s))
+             for c, t, s in zip(z["sg_coords"], z["sg_target"], z["sg_ids"])]
+    cfg = TrainConfig(resolution_schedule=((0, 8), (4, 10)), use_nrf=True, nrf_activation_iter=2, use_ssim=True,
+                      batch_points=2048, seed=11, total_iters=8)
+    runs = []
+    for graph in (False, True):
+        tr = Trainer(_cloud(z), TransformSet(z["t_quats0"], z["t_trans0"]), cfg, slice_grids=grids, graph=graph)
+        reps = tr.run()
+        runs.append((tr, np.array([[r.total, r.data, r.ssim] for r in reps])))
+    (a, la), (b, lb) = runs
+    np.testing.assert_allclose(lb, la, rtol=1e-12)
+    np.testing.assert_array_equal(dv.to_host(b.field.positions), dv.to_host(a.field.positions))
+    np.testing.assert_array_equal(dv.to_host(b.nrf.weights[2]), dv.to_host(a.nrf.weights[2]))
+    assert a.nrf_t == b.nrf_t == 6

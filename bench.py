@@ -423,7 +423,7 @@ def recon_desk64():
     if not os.path.exists(path):
         return None
     cloud, ts, grids, cfg, tgt = load_recon_fixture(path)
-    tr = Trainer(cloud, ts, cfg, slice_grids=grids)
+    tr = Trainer(cloud, ts, cfg, slice_grids=grids, graph=True)
     try:
         vol, t_train, t_total = reconstruct(tr, tgt.dims, tgt.first, tgt.last, tgt.intensity_scale)
     finally:

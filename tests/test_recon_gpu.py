@@ -16,12 +16,13 @@ GOLD = os.path.join(os.path.dirname(__file__), "golden", "recon_desk64.npz")
 
 
 @pytest.mark.skipif(not os.path.exists(GOLD), reason="recon fixture not generated")
-def test_desk64_reconstruction_psnr_matches_reference():
+@pytest.mark.parametrize("graph", [False, True])
+def test_desk64_reconstruction_psnr_matches_reference(graph):
     from paper_2603_00145_b200.recon import load_recon_fixture, psnr, reconstruct
     from paper_2603_00145_b200.train import Trainer
 
     cloud, ts, grids, cfg, tgt = load_recon_fixture(GOLD)
-    tr = Trainer(cloud, ts, cfg, slice_grids=grids)
+    tr = Trainer(cloud, ts, cfg, slice_grids=grids, graph=graph)
     try:
         losses = []
         vol, t_train, _ = reconstruct(tr, tgt.dims, tgt.first, tgt.last, tgt.intensity_scale,

@@ -512,6 +512,36 @@ class Trainer:
         self.reports.append(report)
         return report
 
+    def step_pipelined(self):
+        """Enqueue one optimizer step and return the LossReport of the step
+        enqueued by the previous call (None on the first call; ``flush()``
+        returns the last one).  The host-side batch draw and index upload of
+        this step overlap the device running the previous step; every step
+        still uploads its indices and reads back its losses."""
+        cfg = self.config
+        self._apply_milestones()
+        idx = self._next_batch()
+        slice_j = int(self.rng.integers(len(self.slice_grids))) if cfg.use_ssim else None
+        all_idx, hw = self.host_indices(idx, slice_j)
+        prev = getattr(self, "_pending", None)
+        self._device_step(all_idx, len(idx), hw, sync=False)
+        self._pending = self._enqueue_readback(self._bufs, hw)
+        self.iteration += 1
+        rep = None
+        if prev is not None:
+            rep = self._resolve(prev)
+            self.reports.append(rep)
+        return rep
+
+    def flush(self):
+        """Report of the last pipelined step (None if nothing is pending)."""
+        prev, self._pending = getattr(self, "_pending", None), None
+        if prev is None:
+            return None
+        rep = self._resolve(prev)
+        self.reports.append(rep)
+        return rep
+
     def _buffers(self, b_total):
         g = self.field.resolution
         key = (self.field.count, g, b_total, self.ntaps, self.k)
@@ -527,8 +557,11 @@ class Trainer:
             self._bufs.idx_host = [torch.empty((b_total,), dtype=torch.int64, pin_memory=True) for _ in range(2)]
             self._bufs.idx_done = [None, None]
             self._bufs.slot = 0
-            self._bufs.scalars_host = torch.empty((4,), dtype=torch.float64, pin_memory=True)
-            self._bufs.err_host = torch.empty((1,), dtype=torch.int32, pin_memory=True)
+            # two pinned loss-readback slots (pipelined steps read one while the next fills)
+            self._bufs.scalars_host = [torch.empty((4,), dtype=torch.float64, pin_memory=True) for _ in range(2)]
+            self._bufs.err_host = [torch.empty((1,), dtype=torch.int32, pin_memory=True) for _ in range(2)]
+            self._bufs.r_done = [None, None]
+            self._bufs.rslot = 0
             self._bufs_key = key
             self._graph = None
         return self._bufs
@@ -581,13 +614,28 @@ class Trainer:
         if not sync:
             return LossReport(self.iteration, float("nan"), float("nan"), float("nan"), float("nan"),
                               self.field.resolution, self.nrf_active)
-        B.scalars_host.copy_(B.scalars, non_blocking=True)
-        B.err_host.copy_(B.err, non_blocking=True)
-        done = torch.cuda.Event()
-        done.record()
-        done.synchronize()
-        sc = B.scalars_host.numpy()
-        err = int(B.err_host[0])
+        return self._resolve(self._enqueue_readback(B, hw))
+
+    def _enqueue_readback(self, B, hw):
+        """Async D2H of this step's loss sums and error flag into a pinned slot."""
+        k = B.rslot
+        B.rslot ^= 1
+        if B.r_done[k] is not None:
+            B.r_done[k].synchronize()
+        B.scalars_host[k].copy_(B.scalars, non_blocking=True)
+        B.err_host[k].copy_(B.err, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        B.r_done[k] = ev
+        return (B, k, ev, self.iteration, hw, self.field.resolution, self.nrf_active)
+
+    def _resolve(self, pending):
+        """LossReport of a step whose readback was enqueued (waits for it)."""
+        cfg = self.config
+        B, k, ev, iteration, hw, res, nrf_on = pending
+        ev.synchronize()
+        sc = B.scalars_host[k].numpy().copy()
+        err = int(B.err_host[k][0])
         if err:
             from .errors import DegenerateQuaternion
 
@@ -599,8 +647,8 @@ class Trainer:
             ssim = 1.0 - float(sc[2]) / ((hw[0] - 10) * (hw[1] - 10))
         total = data + cfg.lambda_ssim * ssim + cfg.lambda_aniso * aniso
         if not np.isfinite(total):
-            raise NonFiniteLoss(f"non-finite loss at iteration {self.iteration}")
-        return LossReport(self.iteration, total, data, ssim, aniso, self.field.resolution, self.nrf_active)
+            raise NonFiniteLoss(f"non-finite loss at iteration {iteration}")
+        return LossReport(iteration, total, data, ssim, aniso, res, nrf_on)
 
     def _launch(self, B, coords, sids, tgt, nb, hw):
         """Enqueue the whole step on the current stream (graph-capturable)."""

@@ -137,3 +137,29 @@ def test_graph_with_nrf_matches_eager():
     np.testing.assert_array_equal(dv.to_host(b.field.positions), dv.to_host(a.field.positions))
     np.testing.assert_array_equal(dv.to_host(b.nrf.weights[2]), dv.to_host(a.nrf.weights[2]))
     assert a.nrf_t == b.nrf_t == 6
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_pipelined_steps_report_the_same_losses(graph):
+    """step_pipelined() returns each step's report one call later (flush()
+    returns the last) with exactly the losses of synchronous step()."""
+    from paper_2603_00145_b200.core import TransformSet
+    from paper_2603_00145_b200.train import TrainConfig, Trainer
+
+    z = load_golden("trainer_full")
+    grids = [SimpleNamespace(coords=c, target=t, slice_id=int(s))
+             for c, t, s in zip(z["sg_coords"], z["sg_target"], z["sg_ids"])]
+    cfg = TrainConfig(resolution_schedule=((0, 8), (3, 10)), use_nrf=True, nrf_activation_iter=2, use_ssim=True,
+                      batch_points=2048, seed=11, total_iters=6)
+    mk = lambda: Trainer(_cloud(z), TransformSet(z["t_quats0"], z["t_trans0"]), cfg, slice_grids=grids,  # noqa
+                         graph=graph)
+    a = mk()
+    sync = [a.step() for _ in range(6)]
+    b = mk()
+    piped = [b.step_pipelined() for _ in range(6)]
+    assert piped[0] is None
+    piped = piped[1:] + [b.flush()]
+    assert b.flush() is None
+    for ra, rb in zip(sync, piped):
+        assert ra.iteration == rb.iteration and ra.resolution == rb.resolution
+        np.testing.assert_allclose([rb.total, rb.data, rb.ssim], [ra.total, ra.data, ra.ssim], rtol=1e-12)

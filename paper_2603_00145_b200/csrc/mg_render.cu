@@ -292,8 +292,19 @@ struct LaneSegs {
   int tot;
 };
 
-__device__ __noinline__ LaneSegs build_lane_segs(const Window& w, int c0, int g, const int* __restrict__ starts,
-                                                 SegSmem& sm, int lane) {
+// Column bounds from the global CSR starts (the default source).
+struct CsrCols {
+  const int* __restrict__ starts;
+  __device__ __forceinline__ void bounds(const Window& w, int ii, int jj, int g, int& a, int& b) const {
+    const int base = (ii * g + jj) * g;
+    a = __ldg(starts + base + w.klo);
+    b = __ldg(starts + base + w.khi + 1);
+  }
+};
+
+template <class Cols>
+__device__ __noinline__ LaneSegs build_lane_segs_t(const Window& w, int c0, int g, const Cols& cols, SegSmem& sm,
+                                                   int lane) {
   LaneSegs L;
   int sum = 0, ne = 0;
 #pragma unroll
@@ -303,11 +314,8 @@ __device__ __noinline__ LaneSegs build_lane_segs(const Window& w, int c0, int g,
     L.len[k] = 0;
     if (col < w.ncol) {
       const int q = (int)(((float)col + 0.5f) * w.inv_nj);  // == col / nj (exact for small ints)
-      int ii = w.ilo + q;
-      int jj = w.jlo + (col - q * w.nj);
-      int base = (ii * g + jj) * g;
-      int a = __ldg(starts + base + w.klo);
-      int b = __ldg(starts + base + w.khi + 1);
+      int a, b;
+      cols.bounds(w, w.ilo + q, w.jlo + (col - q * w.nj), g, a, b);
       L.st[k] = a;
       L.len[k] = b - a;
     }
@@ -330,6 +338,11 @@ __device__ __noinline__ LaneSegs build_lane_segs(const Window& w, int c0, int g,
   L.nonempty_before = nbefore;
   L.tot = tot;
   return L;
+}
+
+__device__ __forceinline__ LaneSegs build_lane_segs(const Window& w, int c0, int g, const int* __restrict__ starts,
+                                                    SegSmem& sm, int lane) {
+  return build_lane_segs_t(w, c0, g, CsrCols{starts}, sm, lane);
 }
 
 // Fill the bitmap for flattened window [w0, w0 + 32*kBmWords); returns the
@@ -446,38 +459,18 @@ __device__ __forceinline__ GRec load_rec(const GaussSoA& grec, int gi) {
   return r;
 }
 
-// ---------------------------------------------------------------------------
-// Per-lane record prefetch ring.  Each lane copies the record of its candidate
-// for iteration t + S - 1 into its own slot with cp.async (no registers held,
-// no cross-lane dependency -> no warp syncs) and reads iteration t's record
-// back from shared memory once cp.async.wait_group says it has landed: S - 1
-// record fetches per lane stay in flight behind the math.
-// ---------------------------------------------------------------------------
-#ifndef MG_FWD_STAGES
-#define MG_FWD_STAGES 0  // 0: plain __ldg loop (the ring measured slower: 2 < 4 < 8 stages all lose)
-#endif
-constexpr int kFwdStages = MG_FWD_STAGES;
-static_assert(kFwdStages == 0 || (kFwdStages >= 2 && (kFwdStages & (kFwdStages - 1)) == 0),
-              "MG_FWD_STAGES must be 0 or a power of two >= 2");
-
-#ifndef MG_FWD_PF
-#define MG_FWD_PF 0  // L1 prefetch distance of the forward record loop (0: off; 1-3 measured slower: L1 wavefront-bound)
-#endif
-constexpr int kFwdPf = MG_FWD_PF;
-
-__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
-__device__ __forceinline__ void prefetch_rec(const GaussSoA& grec, int gi) {
-  prefetch_l1(grec.A + gi);
-  prefetch_l1(grec.B + gi);
-  prefetch_l1(grec.C + gi);
-}
-
-template <int S>
-struct RecRing {
-  float4 A[S][32], B[S][32];
-  float2 C[S][32];
+// Record sources of the forward item loops: candidate columns + records from
+// global memory (CSR starts, SoA records), or from a block's staged tile.
+struct GlobalRecs {
+  GaussSoA grec;
+  const int* __restrict__ gstart;
+  __device__ __forceinline__ LaneSegs segs(const Window& w, int c0, int g, SegSmem& sm, int lane) const {
+    return build_lane_segs_t(w, c0, g, CsrCols{gstart}, sm, lane);
+  }
+  __device__ __forceinline__ GRec rec(int i) const { return load_rec(grec, i); }
 };
 
+// cp.async helpers (4/8/16-byte asynchronous global -> shared copies).
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
                : "memory");
@@ -490,22 +483,6 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-template <int S>
-__device__ __forceinline__ void ring_fetch(RecRing<S>& R, int slot, int lane, const GaussSoA& grec, int gi) {
-  cp_async16(&R.A[slot][lane], grec.A + gi);
-  cp_async16(&R.B[slot][lane], grec.B + gi);
-  cp_async8(&R.C[slot][lane], grec.C + gi);
-}
-
-template <int S>
-__device__ __forceinline__ GRec ring_read(const RecRing<S>& R, int slot, int lane) {
-  GRec r;
-  r.A = R.A[slot][lane];
-  r.B = R.B[slot][lane];
-  r.C = R.C[slot][lane];
-  return r;
 }
 
 // Flattened-window cursor, one candidate per lane per 32-wide window.
@@ -574,16 +551,14 @@ __device__ __forceinline__ void fwd_pair_math(const GRec& g, const f2 (&px)[QP],
   }
 }
 
-template <int Q, bool WITH_H, class Ring>
-__device__ __forceinline__ void fwd_item(const GaussSoA grec, const int* __restrict__ gstart, int g, int r,
-                                         const float4* __restrict__ prec, int p0, int np, int cell,
-                                         float4* __restrict__ out4, int* __restrict__ cnt_out, SegSmem& sm,
-                                         Ring* ring, int lane) {
+template <int Q, bool WITH_H, class Src>
+__device__ __forceinline__ void fwd_item(const Src& src, int g, int r, const float4* __restrict__ prec, int p0,
+                                         int np, int cell, float4* __restrict__ out4, int* __restrict__ cnt_out,
+                                         SegSmem& sm, int lane) {
   constexpr int QP = Q / 2;
   // candidates per lane per window: with >= 2 point pairs there are already
-  // >= 2 independent chains per candidate, so one suffices (keeps registers
-  // for the ping-pong prefetch); with one pair, take two.
-  constexpr int GPL = (QP >= 2 || kFwdStages > 0) ? 1 : 2;
+  // >= 2 independent chains per candidate, so one suffices; with one pair, take two.
+  constexpr int GPL = QP >= 2 ? 1 : 2;
   constexpr int WIN = 32 * GPL;
   // stage the item's sub-points coordinate-major in shared memory and read
   // them back as 64-bit pairs: the f32x2 operands then sit in aligned
@@ -610,75 +585,28 @@ __device__ __forceinline__ void fwd_item(const GaussSoA grec, const int* __restr
   const unsigned upto = 0xffffffffu >> (31 - lane);  // bits 0..lane
   int total = 0;
   for (int c0 = 0; c0 < w.ncol; c0 += 128) {
-    const LaneSegs L = build_lane_segs(w, c0, g, gstart, sm, lane);
+    const LaneSegs L = src.segs(w, c0, g, sm, lane);
     const int tot = L.tot;
     total += tot;
     for (int w0 = 0; w0 < tot; w0 += 32 * kBmWords) {
       const int sb0 = build_window(L, w0, sm, lane);
       const int wend = min(tot, w0 + 32 * kBmWords);
-      // one compact loop: prefetching (two register sets) measured slower --
-      // the kernel is sensitive to code size and register pressure
-      if (kFwdStages > 0) {
-        constexpr int S = kFwdStages > 0 ? kFwdStages : 2;
-        Cursor1 cur{sb0};
-        const int n = (wend - w0 + 31) >> 5;
-#pragma unroll
-        for (int t = 0; t < S - 1; ++t) {
-          if (t < n) {
-            int va, ga;
-            cur.next(sm, w0, w0 + 32 * t, upto, lane, va, ga);
-            if (va < wend) ring_fetch(*ring, t, lane, grec, ga);
-          }
-          cp_async_commit();
-        }
-        for (int t = 0; t < n; ++t) {
-          if (t + S - 1 < n) {
-            int va, ga;
-            cur.next(sm, w0, w0 + 32 * (t + S - 1), upto, lane, va, ga);
-            if (va < wend) ring_fetch(*ring, (t + S - 1) & (S - 1), lane, grec, ga);
-          }
-          cp_async_commit();
-          cp_async_wait<S - 1>();
-          if (w0 + 32 * t + lane < wend)
-            fwd_pair_math<QP, WITH_H>(ring_read(*ring, t & (S - 1), lane), px, py, pz, accI, hx, hy, hz);
-        }
-      } else if (GPL == 1 && kFwdPf > 0) {
-        // the cursor runs kFwdPf iterations ahead and pulls those records into
-        // L1 (CCTL.PF1: no destination registers); the loads then hit L1
-        constexpr int D = kFwdPf > 0 ? kFwdPf : 1;
-        Cursor1 cur{sb0};
-        int qg[D];
-#pragma unroll
-        for (int d = 0; d < D; ++d) {
-          int va;
-          cur.next(sm, w0, w0 + 32 * d, upto, lane, va, qg[d]);
-          if (va < wend) prefetch_rec(grec, qg[d]);
-        }
-        for (int base = w0; base < wend; base += WIN) {
-          const int ga = qg[0];
-#pragma unroll
-          for (int d = 0; d + 1 < D; ++d) qg[d] = qg[d + 1];
-          {
-            int va;
-            cur.next(sm, w0, base + 32 * D, upto, lane, va, qg[D - 1]);
-            if (va < wend) prefetch_rec(grec, qg[D - 1]);
-          }
-          if (base + lane < wend) fwd_pair_math<QP, WITH_H>(load_rec(grec, ga), px, py, pz, accI, hx, hy, hz);
-        }
-      } else if (GPL == 1) {
+      // one compact loop: prefetching (register ring, cp.async ring, L1
+      // prefetch) all measured slower -- the kernel is L1/issue-bound
+      if (GPL == 1) {
         Cursor1 cur{sb0};
         for (int base = w0; base < wend; base += WIN) {
           int va, ga;
           cur.next(sm, w0, base, upto, lane, va, ga);
-          if (va < wend) fwd_pair_math<QP, WITH_H>(load_rec(grec, ga), px, py, pz, accI, hx, hy, hz);
+          if (va < wend) fwd_pair_math<QP, WITH_H>(src.rec(ga), px, py, pz, accI, hx, hy, hz);
         }
       } else {
         Cursor2 cur{sb0};
         for (int base = w0; base < wend; base += WIN) {
           int va, vb, ga, gb;
           cur.next(sm, w0, base, upto, lane, va, vb, ga, gb);
-          const GRec ra = load_rec(grec, va < wend ? ga : 0);
-          const GRec rb = load_rec(grec, vb < wend ? gb : 0);
+          const GRec ra = src.rec(va < wend ? ga : 0);
+          const GRec rb = src.rec(vb < wend ? gb : 0);
           if (va < wend) fwd_pair_math<QP, WITH_H>(ra, px, py, pz, accI, hx, hy, hz);
           if (vb < wend) fwd_pair_math<QP, WITH_H>(rb, px, py, pz, accI, hx, hy, hz);
         }
@@ -736,11 +664,10 @@ __device__ __forceinline__ void single_math(const GRec& a, const GRec& b, bool h
   }
 }
 
-template <bool WITH_H>
-__device__ __forceinline__ void fwd_item_single(const GaussSoA grec, const int* __restrict__ gstart, int g,
-                                                int r, const float4* __restrict__ prec, int p0, int cell,
-                                                float4* __restrict__ out4, int* __restrict__ cnt_out, SegSmem& sm,
-                                                int lane) {
+template <bool WITH_H, class Src>
+__device__ __forceinline__ void fwd_item_single(const Src& src, int g, int r, const float4* __restrict__ prec,
+                                                int p0, int cell, float4* __restrict__ out4,
+                                                int* __restrict__ cnt_out, SegSmem& sm, int lane) {
   const float4 pt = prec[p0];
   const f2 X = bc2(pt.x), Y = bc2(pt.y), Z = bc2(pt.z);
   f2 accI = bc2(0.f), hx = accI, hy = accI, hz = accI;
@@ -748,7 +675,7 @@ __device__ __forceinline__ void fwd_item_single(const GaussSoA grec, const int* 
   const unsigned upto = 0xffffffffu >> (31 - lane);
   int total = 0;
   for (int c0 = 0; c0 < w.ncol; c0 += 128) {
-    const LaneSegs L = build_lane_segs(w, c0, g, gstart, sm, lane);
+    const LaneSegs L = src.segs(w, c0, g, sm, lane);
     const int tot = L.tot;
     total += tot;
     for (int w0 = 0; w0 < tot; w0 += 32 * kBmWords) {
@@ -759,8 +686,8 @@ __device__ __forceinline__ void fwd_item_single(const GaussSoA grec, const int* 
         cur.next(sm, w0, base, upto, lane, va, vb, ga, gb);
         if (va < wend) {
           const bool hb = vb < wend;
-          const GRec ra = load_rec(grec, ga);
-          const GRec rb = load_rec(grec, hb ? gb : ga);
+          const GRec ra = src.rec(ga);
+          const GRec rb = src.rec(hb ? gb : ga);
           single_math<WITH_H>(ra, rb, hb, X, Y, Z, accI, hx, hy, hz);
         }
       }
@@ -837,6 +764,20 @@ __device__ __forceinline__ void fwd_item_dense(const GaussSoA& grec, const int* 
   }
 }
 
+template <bool WITH_H, class Src>
+__device__ __forceinline__ void fwd_dispatch(const Src& src, int g, int r, const float4* __restrict__ prec, int p0,
+                                             int np, int cell, float4* __restrict__ out4, int* __restrict__ cnt_out,
+                                             SegSmem& sm, int lane) {
+  if (MG_FWD_QMAX > 4 && np > 4)
+    fwd_item<(MG_FWD_QMAX > 4 ? 8 : 4), WITH_H>(src, g, r, prec, p0, np, cell, out4, cnt_out, sm, lane);
+  else if (np > 2)
+    fwd_item<4, WITH_H>(src, g, r, prec, p0, np, cell, out4, cnt_out, sm, lane);
+  else if (np == 2)
+    fwd_item<2, WITH_H>(src, g, r, prec, p0, np, cell, out4, cnt_out, sm, lane);
+  else
+    fwd_item_single<WITH_H>(src, g, r, prec, p0, cell, out4, cnt_out, sm, lane);
+}
+
 template <bool WITH_H>
 __global__ void __launch_bounds__(kFwdWarps * 32, MG_FWD_MINB) forward_kernel(const GaussSoA grec,
                                                                  const int* __restrict__ gstart, int g, int r,
@@ -846,12 +787,8 @@ __global__ void __launch_bounds__(kFwdWarps * 32, MG_FWD_MINB) forward_kernel(co
                                                                  const int4* __restrict__ items,
                                                                  const int* __restrict__ nitems_dev,
                                                                  float4* __restrict__ out4, int* __restrict__ cnt_out) {
-  using Ring = RecRing<(kFwdStages > 0 ? kFwdStages : 2)>;
-  extern __shared__ __align__(16) unsigned char fwd_dyn[];
-  SegSmem* s_seg = reinterpret_cast<SegSmem*>(fwd_dyn);
-  Ring* s_ring = reinterpret_cast<Ring*>(s_seg + kFwdWarps);
+  __shared__ SegSmem s_seg[kFwdWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  Ring* ring = kFwdStages > 0 ? s_ring + warp : nullptr;
   const int nitems = *nitems_dev;
   const int stride = gridDim.x * kFwdWarps;
   int it = blockIdx.x * kFwdWarps + warp;
@@ -864,16 +801,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32, MG_FWD_MINB) forward_kernel(co
       fwd_item_dense<WITH_H>(grec, gstart, g, r, prec, p0, item.z, cell, out4, cnt_out, s_seg[warp], lane);
       continue;
     }
-    const int np = item.z;
-    if (MG_FWD_QMAX > 4 && np > 4)
-      fwd_item<(MG_FWD_QMAX > 4 ? 8 : 4), WITH_H>(grec, gstart, g, r, prec, p0, np, cell, out4, cnt_out,
-                                                 s_seg[warp], ring, lane);
-    else if (np > 2)
-      fwd_item<4, WITH_H>(grec, gstart, g, r, prec, p0, np, cell, out4, cnt_out, s_seg[warp], ring, lane);
-    else if (np == 2)
-      fwd_item<2, WITH_H>(grec, gstart, g, r, prec, p0, np, cell, out4, cnt_out, s_seg[warp], ring, lane);
-    else
-      fwd_item_single<WITH_H>(grec, gstart, g, r, prec, p0, cell, out4, cnt_out, s_seg[warp], lane);
+    fwd_dispatch<WITH_H>(GlobalRecs{grec, gstart}, g, r, prec, p0, item.z, cell, out4, cnt_out, s_seg[warp], lane);
   }
 }
 
@@ -1497,14 +1425,9 @@ void launch_forward(bool with_h, const float* grec_raw, int64_t n_gauss, const i
   if (max_items <= 0) return;
   const int64_t want = (max_items + kFwdWarps - 1) / kFwdWarps;
   const GaussSoA grec = gauss_soa(grec_raw, n_gauss);
-  const size_t smem = kFwdWarps * (sizeof(SegSmem) + (kFwdStages > 0 ? sizeof(RecRing<(kFwdStages > 0 ? kFwdStages : 2)>) : 0));
   auto k = with_h ? forward_kernel<true> : forward_kernel<false>;
-  static bool attr_set[2] = {false, false};
-  if (!attr_set[with_h]) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr_set[with_h] = true;
-  }
-  const unsigned blocks = (unsigned)persistent_blocks(k, kFwdWarps * 32, want, smem);
+  const unsigned blocks = (unsigned)persistent_blocks(k, kFwdWarps * 32, want);
+  constexpr size_t smem = 0;
   MG_LAUNCH(k<<<blocks, kFwdWarps * 32, smem, st>>>(grec, gstart, g, r, prec, pkey, pstart, items, nitems, out4, cnt));
 }
 

@@ -85,7 +85,7 @@ def nrf_forward_cached(field: ResidualField, x: torch.Tensor):
         z = torch.addmm(field.biases[li], h, field.weights[li])
         pre.append(z)
         if li < depth - 1:
-            h = z * torch.sigmoid(z)
+            h = torch.nn.functional.silu(z)  # z * sigmoid(z), one kernel
             post.append(h)
     t = torch.tanh(pre[-1][:, 0])
     return field.output_bound * t, (t, pre, post)
@@ -98,6 +98,38 @@ def nrf_forward_device(field: ResidualField, x: torch.Tensor, chunk=1 << 20):
     return out
 
 
+def _split_k(n_rows, parts=128, min_rows=512):
+    q = n_rows // parts
+    return (parts, q) if q >= min_rows else (0, 0)
+
+
+def _tn_matmul(a, b):
+    """a^T @ b for tall (K x m), (K x n) operands: split-K over equal row
+    chunks as one batched GEMM plus a fixed-order sum (a plain K = 131k GEMM
+    with a 64 x 64 output runs on a handful of CTAs)."""
+    parts, q = _split_k(a.shape[0])
+    if not parts:
+        return a.T @ b
+    main = parts * q
+    out = torch.bmm(a[:main].reshape(parts, q, a.shape[1]).transpose(1, 2),
+                    b[:main].reshape(parts, q, b.shape[1])).sum(dim=0)
+    if main < a.shape[0]:
+        out = out + a[main:].T @ b[main:]
+    return out
+
+
+def _col_sum(a):
+    """a.sum(dim=0) as a two-stage reduction over equal row chunks."""
+    parts, q = _split_k(a.shape[0])
+    if not parts:
+        return a.sum(dim=0)
+    main = parts * q
+    out = a[:main].reshape(parts, q, a.shape[1]).sum(dim=1).sum(dim=0)
+    if main < a.shape[0]:
+        out = out + a[main:].sum(dim=0)
+    return out
+
+
 def nrf_backward(field: ResidualField, x: torch.Tensor, upstream: torch.Tensor, cache):
     """(d_weights, d_biases, d_points) of sum_b upstream_b r(x_b)."""
     t, pre, post = cache
@@ -106,12 +138,11 @@ def nrf_backward(field: ResidualField, x: torch.Tensor, upstream: torch.Tensor, 
     dz = (upstream * field.output_bound * (1.0 - t * t))[:, None]
     d_enc = None
     for li in range(depth - 1, -1, -1):
-        dws[li] = post[li].T @ dz
-        dbs[li] = dz.sum(dim=0)
+        dws[li] = _tn_matmul(post[li], dz)
+        dbs[li] = _col_sum(dz)
         dh = dz @ field.weights[li].T
-        if li > 0:
-            s = torch.sigmoid(pre[li - 1])
-            dz = dh * (s * (1.0 + pre[li - 1] * (1.0 - s)))
+        if li > 0:  # dh * s (1 + z (1 - s)), s = sigmoid(z): one fused kernel
+            dz = torch.ops.aten.silu_backward(dh, pre[li - 1])
         else:
             d_enc = dh
     bands = field.frequency_bands

@@ -343,6 +343,17 @@ static bool staged_backward_enabled(int64_t r) {
   return env == 1 && (2 * r + 1) * (2 * r + 1) <= 128;
 }
 
+// MGAUSS_BWD_PAIRS: "0" one item per Gaussian, "2" pair items always,
+// default: pair items when the mean candidate window is small
+static int backward_pair_mode() {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("MGAUSS_BWD_PAIRS");
+    env = (e && (e[0] == '0' || e[0] == '2')) ? e[0] - '0' : 1;
+  }
+  return env;
+}
+
 int mg_backward(const void* grec, const uint32_t* gkey_sorted, const int32_t* gstart, int64_t n, int64_t g, int64_t r,
                 const void* prec, const int32_t* pstart, float* acc10, void* ws, size_t wsb, void* stream) {
   if (g < 1 || r < 0 || n < 0) return fail("mg_backward: bad sizes");
@@ -354,9 +365,10 @@ int mg_backward(const void* grec, const uint32_t* gkey_sorted, const int32_t* gs
                            acc10, ws, st);
     return cuda_status();
   }
-  // one work item per sorted Gaussian, implicit: no item build, no workspace
+  // one work item per sorted Gaussian (or per k-adjacent Gaussian pair),
+  // implicit: no item build, no workspace
   launch_backward((const float*)grec, n, gkey_sorted, gstart, (int)g, (int)r, (const float4*)prec, pstart, nullptr,
-                  nullptr, n, acc10, st);
+                  nullptr, n, acc10, st, backward_pair_mode());
   return cuda_status();
 }
 

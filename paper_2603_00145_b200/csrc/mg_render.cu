@@ -847,7 +847,11 @@ struct GaussAcc {
   __device__ __forceinline__ void pair(const float4& a, const float4& b) {
     const f2 px = mk2(a.x, b.x), py = mk2(a.y, b.y), pz = mk2(a.z, b.z), u = mk2(a.w, b.w);
 #pragma unroll
-    for (int k = 0; k < QG; ++k) {
+    for (int k = 0; k < QG; ++k) accum(k, px, py, pz, u);
+  }
+  // Gaussian k over a point pair with upstream u (f32x2)
+  __device__ __forceinline__ void accum(int k, f2 px, f2 py, f2 pz, f2 u) {
+    {
       f2 dx = sub2(px, bc2(mx[k])), dy = sub2(py, bc2(my[k])), dz = sub2(pz, bc2(mz[k]));
       // m' = d^T P' d, Horner with doubled off-diagonals (9 FP32 ops)
       f2 t1 = fma2(bc2(P[k][4]), dz, fma2(bc2(P[k][3]), dy, mul2(bc2(P[k][0]), dx)));
@@ -946,6 +950,10 @@ __device__ __forceinline__ void bwd_window_loop(Acc& acc, const Window& w, int g
 }
 
 template <int QG>
+__device__ __forceinline__ void bwd_store(const GaussAcc<QG>& acc, int g0, int ng, float* __restrict__ acc10,
+                                          int lane);
+
+template <int QG>
 __device__ __forceinline__ void bwd_item(const GaussSoA grec, int g0, int ng, int cell, int g, int r,
                                          const float4* __restrict__ prec, const int* __restrict__ pstart,
                                          float* __restrict__ acc10, SegSmem& sm, int lane) {
@@ -953,7 +961,13 @@ __device__ __forceinline__ void bwd_item(const GaussSoA grec, int g0, int ng, in
 #pragma unroll
   for (int k = 0; k < QG; ++k) acc.load(grec, k, g0 + min(k, ng - 1));
   bwd_window_loop(acc, make_window(cell, g, r), g, prec, pstart, sm, lane);
-  // 10 sums per Gaussian (x QG, padded to 16 / 32) -> transposed reduction.
+  bwd_store(acc, g0, ng, acc10, lane);
+}
+
+// 10 sums per Gaussian (x QG, padded to 16 / 32) -> transposed reduction.
+template <int QG>
+__device__ __forceinline__ void bwd_store(const GaussAcc<QG>& acc, int g0, int ng, float* __restrict__ acc10,
+                                          int lane) {
   constexpr int NV = QG == 1 ? 16 : 32;
   float vals[32];
 #pragma unroll
@@ -971,16 +985,177 @@ __device__ __forceinline__ void bwd_item(const GaussSoA grec, int g0, int ng, in
   if ((lane & ((1 << SH) - 1)) == 0 && c < 10 && k < ng) acc10[(int64_t)(g0 + k) * 10 + c] = red;
 }
 
-__global__ void __launch_bounds__(kBwdWarps * 32, MG_BWD_MINB) backward_kernel(const GaussSoA grec,
+
+// ---------------------------------------------------------------------------
+// Pair items (sparse point densities): sorted Gaussians 2j and 2j+1 whose
+// cells are equal or k-adjacent in one (i, j) column share ONE candidate
+// window -- the union of their (2r+1)^3 neighbourhoods, which differs from
+// each by at most one k-cell per column.  Every column also records two
+// element thresholds: elements before `aend` lie in the A-only cell, elements
+// from `bbeg` on in the B-only cell, and the other Gaussian sees those points
+// with zero upstream -- so each Gaussian still sums over exactly its own
+// candidate set.  Halves the per-item window builds and shares every point
+// load and cursor step between two Gaussians.
+// ---------------------------------------------------------------------------
+struct PairCols {
+  const int* __restrict__ starts;
+  int kae, kbs;  // A-only cells [klo, kae), B-only cells [kbs, khi]
+};
+
+__device__ __noinline__ LaneSegs build_lane_segs_pair(const Window& w, int c0, int g, const PairCols cols,
+                                                      SegSmem& sm, int2* thr, int lane) {
+  LaneSegs L;
+  int2 t[4];
+  int sum = 0, ne = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int col = c0 + lane * 4 + k;
+    L.st[k] = 0;
+    L.len[k] = 0;
+    t[k] = make_int2(0, 0);
+    if (col < w.ncol) {
+      const int q = (int)(((float)col + 0.5f) * w.inv_nj);  // == col / nj
+      const int base = ((w.ilo + q) * g + w.jlo + (col - q * w.nj)) * g;
+      const int a = __ldg(cols.starts + base + w.klo);
+      const int b = __ldg(cols.starts + base + w.khi + 1);
+      t[k] = make_int2(__ldg(cols.starts + base + cols.kae), __ldg(cols.starts + base + cols.kbs));
+      L.st[k] = a;
+      L.len[k] = b - a;
+    }
+    sum += L.len[k];
+    ne += L.len[k] > 0;
+  }
+  int tot, netot;
+  int off = warp_excl_scan(sum, lane, &tot);
+  const int nbefore = warp_excl_scan(ne, lane, &netot);
+  int e = nbefore;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    L.pre[k] = off;
+    if (L.len[k] > 0) {
+      sm.delta[e] = L.st[k] - off;
+      thr[e++] = t[k];
+    }
+    off += L.len[k];
+  }
+  L.nonempty_before = nbefore;
+  L.tot = tot;
+  return L;
+}
+
+// Cursor4 that also classifies each candidate against its column's
+// thresholds: m bit 0 = B-only cell (not A's), bit 1 = A-only cell (not B's).
+struct Cursor4P {
+  int sbase;
+  __device__ __forceinline__ void next(const SegSmem& sm, const int2* thr, int w0, int base, unsigned upto, int lane,
+                                       int (&v)[4], int (&e)[4], int (&m)[4]) {
+    const int wi = (base - w0) >> 5;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t M = sm.bits[wi + i];
+      v[i] = base + 32 * i + lane;
+      const int s = sbase + __popc(M & upto) - 1;
+      e[i] = v[i] + sm.delta[s];
+      const int2 t = thr[s];
+      m[i] = (e[i] >= t.y ? 1 : 0) | (e[i] < t.x ? 2 : 0);
+      sbase += __popc(M);
+    }
+  }
+};
+
+// Points a, b (elements ea, eb) into both Gaussians of a pair item.
+__device__ __forceinline__ void pair_masked(GaussAcc<2>& acc, const float4& a, const float4& b, int ma, int mb) {
+  const f2 px = mk2(a.x, b.x), py = mk2(a.y, b.y), pz = mk2(a.z, b.z);
+  const f2 uA = mk2((ma & 1) ? 0.f : a.w, (mb & 1) ? 0.f : b.w);
+  const f2 uB = mk2((ma & 2) ? 0.f : a.w, (mb & 2) ? 0.f : b.w);
+  acc.accum(0, px, py, pz, uA);
+  acc.accum(1, px, py, pz, uB);
+}
+
+__device__ __forceinline__ void bwd_pair_item(const GaussSoA grec, int j, int cell_a, int cell_b, int g, int r,
+                                              const float4* __restrict__ prec, const int* __restrict__ pstart,
+                                              float* __restrict__ acc10, SegSmem& sm, int2* thr, int lane) {
+  GaussAcc<2> acc;
+  acc.load(grec, 0, j);
+  acc.load(grec, 1, j + 1);
+  Window w = make_window(cell_a, g, r);
+  const int ka = cell_a % g, kb = ka + (cell_b - cell_a);
+  w.khi = min(kb + r, g - 1);
+  const PairCols cols{pstart, max(kb - r, 0), min(ka + r, g - 1) + 1};
+  const unsigned upto = 0xffffffffu >> (31 - lane);
+  for (int c0 = 0; c0 < w.ncol; c0 += 128) {
+    const LaneSegs L = build_lane_segs_pair(w, c0, g, cols, sm, thr, lane);
+    const int tot = L.tot;
+    for (int w0 = 0; w0 < tot; w0 += 32 * kBmWords) {
+      Cursor4P cur{build_window(L, w0, sm, lane)};
+      const int wend = min(tot, w0 + 32 * kBmWords);
+      const int nfull = (wend - w0) >> 7;
+      int v[4], e[4], m[4];
+      for (int it = 0; it < nfull; ++it) {
+        cur.next(sm, thr, w0, w0 + 128 * it, upto, lane, v, e, m);
+        float4 q[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) q[i] = __ldg(prec + e[i]);
+        pair_masked(acc, q[0], q[1], m[0], m[1]);
+        pair_masked(acc, q[2], q[3], m[2], m[3]);
+      }
+      const int tb = w0 + (nfull << 7);
+      if (tb < wend) {  // ragged tail window: missing points are zero records
+        cur.next(sm, thr, w0, tb, upto, lane, v, e, m);
+        float4 q[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) q[i] = v[i] < wend ? __ldg(prec + e[i]) : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (v[0] < wend) pair_masked(acc, q[0], q[1], m[0], m[1]);
+        if (v[2] < wend) pair_masked(acc, q[2], q[3], m[2], m[3]);
+      }
+      __syncwarp();
+    }
+  }
+  bwd_store(acc, j, 2, acc10, lane);
+}
+
+#ifndef MG_BWD_PAIR_MAXWIN
+#define MG_BWD_PAIR_MAXWIN 6144  // mean candidate points per Gaussian below which pairs run (C1 ~29k: singles)
+#endif
+#ifndef MG_BWD_PAIR_MINB
+#define MG_BWD_PAIR_MINB 2  // two Gaussians' accumulators: 126 registers, no spills (3 spills ~350 B)
+#endif
+template <bool PAIR>
+__global__ void __launch_bounds__(kBwdWarps * 32, PAIR ? MG_BWD_PAIR_MINB : MG_BWD_MINB) backward_kernel(const GaussSoA grec,
                                                                   const uint32_t* __restrict__ gkey,
                                                                   const int* __restrict__ gstart, int g, int r,
                                                                   const float4* __restrict__ prec,
                                                                   const int* __restrict__ pstart,
                                                                   const int4* __restrict__ items,
                                                                   const int* __restrict__ nitems_dev,
-                                                                  int n_implicit, float* __restrict__ acc10) {
+                                                                  int n_implicit, float* __restrict__ acc10,
+                                                                  int64_t pair_maxwin) {
   __shared__ SegSmem s_seg[kBwdWarps];
+  __shared__ int2 s_thr[PAIR ? kBwdWarps : 1][128];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // implicit pair items (sorted Gaussians 2j, 2j+1) where the mean candidate
+  // window is small enough for the per-item window build to matter; dense
+  // windows keep one Gaussian per warp (twice the items to balance over)
+  bool use_pairs = false;
+  if (PAIR && items == nullptr) {
+    const int64_t g3 = (int64_t)g * g * g, w = 2 * r + 1;
+    use_pairs = (int64_t)pstart[g3] * w * w * w < pair_maxwin * g3;
+  }
+  if (use_pairs) {
+    const int npairs = (n_implicit + 1) >> 1;
+    for (int it = blockIdx.x * kBwdWarps + warp; it < npairs; it += gridDim.x * kBwdWarps) {
+      const int j = 2 * it;
+      const int ca = (int)gkey[j];
+      const int cb = j + 1 < n_implicit ? (int)gkey[j + 1] : -1;
+      if (cb == ca || (cb == ca + 1 && ca % g != g - 1)) {
+        bwd_pair_item(grec, j, ca, cb, g, r, prec, pstart, acc10, s_seg[warp], s_thr[warp], lane);
+      } else {
+        bwd_item<1>(grec, j, 1, ca, g, r, prec, pstart, acc10, s_seg[warp], lane);
+        if (cb >= 0) bwd_item<1>(grec, j + 1, 1, cb, g, r, prec, pstart, acc10, s_seg[warp], lane);
+      }
+    }
+    return;
+  }
   // item {Gaussian, cell, -1, 0} (staged-path overflow list); items ==
   // nullptr: one item per sorted Gaussian, in cell order, so concurrently
   // running warps share their candidate point windows
@@ -1481,18 +1656,23 @@ void launch_backward_staged(const float* grec_raw, int64_t n_gauss, const uint32
   MG_LAUNCH(item_compact_kernel<<<grid_for(n_gauss), 256, 0, st>>>(oflags, oscan, gkey, gstart, n_gauss, 1, 0,
                                                                     oitems, counts + 1, 1));
   const int64_t want = (n_gauss / 2 + kBwdWarps) / kBwdWarps;
-  MG_LAUNCH(backward_kernel<<<(unsigned)persistent_blocks(backward_kernel, kBwdWarps * 32, want), kBwdWarps * 32, 0,
-                              st>>>(grec, gkey, gstart, g, r, prec, pstart, oitems, counts + 1, 0, acc10));
+  MG_LAUNCH(backward_kernel<false><<<(unsigned)persistent_blocks(backward_kernel<false>, kBwdWarps * 32, want),
+                                     kBwdWarps * 32, 0, st>>>(grec, gkey, gstart, g, r, prec, pstart, oitems,
+                                                              counts + 1, 0, acc10, 0));
 }
 
 void launch_backward(const float* grec_raw, int64_t n_gauss, const uint32_t* gkey, const int* gstart, int g, int r,
                      const float4* prec, const int* pstart, const int4* items, const int* nitems, int64_t max_items,
-                     float* acc10, cudaStream_t st) {
+                     float* acc10, cudaStream_t st, int pair_mode) {
   if (max_items <= 0) return;
   const GaussSoA grec = gauss_soa(grec_raw, n_gauss);
+  // pair_mode 1: the kernel picks pairs or singles from the point density; 2: pairs
+  const bool pairs = pair_mode > 0 && items == nullptr;
+  const int64_t maxwin = pair_mode == 2 ? ((int64_t)1 << 40) : (int64_t)MG_BWD_PAIR_MAXWIN;
   const int64_t want = (max_items + kBwdWarps - 1) / kBwdWarps;
-  MG_LAUNCH(backward_kernel<<<(unsigned)persistent_blocks(backward_kernel, kBwdWarps * 32, want), kBwdWarps * 32, 0, st>>>(
-      grec, gkey, gstart, g, r, prec, pstart, items, nitems, (int)n_gauss, acc10));
+  auto k = pairs ? backward_kernel<true> : backward_kernel<false>;
+  MG_LAUNCH(k<<<(unsigned)persistent_blocks(k, kBwdWarps * 32, want), kBwdWarps * 32, 0, st>>>(
+      grec, gkey, gstart, g, r, prec, pstart, items, nitems, (int)n_gauss, acc10, maxwin));
 }
 
 }  // namespace mg

@@ -31,7 +31,7 @@ void launch_forward(bool with_h, const float* grec, int64_t n_gauss, const int* 
                     float4* out4, int* cnt, cudaStream_t st);
 void launch_backward(const float* grec, int64_t n_gauss, const uint32_t* gkey, const int* gstart, int g, int r,
                      const float4* prec, const int* pstart, const int4* items, const int* nitems, int64_t max_items,
-                     float* acc10, cudaStream_t st);
+                     float* acc10, cudaStream_t st, int pair_mode = 0);
 
 size_t backward_staged_ws_bytes(int64_t n, int g);
 void launch_backward_staged(const float* grec, int64_t n_gauss, const uint32_t* gkey, const int* gstart, int g, int r,

@@ -601,10 +601,8 @@ class Trainer:
             if self._graph is None or self._graph_key != key:
                 self._body(B, nb, hw)  # eager warm-up of this shape (also lazily inits kernels)
                 torch.cuda.synchronize()
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g):
-                    self._body(B, nb, hw)
-                self._graph, self._graph_key = g, key
+                self._graph = None  # release the previous shape's graph (and its pool) first
+                self._graph, self._graph_key = self._capture(lambda: self._body(B, nb, hw)), key
                 # the warm-up already performed this step's update; undo nothing: the
                 # captured graph is replayed from the next step on.
             else:
@@ -615,6 +613,28 @@ class Trainer:
             return LossReport(self.iteration, float("nan"), float("nan"), float("nan"), float("nan"),
                               self.field.resolution, self.nrf_active)
         return self._resolve(self._enqueue_readback(B, hw))
+
+    def _capture(self, fn):
+        """Capture ``fn``'s launches into a CUDA graph on a side stream.
+
+        Not ``torch.cuda.graph``: its ``__enter__`` empties the device and
+        pinned-host caching allocators every time (measured 0.1-0.7 s per
+        capture after a large prior allocation, i.e. most of a desk-scale
+        reconstruction's wall time across its milestone re-captures)."""
+        cur = torch.cuda.current_stream()
+        if getattr(self, "_cap_stream", None) is None:
+            self._cap_stream = torch.cuda.Stream()
+        cs = self._cap_stream
+        cs.wait_stream(cur)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(cs):
+            g.capture_begin()
+            try:
+                fn()
+            finally:
+                g.capture_end()
+        cur.wait_stream(cs)
+        return g
 
     def _enqueue_readback(self, B, hw):
         """Async D2H of this step's loss sums and error flag into a pinned slot."""

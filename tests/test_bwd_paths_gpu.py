@@ -1,0 +1,86 @@
+"""The three backward work decompositions must each match the reference's
+gradients (SURVEY §8(c) tolerance) on the lattice golden and on a dense random
+cloud (several Gaussians per cell, odd N, non-adjacent cells):
+
+- pair items (MGAUSS_BWD_PAIRS=2 forces them; by default they run when the
+  mean candidate window is small): k-adjacent sorted Gaussians share one
+  union window with per-column edge masks;
+- single items (MGAUSS_BWD_PAIRS=0): one window per Gaussian;
+- staged strips (MGAUSS_STAGED_BWD=1, opt-in): TMA bulk copies of each strip's
+  point neighbourhood into shared memory under an mbarrier.
+
+The switches are read once per process, so every variant runs in a
+subprocess; the oracle gradients come from the committed golden (lattice) and
+the CPU oracle (random cloud)."""
+
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import assert_grad_close, load_golden
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+sys.path.insert(0, sys.argv[1] + "/tests")
+from test_render_gpu import Batch
+from test_bwd_paths_gpu import case
+from paper_2603_00145_b200.render import render_backward
+from paper_2603_00145_b200.spatial import build
+f, g, r, ts, coords, sids, up = case(sys.argv[3])
+gr = render_backward(f, build(f, g, r), ts, Batch(coords, sids), up)
+np.savez(sys.argv[2], dp=gr.d_positions, dq=gr.d_quaternions, ds=gr.d_log_scales, dl=gr.d_intensity_logits)
+"""
+
+
+def case(name):
+    from paper_2603_00145_b200.core import GaussianField, TransformSet
+    from test_render_gpu import field_of, transforms_of
+
+    if name == "lattice":
+        z = load_golden("render_lattice12")
+        return field_of(z), int(z["g"]), 5, transforms_of(z), z["coords"], z["sids"], z["upstream"]
+    rng = np.random.default_rng(7)
+    n = 2999
+    f32 = lambda a: np.asarray(a, np.float32).astype(np.float64)  # noqa: E731
+    f = GaussianField(f32(rng.uniform(-0.95, 0.95, (n, 3))), f32(rng.normal(0, 0.3, (n, 4)) + [1, 0, 0, 0]),
+                      f32(np.log(1 / 20) + rng.normal(0, 0.2, (n, 3))), f32(rng.normal(0, 1, n)))
+    k = 3
+    ts = TransformSet(f32(rng.normal(0, 0.05, (k, 4)) + [1, 0, 0, 0]), f32(rng.normal(0, 0.02, (k, 3))))
+    b = 12000
+    return f, 12, 3, ts, rng.uniform(-1, 1, (b, 3)), rng.integers(-1, k, b), rng.normal(size=b)
+
+
+def _want(name):
+    if name == "lattice":
+        z = load_golden("render_lattice12")
+        return dict(dp=z["d_positions"], dq=z["d_quaternions"], ds=z["d_log_scales"], dl=z["d_logits"])
+    from oracle import oracle as O
+    f, g, r, ts, coords, sids, up = case(name)
+    og = O.render_backward(f.positions, f.quaternions, f.log_scales, f.intensity_logits, g, r, coords, up, sids,
+                           ts.quats, ts.translations, threads=4)
+    return dict(dp=og.d_positions, dq=og.d_quaternions, ds=og.d_log_scales, dl=og.d_intensity_logits)
+
+
+VARIANTS = {"auto": {}, "pairs": {"MGAUSS_BWD_PAIRS": "2"}, "singles": {"MGAUSS_BWD_PAIRS": "0"},
+            "staged": {"MGAUSS_STAGED_BWD": "1"}}
+
+
+@pytest.mark.parametrize("name", ["lattice", "random"])
+@pytest.mark.parametrize("variant", sorted(VARIANTS))
+def test_backward_path_matches_reference(tmp_path, variant, name):
+    out = tmp_path / f"{variant}_{name}.npz"
+    env = dict(os.environ, MGAUSS_STAGED_BWD="0")
+    env.pop("MGAUSS_BWD_PAIRS", None)
+    env.update(VARIANTS[variant])
+    subprocess.run([sys.executable, "-c", SCRIPT, ROOT, str(out), name], env=env, check=True, timeout=600)
+    got, want = np.load(out), _want(name)
+    for k in ("dp", "dq", "ds", "dl"):
+        assert_grad_close(got[k], want[k], name=f"{variant}:{name}:{k}")

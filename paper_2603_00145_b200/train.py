@@ -35,7 +35,7 @@ from .render import SlicePSF, sample_volume_device
 DEFAULT_SCHEDULE = ((0, 70), (500, 100), (1000, 130), (2000, 165), (3000, 200))
 
 
-_PERM_PREFETCH_MIN = 1 << 18  # pools from this size draw epoch permutations ahead
+_PERM_PREFETCH_MIN = 1 << 16  # pools from this size draw epoch permutations ahead
 
 
 @dataclass

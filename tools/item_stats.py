@@ -55,6 +55,16 @@ def main():
     for q in (1, 2, 4, 8):
         items = np.sum(np.ceil(pc / q))
         print(f"fwd items at Q={q}: {items:.0f}, mean pts/item {ps[-1] / items:.2f}")
+    # k-runs of c adjacent cells merged into one item when their points fit Q=8
+    P3 = pc.reshape(g * g, g)
+    for c in (2, 4):
+        items = 0
+        for k0 in range(0, g, c):
+            run = P3[:, k0:k0 + c]
+            tot = run.sum(1)
+            fit = tot <= 8
+            items += int(np.sum((tot > 0) & fit)) + int(np.sum(np.ceil(run[~fit] / 8)))
+        print(f"fwd items with {c}-cell k-runs (<= 8 pts merged): {items}, mean pts/item {ps[-1] / items:.2f}")
 
 
 if __name__ == "__main__":

@@ -343,13 +343,12 @@ static bool staged_backward_enabled(int64_t r) {
   return env == 1 && (2 * r + 1) * (2 * r + 1) <= 128;
 }
 
-// MGAUSS_BWD_PAIRS: "0" one item per Gaussian, "2" pair items always,
-// default: pair items when the mean candidate window is small
+// MGAUSS_BWD_PAIRS=0: one item per Gaussian (default: k-adjacent pairs)
 static int backward_pair_mode() {
   static int env = -1;
   if (env < 0) {
     const char* e = getenv("MGAUSS_BWD_PAIRS");
-    env = (e && (e[0] == '0' || e[0] == '2')) ? e[0] - '0' : 1;
+    env = (e && e[0] == '0') ? 0 : 1;
   }
   return env;
 }

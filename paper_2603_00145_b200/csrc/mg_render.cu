@@ -441,6 +441,9 @@ __device__ __forceinline__ void write_point_out(float4* __restrict__ out4, int* 
 #ifndef MG_BWD_IPF
 #define MG_BWD_IPF 0  // off: with implicit items the prefetch measured ~2% slower
 #endif
+#ifndef MG_BWD_PAIR_GPACK
+#define MG_BWD_PAIR_GPACK 1  // pair items: Gaussian-packed f32x2 (points broadcast)
+#endif
 #ifndef MG_BWD_WARPS
 #define MG_BWD_WARPS 8
 #endif
@@ -949,9 +952,8 @@ __device__ __forceinline__ void bwd_window_loop(Acc& acc, const Window& w, int g
   }
 }
 
-template <int QG>
-__device__ __forceinline__ void bwd_store(const GaussAcc<QG>& acc, int g0, int ng, float* __restrict__ acc10,
-                                          int lane);
+template <int QG, class Acc>
+__device__ __forceinline__ void bwd_store(const Acc& acc, int g0, int ng, float* __restrict__ acc10, int lane);
 
 template <int QG>
 __device__ __forceinline__ void bwd_item(const GaussSoA grec, int g0, int ng, int cell, int g, int r,
@@ -961,13 +963,12 @@ __device__ __forceinline__ void bwd_item(const GaussSoA grec, int g0, int ng, in
 #pragma unroll
   for (int k = 0; k < QG; ++k) acc.load(grec, k, g0 + min(k, ng - 1));
   bwd_window_loop(acc, make_window(cell, g, r), g, prec, pstart, sm, lane);
-  bwd_store(acc, g0, ng, acc10, lane);
+  bwd_store<QG>(acc, g0, ng, acc10, lane);
 }
 
 // 10 sums per Gaussian (x QG, padded to 16 / 32) -> transposed reduction.
-template <int QG>
-__device__ __forceinline__ void bwd_store(const GaussAcc<QG>& acc, int g0, int ng, float* __restrict__ acc10,
-                                          int lane) {
+template <int QG, class Acc>
+__device__ __forceinline__ void bwd_store(const Acc& acc, int g0, int ng, float* __restrict__ acc10, int lane) {
   constexpr int NV = QG == 1 ? 16 : 32;
   float vals[32];
 #pragma unroll
@@ -1063,6 +1064,88 @@ struct Cursor4P {
   }
 };
 
+// Gaussian-packed accumulators of a pair item: every f32x2 register holds
+// (Gaussian A, Gaussian B), and each candidate point enters as broadcast
+// scalars straight from its loaded record (no re-pairing moves), with its own
+// upstream per half (the edge masks).  d is formed as mu - x (the broadcast
+// operand must be the second source), so D1 is negated in totals().
+struct GaussPairAcc {
+  f2 mx, my, mz, P[6];  // P: P'00, P'11, P'22, 2P'01, 2P'02, 2P'12
+  f2 S, T[3], A6[6];
+
+  // The 9 parameter pairs are staged through shared memory (18 floats, pair
+  // interleaved) and read back as 64-bit loads, so they live in aligned
+  // register pairs: built with register moves, ptxas re-pairs them before
+  // every FFMA2 in the loop.
+  __device__ __forceinline__ void load(const GaussSoA& grec, int ja, int jb, float* stage, int lane) {
+    if (lane < 2) {
+      const int j = lane ? jb : ja;
+      const float4 A = grec.A[j], B = grec.B[j];
+      const float2 C = grec.C[j];
+      stage[0 + lane] = A.x;
+      stage[2 + lane] = A.y;
+      stage[4 + lane] = A.z;
+      stage[6 + lane] = B.x;
+      stage[8 + lane] = B.y;
+      stage[10 + lane] = B.z;
+      stage[12 + lane] = 2.f * B.w;  // doubling is exact
+      stage[14 + lane] = 2.f * C.x;
+      stage[16 + lane] = 2.f * C.y;
+    }
+    __syncwarp();
+    const unsigned long long* st2 = reinterpret_cast<const unsigned long long*>(stage);
+    mx.v = st2[0];
+    my.v = st2[1];
+    mz.v = st2[2];
+#pragma unroll
+    for (int c = 0; c < 6; ++c) P[c].v = st2[3 + c];
+    __syncwarp();
+    S = bc2(0.f);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) T[c] = bc2(0.f);
+#pragma unroll
+    for (int c = 0; c < 6; ++c) A6[c] = bc2(0.f);
+  }
+  // one candidate point p with upstream u = (u seen by A, u seen by B)
+  __device__ __forceinline__ void point(const float4& p, f2 u) {
+    const f2 dx = sub2(mx, bc2(p.x)), dy = sub2(my, bc2(p.y)), dz = sub2(mz, bc2(p.z));
+    f2 t1 = fma2(P[4], dz, fma2(P[3], dy, mul2(P[0], dx)));
+    f2 m = mul2(dx, t1);
+    m = fma2(dy, fma2(P[5], dz, mul2(P[1], dy)), m);
+    m = fma2(dz, mul2(P[2], dz), m);
+    const f2 ug = mul2(u, gauss_w2(m));
+    S = add2(S, ug);
+    const f2 cx = mul2(ug, dx), cy = mul2(ug, dy), cz = mul2(ug, dz);
+    T[0] = add2(T[0], cx);
+    T[1] = add2(T[1], cy);
+    T[2] = add2(T[2], cz);
+    A6[0] = fma2(cx, dx, A6[0]);
+    A6[1] = fma2(cx, dy, A6[1]);
+    A6[2] = fma2(cx, dz, A6[2]);
+    A6[3] = fma2(cy, dy, A6[3]);
+    A6[4] = fma2(cy, dz, A6[4]);
+    A6[5] = fma2(cz, dz, A6[5]);
+  }
+  __device__ __forceinline__ static float half(f2 v, int k) { return k ? hi(v) : lo(v); }
+  // lane-local totals of Gaussian k (0 = A, 1 = B); T = P' D1, D1 = -sum u g (mu - x)
+  __device__ __forceinline__ void totals(int k, float* v) const {
+    v[0] = half(S, k);
+    const float d1x = -half(T[0], k), d1y = -half(T[1], k), d1z = -half(T[2], k);
+    const float p00 = half(P[0], k), p11 = half(P[1], k), p22 = half(P[2], k);
+    const float h01 = 0.5f * half(P[3], k), h02 = 0.5f * half(P[4], k), h12 = 0.5f * half(P[5], k);
+    v[1] = p00 * d1x + h01 * d1y + h02 * d1z;
+    v[2] = h01 * d1x + p11 * d1y + h12 * d1z;
+    v[3] = h02 * d1x + h12 * d1y + p22 * d1z;
+#pragma unroll
+    for (int c = 0; c < 6; ++c) v[4 + c] = half(A6[c], k);
+  }
+};
+
+__device__ __forceinline__ void pair_masked(GaussPairAcc& acc, const float4& a, const float4& b, int ma, int mb) {
+  acc.point(a, mk2((ma & 1) ? 0.f : a.w, (ma & 2) ? 0.f : a.w));
+  acc.point(b, mk2((mb & 1) ? 0.f : b.w, (mb & 2) ? 0.f : b.w));
+}
+
 // Points a, b (elements ea, eb) into both Gaussians of a pair item.
 __device__ __forceinline__ void pair_masked(GaussAcc<2>& acc, const float4& a, const float4& b, int ma, int mb) {
   const f2 px = mk2(a.x, b.x), py = mk2(a.y, b.y), pz = mk2(a.z, b.z);
@@ -1075,9 +1158,14 @@ __device__ __forceinline__ void pair_masked(GaussAcc<2>& acc, const float4& a, c
 __device__ __forceinline__ void bwd_pair_item(const GaussSoA grec, int j, int cell_a, int cell_b, int g, int r,
                                               const float4* __restrict__ prec, const int* __restrict__ pstart,
                                               float* __restrict__ acc10, SegSmem& sm, int2* thr, int lane) {
+#if MG_BWD_PAIR_GPACK
+  GaussPairAcc acc;
+  acc.load(grec, j, j + 1, &sm.pts[0][0], lane);
+#else
   GaussAcc<2> acc;
   acc.load(grec, 0, j);
   acc.load(grec, 1, j + 1);
+#endif
   Window w = make_window(cell_a, g, r);
   const int ka = cell_a % g, kb = ka + (cell_b - cell_a);
   w.khi = min(kb + r, g - 1);
@@ -1111,12 +1199,9 @@ __device__ __forceinline__ void bwd_pair_item(const GaussSoA grec, int j, int ce
       __syncwarp();
     }
   }
-  bwd_store(acc, j, 2, acc10, lane);
+  bwd_store<2>(acc, j, 2, acc10, lane);
 }
 
-#ifndef MG_BWD_PAIR_MAXWIN
-#define MG_BWD_PAIR_MAXWIN 6144  // mean candidate points per Gaussian below which pairs run (C1 ~29k: singles)
-#endif
 #ifndef MG_BWD_PAIR_MINB
 #define MG_BWD_PAIR_MINB 2  // two Gaussians' accumulators: 126 registers, no spills (3 spills ~350 B)
 #endif
@@ -1128,20 +1213,12 @@ __global__ void __launch_bounds__(kBwdWarps * 32, PAIR ? MG_BWD_PAIR_MINB : MG_B
                                                                   const int* __restrict__ pstart,
                                                                   const int4* __restrict__ items,
                                                                   const int* __restrict__ nitems_dev,
-                                                                  int n_implicit, float* __restrict__ acc10,
-                                                                  int64_t pair_maxwin) {
+                                                                  int n_implicit, float* __restrict__ acc10) {
   __shared__ SegSmem s_seg[kBwdWarps];
   __shared__ int2 s_thr[PAIR ? kBwdWarps : 1][128];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // implicit pair items (sorted Gaussians 2j, 2j+1) where the mean candidate
-  // window is small enough for the per-item window build to matter; dense
-  // windows keep one Gaussian per warp (twice the items to balance over)
-  bool use_pairs = false;
+  // implicit pair items: sorted Gaussians (2j, 2j+1)
   if (PAIR && items == nullptr) {
-    const int64_t g3 = (int64_t)g * g * g, w = 2 * r + 1;
-    use_pairs = (int64_t)pstart[g3] * w * w * w < pair_maxwin * g3;
-  }
-  if (use_pairs) {
     const int npairs = (n_implicit + 1) >> 1;
     for (int it = blockIdx.x * kBwdWarps + warp; it < npairs; it += gridDim.x * kBwdWarps) {
       const int j = 2 * it;
@@ -1658,7 +1735,7 @@ void launch_backward_staged(const float* grec_raw, int64_t n_gauss, const uint32
   const int64_t want = (n_gauss / 2 + kBwdWarps) / kBwdWarps;
   MG_LAUNCH(backward_kernel<false><<<(unsigned)persistent_blocks(backward_kernel<false>, kBwdWarps * 32, want),
                                      kBwdWarps * 32, 0, st>>>(grec, gkey, gstart, g, r, prec, pstart, oitems,
-                                                              counts + 1, 0, acc10, 0));
+                                                              counts + 1, 0, acc10));
 }
 
 void launch_backward(const float* grec_raw, int64_t n_gauss, const uint32_t* gkey, const int* gstart, int g, int r,
@@ -1666,13 +1743,11 @@ void launch_backward(const float* grec_raw, int64_t n_gauss, const uint32_t* gke
                      float* acc10, cudaStream_t st, int pair_mode) {
   if (max_items <= 0) return;
   const GaussSoA grec = gauss_soa(grec_raw, n_gauss);
-  // pair_mode 1: the kernel picks pairs or singles from the point density; 2: pairs
   const bool pairs = pair_mode > 0 && items == nullptr;
-  const int64_t maxwin = pair_mode == 2 ? ((int64_t)1 << 40) : (int64_t)MG_BWD_PAIR_MAXWIN;
   const int64_t want = (max_items + kBwdWarps - 1) / kBwdWarps;
   auto k = pairs ? backward_kernel<true> : backward_kernel<false>;
   MG_LAUNCH(k<<<(unsigned)persistent_blocks(k, kBwdWarps * 32, want), kBwdWarps * 32, 0, st>>>(
-      grec, gkey, gstart, g, r, prec, pstart, items, nitems, (int)n_gauss, acc10, maxwin));
+      grec, gkey, gstart, g, r, prec, pstart, items, nitems, (int)n_gauss, acc10));
 }
 
 }  // namespace mg

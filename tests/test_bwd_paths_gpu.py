@@ -2,9 +2,8 @@
 gradients (SURVEY §8(c) tolerance) on the lattice golden and on a dense random
 cloud (several Gaussians per cell, odd N, non-adjacent cells):
 
-- pair items (MGAUSS_BWD_PAIRS=2 forces them; by default they run when the
-  mean candidate window is small): k-adjacent sorted Gaussians share one
-  union window with per-column edge masks;
+- pair items (default): k-adjacent sorted Gaussians share one union window
+  with per-column edge masks, Gaussian-packed f32x2;
 - single items (MGAUSS_BWD_PAIRS=0): one window per Gaussian;
 - staged strips (MGAUSS_STAGED_BWD=1, opt-in): TMA bulk copies of each strip's
   point neighbourhood into shared memory under an mbarrier.
@@ -69,8 +68,7 @@ def _want(name):
     return dict(dp=og.d_positions, dq=og.d_quaternions, ds=og.d_log_scales, dl=og.d_intensity_logits)
 
 
-VARIANTS = {"auto": {}, "pairs": {"MGAUSS_BWD_PAIRS": "2"}, "singles": {"MGAUSS_BWD_PAIRS": "0"},
-            "staged": {"MGAUSS_STAGED_BWD": "1"}}
+VARIANTS = {"pairs": {}, "singles": {"MGAUSS_BWD_PAIRS": "0"}, "staged": {"MGAUSS_STAGED_BWD": "1"}}
 
 
 @pytest.mark.parametrize("name", ["lattice", "random"])

@@ -430,7 +430,7 @@ __device__ __forceinline__ void write_point_out(float4* __restrict__ out4, int* 
 #define MG_BWD_MINB 3
 #endif
 #ifndef MG_FWD_QMAX
-#define MG_FWD_QMAX 8  // up to 8 sub-points per item (measured ~2.5% faster than 4 at C2)
+#define MG_FWD_QMAX 6  // up to 6 sub-points per item: Q=8 spills at 80 registers (C2: 0.618 -> 0.593 ms)
 #endif
 #ifndef MG_FWD_WARPS
 #define MG_FWD_WARPS 8
@@ -617,7 +617,7 @@ __device__ __forceinline__ void fwd_item(const Src& src, int g, int r, const flo
       __syncwarp();
     }
   }
-  constexpr int NV = 4 * Q;  // 8 or 16 (32 at Q = 8)
+  constexpr int NV = Q == 6 ? 32 : 4 * Q;  // 8 or 16 (32 at Q = 6, 8)
   float vals[32];
 #pragma unroll
   for (int q = 0; q < QP; ++q) {
@@ -772,7 +772,8 @@ __device__ __forceinline__ void fwd_dispatch(const Src& src, int g, int r, const
                                              int np, int cell, float4* __restrict__ out4, int* __restrict__ cnt_out,
                                              SegSmem& sm, int lane) {
   if (MG_FWD_QMAX > 4 && np > 4)
-    fwd_item<(MG_FWD_QMAX > 4 ? 8 : 4), WITH_H>(src, g, r, prec, p0, np, cell, out4, cnt_out, sm, lane);
+    fwd_item<(MG_FWD_QMAX > 6 ? 8 : (MG_FWD_QMAX > 4 ? 6 : 4)), WITH_H>(src, g, r, prec, p0, np, cell, out4, cnt_out,
+                                                                        sm, lane);
   else if (np > 2)
     fwd_item<4, WITH_H>(src, g, r, prec, p0, np, cell, out4, cnt_out, sm, lane);
   else if (np == 2)

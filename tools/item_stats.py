@@ -55,7 +55,7 @@ def main():
     for q in (1, 2, 4, 8):
         items = np.sum(np.ceil(pc / q))
         print(f"fwd items at Q={q}: {items:.0f}, mean pts/item {ps[-1] / items:.2f}")
-    # k-runs of c adjacent cells merged into one item when their points fit Q=8
+    # k-runs of c adjacent cells merged into one item when their points fit 8 points
     P3 = pc.reshape(g * g, g)
     for c in (2, 4):
         items = 0

@@ -461,18 +461,25 @@ def recon_desk64():
     if not os.path.exists(path):
         return None
     cloud, ts, grids, cfg, tgt = load_recon_fixture(path)
-    tr = Trainer(cloud, ts, cfg, slice_grids=grids, graph=True)
-    try:
-        vol, t_train, t_total = reconstruct(tr, tgt.dims, tgt.first, tgt.last, tgt.intensity_scale)
-    finally:
-        tr.close()
+    runs = []
+    for _ in range(2):  # cold (first in the process: lazy kernel loading), then warm
+        tr = Trainer(cloud, ts, cfg, slice_grids=grids, graph=True)
+        try:
+            runs.append(reconstruct(tr, tgt.dims, tgt.first, tgt.last, tgt.intensity_scale))
+        finally:
+            tr.close()
+        del tr
+        torch.cuda.empty_cache()
+    (vol, t_train, t_total), cold = runs[1], runs[0]
     db = psnr(vol.astype(np.float64), tgt.gt.astype(np.float64))
-    del tr
-    torch.cuda.empty_cache()
+    assert np.array_equal(vol, cold[0]), "reconstruction is not deterministic"
     return {"workload": f"desk64: 64^3 nested-ellipsoids, 3 stacks x 16 slices at 4 mm, {cfg.total_iters} iters, "
                         f"lattice {cfg.resolution_schedule[0][1]}^3 -> {cfg.final_resolution}^3, NRF@"
                         f"{cfg.nrf_activation_iter}, batch {cfg.batch_points} + SSIM slice",
             "train_seconds": t_train, "seconds_incl_volume": t_total, "psnr_db": db,
+            "train_seconds_cold": cold[1],
+            "timing": "second of two identical runs in the process (the first, cold, pays lazy CUDA module "
+                      "loading and first graph captures); both give the bit-identical volume",
             "reference_psnr_db": tgt.ref_psnr_db, "reference_train_seconds": tgt.ref_seconds,
             "reference_threads": tgt.ref_threads}
 

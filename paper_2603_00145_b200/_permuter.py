@@ -9,7 +9,9 @@ will make before its next epoch boundary, computes the permutation into a
 memory-mapped buffer and reports the generator state just before and just
 after it.  The trainer adopts the result only if its own state at the boundary
 equals the reported pre-state, so the batch sequence is bit-identical to
-drawing the permutation inline; on any mismatch it draws inline.
+drawing the permutation inline; on any mismatch, or when the result is not
+ready at the boundary (the trainer never waits for the helper), it draws
+inline.
 
 Two buffer slots alternate: the permutation in use stays valid while the
 helper fills the other one.
@@ -19,6 +21,7 @@ from __future__ import annotations
 
 import os
 import pickle
+import select
 import subprocess
 import sys
 import tempfile
@@ -62,16 +65,28 @@ class EpochPermuter:
         self._proc = subprocess.Popen([sys.executable, "-m", "paper_2603_00145_b200._permuter", self._path,
                                        str(self.m)], stdin=subprocess.PIPE, stdout=subprocess.PIPE, env=env)
         self._pending = None  # slot being filled
+        self._stale = False  # a result nobody will take is still on its way
         self._slot = 0
+        self.adopted = 0  # epochs served from the helper
 
     def _recv(self):
         return pickle.load(self._proc.stdout)
 
+    def _ready(self):
+        """A response can be read without blocking (at most one is ever in
+        flight, so nothing is left in the reader's buffer between responses)."""
+        return bool(select.select([self._proc.stdout], [], [], 0.0)[0])
+
     def request(self, rng, integer_calls):
         """Start computing the permutation that follows the given further
-        ``rng.integers(n)`` draws (one n per call) from rng's current state."""
-        if self._pending is not None:
-            self._recv()  # drop a stale result
+        ``rng.integers(n)`` draws (one n per call) from rng's current state.
+        Skipped (the trainer then draws that epoch inline) while the helper is
+        still busy with an earlier request."""
+        if self._pending is not None or self._stale:
+            if not self._ready():
+                return
+            self._recv()  # drop the stale result
+            self._pending, self._stale = None, False
         self._slot ^= 1
         self._pending = self._slot
         pickle.dump((self._slot, rng.bit_generator.state, list(integer_calls)), self._proc.stdin)
@@ -83,6 +98,9 @@ class EpochPermuter:
         if self._pending is None:
             return None
         slot, self._pending = self._pending, None
+        if not self._ready():  # not done yet (e.g. the helper is still starting): draw inline
+            self._stale = True
+            return None
         try:
             pre, post = self._recv()
         except Exception:
@@ -90,6 +108,7 @@ class EpochPermuter:
         if pre != rng.bit_generator.state:
             return None
         rng.bit_generator.state = post
+        self.adopted += 1
         return self._slots[slot]
 
     def close(self):

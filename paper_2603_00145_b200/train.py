@@ -557,6 +557,11 @@ class Trainer:
             self._bufs.idx_host = [torch.empty((b_total,), dtype=torch.int64, pin_memory=True) for _ in range(2)]
             self._bufs.idx_done = [None, None]
             self._bufs.slot = 0
+            # device landing slots for the H2D copies, which run on a copy
+            # stream under the previous step; the step itself reads B.idx
+            # (a fixed address for the graph), filled by a short D2D copy
+            self._bufs.idx_stage = [dv.empty((b_total,), torch.int64) for _ in range(2)]
+            self._bufs.stage_free = [None, None]
             # two pinned loss-readback slots (pipelined steps read one while the next fills)
             self._bufs.scalars_host = [torch.empty((4,), dtype=torch.float64, pin_memory=True) for _ in range(2)]
             self._bufs.err_host = [torch.empty((1,), dtype=torch.int32, pin_memory=True) for _ in range(2)]
@@ -578,11 +583,26 @@ class Trainer:
         if B.idx_done[k] is not None:
             B.idx_done[k].synchronize()  # the slot's previous H2D copy has landed
         np.copyto(B.idx_host[k].numpy(), all_idx, casting="unsafe")
-        B.idx.copy_(B.idx_host[k], non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record()
+        cur = torch.cuda.current_stream()
+        cs = self._copy_stream()
+        if B.stage_free[k] is not None:
+            cs.wait_event(B.stage_free[k])  # the D2D that read this landing slot has run
+        with torch.cuda.stream(cs):
+            B.idx_stage[k].copy_(B.idx_host[k], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(cs)
         B.idx_done[k] = ev
+        cur.wait_event(ev)
+        B.idx.copy_(B.idx_stage[k], non_blocking=True)
+        free = torch.cuda.Event()
+        free.record(cur)
+        B.stage_free[k] = free
         return B
+
+    def _copy_stream(self):
+        if getattr(self, "_h2d_stream", None) is None:
+            self._h2d_stream = torch.cuda.Stream()
+        return self._h2d_stream
 
     def _body(self, B, nb, hw):
         N.check(N.lib().mg_gather_batch(N.ptr(B.idx), B.idx.numel(), N.ptr(self.src_coords), N.ptr(self.src_sids),

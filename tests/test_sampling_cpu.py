@@ -2,6 +2,8 @@
 next-epoch permutation drawn ahead in the helper process must give exactly
 the batch / slice sequence of drawing it inline, across several epochs."""
 
+import time
+
 import numpy as np
 
 from paper_2603_00145_b200 import train as T
@@ -16,11 +18,13 @@ def _sampler(seed, m, b, prefetch, monkeypatch):
     return t
 
 
-def _draw(t, steps):
+def _draw(t, steps, pause=0.0):
     out = []
-    for _ in range(steps):
+    for i in range(steps):
         idx = t._next_batch()
         out.append((idx.copy(), int(t.rng.integers(len(t.slice_grids)))))
+        if pause:  # let the helper finish (it is never waited for)
+            time.sleep(2.0 if i == 0 else pause)
     return out
 
 
@@ -29,9 +33,19 @@ def test_prefetched_permutations_match_inline(monkeypatch):
     a = _draw(_sampler(3, m, b, False, monkeypatch), 25)
     t = _sampler(3, m, b, True, monkeypatch)
     try:
-        got = _draw(t, 25)
+        got = _draw(t, 25, pause=0.05)
+        assert t._permuter.adopted >= 3  # the prefetch path was exercised
+        # a trainer that outruns its helper draws inline, with the same result
+        t2 = _sampler(3, m, b, True, monkeypatch)
+        try:
+            got2 = _draw(t2, 25)
+        finally:
+            t2.close()
     finally:
         t.close()
+    for (ia, ja), (ib, jb) in zip(a, got2):
+        np.testing.assert_array_equal(ia, ib)
+        assert ja == jb
     for (ia, ja), (ib, jb) in zip(a, got):
         np.testing.assert_array_equal(ia, ib)
         assert ja == jb

@@ -398,20 +398,22 @@ def run_ours(args):
                          f"fwd+bwd incl. host epilogue",
                "value_1thread": v1, "sample_1thread": f"{npts1} batch points ({p1} pairs, {dt1:.1f} s)"}
     graph_used = tr._graph is not None
+    tr.close()
+    del tr
+    torch.cuda.empty_cache()
+    infer = None
+    if not args.no_inference:
+        try:
+            infer = inference_c5()
+        except Exception as exc:  # report, never fail the training bench
+            infer = {"error": repr(exc)[:200]}
+        torch.cuda.empty_cache()
     recon = None
     if not args.no_recon and rank == 0:
         try:
             recon = recon_desk64()
         except Exception as exc:
             recon = {"error": repr(exc)[:200]}
-    infer = None
-    if not args.no_inference:
-        try:
-            del tr
-            torch.cuda.empty_cache()
-            infer = inference_c5()
-        except Exception as exc:  # report, never fail the training bench
-            infer = {"error": repr(exc)[:200]}
     bytes_h2d = int(steps_idx[0].numel() * 8)
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -306,7 +306,7 @@ int mg_forward(const void* grec, int64_t n_gauss, const int32_t* gstart, int64_t
   int* nitems = w.take<int>(1);
   if (!w.ok) return fail("mg_forward: workspace too small");
   if (ns == 0) return 0;
-  build_items_cells(pstart, ncell_of(g), fwd_qmax(), items, nitems, st, fwd_dense_min());
+  build_items_cells(pstart, (int)g, fwd_qmax(), items, nitems, st, fwd_dense_min());
   launch_forward(with_h != 0, (const float*)grec, n_gauss, gstart, (int)g, (int)r, (const float4*)prec, pkey_sorted,
                  pstart,
                  items, nitems, ns, (float4*)out4, counts, st);

@@ -227,45 +227,6 @@ __device__ __noinline__ Window make_window(int cell, int g, int r) {
   return w;
 }
 
-// Fills s_start[0..127], s_pre[0..128] for columns [c0, c0+128); returns total.
-__device__ __forceinline__ int build_segments(const Window& w, int c0, int g, const int* __restrict__ starts,
-                                              int* s_start, int* s_pre, int lane) {
-  int st[4], ln[4], sum = 0;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    int col = c0 + lane * 4 + k;
-    st[k] = 0;
-    ln[k] = 0;
-    if (col < w.ncol) {
-      int ii = w.ilo + col / w.nj;
-      int jj = w.jlo + col % w.nj;
-      int base = (ii * g + jj) * g;
-      int a = __ldg(starts + base + w.klo);
-      int b = __ldg(starts + base + w.khi + 1);
-      st[k] = a;
-      ln[k] = b - a;
-    }
-    sum += ln[k];
-  }
-  int tot;
-  int off = warp_excl_scan(sum, lane, &tot);
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    s_start[lane * 4 + k] = st[k];
-    s_pre[lane * 4 + k] = off;
-    off += ln[k];
-  }
-  if (lane == 31) s_pre[128] = tot;
-  __syncwarp();
-  return tot;
-}
-
-// Monotone virtual-index -> element map within the current segment batch.
-__device__ __forceinline__ int seg_lookup(int v, int& s, const int* s_start, const int* s_pre) {
-  while (v >= s_pre[s + 1]) ++s;
-  return s_start[s] + (v - s_pre[s]);
-}
-
 // ---------------------------------------------------------------------------
 // Bitmap segment cursor.  For a batch of <= 128 columns the candidate list is
 // the concatenation of the non-empty column segments.  Each warp keeps, in
@@ -278,8 +239,6 @@ __device__ __forceinline__ int seg_lookup(int v, int& s, const int* s_start, con
 constexpr int kBmWords = 128;  // window of 4096 flattened indices
 
 struct SegSmem {
-  int start[128];
-  int pre[132];
   int delta[128];
   uint32_t bits[kBmWords];
   __align__(16) float pts[3][8];  // an item's sub-points, coordinate-major (pairs load as 64-bit)
@@ -329,12 +288,9 @@ __device__ __noinline__ LaneSegs build_lane_segs_t(const Window& w, int c0, int 
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     L.pre[k] = off;
-    sm.start[lane * 4 + k] = L.st[k];
-    sm.pre[lane * 4 + k] = off;
     if (L.len[k] > 0) sm.delta[e++] = L.st[k] - off;
     off += L.len[k];
   }
-  if (lane == 31) sm.pre[128] = tot;
   L.nonempty_before = nbefore;
   L.tot = tot;
   return L;
@@ -423,17 +379,21 @@ __device__ __forceinline__ void write_point_out(float4* __restrict__ out4, int* 
 // operands.  Every sub-point of an item shares the exact candidate set, so
 // contributor_counts is the item's total candidate count.
 // ---------------------------------------------------------------------------
+// One CTA per SM: all resident warps take consecutive (neighbouring-cell)
+// items, so their candidate windows overlap in L1 (3 CTAs x 8 warps ran
+// three unrelated regions per SM: forward 0.584 -> 0.552 ms, backward
+// 0.598 -> 0.560 ms at C2).
 #ifndef MG_FWD_MINB
-#define MG_FWD_MINB 3
+#define MG_FWD_MINB 1
 #endif
 #ifndef MG_BWD_MINB
-#define MG_BWD_MINB 3
+#define MG_BWD_MINB 1
 #endif
 #ifndef MG_FWD_QMAX
 #define MG_FWD_QMAX 6  // up to 6 sub-points per item: Q=8 spills at 80 registers (C2: 0.618 -> 0.593 ms)
 #endif
 #ifndef MG_FWD_WARPS
-#define MG_FWD_WARPS 8
+#define MG_FWD_WARPS 24
 #endif
 #ifndef MG_FWD_IPF
 #define MG_FWD_IPF 1  // prefetch the next work item's record while this one runs
@@ -445,7 +405,7 @@ __device__ __forceinline__ void write_point_out(float4* __restrict__ out4, int* 
 #define MG_BWD_PAIR_GPACK 1  // pair items: Gaussian-packed f32x2 (points broadcast)
 #endif
 #ifndef MG_BWD_WARPS
-#define MG_BWD_WARPS 8
+#define MG_BWD_WARPS 16
 #endif
 constexpr int kFwdWarps = MG_FWD_WARPS;
 
@@ -726,8 +686,8 @@ __device__ __forceinline__ void fwd_item_dense(const GaussSoA& grec, const int* 
                                                int lane) {
   // lane owns points lane (lo half) and lane + 32 (hi half); staged adjacently
   // in shared memory so each coordinate pair reloads as one 64-bit value
-  static_assert(sizeof(SegSmem::start) + sizeof(SegSmem::pre) >= 3 * 64 * sizeof(float), "dense staging");
-  float* buf = reinterpret_cast<float*>(sm.start);  // 3 x 64 floats in start[] + pre[] (unused on this path)
+  static_assert(sizeof(SegSmem::delta) + sizeof(SegSmem::bits) >= 3 * 64 * sizeof(float), "dense staging");
+  float* buf = reinterpret_cast<float*>(sm.delta);  // 3 x 64 floats in delta[] + bits[] (unused on this path)
   {
     const float4 a = prec[p0 + min(lane, np - 1)];
     const float4 b = prec[p0 + min(lane + 32, np - 1)];
@@ -794,8 +754,9 @@ __global__ void __launch_bounds__(kFwdWarps * 32, MG_FWD_MINB) forward_kernel(co
   __shared__ SegSmem s_seg[kFwdWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nitems = *nitems_dev;
-  const int stride = gridDim.x * kFwdWarps;
-  int it = blockIdx.x * kFwdWarps + warp;
+  const int nw = blockDim.x >> 5;  // kFwdWarps, or 8 for small launches
+  const int stride = gridDim.x * nw;
+  int it = blockIdx.x * nw + warp;
   int4 next = (MG_FWD_IPF && it < nitems) ? items[it] : make_int4(0, 0, 0, 0);
   for (; it < nitems; it += stride) {
     const int4 item = MG_FWD_IPF ? next : items[it];  // {first, cell, count, 0}
@@ -1204,7 +1165,7 @@ __device__ __forceinline__ void bwd_pair_item(const GaussSoA grec, int j, int ce
 }
 
 #ifndef MG_BWD_PAIR_MINB
-#define MG_BWD_PAIR_MINB 2  // two Gaussians' accumulators: 126 registers, no spills (3 spills ~350 B)
+#define MG_BWD_PAIR_MINB 1  // 16 warps x 1 CTA: two Gaussians' accumulators need ~122 registers
 #endif
 template <bool PAIR>
 __global__ void __launch_bounds__(kBwdWarps * 32, PAIR ? MG_BWD_PAIR_MINB : MG_BWD_MINB) backward_kernel(const GaussSoA grec,
@@ -1218,10 +1179,11 @@ __global__ void __launch_bounds__(kBwdWarps * 32, PAIR ? MG_BWD_PAIR_MINB : MG_B
   __shared__ SegSmem s_seg[kBwdWarps];
   __shared__ int2 s_thr[PAIR ? kBwdWarps : 1][128];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;  // kBwdWarps, or 8 for small launches
   // implicit pair items: sorted Gaussians (2j, 2j+1)
   if (PAIR && items == nullptr) {
     const int npairs = (n_implicit + 1) >> 1;
-    for (int it = blockIdx.x * kBwdWarps + warp; it < npairs; it += gridDim.x * kBwdWarps) {
+    for (int it = blockIdx.x * nw + warp; it < npairs; it += gridDim.x * nw) {
       const int j = 2 * it;
       const int ca = (int)gkey[j];
       const int cb = j + 1 < n_implicit ? (int)gkey[j + 1] : -1;
@@ -1241,8 +1203,8 @@ __global__ void __launch_bounds__(kBwdWarps * 32, PAIR ? MG_BWD_PAIR_MINB : MG_B
   auto load_item = [&](int j) {
     return items ? items[j] : make_int4(j, (int)gkey[j], -1, 0);
   };
-  const int stride = gridDim.x * kBwdWarps;
-  int it = blockIdx.x * kBwdWarps + warp;
+  const int stride = gridDim.x * nw;
+  int it = blockIdx.x * nw + warp;
   int4 next = (MG_BWD_IPF && it < nitems) ? load_item(it) : make_int4(0, 0, 0, 0);
   for (; it < nitems; it += stride) {
     const int4 item = MG_BWD_IPF ? next : load_item(it);  // {first, cell, count, 0}
@@ -1610,15 +1572,18 @@ size_t items_workspace_bytes(int64_t n) { return 2 * (((size_t)n * 4 + 255) & ~(
 // One pass over cells: each occupied cell appends its ceil(count / q) item
 // records with one warp-aggregated atomic per warp.  Item ORDER only affects
 // scheduling (every item's arithmetic is self-contained), and cells are
-// visited in index order, so neighbouring warps still get neighbouring cells.
-__global__ void cell_items_kernel(const int* __restrict__ starts, int64_t ncell, int q, int dense_min,
+// visited in index order, so neighbouring warps get neighbouring cells (a
+// 2 x 2 x 8-cell tiled visiting order measured the same).
+__global__ void cell_items_kernel(const int* __restrict__ starts, int g, int q, int dense_min,
                                   int4* __restrict__ items, int* __restrict__ nitems) {
   const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t c0 = (int64_t)blockIdx.x * blockDim.x; c0 < ncell; c0 += stride) {
-    const int64_t c = c0 + threadIdx.x;
+  const int64_t nvisit = (int64_t)g * g * g;
+  for (int64_t t0 = (int64_t)blockIdx.x * blockDim.x; t0 < nvisit; t0 += stride) {
+    const int64_t t = t0 + threadIdx.x;
+    const int64_t c = t < nvisit ? t : -1;
     int s = 0, e = 0;
-    if (c < ncell) {
+    if (c >= 0) {
       s = starts[c];
       e = starts[c + 1];
     }
@@ -1637,14 +1602,14 @@ __global__ void cell_items_kernel(const int* __restrict__ starts, int64_t ncell,
   }
 }
 
-void build_items_cells(const int* starts, int64_t ncell, int q, int4* items, int* nitems, cudaStream_t st,
-                       int dense_min) {
+void build_items_cells(const int* starts, int g, int q, int4* items, int* nitems, cudaStream_t st, int dense_min) {
   cudaMemsetAsync(nitems, 0, sizeof(int), st);
-  if (ncell <= 0) return;
+  if (g <= 0) return;
+  const int64_t ncell = (int64_t)g * g * g;
   int64_t blocks = (ncell + 255) / 256;
   const int64_t cap = (int64_t)num_sms() * 8;
   if (blocks > cap) blocks = cap;
-  MG_LAUNCH(cell_items_kernel<<<(unsigned)blocks, 256, 0, st>>>(starts, ncell, q, dense_min, items, nitems));
+  MG_LAUNCH(cell_items_kernel<<<(unsigned)blocks, 256, 0, st>>>(starts, g, q, dense_min, items, nitems));
 }
 
 void build_items(const uint32_t* keys, const int* starts, int64_t n, int q, int4* items, int* nitems, void* ws,
@@ -1662,6 +1627,13 @@ void build_items(const uint32_t* keys, const int* starts, int64_t n, int q, int4
                                                              nitems));
 }
 
+// Warps per CTA for a persistent pair-kernel launch: the full one-CTA-per-SM
+// shape when every SM gets >= 8 items per warp, else 8-warp CTAs (several
+// per SM), so small launches (early reconstruction levels) still cover all SMs.
+static int block_warps(int full, int64_t items) {
+  return items >= (int64_t)num_sms() * full * 8 ? full : 8;
+}
+
 template <class K>
 static int64_t persistent_blocks(K kernel, int threads, int64_t max_blocks, size_t dyn_smem = 0) {
   int per_sm = 0;
@@ -1676,12 +1648,13 @@ void launch_forward(bool with_h, const float* grec_raw, int64_t n_gauss, const i
                     const uint32_t* pkey, const int* pstart, const int4* items, const int* nitems, int64_t max_items,
                     float4* out4, int* cnt, cudaStream_t st) {
   if (max_items <= 0) return;
-  const int64_t want = (max_items + kFwdWarps - 1) / kFwdWarps;
+  const int nw = block_warps(kFwdWarps, max_items / 2);  // ~2+ sub-points per item
+  const int64_t want = (max_items + nw - 1) / nw;
   const GaussSoA grec = gauss_soa(grec_raw, n_gauss);
   auto k = with_h ? forward_kernel<true> : forward_kernel<false>;
-  const unsigned blocks = (unsigned)persistent_blocks(k, kFwdWarps * 32, want);
+  const unsigned blocks = (unsigned)persistent_blocks(k, nw * 32, want);
   constexpr size_t smem = 0;
-  MG_LAUNCH(k<<<blocks, kFwdWarps * 32, smem, st>>>(grec, gstart, g, r, prec, pkey, pstart, items, nitems, out4, cnt));
+  MG_LAUNCH(k<<<blocks, nw * 32, smem, st>>>(grec, gstart, g, r, prec, pkey, pstart, items, nitems, out4, cnt));
 }
 
 size_t staged_smem_bytes() { return sizeof(float4) * kSbCap + sizeof(SegSmem) * kSbS + sizeof(StageSmem); }
@@ -1745,9 +1718,10 @@ void launch_backward(const float* grec_raw, int64_t n_gauss, const uint32_t* gke
   if (max_items <= 0) return;
   const GaussSoA grec = gauss_soa(grec_raw, n_gauss);
   const bool pairs = pair_mode > 0 && items == nullptr;
-  const int64_t want = (max_items + kBwdWarps - 1) / kBwdWarps;
+  const int nw = block_warps(kBwdWarps, pairs ? (max_items + 1) / 2 : max_items);
+  const int64_t want = (max_items + nw - 1) / nw;
   auto k = pairs ? backward_kernel<true> : backward_kernel<false>;
-  MG_LAUNCH(k<<<(unsigned)persistent_blocks(k, kBwdWarps * 32, want), kBwdWarps * 32, 0, st>>>(
+  MG_LAUNCH(k<<<(unsigned)persistent_blocks(k, nw * 32, want), nw * 32, 0, st>>>(
       grec, gkey, gstart, g, r, prec, pstart, items, nitems, (int)n_gauss, acc10));
 }
 

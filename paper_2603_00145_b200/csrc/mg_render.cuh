@@ -19,7 +19,7 @@ void launch_points_prepare(const double* coords, const int64_t* sids64, const in
                            int nslices, int g, uint32_t* keys, float4* xf, double* xout, cudaStream_t st);
 void launch_points_gather(const float4* xf, const int* perm, int64_t n, float4* prec, int* inv, cudaStream_t st);
 size_t items_workspace_bytes(int64_t n);
-void build_items_cells(const int* starts, int64_t ncell, int q, int4* items, int* nitems, cudaStream_t st,
+void build_items_cells(const int* starts, int g, int q, int4* items, int* nitems, cudaStream_t st,
                        int dense_min = 0);
 void build_items(const uint32_t* keys, const int* starts, int64_t n, int q, int4* items, int* nitems, void* ws,
                  cudaStream_t st, int dense_min = 0);

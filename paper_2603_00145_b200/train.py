@@ -35,6 +35,61 @@ from .render import SlicePSF, sample_volume_device
 DEFAULT_SCHEDULE = ((0, 70), (500, 100), (1000, 130), (2000, 165), (3000, 200))
 
 
+_GC_FROZEN = False
+_STREAMS = {}
+
+
+def _graph_pool():
+    """One private memory pool for every step graph on the device.  Only one
+    step graph is alive at a time (a new shape drops the old graph first), so
+    a capture reuses the blocks its predecessor released instead of freeing
+    them and allocating fresh ones (cudaFree/cudaMalloc: 0.05-0.17 s per
+    recapture at the reconstruction's lattice milestones)."""
+    key = ("graph_pool", dv.device())
+    ent = _STREAMS.get(key)
+    if ent is None:
+        # a pool lives while some graph captured into it does: a one-op keeper
+        # graph holds it across the gaps between step graphs
+        h = torch.cuda.graph_pool_handle()
+        keeper = torch.cuda.CUDAGraph()
+        cs = _stream("capture")
+        cs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cs):
+            keeper.capture_begin(pool=h)
+            torch.zeros((1,), device=dv.device())
+            keeper.capture_end()
+        ent = _STREAMS[key] = (h, keeper)
+    return ent[0]
+
+
+def _stream(name):
+    """Process-wide side streams (copy / capture / parallel branch), shared by
+    all trainers on the device: a fresh stream per trainer pays new cuBLAS
+    workspaces and handles on its first use (up to 0.3 s at the NRF switch)."""
+    key = (name, dv.device())
+    st = _STREAMS.get(key)
+    if st is None:
+        st = _STREAMS[key] = torch.cuda.Stream(device=dv.device())
+    return st
+
+
+def _freeze_gc_once():
+    """Move everything alive at the first Trainer construction (torch, numpy
+    and the caller's module state: several hundred thousand objects) out of
+    the cyclic collector's reach.  A full collection over them took 0.1-0.4 s
+    and landed at random inside the step loop (measured as 0.3 s stalls in a
+    0.7 s desk-scale reconstruction).  Objects created later are collected as
+    usual.  MGAUSS_GC_FREEZE=0 disables this."""
+    global _GC_FROZEN
+    if _GC_FROZEN or os.environ.get("MGAUSS_GC_FREEZE", "1") == "0":
+        return
+    import gc
+
+    gc.collect()
+    gc.freeze()
+    _GC_FROZEN = True
+
+
 _PERM_PREFETCH_MIN = 1 << 16  # pools from this size draw epoch permutations ahead
 
 
@@ -245,6 +300,7 @@ class Trainer:
     def __init__(self, cloud, transforms: TransformSet, config: TrainConfig, slice_grids=None,
                  slice_psf: SlicePSF | None = None, graph=False, dist=None):
         config.validate()
+        _freeze_gc_once()
         if config.use_ssim and not slice_grids:
             raise ValueError("use_ssim requires slice sample grids")
         self.config = config
@@ -600,9 +656,7 @@ class Trainer:
         return B
 
     def _copy_stream(self):
-        if getattr(self, "_h2d_stream", None) is None:
-            self._h2d_stream = torch.cuda.Stream()
-        return self._h2d_stream
+        return _stream("h2d")
 
     def _body(self, B, nb, hw):
         N.check(N.lib().mg_gather_batch(N.ptr(B.idx), B.idx.numel(), N.ptr(self.src_coords), N.ptr(self.src_sids),
@@ -642,13 +696,11 @@ class Trainer:
         capture after a large prior allocation, i.e. most of a desk-scale
         reconstruction's wall time across its milestone re-captures)."""
         cur = torch.cuda.current_stream()
-        if getattr(self, "_cap_stream", None) is None:
-            self._cap_stream = torch.cuda.Stream()
-        cs = self._cap_stream
+        cs = _stream("capture")
         cs.wait_stream(cur)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.stream(cs):
-            g.capture_begin()
+            g.capture_begin(pool=_graph_pool())
             try:
                 fn()
             finally:
@@ -794,9 +846,7 @@ class Trainer:
             self._nrf_adam(*ng)
 
     def _side_stream(self):
-        if getattr(self, "_side", None) is None:
-            self._side = torch.cuda.Stream(device=dv.device())
-        return self._side
+        return _stream("side")
 
     def _centre_points(self, B, bt, t):
         """Transformed (un-shifted) sample positions for the NRF (train.py:414-419)."""

@@ -19,8 +19,26 @@ def main():
     ap.add_argument("--repeat", type=int, default=2)
     ap.add_argument("--cprofile", type=int, default=-1, help="cProfile this run index")
     ap.add_argument("--phases", type=int, default=1, help="synchronised timing of milestone phases")
+    ap.add_argument("--nogc", type=int, default=0, help="disable the Python cyclic GC")
     a = ap.parse_args()
     import torch
+
+    import gc
+
+    if a.nogc:
+        gc.disable()
+    gc_log = []
+    gc_t = {}
+
+    def _gc_cb(phase, info):
+        if phase == "start":
+            gc_t["t"] = time.perf_counter()
+        else:
+            dt = time.perf_counter() - gc_t.get("t", time.perf_counter())
+            if dt > 0.005:
+                gc_log.append((info["generation"], round(dt, 4), info["collected"]))
+
+    gc.callbacks.append(_gc_cb)
 
     from paper_2603_00145_b200.recon import load_recon_fixture
     from paper_2603_00145_b200.train import Trainer
@@ -72,6 +90,9 @@ def main():
         if phase_log:
             print(f"run {rep}: phases > 5 ms", phase_log, flush=True)
             phase_log.clear()
+        print(f"run {rep}: gc collections > 5 ms (gen, s, collected) {gc_log}; tracked objects "
+              f"{len(gc.get_objects())}, frozen {gc.get_freeze_count()}", flush=True)
+        gc_log.clear()
         tr.close()
         del tr
 

@@ -392,6 +392,10 @@ __device__ __forceinline__ void write_point_out(float4* __restrict__ out4, int* 
 #ifndef MG_FWD_QMAX
 #define MG_FWD_QMAX 6  // up to 6 sub-points per item: Q=8 spills at 80 registers (C2: 0.618 -> 0.593 ms)
 #endif
+#ifndef MG_FWD_GPL1_QP
+#define MG_FWD_GPL1_QP 4  // items with >= this many point pairs take one candidate per lane per window:
+                          // two per lane (two record loads in flight) measured 3% faster up to Q = 6
+#endif
 #ifndef MG_FWD_WARPS
 #define MG_FWD_WARPS 24
 #endif
@@ -519,9 +523,9 @@ __device__ __forceinline__ void fwd_item(const Src& src, int g, int r, const flo
                                          int np, int cell, float4* __restrict__ out4, int* __restrict__ cnt_out,
                                          SegSmem& sm, int lane) {
   constexpr int QP = Q / 2;
-  // candidates per lane per window: with >= 2 point pairs there are already
-  // >= 2 independent chains per candidate, so one suffices; with one pair, take two.
-  constexpr int GPL = QP >= 2 ? 1 : 2;
+  // candidates per lane per window: two, so two record loads are in flight
+  // per lane (the loop is L1/L2-latency bound), unless QP >= MG_FWD_GPL1_QP.
+  constexpr int GPL = QP >= MG_FWD_GPL1_QP ? 1 : 2;
   constexpr int WIN = 32 * GPL;
   // stage the item's sub-points coordinate-major in shared memory and read
   // them back as 64-bit pairs: the f32x2 operands then sit in aligned

@@ -2,23 +2,26 @@
 
 The reference draws every epoch's sample order with ``rng.permutation(m)`` on
 the trainer's generator (train.py:332-347).  For a multi-million-sample pool
-that is ~0.1 s of host time per epoch, more than a whole GPU step.  Here a
+that is ~0.05 s of host time per epoch, more than a whole GPU step.  Here a
 helper process (``python -m paper_2603_00145_b200._permuter``: numpy only, no
-CUDA) takes a copy of the generator state, replays the RNG calls the trainer
-will make before its next epoch boundary, computes the permutation into a
-memory-mapped buffer and reports the generator state just before and just
-after it.  The trainer adopts the result only if its own state at the boundary
-equals the reported pre-state, so the batch sequence is bit-identical to
-drawing the permutation inline; on any mismatch, or when the result is not
-ready at the boundary (the trainer never waits for the helper), it draws
-inline.
+CUDA) keeps a copy of the generator, replays the RNG calls the trainer will
+make between epoch boundaries (one ``integers(n)`` slice pick per step),
+computes each permutation into a memory-mapped slot and reports the generator
+state just before and just after it.  The helper runs TWO epochs ahead of the
+trainer, so a permutation has a whole epoch of GPU steps to be computed in.
+The trainer adopts a permutation only if its own generator state at the
+boundary equals the reported pre-state, so the batch sequence is bit-identical
+to drawing inline; on any mismatch (an RNG call the schedule did not predict)
+it draws inline and restarts the chain, and while the helper is still starting
+up it draws inline rather than wait.
 
-Two buffer slots alternate: the permutation in use stays valid while the
-helper fills the other one.
+Three slots rotate: the permutation in use, the next one, and the one being
+computed.
 """
 
 from __future__ import annotations
 
+import collections
 import os
 import pickle
 import select
@@ -28,10 +31,13 @@ import tempfile
 
 import numpy as np
 
+NSLOTS = 3
+
 
 def _serve(path, m):
-    slots = np.memmap(path, dtype=np.int64, mode="r+", shape=(2, m))
+    slots = np.memmap(path, dtype=np.int64, mode="r+", shape=(NSLOTS, m))
     inp, out = sys.stdin.buffer, sys.stdout.buffer
+    rng = None
     while True:
         try:
             msg = pickle.load(inp)
@@ -39,9 +45,11 @@ def _serve(path, m):
             break
         if msg is None:
             break
-        slot, state, calls = msg
-        rng = np.random.Generator(getattr(np.random, state["bit_generator"])())
-        rng.bit_generator.state = state
+        kind, slot, calls = msg[0], msg[1], msg[2]
+        if kind == "init":
+            state = msg[3]
+            rng = np.random.Generator(getattr(np.random, state["bit_generator"])())
+            rng.bit_generator.state = state
         for n in calls:
             rng.integers(n)
         pre = rng.bit_generator.state
@@ -51,61 +59,97 @@ def _serve(path, m):
 
 
 class EpochPermuter:
-    """Prefetches ``rng.permutation(m)`` for the trainer's next epoch."""
+    """Prefetches ``rng.permutation(m)`` two epochs ahead of the trainer."""
 
     def __init__(self, m):
         self.m = int(m)
         d = "/dev/shm" if os.path.isdir("/dev/shm") else None
         fd, self._path = tempfile.mkstemp(prefix="mgauss_perm_", dir=d)
         os.close(fd)
-        self._slots = np.memmap(self._path, dtype=np.int64, mode="w+", shape=(2, self.m))
+        self._slots = np.memmap(self._path, dtype=np.int64, mode="w+", shape=(NSLOTS, self.m))
         env = dict(os.environ)
         pkg_parent = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
         env["PYTHONPATH"] = pkg_parent + (os.pathsep + env["PYTHONPATH"] if env.get("PYTHONPATH") else "")
         self._proc = subprocess.Popen([sys.executable, "-m", "paper_2603_00145_b200._permuter", self._path,
                                        str(self.m)], stdin=subprocess.PIPE, stdout=subprocess.PIPE, env=env)
-        self._pending = None  # slot being filled
-        self._stale = False  # a result nobody will take is still on its way
-        self._slot = 0
+        self._queue = collections.deque()  # slots of requested permutations, oldest first
+        self._stale = 0  # responses still to come for abandoned requests
+        self._next_slot = 0
+        self._answered = False  # the helper has finished starting up (answered once)
         self.adopted = 0  # epochs served from the helper
 
-    def _recv(self):
-        return pickle.load(self._proc.stdout)
-
+    # -- transport -----------------------------------------------------------
     def _ready(self):
-        """A response can be read without blocking (at most one is ever in
-        flight, so nothing is left in the reader's buffer between responses)."""
+        """A response can be read without blocking (responses are written
+        whole and read one at a time, so none is left buffered between)."""
         return bool(select.select([self._proc.stdout], [], [], 0.0)[0])
 
-    def request(self, rng, integer_calls):
-        """Start computing the permutation that follows the given further
-        ``rng.integers(n)`` draws (one n per call) from rng's current state.
-        Skipped (the trainer then draws that epoch inline) while the helper is
-        still busy with an earlier request."""
-        if self._pending is not None or self._stale:
-            if not self._ready():
-                return
-            self._recv()  # drop the stale result
-            self._pending, self._stale = None, False
-        self._slot ^= 1
-        self._pending = self._slot
-        pickle.dump((self._slot, rng.bit_generator.state, list(integer_calls)), self._proc.stdin)
+    def _recv(self):
+        out = pickle.load(self._proc.stdout)
+        self._answered = True
+        return out
+
+    def _send(self, msg):
+        pickle.dump(msg, self._proc.stdin)
         self._proc.stdin.flush()
 
+    def _slot(self):
+        s = self._next_slot
+        self._next_slot = (s + 1) % NSLOTS
+        return s
+
+    def _drain(self):
+        """Drop stale responses that have arrived; True once none are left."""
+        while self._stale and self._ready():
+            self._recv()
+            self._stale -= 1
+        return self._stale == 0
+
+    def _abandon(self):
+        self._stale += len(self._queue)
+        self._queue.clear()
+
+    # -- trainer interface ---------------------------------------------------
+    @property
+    def chained(self):
+        """Requests are outstanding (the helper's generator follows the trainer's)."""
+        return bool(self._queue)
+
+    def start(self, rng, calls_next, calls_after):
+        """(Re)start the chain from rng's current state: the permutation after
+        the ``integers(n)`` draws ``calls_next``, then the one after the further
+        draws ``calls_after``.  Skipped while stale responses are in flight."""
+        if not self._drain():
+            return
+        s = self._slot()
+        self._send(("init", s, list(calls_next), rng.bit_generator.state))
+        self._queue.append(s)
+        self.extend(calls_after)
+
+    def extend(self, calls):
+        """Queue the permutation that follows the last requested one and the
+        further draws ``calls``."""
+        s = self._slot()
+        self._send(("next", s, list(calls)))
+        self._queue.append(s)
+
     def take(self, rng):
-        """The prefetched permutation if it was drawn from rng's current
-        state (rng then advances past it), else None."""
-        if self._pending is None:
+        """The oldest requested permutation if it was drawn from rng's current
+        state (rng then advances past it), else None (the chain is dropped)."""
+        if not self._queue:
             return None
-        slot, self._pending = self._pending, None
-        if not self._ready():  # not done yet (e.g. the helper is still starting): draw inline
-            self._stale = True
+        if not self._answered and not self._ready():
+            # still starting up (importing numpy): draw inline rather than wait
+            self._abandon()
             return None
+        slot = self._queue.popleft()
         try:
             pre, post = self._recv()
         except Exception:
+            self._abandon()
             return None
         if pre != rng.bit_generator.state:
+            self._abandon()
             return None
         rng.bit_generator.state = post
         self.adopted += 1

@@ -396,6 +396,13 @@ __device__ __forceinline__ void write_point_out(float4* __restrict__ out4, int* 
 #define MG_FWD_GPL1_QP 4  // items with >= this many point pairs take one candidate per lane per window:
                           // two per lane (two record loads in flight) measured 3% faster up to Q = 6
 #endif
+#ifndef MG_FWD_SCHED
+#define MG_FWD_SCHED 1  // CTA-contiguous item ranges + shared-counter hand-out (0: fixed stride)
+#endif
+#ifndef MG_BWD_SCHED
+#define MG_BWD_SCHED 0  // off: a pair's cost follows the local point density, so static CTA ranges
+                        // leave a long tail (C2 backward 0.56 -> 0.90 ms)
+#endif
 #ifndef MG_FWD_WARPS
 #define MG_FWD_WARPS 24
 #endif
@@ -758,6 +765,29 @@ __global__ void __launch_bounds__(kFwdWarps * 32, MG_FWD_MINB) forward_kernel(co
   __shared__ SegSmem s_seg[kFwdWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nitems = *nitems_dev;
+#if MG_FWD_SCHED
+  // CTA-contiguous item range, items handed to warps by a shared counter:
+  // the CTA's warps stay on neighbouring cells (L1 reuse) and balance
+  // dynamically (a warp's share is no longer a fixed stride of items)
+  __shared__ int s_next;
+  if (threadIdx.x == 0) s_next = 0;
+  __syncthreads();
+  const int per = (nitems + gridDim.x - 1) / gridDim.x;
+  const int beg = blockIdx.x * per, end = min(nitems, beg + per);
+  auto grab = [&]() {
+    int t = 0;
+    if (lane == 0) t = atomicAdd(&s_next, 1);
+    return beg + __shfl_sync(MG_FULL, t, 0);
+  };
+  int it = grab();
+  int nx = it < end ? grab() : end;
+  int4 next = (MG_FWD_IPF && it < end) ? items[it] : make_int4(0, 0, 0, 0);
+  while (it < end) {
+    const int4 item = MG_FWD_IPF ? next : items[it];  // {first, cell, count, 0}
+    if (MG_FWD_IPF && nx < end) next = items[nx];  // loads under this item
+    it = nx;
+    nx = it < end ? grab() : end;
+#else
   const int nw = blockDim.x >> 5;  // kFwdWarps, or 8 for small launches
   const int stride = gridDim.x * nw;
   int it = blockIdx.x * nw + warp;
@@ -765,6 +795,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32, MG_FWD_MINB) forward_kernel(co
   for (; it < nitems; it += stride) {
     const int4 item = MG_FWD_IPF ? next : items[it];  // {first, cell, count, 0}
     if (MG_FWD_IPF && it + stride < nitems) next = items[it + stride];  // loads under this item
+#endif
     const int p0 = item.x, cell = item.y;
     if (kFwdDenseMin > 0 && item.z > MG_FWD_QMAX) {
       fwd_item_dense<WITH_H>(grec, gstart, g, r, prec, p0, item.z, cell, out4, cnt_out, s_seg[warp], lane);
@@ -1187,7 +1218,21 @@ __global__ void __launch_bounds__(kBwdWarps * 32, PAIR ? MG_BWD_PAIR_MINB : MG_B
   // implicit pair items: sorted Gaussians (2j, 2j+1)
   if (PAIR && items == nullptr) {
     const int npairs = (n_implicit + 1) >> 1;
+#if MG_BWD_SCHED
+    // CTA-contiguous pair range handed out by a shared counter (see forward_kernel)
+    __shared__ int s_next;
+    if (threadIdx.x == 0) s_next = 0;
+    __syncthreads();
+    const int per = (npairs + gridDim.x - 1) / gridDim.x;
+    const int beg = blockIdx.x * per, end = min(npairs, beg + per);
+    for (;;) {
+      int t = 0;
+      if (lane == 0) t = atomicAdd(&s_next, 1);
+      const int it = beg + __shfl_sync(MG_FULL, t, 0);
+      if (it >= end) break;
+#else
     for (int it = blockIdx.x * nw + warp; it < npairs; it += gridDim.x * nw) {
+#endif
       const int j = 2 * it;
       const int ca = (int)gkey[j];
       const int cb = j + 1 < n_implicit ? (int)gkey[j + 1] : -1;

@@ -388,15 +388,21 @@ class Trainer:
         # copy the batch out before the helper may refill the old slot
         out = np.concatenate(picked) if len(picked) > 1 else picked[0].copy()
         if drew and m >= _PERM_PREFETCH_MIN and os.environ.get("MGAUSS_PERM_PREFETCH", "1") != "0":
-            # the draws before the next epoch boundary: this step's slice pick
-            # and one per full step still served by the current permutation
-            q = (m - self._cursor) // b
-            calls = [len(self.slice_grids)] * (1 + q) if self.config.use_ssim else []
+            # RNG draws between epoch boundaries: this step's slice pick and one
+            # per full step still served by the current permutation; the next
+            # epoch starts with cursor b - ((m - cursor) % b)
+            ns = [len(self.slice_grids)] if self.config.use_ssim else []
+            calls_e = ns * (1 + (m - self._cursor) // b)
+            c_next = b - (m - self._cursor) % b
+            calls_next = ns * (1 + (m - c_next) // b)
             if self._permuter is None:
                 from ._permuter import EpochPermuter
 
                 self._permuter = EpochPermuter(m)
-            self._permuter.request(self.rng, calls)
+            if self._permuter.chained:  # the next epoch is queued: queue the one after it
+                self._permuter.extend(calls_next)
+            else:
+                self._permuter.start(self.rng, calls_e, calls_next)
         return out
 
     def _apply_milestones(self):

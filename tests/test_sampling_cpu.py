@@ -34,7 +34,10 @@ def test_prefetched_permutations_match_inline(monkeypatch):
     t = _sampler(3, m, b, True, monkeypatch)
     try:
         got = _draw(t, 25, pause=0.05)
-        assert t._permuter.adopted >= 3  # the prefetch path was exercised
+        # 25 x 1536 draws from a 5000-sample pool cross 7 epoch boundaries; the
+        # first is drawn inline (the helper is still starting), the rest come
+        # from the helper's two-ahead chain
+        assert t._permuter.adopted >= 5
         # a trainer that outruns its helper draws inline, with the same result
         t2 = _sampler(3, m, b, True, monkeypatch)
         try:

@@ -168,12 +168,18 @@ __global__ void __launch_bounds__(kVolWarps * 32) volume_kernel(const GaussSoA g
 #endif
 
 #ifndef MG_VOL_TZ
-#define MG_VOL_TZ 4  // runs per tile along k (2 x 2 x TZ cells; TZ / 2 cells per warp)
+#define MG_VOL_TZ 6  // runs per tile along k: 2 x 2 x 6 cells over 12 warps, 2 CTAs (2 x 104 KB) per SM
+                     // (2 x 2 x 4 over 8 warps: 130 ms at C5; this shape: 116 ms)
+#endif
+#ifndef MG_VOL_WARPS
+#define MG_VOL_WARPS 12  // warps per tile CTA; the tile's 2 x 2 x TZ cells are dealt round-robin
 #endif
 constexpr int kTileTZ = MG_VOL_TZ;
-constexpr int kTileCap = kTileTZ == 2 ? 1792 : 2048;   // staged Gaussians per tile
+constexpr int kVolTileWarps = MG_VOL_WARPS;
+// staged Gaussians per tile: the (2 + 2r)^2 x (TZ + 2r) union at one Gaussian per cell (r = 5), rounded up
+constexpr int kTileCap = kTileTZ == 2 ? 1792 : (kTileTZ == 4 ? 2048 : ((144 * (kTileTZ + 10) + 63) / 64) * 64);
 constexpr int kTileCols = 144;   // union columns ((2 + 2r)^2 at r = 5)
-constexpr int kTileK = 16;       // union k-cells + 1 (table width)
+constexpr int kTileK = kTileTZ + 12 > 16 ? kTileTZ + 12 : 16;  // union k-cells + 1 (table width)
 
 struct VolTileSmem {
   float4 A[kTileCap];
@@ -258,7 +264,7 @@ __device__ __forceinline__ void cpa8(void* dst, const void* src) {
                : "memory");
 }
 
-__global__ void __launch_bounds__(256) volume_tile_kernel(const GaussSoA grec, const int* __restrict__ gstart, int g,
+__global__ void __launch_bounds__(kVolTileWarps * 32) volume_tile_kernel(const GaussSoA grec, const int* __restrict__ gstart, int g,
                                                           int r, VolAxes ax, const float* __restrict__ residual,
                                                           float* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char vt_dyn[];
@@ -337,10 +343,10 @@ __global__ void __launch_bounds__(256) volume_tile_kernel(const GaussSoA grec, c
         __syncthreads();
       }
     }
-    // this warp's runs (cells): (x, y) from the warp id, z = (warp & 1) + 2s
+    // this warp's runs (cells) of the tile's 2 x 2 x TZ, dealt round-robin
 #pragma unroll 1
-    for (int s2 = 0; s2 < kTileTZ / 2; ++s2) {
-    const int rx = rx0 + ((warp >> 2) & 1), ry = ry0 + ((warp >> 1) & 1), rz = rz0 + (warp & 1) + 2 * s2;
+    for (int c = warp; c < 4 * kTileTZ; c += kVolTileWarps) {
+    const int rx = rx0 + ((c >> 2) & 1), ry = ry0 + ((c >> 1) & 1), rz = rz0 + (c & 1) + 2 * (c >> 3);
     if (rx < nrx && ry < nry && rz < nrz) {
       const int bx0 = ax.rs[0][rx], nbx = ax.rs[0][rx + 1] - bx0;
       const int by0 = ax.rs[1][ry], nby = ax.rs[1][ry + 1] - by0;
@@ -425,11 +431,11 @@ void launch_sample_volume(const float* grec_raw, int64_t n_gauss, const int* gst
       attr = true;
     }
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, volume_tile_kernel, 256, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, volume_tile_kernel, kVolTileWarps * 32, smem);
     const int64_t tiles = (int64_t)((i1 - i0 + 1) / 2 + 1) * ((n[1] + 1) / 2 + 1) * (n[2] / kTileTZ + 1);
     int64_t tb = (int64_t)num_sms() * (per_sm > 0 ? per_sm : 1);
     if (tb > tiles) tb = tiles;
-    MG_LAUNCH(volume_tile_kernel<<<(unsigned)tb, 256, smem, st>>>(gauss_soa(grec_raw, n_gauss), gstart, g, r, ax,
+    MG_LAUNCH(volume_tile_kernel<<<(unsigned)tb, kVolTileWarps * 32, smem, st>>>(gauss_soa(grec_raw, n_gauss), gstart, g, r, ax,
                                                                    residual, out));
     return;
   }

@@ -399,10 +399,6 @@ __device__ __forceinline__ void write_point_out(float4* __restrict__ out4, int* 
 #ifndef MG_FWD_SCHED
 #define MG_FWD_SCHED 1  // CTA-contiguous item ranges + shared-counter hand-out (0: fixed stride)
 #endif
-#ifndef MG_BWD_SCHED
-#define MG_BWD_SCHED 0  // off: a pair's cost follows the local point density, so static CTA ranges
-                        // leave a long tail (C2 backward 0.56 -> 0.90 ms)
-#endif
 #ifndef MG_FWD_WARPS
 #define MG_FWD_WARPS 24
 #endif
@@ -1218,21 +1214,10 @@ __global__ void __launch_bounds__(kBwdWarps * 32, PAIR ? MG_BWD_PAIR_MINB : MG_B
   // implicit pair items: sorted Gaussians (2j, 2j+1)
   if (PAIR && items == nullptr) {
     const int npairs = (n_implicit + 1) >> 1;
-#if MG_BWD_SCHED
-    // CTA-contiguous pair range handed out by a shared counter (see forward_kernel)
-    __shared__ int s_next;
-    if (threadIdx.x == 0) s_next = 0;
-    __syncthreads();
-    const int per = (npairs + gridDim.x - 1) / gridDim.x;
-    const int beg = blockIdx.x * per, end = min(npairs, beg + per);
-    for (;;) {
-      int t = 0;
-      if (lane == 0) t = atomicAdd(&s_next, 1);
-      const int it = beg + __shfl_sync(MG_FULL, t, 0);
-      if (it >= end) break;
-#else
+    // strided: CTA-contiguous pair ranges (as the forward uses) were much
+    // slower, because a pair's cost follows the local point density; loading
+    // the next pair's keys ahead measured 2% slower (registers)
     for (int it = blockIdx.x * nw + warp; it < npairs; it += gridDim.x * nw) {
-#endif
       const int j = 2 * it;
       const int ca = (int)gkey[j];
       const int cb = j + 1 < n_implicit ? (int)gkey[j + 1] : -1;

@@ -403,7 +403,7 @@ __device__ __forceinline__ void write_point_out(float4* __restrict__ out4, int* 
 #define MG_FWD_WARPS 24
 #endif
 #ifndef MG_FWD_IPF
-#define MG_FWD_IPF 1  // prefetch the next work item's record while this one runs
+#define MG_FWD_IPF 0  // next-item prefetch: was 2% faster at 3 CTAs/SM, is 1.5% slower with the per-CTA hand-out
 #endif
 #ifndef MG_BWD_IPF
 #define MG_BWD_IPF 0  // off: with implicit items the prefetch measured ~2% slower

@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define MG_ABI_VERSION 3
+#define MG_ABI_VERSION 4
 #define MG_EINVAL 1
 
 int mg_abi_version(void);
@@ -166,6 +166,20 @@ int mg_sample_volume(const void *grec, int64_t n_gauss, const int32_t *gstart, i
  * predictions (mean), loss_acc += L (float64 device scalar). */
 int mg_smooth_l1(const float *pred, const float *target, int64_t b, float *upstream_out, double *loss_acc,
                  void *stream);
+/* Residual field r(x) = 0.1 tanh(MLP(enc(x))) with the reference widths
+ * 39-64-64-64-64-1, SiLU, 6 Fourier bands (nrf.py:23-182; ResidualField.forward /
+ * backward).  w[l] are (fan_in, fan_out) row-major float32, bias[l] (fan_out).
+ * Forward: r_out / pred_add (+= r) / t_out = tanh(.) / z_out = 4 x b x 64 hidden
+ * pre-activations (point-major; needed by the backward), each optional except
+ * t_out.  Backward: d_points (b x 3) and the parameter gradients of
+ * sum_b upstream_b r(x_b), deterministic (fixed-order partial sums). */
+int mg_nrf_forward(const float *x, int64_t b, const float *const *w, const float *const *bias, float *pred_add,
+                   float *r_out, float *t_out, float *z_out, void *stream);
+size_t mg_nrf_backward_workspace_bytes(int64_t b);
+int mg_nrf_backward(const float *x, int64_t b, const float *const *w, const float *const *bias,
+                    const float *upstream, const float *t, const float *z, float *d_points, float *const *dw,
+                    float *const *db, void *ws, size_t ws_bytes, void *stream);
+
 /* 2D SSIM (ssim.py:59-122) of an (H,W) slice: upstream_out = scale * d(1-SSIM)/dpred,
  * ssim_sum += sum of the SSIM map over the (H-10)(W-10) valid windows. */
 size_t mg_ssim_workspace_bytes(int64_t h, int64_t w);

@@ -55,6 +55,9 @@ SIGNATURES = {
     "mg_volume_workspace_bytes": (SZ, [I64, I64, I64]),
     "mg_sample_volume": (ctypes.c_int, [P, I64, P, I64, I64, I64, I64, I64, P, P, I64, I64, P, P, P, SZ, P]),
     "mg_smooth_l1": (ctypes.c_int, [P, P, I64, P, P, P]),
+    "mg_nrf_forward": (ctypes.c_int, [P, I64, P, P, P, P, P, P, P]),
+    "mg_nrf_backward_workspace_bytes": (SZ, [I64]),
+    "mg_nrf_backward": (ctypes.c_int, [P, I64, P, P, P, P, P, P, P, P, P, SZ, P]),
     "mg_ssim_workspace_bytes": (SZ, [I64, I64]),
     "mg_ssim_loss_grad": (ctypes.c_int, [P, P, I64, I64, D, P, P, P, SZ, P]),
     "mg_quat_to_rot_f64": (ctypes.c_int, [P, I64, P, P]),
@@ -75,7 +78,7 @@ _lib = None
 _lock = threading.Lock()
 
 
-ABI_VERSION = 3  # include/mgauss_b200.h MG_ABI_VERSION
+ABI_VERSION = 4  # include/mgauss_b200.h MG_ABI_VERSION
 
 
 def load_library(path=LIB_PATH):

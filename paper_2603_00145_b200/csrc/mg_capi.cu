@@ -430,6 +430,25 @@ int mg_smooth_l1(const float* pred, const float* target, int64_t b, float* up_ou
   return cuda_status();
 }
 
+size_t mg_nrf_backward_workspace_bytes(int64_t b) { return b < 0 ? 0 : nrf_backward_ws_bytes(b); }
+
+int mg_nrf_forward(const float* x, int64_t b, const float* const* w, const float* const* bias, float* pred_add,
+                   float* r_out, float* t_out, float* z_out, void* stream) {
+  if (b < 0 || !w || !bias) return fail("mg_nrf_forward: bad arguments");
+  if (b == 0) return 0;
+  launch_nrf_forward(x, b, w, bias, pred_add, r_out, t_out, z_out, S(stream));
+  return cuda_status();
+}
+
+int mg_nrf_backward(const float* x, int64_t b, const float* const* w, const float* const* bias, const float* up,
+                    const float* t, const float* z, float* d_points, float* const* dw, float* const* db, void* ws,
+                    size_t wsb, void* stream) {
+  if (b < 0 || !w || !bias || !dw || !db) return fail("mg_nrf_backward: bad arguments");
+  if (wsb < nrf_backward_ws_bytes(b)) return fail("mg_nrf_backward: workspace too small");
+  launch_nrf_backward(x, b, w, bias, up, t, z, d_points, dw, db, ws, S(stream));
+  return cuda_status();
+}
+
 size_t mg_ssim_workspace_bytes(int64_t h, int64_t w) { return ssim_workspace_bytes((int)h, (int)w); }
 
 int mg_ssim_loss_grad(const float* pred, const float* target, int64_t h, int64_t w, double scale, float* up,

@@ -58,6 +58,13 @@ void launch_transform_grads(const double* dpoints, const double* coords, const i
 size_t transform_grads_ws_bytes(int64_t k);
 void launch_smooth_l1(const float* pred, const float* target, int64_t b, float* up_out, double* loss_acc,
                       cudaStream_t st);
+// fused residual field (mg_nrf.cu)
+size_t nrf_backward_ws_bytes(int64_t b);
+void launch_nrf_forward(const float* x, int64_t b, const float* const* w, const float* const* bias, float* pred_add,
+                        float* r_out, float* t_out, float* z_out, cudaStream_t st);
+void launch_nrf_backward(const float* x, int64_t b, const float* const* w, const float* const* bias, const float* up,
+                         const float* t, const float* z, float* dp, float* const* dw, float* const* db, void* ws,
+                         cudaStream_t st);
 size_t ssim_workspace_bytes(int H, int W);
 void launch_ssim(const float* pred, const float* tgt, int H, int W, double scale, float* up, double* ssim_sum,
                  void* ws, cudaStream_t st);

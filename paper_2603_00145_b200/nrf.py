@@ -10,6 +10,7 @@ Manual backward identical to nrf.py:147-182 (including d/dx into transforms).
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass, field as dc_field
 
 import numpy as np
@@ -94,8 +95,69 @@ def nrf_forward_cached(field: ResidualField, x: torch.Tensor):
 def nrf_forward_device(field: ResidualField, x: torch.Tensor, chunk=1 << 20):
     out = torch.empty(x.shape[0], dtype=torch.float32, device=x.device)
     for lo in range(0, x.shape[0], chunk):
-        out[lo:lo + chunk] = nrf_forward_cached(field, x[lo:lo + chunk])[0]
+        if fused_supported(field):
+            xs = x[lo:lo + chunk].contiguous()
+            t = torch.empty(xs.shape[0], dtype=torch.float32, device=x.device)
+            _fused_forward(field, xs, None, out[lo:lo + chunk], t, None)
+        else:
+            out[lo:lo + chunk] = nrf_forward_cached(field, x[lo:lo + chunk])[0]
     return out
+
+
+# -- fused kernels (csrc/mg_nrf.cu): the reference widths in 4 launches -------
+FUSED_WIDTHS = (39, 64, 64, 64, 64, 1)
+
+
+def fused_supported(field: ResidualField) -> bool:
+    """The fused kernels are written for the reference configuration
+    (6 bands, hidden 64 x 4, output 1, output bound 0.1)."""
+    return (tuple(field.layer_widths) == FUSED_WIDTHS and field.frequency_bands == 6
+            and abs(field.output_bound - 0.1) < 1e-12 and all(w.is_contiguous() for w in field.weights))
+
+
+def _ptr_array(tensors):
+    return (ctypes.c_void_p * len(tensors))(*[t.data_ptr() for t in tensors])
+
+
+def _fused_forward(field, x, pred_add, r_out, t_out, z_out):
+    from . import _native as N
+
+    w, b = _ptr_array(field.weights), _ptr_array(field.biases)
+    N.check(N.lib().mg_nrf_forward(N.ptr(x), x.shape[0], ctypes.addressof(w), ctypes.addressof(b), N.ptr(pred_add),
+                                   N.ptr(r_out), N.ptr(t_out), N.ptr(z_out), dv.sptr()), "nrf_forward")
+
+
+def nrf_forward_fused(field: ResidualField, x: torch.Tensor, pred_add: torch.Tensor | None = None):
+    """nrf_forward_cached on the fused kernel: (r or None, cache).  With
+    ``pred_add`` the residual is added into it in place and r is not returned."""
+    x = x.contiguous()
+    n = x.shape[0]
+    t = torch.empty(n, dtype=torch.float32, device=x.device)
+    z = torch.empty((4, n, 64), dtype=torch.float32, device=x.device)
+    r = None if pred_add is not None else torch.empty(n, dtype=torch.float32, device=x.device)
+    _fused_forward(field, x, pred_add, r, t, z)
+    return r, ("fused", t, z)
+
+
+def nrf_backward_fused(field: ResidualField, x: torch.Tensor, upstream: torch.Tensor, cache):
+    """nrf_backward on the fused kernels: (d_weights, d_biases, d_points)."""
+    from . import _native as N
+
+    _, t, z = cache
+    x = x.contiguous()
+    up = upstream[:x.shape[0]].to(torch.float32).contiguous()
+    n = x.shape[0]
+    L = N.lib()
+    dws = [torch.empty_like(w) for w in field.weights]
+    dbs = [torch.empty_like(b) for b in field.biases]
+    dp = torch.empty((n, 3), dtype=torch.float32, device=x.device)
+    ws = torch.empty((max(1, L.mg_nrf_backward_workspace_bytes(n)),), dtype=torch.uint8, device=x.device)
+    w, b = _ptr_array(field.weights), _ptr_array(field.biases)
+    gw, gb = _ptr_array(dws), _ptr_array(dbs)
+    N.check(L.mg_nrf_backward(N.ptr(x), n, ctypes.addressof(w), ctypes.addressof(b), N.ptr(up), N.ptr(t), N.ptr(z),
+                              N.ptr(dp), ctypes.addressof(gw), ctypes.addressof(gb), N.ptr(ws), ws.numel(),
+                              dv.sptr()), "nrf_backward")
+    return dws, dbs, dp
 
 
 def _split_k(n_rows, parts=128, min_rows=512):

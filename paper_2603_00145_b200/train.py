@@ -791,11 +791,14 @@ class Trainer:
                                     N.ptr(B.pred), None, N.ptr(B.pairs), st), "finish")
         nrf_cache = None
         if self.nrf_active:
-            from .nrf import nrf_forward_cached
+            from .nrf import fused_supported, nrf_forward_cached, nrf_forward_fused
 
             xc = self._centre_points(B, bt, t)
-            res, nrf_cache = nrf_forward_cached(self.nrf, xc)
-            B.pred.add_(res)
+            if fused_supported(self.nrf) and os.environ.get("MGAUSS_NRF_FUSED", "1") != "0":
+                _, nrf_cache = nrf_forward_fused(self.nrf, xc, pred_add=B.pred)  # pred += r in the kernel
+            else:
+                res, nrf_cache = nrf_forward_cached(self.nrf, xc)
+                B.pred.add_(res)
         # losses (train.py:424-436)
         N.check(L.mg_smooth_l1(N.ptr(B.pred), N.ptr(tgt), nb, N.ptr(B.up), N.ptr(B.scalars[0:1]), st), "smooth_l1")
         if hw is not None:
@@ -825,9 +828,12 @@ class Trainer:
             main.wait_stream(side)
         ng = None
         if nrf_cache is not None:
-            from .nrf import nrf_backward
+            from .nrf import nrf_backward, nrf_backward_fused
 
-            dws, dbs, dp = nrf_backward(self.nrf, self._centre_x, B.up, nrf_cache)
+            if isinstance(nrf_cache[0], str):  # ("fused", t, z)
+                dws, dbs, dp = nrf_backward_fused(self.nrf, self._centre_x, B.up, nrf_cache)
+            else:
+                dws, dbs, dp = nrf_backward(self.nrf, self._centre_x, B.up, nrf_cache)
             ng = (dws, dbs)
             if self.k:
                 dp64 = dp.double().contiguous()

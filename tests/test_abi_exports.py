@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol():
     assert not missing, missing
     # and the ctypes table covers exactly the declared ABI
     assert set(_native.SIGNATURES) == set(declared_symbols())
-    assert lib.mg_abi_version() == _native.ABI_VERSION == 3
+    assert lib.mg_abi_version() == _native.ABI_VERSION == 4
 
 
 def test_library_is_sm100a():

@@ -75,6 +75,12 @@ __device__ __forceinline__ float nrf_dsilu(float z) {
   const float s = nrf_sigmoid(z);
   return s * (1.0f + z * (1.0f - s));
 }
+// silu'(z), with silu(z) = z s as a by-product
+__device__ __forceinline__ float nrf_dsilu_h(float z, float& h) {
+  const float s = nrf_sigmoid(z);
+  h = z * s;
+  return s * (1.0f + z * (1.0f - s));
+}
 
 // acc[jj][q] += sum_k W[k][4jb + jj] * A[k][4pb + 2q .. +1]: A feature-major
 // [K][kNT], W row-major [K][kNH] (one layer of the forward).
@@ -218,7 +224,8 @@ struct NrfBwdSmem {
 __global__ void __launch_bounds__(kNThr) nrf_bwd_kernel(const float* __restrict__ x, int64_t b, NrfParams P,
                                                         const float* __restrict__ up, const float* __restrict__ tin,
                                                         const float* __restrict__ z, float* __restrict__ dz,
-                                                        float* __restrict__ d4g, float* __restrict__ dp) {
+                                                        float* __restrict__ d4g, float* __restrict__ dp,
+                                                        float* __restrict__ hout, float* __restrict__ encout) {
   extern __shared__ __align__(16) unsigned char nrf_dyn[];
   NrfBwdSmem& sm = *reinterpret_cast<NrfBwdSmem*>(nrf_dyn);
   nrf_load_params(sm.prm, P);
@@ -252,13 +259,16 @@ __global__ void __launch_bounds__(kNThr) nrf_bwd_kernel(const float* __restrict_
         float4 zz = make_float4(0.f, 0.f, 0.f, 0.f);
         if (p < b) zz = *reinterpret_cast<const float4*>(z + ((int64_t)3 * b + p) * kNH + 4 * jb);
         const float d = sm.d4[4 * pb + s];
-        dv[0][s] = d * sm.prm[oW4 + 4 * jb + 0] * nrf_dsilu(zz.x);
-        dv[1][s] = d * sm.prm[oW4 + 4 * jb + 1] * nrf_dsilu(zz.y);
-        dv[2][s] = d * sm.prm[oW4 + 4 * jb + 2] * nrf_dsilu(zz.z);
-        dv[3][s] = d * sm.prm[oW4 + 4 * jb + 3] * nrf_dsilu(zz.w);
-        if (p < b)
+        float4 hh;
+        dv[0][s] = d * sm.prm[oW4 + 4 * jb + 0] * nrf_dsilu_h(zz.x, hh.x);
+        dv[1][s] = d * sm.prm[oW4 + 4 * jb + 1] * nrf_dsilu_h(zz.y, hh.y);
+        dv[2][s] = d * sm.prm[oW4 + 4 * jb + 2] * nrf_dsilu_h(zz.z, hh.z);
+        dv[3][s] = d * sm.prm[oW4 + 4 * jb + 3] * nrf_dsilu_h(zz.w, hh.w);
+        if (p < b) {
           *reinterpret_cast<float4*>(dz + ((int64_t)3 * b + p) * kNH + 4 * jb) =
               make_float4(dv[0][s], dv[1][s], dv[2][s], dv[3][s]);
+          *reinterpret_cast<float4*>(hout + ((int64_t)3 * b + p) * kNH + 4 * jb) = hh;
+        }
       }
 #pragma unroll
       for (int jj = 0; jj < 4; ++jj)
@@ -278,13 +288,16 @@ __global__ void __launch_bounds__(kNThr) nrf_bwd_kernel(const float* __restrict_
         const int64_t p = p0 + 4 * pb + s;
         float4 zz = make_float4(0.f, 0.f, 0.f, 0.f);
         if (p < b) zz = *reinterpret_cast<const float4*>(z + ((int64_t)(l - 1) * b + p) * kNH + 4 * jb);
-        dv[0][s] = acc_at(acc, 0, s) * nrf_dsilu(zz.x);
-        dv[1][s] = acc_at(acc, 1, s) * nrf_dsilu(zz.y);
-        dv[2][s] = acc_at(acc, 2, s) * nrf_dsilu(zz.z);
-        dv[3][s] = acc_at(acc, 3, s) * nrf_dsilu(zz.w);
-        if (p < b)
+        float4 hh;
+        dv[0][s] = acc_at(acc, 0, s) * nrf_dsilu_h(zz.x, hh.x);
+        dv[1][s] = acc_at(acc, 1, s) * nrf_dsilu_h(zz.y, hh.y);
+        dv[2][s] = acc_at(acc, 2, s) * nrf_dsilu_h(zz.z, hh.z);
+        dv[3][s] = acc_at(acc, 3, s) * nrf_dsilu_h(zz.w, hh.w);
+        if (p < b) {
           *reinterpret_cast<float4*>(dz + ((int64_t)(l - 1) * b + p) * kNH + 4 * jb) =
               make_float4(dv[0][s], dv[1][s], dv[2][s], dv[3][s]);
+          *reinterpret_cast<float4*>(hout + ((int64_t)(l - 1) * b + p) * kNH + 4 * jb) = hh;
+        }
       }
 #pragma unroll
       for (int jj = 0; jj < 4; ++jj)
@@ -306,11 +319,17 @@ __global__ void __launch_bounds__(kNThr) nrf_bwd_kernel(const float* __restrict_
       const int p = tid & (kNT - 1), c = tid >> 6;
       if (p0 + p < b) {
         const float xc = sm.xs[p][c];
+        float* er = encout + (p0 + p) * (kNE + 1);  // the encoding row, for the dW pass
+        er[c] = xc;
+        if (c == 0) er[kNE] = 0.f;
         float v = sm.denc[c][p];
         for (int band = 0; band < kNBands; ++band) {
           const float f = ldexpf(3.14159265358979323846f, band);
           const float s = xc * f;
-          v += f * (cosf(s) * sm.denc[3 + 6 * band + c][p] - sinf(s) * sm.denc[3 + 6 * band + 3 + c][p]);
+          const float sn = sinf(s), cs = cosf(s);
+          er[3 + 6 * band + c] = sn;
+          er[3 + 6 * band + 3 + c] = cs;
+          v += f * (cs * sm.denc[3 + 6 * band + c][p] - sn * sm.denc[3 + 6 * band + 3 + c][p]);
         }
         dp[(p0 + p) * 3 + c] = v;
       }
@@ -325,106 +344,65 @@ struct NrfDwSmem {
 
 // blockIdx.y = layer (0..3: 64-wide deltas; 4: output layer); each CTA sums
 // chunks blockIdx.x, blockIdx.x + gridDim.x, ... into one partial:
-// part[l] = [gridDim.x][kin * 64 + 64] (dW row-major, then db).
-__global__ void __launch_bounds__(kNThr) nrf_dw_kernel(const float* __restrict__ x, int64_t b,
-                                                       const float* __restrict__ z, const float* __restrict__ dz,
+// part[l] = [gridDim.x][kin * 64 + 64] (dW row-major, then db).  The layer
+// inputs come from the backward pass (enc rows, h = SiLU(z) rows), so staging
+// is a plain copy.
+__global__ void __launch_bounds__(kNThr) nrf_dw_kernel(int64_t b, const float* __restrict__ enc,
+                                                       const float* __restrict__ h, const float* __restrict__ dz,
                                                        const float* __restrict__ d4g, float* __restrict__ part) {
   extern __shared__ __align__(16) unsigned char nrf_dyn[];
   NrfDwSmem& sm = *reinterpret_cast<NrfDwSmem*>(nrf_dyn);
   const int l = blockIdx.y, tid = threadIdx.x;
   const int64_t nchunks = (b + kNChunk - 1) / kNChunk;
   const int G = gridDim.x;
-  // partial offsets: layers 0..3 hold kin * 64 + 64 floats per CTA, layer 4 holds 65
   const int64_t sz0 = kNE * kNH + kNH, sz = kNH * kNH + kNH;
-  float* out = part + (l == 0 ? 0 : G * (sz0 + (int64_t)(l - 1) * sz)) + (int64_t)blockIdx.x * (l == 0 ? sz0 : (l < 4 ? sz : 65));
-  if (l == 4) {  // dW4[j] = sum_p silu(z3[p][j]) d4[p]; db4 = sum_p d4[p] (staged like the other layers)
-    float s = 0.f, sb = 0.f;
-    for (int64_t c = blockIdx.x; c < nchunks; c += G) {
-      const int64_t q0 = c * kNChunk;
-      const int n = (int)min((int64_t)kNChunk, b - q0);
-      __syncthreads();
-      constexpr int kPer = kNChunk * kNH / kNThr;
-      {
-        float zv[kPer];
-#pragma unroll
-        for (int u = 0; u < kPer; ++u) {
-          const int e = tid + u * kNThr, p = e / kNH, i = e - p * kNH;
-          zv[u] = z[((int64_t)3 * b + q0 + min(p, n - 1)) * kNH + i];
-        }
-#pragma unroll
-        for (int u = 0; u < kPer; ++u) {
-          const int e = tid + u * kNThr, p = e / kNH, i = e - p * kNH;
-          sm.a[p][i] = zv[u];
-        }
-      }
-#pragma unroll 1
-      for (int u = 0; u < kPer; ++u) {
-        const int e = tid + u * kNThr, p = e / kNH, i = e - p * kNH;
-        sm.a[p][i] = p < n ? nrf_silu(sm.a[p][i]) : 0.f;
-      }
-      if (tid < kNChunk) sm.d[tid][0] = tid < n ? d4g[q0 + tid] : 0.f;
-      __syncthreads();
-      if (tid < kNH) {
-        for (int p = 0; p < n; ++p) s = fmaf(sm.a[p][tid], sm.d[p][0], s);
-      } else if (tid == kNH) {
-        for (int p = 0; p < n; ++p) sb += sm.d[p][0];
-      }
-    }
-    if (tid < kNH) out[tid] = s;
-    if (tid == kNH) out[kNH] = sb;
-    return;
-  }
+  float* out = part + (l == 0 ? 0 : G * (sz0 + (int64_t)(l - 1) * sz)) +
+               (int64_t)blockIdx.x * (l == 0 ? sz0 : (l < 4 ? sz : 65));
   const int kin = l == 0 ? kNE : kNH;
+  const int astride = l == 0 ? kNE + 1 : kNH;  // floats per A row in global memory
+  const float* A = l == 0 ? enc : h + (int64_t)(l == 4 ? 3 : l - 1) * b * kNH;
   const int ib = tid >> 4, jb = tid & 15;
   f2 acc[4][2];
 #pragma unroll
   for (int ii = 0; ii < 4; ++ii) acc[ii][0] = acc[ii][1] = bc2(0.f);
   f2 dba[2] = {bc2(0.f), bc2(0.f)};
+  float s4 = 0.f, sb4 = 0.f;
   for (int64_t c = blockIdx.x; c < nchunks; c += G) {
     const int64_t q0 = c * kNChunk;
     const int n = (int)min((int64_t)kNChunk, b - q0);
     __syncthreads();
-    // staging: all of a thread's 32 element loads are issued before any use
-    // (a load-use loop was latency-bound), raw values go to shared memory,
-    // and the activation / encoding pass runs as a rolled loop (compact code)
-    constexpr int kPer = kNChunk * kNH / kNThr;
-    {
-      float dv[kPer], zv[kPer];
+    {  // A rows (astride floats each, 16-byte pieces) and delta rows, all loads issued first
+      constexpr int kA = kNChunk * kNH / 4 / kNThr;  // float4 pieces per thread (64-wide rows)
+      float4 av[kA], dv[kA];
 #pragma unroll
-      for (int u = 0; u < kPer; ++u) {
-        const int e = tid + u * kNThr, p = e / kNH, i = e - p * kNH;
+      for (int u = 0; u < kA; ++u) {
+        const int e = tid + u * kNThr, p = e / (kNH / 4), i4 = e - p * (kNH / 4);
         const int64_t q = q0 + min(p, n - 1);
-        dv[u] = dz[((int64_t)l * b + q) * kNH + i];
-        zv[u] = l > 0 ? z[((int64_t)(l - 1) * b + q) * kNH + i] : 0.f;
+        av[u] = 4 * i4 < astride ? *reinterpret_cast<const float4*>(A + q * astride + 4 * i4)
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+        dv[u] = l < 4 ? *reinterpret_cast<const float4*>(dz + ((int64_t)l * b + q) * kNH + 4 * i4)
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
       }
 #pragma unroll
-      for (int u = 0; u < kPer; ++u) {
-        const int e = tid + u * kNThr, p = e / kNH, i = e - p * kNH;
-        sm.a[p][i] = zv[u];
-        sm.d[p][i] = p < n ? dv[u] : 0.f;
+      for (int u = 0; u < kA; ++u) {
+        const int e = tid + u * kNThr, p = e / (kNH / 4), i4 = e - p * (kNH / 4);
+        const bool ok = p < n;
+        *reinterpret_cast<float4*>(&sm.a[p][4 * i4]) = ok ? av[u] : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (l < 4) *reinterpret_cast<float4*>(&sm.d[p][4 * i4]) = ok ? dv[u] : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-    }
-#pragma unroll 1
-    for (int u = 0; u < kPer; ++u) {
-      const int e = tid + u * kNThr, p = e / kNH, i = e - p * kNH;
-      float av = 0.f;
-      if (p < n) {
-        if (l == 0) {
-          if (i < kNE) {
-            const int64_t q = q0 + p;
-            const float xv[3] = {x[q * 3 + 0], x[q * 3 + 1], x[q * 3 + 2]};
-            av = nrf_enc(xv, i);
-          }
-        } else {
-          av = nrf_silu(sm.a[p][i]);
-        }
-      }
-      sm.a[p][i] = av;
+      if (l == 4 && tid < kNChunk) sm.d[tid][0] = tid < n ? d4g[q0 + tid] : 0.f;  // only column 0 is used
     }
     __syncthreads();
+    if (l == 4) {  // dW4[j] = sum_p h3[p][j] d4[p]; db4 = sum_p d4[p]
+      if (tid < kNH) {
+        for (int p = 0; p < n; ++p) s4 = fmaf(sm.a[p][tid], sm.d[p][0], s4);
+      } else if (tid == kNH) {
+        for (int p = 0; p < n; ++p) sb4 += sm.d[p][0];
+      }
+      continue;
+    }
     if (4 * ib < kin) {
-      // padded rows (p >= n) are zero, so the loop runs over the whole chunk
-      // in groups of 8 points with all loads issued ahead of the FFMA2s
+      // padded rows (p >= n) are zero, so groups of 8 points may run past n
 #pragma unroll 1
       for (int p0 = 0; p0 < n; p0 += 8) {
         float4 a[8];
@@ -452,6 +430,11 @@ __global__ void __launch_bounds__(kNThr) nrf_dw_kernel(const float* __restrict__
         }
       }
     }
+  }
+  if (l == 4) {
+    if (tid < kNH) out[tid] = s4;
+    if (tid == kNH) out[kNH] = sb4;
+    return;
   }
 #pragma unroll
   for (int ii = 0; ii < 4; ++ii) {
@@ -500,8 +483,9 @@ size_t nrf_backward_ws_bytes(int64_t b) {
   const size_t sz0 = kNE * kNH + kNH, sz = kNH * kNH + kNH;
   const size_t part = (size_t)G * (sz0 + 3 * sz + 65) * sizeof(float);
   const size_t dz = (size_t)4 * b * kNH * sizeof(float), d4 = (size_t)b * sizeof(float);
+  const size_t enc = (size_t)b * (kNE + 1) * sizeof(float);
   auto al = [](size_t v) { return (v + 255) & ~(size_t)255; };
-  return al(dz) + al(d4) + al(part);
+  return 2 * al(dz) + al(d4) + al(enc) + al(part);
 }
 
 static void nrf_attrs() {
@@ -546,12 +530,16 @@ void launch_nrf_backward(const float* x, int64_t b, const float* const* w, const
   p += al((size_t)4 * b * kNH * sizeof(float));
   float* d4 = (float*)p;
   p += al((size_t)b * sizeof(float));
+  float* hb = (float*)p;
+  p += al((size_t)4 * b * kNH * sizeof(float));
+  float* enc = (float*)p;
+  p += al((size_t)b * (kNE + 1) * sizeof(float));
   float* part = (float*)p;
   const size_t smem = sizeof(NrfBwdSmem);
   MG_LAUNCH(nrf_bwd_kernel<<<nrf_tile_grid((const void*)nrf_bwd_kernel, smem, b), kNThr, smem, st>>>(
-      x, b, P, up, t, z, dz, d4, dp));
+      x, b, P, up, t, z, dz, d4, dp, hb, enc));
   const int G = nrf_dw_grid(b);
-  MG_LAUNCH(nrf_dw_kernel<<<dim3(G, 5), kNThr, sizeof(NrfDwSmem), st>>>(x, b, z, dz, d4, part));
+  MG_LAUNCH(nrf_dw_kernel<<<dim3(G, 5), kNThr, sizeof(NrfDwSmem), st>>>(b, enc, hb, dz, d4, part));
   const int64_t total = (kNE * kNH + kNH) + 3 * (kNH * kNH + kNH) + 65;
   MG_LAUNCH(nrf_reduce_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(part, G, Gd));
 }

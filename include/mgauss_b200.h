@@ -180,6 +180,13 @@ int mg_nrf_backward(const float *x, int64_t b, const float *const *w, const floa
                     const float *upstream, const float *t, const float *z, float *d_points, float *const *dw,
                     float *const *db, void *ws, size_t ws_bytes, void *stream);
 
+/* Adam over up to 10 float32 parameter tensors (AdamState.step, train.py:251-271):
+ * reads the device step counter *tstep (float64), uses t = *tstep + 1 for the bias
+ * corrections and stores it back; sizes[k] elements in params[k], grads[k], m[k], v[k]. */
+int mg_nrf_adam(const float *const *grads, float *const *params, float *const *m, float *const *v,
+                const int64_t *sizes, int32_t count, double *tstep, double lr, double beta1, double beta2,
+                double eps, void *stream);
+
 /* 2D SSIM (ssim.py:59-122) of an (H,W) slice: upstream_out = scale * d(1-SSIM)/dpred,
  * ssim_sum += sum of the SSIM map over the (H-10)(W-10) valid windows. */
 size_t mg_ssim_workspace_bytes(int64_t h, int64_t w);

@@ -58,6 +58,7 @@ SIGNATURES = {
     "mg_nrf_forward": (ctypes.c_int, [P, I64, P, P, P, P, P, P, P]),
     "mg_nrf_backward_workspace_bytes": (SZ, [I64]),
     "mg_nrf_backward": (ctypes.c_int, [P, I64, P, P, P, P, P, P, P, P, P, SZ, P]),
+    "mg_nrf_adam": (ctypes.c_int, [P, P, P, P, P, I32, P, D, D, D, D, P]),
     "mg_ssim_workspace_bytes": (SZ, [I64, I64]),
     "mg_ssim_loss_grad": (ctypes.c_int, [P, P, I64, I64, D, P, P, P, SZ, P]),
     "mg_quat_to_rot_f64": (ctypes.c_int, [P, I64, P, P]),

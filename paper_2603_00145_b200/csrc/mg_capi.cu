@@ -449,6 +449,15 @@ int mg_nrf_backward(const float* x, int64_t b, const float* const* w, const floa
   return cuda_status();
 }
 
+int mg_nrf_adam(const float* const* grads, float* const* params, float* const* m, float* const* v,
+                const int64_t* sizes, int32_t count, double* tstep, double lr, double beta1, double beta2, double eps,
+                void* stream) {
+  if (count < 0 || count > 10 || !tstep) return fail("mg_nrf_adam: bad arguments");
+  if (count == 0) return 0;
+  launch_nrf_adam(grads, params, m, v, sizes, count, tstep, lr, beta1, beta2, eps, S(stream));
+  return cuda_status();
+}
+
 size_t mg_ssim_workspace_bytes(int64_t h, int64_t w) { return ssim_workspace_bytes((int)h, (int)w); }
 
 int mg_ssim_loss_grad(const float* pred, const float* target, int64_t h, int64_t w, double scale, float* up,

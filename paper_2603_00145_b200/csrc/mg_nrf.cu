@@ -545,3 +545,51 @@ void launch_nrf_backward(const float* x, int64_t b, const float* const* w, const
 }
 
 }  // namespace mg
+
+namespace mg {
+
+// Adam over the NRF parameter tensors (AdamState.step "nrf", train.py:251-271)
+// in one single-CTA launch: the device step counter is read, used and
+// incremented here so the update replays inside the step graph.
+struct NrfAdamArgs {
+  const float* g[10];
+  float* p[10];
+  float* m[10];
+  float* v[10];
+  int64_t n[10];
+  int count;
+};
+
+__global__ void __launch_bounds__(1024) nrf_adam_kernel(NrfAdamArgs a, double* __restrict__ tstep, float lr,
+                                                        double b1, double b2, float eps) {
+  const double t = *tstep + 1.0;
+  const float bc1 = (float)(1.0 - pow(b1, t)), bc2 = (float)(1.0 - pow(b2, t));
+  const float fb1 = (float)b1, fb2 = (float)b2, a1 = (float)(1.0 - b1), a2 = (float)(1.0 - b2);
+  for (int k = 0; k < a.count; ++k) {
+    const float* __restrict__ g = a.g[k];
+    float* __restrict__ p = a.p[k];
+    float* __restrict__ m = a.m[k];
+    float* __restrict__ v = a.v[k];
+    for (int64_t i = threadIdx.x; i < a.n[k]; i += blockDim.x) {
+      const float gi = g[i];
+      const float mi = m[i] * fb1 + a1 * gi;
+      const float vi = v[i] * fb2 + a2 * gi * gi;
+      m[i] = mi;
+      v[i] = vi;
+      const float den = sqrtf(vi / bc2) + eps;
+      p[i] -= lr * ((mi / bc1) / den);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *tstep = t;
+}
+
+void launch_nrf_adam(const float* const* g, float* const* p, float* const* m, float* const* v, const int64_t* n,
+                     int count, double* tstep, double lr, double b1, double b2, double eps, cudaStream_t st) {
+  NrfAdamArgs a;
+  a.count = count < 10 ? count : 10;
+  for (int k = 0; k < a.count; ++k) a.g[k] = g[k], a.p[k] = p[k], a.m[k] = m[k], a.v[k] = v[k], a.n[k] = n[k];
+  MG_LAUNCH(nrf_adam_kernel<<<1, 1024, 0, st>>>(a, tstep, (float)lr, b1, b2, (float)eps));
+}
+
+}  // namespace mg

@@ -65,6 +65,8 @@ void launch_nrf_forward(const float* x, int64_t b, const float* const* w, const 
 void launch_nrf_backward(const float* x, int64_t b, const float* const* w, const float* const* bias, const float* up,
                          const float* t, const float* z, float* dp, float* const* dw, float* const* db, void* ws,
                          cudaStream_t st);
+void launch_nrf_adam(const float* const* g, float* const* p, float* const* m, float* const* v, const int64_t* n,
+                     int count, double* tstep, double lr, double b1, double b2, double eps, cudaStream_t st);
 size_t ssim_workspace_bytes(int H, int W);
 void launch_ssim(const float* pred, const float* tgt, int H, int W, double scale, float* up, double* ssim_sum,
                  void* ws, cudaStream_t st);

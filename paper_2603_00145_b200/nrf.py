@@ -139,8 +139,9 @@ def nrf_forward_fused(field: ResidualField, x: torch.Tensor, pred_add: torch.Ten
     return r, ("fused", t, z)
 
 
-def nrf_backward_fused(field: ResidualField, x: torch.Tensor, upstream: torch.Tensor, cache):
-    """nrf_backward on the fused kernels: (d_weights, d_biases, d_points)."""
+def nrf_backward_fused(field: ResidualField, x: torch.Tensor, upstream: torch.Tensor, cache, out=None):
+    """nrf_backward on the fused kernels: (d_weights, d_biases, d_points);
+    ``out = (d_weights, d_biases)`` writes the gradients into given tensors."""
     from . import _native as N
 
     _, t, z = cache
@@ -148,8 +149,11 @@ def nrf_backward_fused(field: ResidualField, x: torch.Tensor, upstream: torch.Te
     up = upstream[:x.shape[0]].to(torch.float32).contiguous()
     n = x.shape[0]
     L = N.lib()
-    dws = [torch.empty_like(w) for w in field.weights]
-    dbs = [torch.empty_like(b) for b in field.biases]
+    if out is not None:
+        dws, dbs = list(out[0]), list(out[1])
+    else:
+        dws = [torch.empty_like(w) for w in field.weights]
+        dbs = [torch.empty_like(b) for b in field.biases]
     dp = torch.empty((n, 3), dtype=torch.float32, device=x.device)
     ws = torch.empty((max(1, L.mg_nrf_backward_workspace_bytes(n)),), dtype=torch.uint8, device=x.device)
     w, b = _ptr_array(field.weights), _ptr_array(field.biases)

@@ -830,11 +830,18 @@ class Trainer:
         if nrf_cache is not None:
             from .nrf import nrf_backward, nrf_backward_fused
 
+            # gradients land in one persistent flat buffer (all-reduced with the
+            # step's other partial sums when distributed, then the fused Adam)
+            gv = self._nrf_grad_views()
+            nl = len(self.nrf.weights)
+            gws, gbs = [gv[f"w{i}"] for i in range(nl)], [gv[f"b{i}"] for i in range(nl)]
             if isinstance(nrf_cache[0], str):  # ("fused", t, z)
-                dws, dbs, dp = nrf_backward_fused(self.nrf, self._centre_x, B.up, nrf_cache)
+                _, _, dp = nrf_backward_fused(self.nrf, self._centre_x, B.up, nrf_cache, out=(gws, gbs))
             else:
                 dws, dbs, dp = nrf_backward(self.nrf, self._centre_x, B.up, nrf_cache)
-            ng = (dws, dbs)
+                for dst, src in zip(gws + gbs, dws + dbs):
+                    dst.copy_(src)
+            ng = True
             if self.k:
                 dp64 = dp.double().contiguous()
                 N.check(L.mg_transform_grads(N.ptr(dp64), N.ptr(coords), N.ptr(sids), bt, 1, None, None,
@@ -855,7 +862,7 @@ class Trainer:
                                         self.k, cfg.lr_transform, cfg.adam_beta1, cfg.adam_beta2, cfg.adam_eps,
                                         N.ptr(self.counters[1:2]), st), "transform_adam")
         if ng is not None:
-            self._nrf_adam(*ng)
+            self._nrf_adam()
 
     def _side_stream(self):
         return _stream("side")
@@ -880,42 +887,48 @@ class Trainer:
     def nrf_t(self, value):
         self._nrf_tdev = torch.full((), float(value), dtype=torch.float64, device=dv.device())
 
-    def _nrf_adam(self, dws, dbs):
-        """AdamState.step("nrf", ...) (train.py:251-271) as multi-tensor device
-        ops with a device step counter, so the update replays inside the graph."""
+    def _nrf_grad_views(self):
+        """Persistent flat NRF gradient buffer with one view per parameter."""
+        params = self.nrf.parameter_arrays()
+        key = tuple((k, tuple(v.shape)) for k, v in params.items())
+        if getattr(self, "_nrf_gkey", None) != key:
+            self._nrf_gflat = dv.zeros((sum(v.numel() for v in params.values()),), torch.float32)
+            views, off = {}, 0
+            for k, v in params.items():
+                views[k] = self._nrf_gflat[off:off + v.numel()].view(v.shape)
+                off += v.numel()
+            self._nrf_gviews, self._nrf_gkey = views, key
+        return self._nrf_gviews
+
+    def _nrf_adam(self):
+        """AdamState.step("nrf", ...) (train.py:251-271): one launch over all
+        NRF tensors, with the device step counter read and advanced in the
+        kernel so the update replays inside the graph."""
+        import ctypes
+
         cfg = self.config
-        t = self._nrf_tdev
-        t.add_(1.0)
-        bc1 = (1.0 - torch.pow(cfg.adam_beta1, t)).to(torch.float32)
-        bc2 = (1.0 - torch.pow(cfg.adam_beta2, t)).to(torch.float32)
         params = self.nrf.parameter_arrays()
         keys = list(params)
-        grads = {}
-        for li, (dw, db) in enumerate(zip(dws, dbs)):
-            grads[f"w{li}"], grads[f"b{li}"] = dw, db
-        ps = [params[k] for k in keys]
-        gs = [grads[k] for k in keys]
-        ms = [self.nrf_m[k] for k in keys]
-        vs = [self.nrf_v[k] for k in keys]
-        torch._foreach_mul_(ms, cfg.adam_beta1)
-        torch._foreach_add_(ms, gs, alpha=1.0 - cfg.adam_beta1)
-        torch._foreach_mul_(vs, cfg.adam_beta2)
-        torch._foreach_addcmul_(vs, gs, gs, value=1.0 - cfg.adam_beta2)
-        den = torch._foreach_div(vs, bc2)
-        torch._foreach_sqrt_(den)
-        torch._foreach_add_(den, cfg.adam_eps)
-        num = torch._foreach_div(ms, bc1)
-        torch._foreach_div_(num, den)
-        torch._foreach_mul_(num, cfg.lr_nrf)
-        torch._foreach_sub_(ps, num)
+        gv = self._nrf_grad_views()
+
+        def arr(ts):
+            return (ctypes.c_void_p * len(ts))(*[t.data_ptr() for t in ts])
+
+        ps, gs = arr([params[k] for k in keys]), arr([gv[k] for k in keys])
+        ms, vs = arr([self.nrf_m[k] for k in keys]), arr([self.nrf_v[k] for k in keys])
+        sizes = (ctypes.c_int64 * len(keys))(*[params[k].numel() for k in keys])
+        N.check(N.lib().mg_nrf_adam(ctypes.addressof(gs), ctypes.addressof(ps), ctypes.addressof(ms),
+                                    ctypes.addressof(vs), ctypes.addressof(sizes), len(keys), N.ptr(self._nrf_tdev),
+                                    cfg.lr_nrf, cfg.adam_beta1, cfg.adam_beta2, cfg.adam_eps, dv.sptr()), "nrf_adam")
 
     def _allreduce(self, B):
         """One flat all-reduce(sum) of the step's partial sums (parallel.py)."""
         from .parallel import FlatAllReduce
 
-        key = id(B)
+        nrf_g = self._nrf_gflat if (self.nrf_active and getattr(self, "_nrf_gflat", None) is not None) else None
+        key = (id(B), None if nrf_g is None else id(nrf_g))
         if getattr(self, "_ar_key", None) != key:
-            f32 = [B.acc10]
+            f32 = [B.acc10] + ([nrf_g] if nrf_g is not None else [])
             f64 = [B.scalars] + ([B.g7] if self.k else [])
             self._ar = (FlatAllReduce(f32, self.dist), FlatAllReduce(f64, self.dist))
             self._ar_key = key

@@ -381,7 +381,7 @@ def run_ours(args):
     kt = kernel_times(tr, steps_idx[: min(5, len(steps_idx))], nb, hw)
 
     # --- end to end through the public API: Trainer.step() with host RNG batches (H2D) + loss D2H ---
-    e2e_steps = max(3, args.steps)
+    e2e_steps = max(30, args.steps)  # enough steps that the one-step pipeline fill/drain is amortised
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     p_before = int(B.pairs.item())

@@ -3,8 +3,7 @@
 The reference draws every epoch's sample order with ``rng.permutation(m)`` on
 the trainer's generator (train.py:332-347).  For a multi-million-sample pool
 that is ~0.05 s of host time per epoch, more than a whole GPU step.  Here a
-helper process (``python -m paper_2603_00145_b200._permuter``: numpy only, no
-CUDA) keeps a copy of the generator, replays the RNG calls the trainer will
+helper process (this file run as a script: numpy only, no torch or CUDA) keeps a copy of the generator, replays the RNG calls the trainer will
 make between epoch boundaries (one ``integers(n)`` slice pick per step),
 computes each permutation into a memory-mapped slot and reports the generator
 state just before and just after it.  The helper runs TWO epochs ahead of the
@@ -67,11 +66,10 @@ class EpochPermuter:
         fd, self._path = tempfile.mkstemp(prefix="mgauss_perm_", dir=d)
         os.close(fd)
         self._slots = np.memmap(self._path, dtype=np.int64, mode="w+", shape=(NSLOTS, self.m))
-        env = dict(os.environ)
-        pkg_parent = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-        env["PYTHONPATH"] = pkg_parent + (os.pathsep + env["PYTHONPATH"] if env.get("PYTHONPATH") else "")
-        self._proc = subprocess.Popen([sys.executable, "-m", "paper_2603_00145_b200._permuter", self._path,
-                                       str(self.m)], stdin=subprocess.PIPE, stdout=subprocess.PIPE, env=env)
+        # run this file as a script: numpy only (``-m package._permuter`` would
+        # import the package, i.e. torch, and take seconds to start)
+        self._proc = subprocess.Popen([sys.executable, os.path.abspath(__file__), self._path, str(self.m)],
+                                      stdin=subprocess.PIPE, stdout=subprocess.PIPE)
         self._queue = collections.deque()  # slots of requested permutations, oldest first
         self._stale = 0  # responses still to come for abandoned requests
         self._next_slot = 0

@@ -981,12 +981,12 @@ __device__ __forceinline__ void bwd_store(const Acc& acc, int g0, int ng, float*
 
 
 // ---------------------------------------------------------------------------
-// Pair items (sparse point densities): sorted Gaussians 2j and 2j+1 whose
-// cells are equal or k-adjacent in one (i, j) column share ONE candidate
-// window -- the union of their (2r+1)^3 neighbourhoods, which differs from
-// each by at most one k-cell per column.  Every column also records two
-// element thresholds: elements before `aend` lie in the A-only cell, elements
-// from `bbeg` on in the B-only cell, and the other Gaussian sees those points
+// Pair items: sorted Gaussians 2j and 2j+1 whose cells lie in one (i, j)
+// column at most MG_BWD_PAIR_DMAX k-cells apart share ONE candidate window --
+// the union of their (2r+1)^3 neighbourhoods, which differs from each by dk
+// k-cells per column.  Every column also records two element thresholds:
+// elements before `aend` lie in the A-only cells, elements from `bbeg` on in
+// the B-only cells, and the other Gaussian sees those points
 // with zero upstream -- so each Gaussian still sums over exactly its own
 // candidate set.  Halves the per-item window builds and shares every point
 // load and cursor step between two Gaussians.
@@ -1195,6 +1195,14 @@ __device__ __forceinline__ void bwd_pair_item(const GaussSoA grec, int j, int ce
   bwd_store<2>(acc, j, 2, acc10, lane);
 }
 
+#ifndef MG_BWD_PAIR_DMAX
+// pair Gaussians up to this many k-cells apart in one column: the union
+// window grows by dk cells, still cheaper than two windows.  Training drift
+// empties about half the lattice cells within ~200 steps at C4; with dk <= 1
+// the backward then slowed 2.13 -> 3.30 ms, with dk <= 4 only to 2.28 ms
+// (dk <= 6 and <= 10 measured the same)
+#define MG_BWD_PAIR_DMAX 4
+#endif
 #ifndef MG_BWD_PAIR_MINB
 #define MG_BWD_PAIR_MINB 1  // 16 warps x 1 CTA: two Gaussians' accumulators need ~122 registers
 #endif
@@ -1221,7 +1229,8 @@ __global__ void __launch_bounds__(kBwdWarps * 32, PAIR ? MG_BWD_PAIR_MINB : MG_B
       const int j = 2 * it;
       const int ca = (int)gkey[j];
       const int cb = j + 1 < n_implicit ? (int)gkey[j + 1] : -1;
-      if (cb == ca || (cb == ca + 1 && ca % g != g - 1)) {
+      const int dk = cb - ca;  // cells of one column, dk apart (sorted, so dk >= 0 when cb >= 0)
+      if (cb >= 0 && dk <= MG_BWD_PAIR_DMAX && ca % g + dk <= g - 1) {
         bwd_pair_item(grec, j, ca, cb, g, r, prec, pstart, acc10, s_seg[warp], s_thr[warp], lane);
       } else {
         bwd_item<1>(grec, j, 1, ca, g, r, prec, pstart, acc10, s_seg[warp], lane);

@@ -338,6 +338,14 @@ class Trainer:
         self._perm = None
         self._cursor = 0
         self._permuter = None  # next-epoch permutation prefetch (large pools)
+        b = min(config.batch_points, self.m_points)
+        if (self.m_points >= _PERM_PREFETCH_MIN and b < self.m_points
+                and os.environ.get("MGAUSS_PERM_PREFETCH", "1") != "0"):
+            from ._permuter import EpochPermuter
+
+            # spawned now so its interpreter start-up (~0.5 s) overlaps the
+            # set-up and warm-up instead of the first epochs
+            self._permuter = EpochPermuter(self.m_points)
         self.reports = []
         self._bufs = None
         self._bufs_key = None

@@ -474,9 +474,13 @@ __global__ void nrf_reduce_kernel(const float* __restrict__ part, int G, NrfGrad
   }
 }
 
+#ifndef MG_NRF_DW_G
+#define MG_NRF_DW_G 64
+#endif
 static int nrf_dw_grid(int64_t b) {
   const int64_t nchunks = (b + kNChunk - 1) / kNChunk;
-  return (int)(nchunks < 64 ? (nchunks < 1 ? 1 : nchunks) : 64);
+  const int64_t g = MG_NRF_DW_G;
+  return (int)(nchunks < g ? (nchunks < 1 ? 1 : nchunks) : g);
 }
 
 size_t nrf_backward_ws_bytes(int64_t b) {

@@ -392,6 +392,9 @@ __device__ __forceinline__ void write_point_out(float4* __restrict__ out4, int* 
 #ifndef MG_FWD_QMAX
 #define MG_FWD_QMAX 6  // up to 6 sub-points per item: Q=8 spills at 80 registers (C2: 0.618 -> 0.593 ms)
 #endif
+#ifndef MG_FWD_GPL_Q2
+#define MG_FWD_GPL_Q2 2  // candidates per lane per window for 2-point items (2 or 4)
+#endif
 #ifndef MG_FWD_GPL1_QP
 #define MG_FWD_GPL1_QP 4  // items with >= this many point pairs take one candidate per lane per window:
                           // two per lane (two record loads in flight) measured 3% faster up to Q = 6
@@ -486,6 +489,23 @@ struct Cursor2 {
   }
 };
 
+// Flattened-window cursor for 128-wide windows: lane owns v_i = base + 32 i +
+// lane (i = 0..3), so each warp-wide point load reads 512 contiguous bytes.
+struct Cursor4 {
+  int sbase;
+  __device__ __forceinline__ void next(const SegSmem& sm, int w0, int base, unsigned upto, int lane, int (&v)[4],
+                                       int (&e)[4]) {
+    const int wi = (base - w0) >> 5;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t M = sm.bits[wi + i];
+      v[i] = base + 32 * i + lane;
+      e[i] = v[i] + sm.delta[sbase + __popc(M & upto) - 1];
+      sbase += __popc(M);
+    }
+  }
+};
+
 template <int QP, bool WITH_H>
 __device__ __forceinline__ void fwd_pair_math(const GRec& g, const f2 (&px)[QP], const f2 (&py)[QP],
                                               const f2 (&pz)[QP], f2 (&accI)[QP], f2 (&hx)[QP], f2 (&hy)[QP],
@@ -528,7 +548,7 @@ __device__ __forceinline__ void fwd_item(const Src& src, int g, int r, const flo
   constexpr int QP = Q / 2;
   // candidates per lane per window: two, so two record loads are in flight
   // per lane (the loop is L1/L2-latency bound), unless QP >= MG_FWD_GPL1_QP.
-  constexpr int GPL = QP >= MG_FWD_GPL1_QP ? 1 : 2;
+  constexpr int GPL = QP >= MG_FWD_GPL1_QP ? 1 : (QP == 1 ? MG_FWD_GPL_Q2 : 2);
   constexpr int WIN = 32 * GPL;
   // stage the item's sub-points coordinate-major in shared memory and read
   // them back as 64-bit pairs: the f32x2 operands then sit in aligned
@@ -570,7 +590,7 @@ __device__ __forceinline__ void fwd_item(const Src& src, int g, int r, const flo
           cur.next(sm, w0, base, upto, lane, va, ga);
           if (va < wend) fwd_pair_math<QP, WITH_H>(src.rec(ga), px, py, pz, accI, hx, hy, hz);
         }
-      } else {
+      } else if (GPL == 2) {
         Cursor2 cur{sb0};
         for (int base = w0; base < wend; base += WIN) {
           int va, vb, ga, gb;
@@ -579,6 +599,18 @@ __device__ __forceinline__ void fwd_item(const Src& src, int g, int r, const flo
           const GRec rb = src.rec(vb < wend ? gb : 0);
           if (va < wend) fwd_pair_math<QP, WITH_H>(ra, px, py, pz, accI, hx, hy, hz);
           if (vb < wend) fwd_pair_math<QP, WITH_H>(rb, px, py, pz, accI, hx, hy, hz);
+        }
+      } else {  // four candidates per lane (four record loads in flight)
+        Cursor4 cur{sb0};
+        for (int base = w0; base < wend; base += WIN) {
+          int v[4], e[4];
+          cur.next(sm, w0, base, upto, lane, v, e);
+          GRec rr[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) rr[i] = src.rec(v[i] < wend ? e[i] : 0);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (v[i] < wend) fwd_pair_math<QP, WITH_H>(rr[i], px, py, pz, accI, hx, hy, hz);
         }
       }
       __syncwarp();
@@ -815,23 +847,6 @@ constexpr int kBwdWarps = MG_BWD_WARPS;
 
 struct Pts4 {
   float4 p[4];
-};
-
-// Flattened-window cursor for 128-wide windows: lane owns v_i = base + 32 i +
-// lane (i = 0..3), so each warp-wide point load reads 512 contiguous bytes.
-struct Cursor4 {
-  int sbase;
-  __device__ __forceinline__ void next(const SegSmem& sm, int w0, int base, unsigned upto, int lane, int (&v)[4],
-                                       int (&e)[4]) {
-    const int wi = (base - w0) >> 5;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint32_t M = sm.bits[wi + i];
-      v[i] = base + 32 * i + lane;
-      e[i] = v[i] + sm.delta[sbase + __popc(M & upto) - 1];
-      sbase += __popc(M);
-    }
-  }
 };
 
 template <int QG>

@@ -418,7 +418,7 @@ def run_ours(args):
             traffic = None
     nlaunch = kt.get("launches_per_step")
     cpu = None
-    if world == 1 or rank == 0:
+    if world == 1:  # the CPU baseline is an N = 1 figure (rank 0 alone at N > 1 would only add minutes)
         threads = os.cpu_count() or 1
         v, p, dt, npts = cpu_baseline(tr, data, psf, args.cpu_sample_points, threads)
         v1, p1, dt1, npts1 = cpu_baseline(tr, data, psf, max(1024, args.cpu_sample_points // 16), 1)

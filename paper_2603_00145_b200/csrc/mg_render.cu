@@ -239,8 +239,8 @@ __device__ __noinline__ Window make_window(int cell, int g, int r) {
 constexpr int kBmWords = 128;  // window of 4096 flattened indices
 
 struct SegSmem {
+  uint32_t bits[kBmWords];  // first: pair items alias this struct (PairSmem) and share the bitmap
   int delta[128];
-  uint32_t bits[kBmWords];
   __align__(16) float pts[3][8];  // an item's sub-points, coordinate-major (pairs load as 64-bit)
 };
 
@@ -726,7 +726,7 @@ __device__ __forceinline__ void fwd_item_dense(const GaussSoA& grec, const int* 
   // lane owns points lane (lo half) and lane + 32 (hi half); staged adjacently
   // in shared memory so each coordinate pair reloads as one 64-bit value
   static_assert(sizeof(SegSmem::delta) + sizeof(SegSmem::bits) >= 3 * 64 * sizeof(float), "dense staging");
-  float* buf = reinterpret_cast<float*>(sm.delta);  // 3 x 64 floats in delta[] + bits[] (unused on this path)
+  float* buf = reinterpret_cast<float*>(sm.bits);  // 3 x 64 floats in bits[] + delta[] (unused on this path)
   {
     const float4 a = prec[p0 + min(lane, np - 1)];
     const float4 b = prec[p0 + min(lane + 32, np - 1)];
@@ -1006,13 +1006,26 @@ __device__ __forceinline__ void bwd_store(const Acc& acc, int g0, int ng, float*
 // candidate set.  Halves the per-item window builds and shares every point
 // load and cursor step between two Gaussians.
 // ---------------------------------------------------------------------------
+// Per-warp shared memory of a pair item; aliases SegSmem (the bitmap is the
+// first member of both, so build_window serves either).
+struct PairSmem {
+  uint32_t bits[kBmWords];
+  int4 dt[128];            // per non-empty column segment: {delta, A-only end, B-only start, -} (flattened index)
+  __align__(16) float stage[24];  // the pair's 9 parameter pairs (read back as 64-bit)
+};
+union WarpSmem {
+  SegSmem seg;
+  PairSmem pair;
+};
+static_assert(offsetof(SegSmem, bits) == 0 && offsetof(PairSmem, bits) == 0, "bitmap must alias");
+
 struct PairCols {
   const int* __restrict__ starts;
   int kae, kbs;  // A-only cells [klo, kae), B-only cells [kbs, khi]
 };
 
 __device__ __noinline__ LaneSegs build_lane_segs_pair(const Window& w, int c0, int g, const PairCols cols,
-                                                      SegSmem& sm, int2* thr, int lane) {
+                                                      PairSmem& ps, int lane) {
   LaneSegs L;
   int2 t[4];
   int sum = 0, ne = 0;
@@ -1041,9 +1054,9 @@ __device__ __noinline__ LaneSegs build_lane_segs_pair(const Window& w, int c0, i
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     L.pre[k] = off;
-    if (L.len[k] > 0) {
-      sm.delta[e] = L.st[k] - off;
-      thr[e++] = t[k];
+    if (L.len[k] > 0) {  // {delta, A-only end, B-only start} with thresholds in flattened-index space
+      const int d = L.st[k] - off;
+      ps.dt[e++] = make_int4(d, t[k].x - d, t[k].y - d, 0);
     }
     off += L.len[k];
   }
@@ -1056,17 +1069,16 @@ __device__ __noinline__ LaneSegs build_lane_segs_pair(const Window& w, int c0, i
 // thresholds: m bit 0 = B-only cell (not A's), bit 1 = A-only cell (not B's).
 struct Cursor4P {
   int sbase;
-  __device__ __forceinline__ void next(const SegSmem& sm, const int2* thr, int w0, int base, unsigned upto, int lane,
-                                       int (&v)[4], int (&e)[4], int (&m)[4]) {
+  __device__ __forceinline__ void next(const PairSmem& ps, int w0, int base, unsigned upto, int lane, int (&v)[4],
+                                       int (&e)[4], int (&m)[4]) {
     const int wi = (base - w0) >> 5;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const uint32_t M = sm.bits[wi + i];
+      const uint32_t M = ps.bits[wi + i];
       v[i] = base + 32 * i + lane;
-      const int s = sbase + __popc(M & upto) - 1;
-      e[i] = v[i] + sm.delta[s];
-      const int2 t = thr[s];
-      m[i] = (e[i] >= t.y ? 1 : 0) | (e[i] < t.x ? 2 : 0);
+      const int4 d = ps.dt[sbase + __popc(M & upto) - 1];  // one LDS.128: delta + both thresholds
+      e[i] = v[i] + d.x;
+      m[i] = (v[i] >= d.z ? 1 : 0) | (v[i] < d.y ? 2 : 0);
       sbase += __popc(M);
     }
   }
@@ -1165,10 +1177,10 @@ __device__ __forceinline__ void pair_masked(GaussAcc<2>& acc, const float4& a, c
 
 __device__ __forceinline__ void bwd_pair_item(const GaussSoA grec, int j, int cell_a, int cell_b, int g, int r,
                                               const float4* __restrict__ prec, const int* __restrict__ pstart,
-                                              float* __restrict__ acc10, SegSmem& sm, int2* thr, int lane) {
+                                              float* __restrict__ acc10, PairSmem& ps, int lane) {
 #if MG_BWD_PAIR_GPACK
   GaussPairAcc acc;
-  acc.load(grec, j, j + 1, &sm.pts[0][0], lane);
+  acc.load(grec, j, j + 1, &ps.stage[0], lane);
 #else
   GaussAcc<2> acc;
   acc.load(grec, 0, j);
@@ -1180,15 +1192,15 @@ __device__ __forceinline__ void bwd_pair_item(const GaussSoA grec, int j, int ce
   const PairCols cols{pstart, max(kb - r, 0), min(ka + r, g - 1) + 1};
   const unsigned upto = 0xffffffffu >> (31 - lane);
   for (int c0 = 0; c0 < w.ncol; c0 += 128) {
-    const LaneSegs L = build_lane_segs_pair(w, c0, g, cols, sm, thr, lane);
+    const LaneSegs L = build_lane_segs_pair(w, c0, g, cols, ps, lane);
     const int tot = L.tot;
     for (int w0 = 0; w0 < tot; w0 += 32 * kBmWords) {
-      Cursor4P cur{build_window(L, w0, sm, lane)};
+      Cursor4P cur{build_window(L, w0, reinterpret_cast<SegSmem&>(ps), lane)};
       const int wend = min(tot, w0 + 32 * kBmWords);
       const int nfull = (wend - w0) >> 7;
       int v[4], e[4], m[4];
       for (int it = 0; it < nfull; ++it) {
-        cur.next(sm, thr, w0, w0 + 128 * it, upto, lane, v, e, m);
+        cur.next(ps, w0, w0 + 128 * it, upto, lane, v, e, m);
         float4 q[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) q[i] = __ldg(prec + e[i]);
@@ -1197,7 +1209,7 @@ __device__ __forceinline__ void bwd_pair_item(const GaussSoA grec, int j, int ce
       }
       const int tb = w0 + (nfull << 7);
       if (tb < wend) {  // ragged tail window: missing points are zero records
-        cur.next(sm, thr, w0, tb, upto, lane, v, e, m);
+        cur.next(ps, w0, tb, upto, lane, v, e, m);
         float4 q[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) q[i] = v[i] < wend ? __ldg(prec + e[i]) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1230,8 +1242,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, PAIR ? MG_BWD_PAIR_MINB : MG_B
                                                                   const int4* __restrict__ items,
                                                                   const int* __restrict__ nitems_dev,
                                                                   int n_implicit, float* __restrict__ acc10) {
-  __shared__ SegSmem s_seg[kBwdWarps];
-  __shared__ int2 s_thr[PAIR ? kBwdWarps : 1][128];
+  __shared__ WarpSmem s_ws[kBwdWarps];  // per warp: SegSmem for single items, PairSmem for pairs (aliased)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;  // kBwdWarps, or 8 for small launches
   // implicit pair items: sorted Gaussians (2j, 2j+1)
@@ -1246,10 +1257,10 @@ __global__ void __launch_bounds__(kBwdWarps * 32, PAIR ? MG_BWD_PAIR_MINB : MG_B
       const int cb = j + 1 < n_implicit ? (int)gkey[j + 1] : -1;
       const int dk = cb - ca;  // cells of one column, dk apart (sorted, so dk >= 0 when cb >= 0)
       if (cb >= 0 && dk <= MG_BWD_PAIR_DMAX && ca % g + dk <= g - 1) {
-        bwd_pair_item(grec, j, ca, cb, g, r, prec, pstart, acc10, s_seg[warp], s_thr[warp], lane);
+        bwd_pair_item(grec, j, ca, cb, g, r, prec, pstart, acc10, s_ws[warp].pair, lane);
       } else {
-        bwd_item<1>(grec, j, 1, ca, g, r, prec, pstart, acc10, s_seg[warp], lane);
-        if (cb >= 0) bwd_item<1>(grec, j + 1, 1, cb, g, r, prec, pstart, acc10, s_seg[warp], lane);
+        bwd_item<1>(grec, j, 1, ca, g, r, prec, pstart, acc10, s_ws[warp].seg, lane);
+        if (cb >= 0) bwd_item<1>(grec, j + 1, 1, cb, g, r, prec, pstart, acc10, s_ws[warp].seg, lane);
       }
     }
     return;
@@ -1267,7 +1278,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, PAIR ? MG_BWD_PAIR_MINB : MG_B
   for (; it < nitems; it += stride) {
     const int4 item = MG_BWD_IPF ? next : load_item(it);  // {first, cell, count, 0}
     if (MG_BWD_IPF && it + stride < nitems) next = load_item(it + stride);  // loads under this item
-    bwd_item<1>(grec, item.x, 1, item.y, g, r, prec, pstart, acc10, s_seg[warp], lane);
+    bwd_item<1>(grec, item.x, 1, item.y, g, r, prec, pstart, acc10, s_ws[warp].seg, lane);
   }
 }
 

@@ -24,6 +24,7 @@ import collections
 import os
 import pickle
 import select
+import struct
 import subprocess
 import sys
 import tempfile
@@ -53,7 +54,8 @@ def _serve(path, m):
             rng.integers(n)
         pre = rng.bit_generator.state
         slots[slot] = rng.permutation(m)
-        pickle.dump((pre, rng.bit_generator.state), out)
+        msg = pickle.dumps((pre, rng.bit_generator.state))
+        out.write(struct.pack("<I", len(msg)) + msg)  # length-framed: the reader never over-reads
         out.flush()
 
 
@@ -74,16 +76,35 @@ class EpochPermuter:
         self._stale = 0  # responses still to come for abandoned requests
         self._next_slot = 0
         self._answered = False  # the helper has finished starting up (answered once)
+        self._rbuf = bytearray()  # bytes read from the helper, not yet parsed
+        self._fd = self._proc.stdout.fileno()
         self.adopted = 0  # epochs served from the helper
 
     # -- transport -----------------------------------------------------------
+    def _complete(self):
+        if len(self._rbuf) < 4:
+            return False
+        return len(self._rbuf) >= 4 + struct.unpack_from("<I", self._rbuf)[0]
+
     def _ready(self):
-        """A response can be read without blocking (responses are written
-        whole and read one at a time, so none is left buffered between)."""
-        return bool(select.select([self._proc.stdout], [], [], 0.0)[0])
+        """A whole response is available without blocking (several may be in
+        flight, so bytes are buffered here rather than in a file object)."""
+        while not self._complete() and select.select([self._fd], [], [], 0.0)[0]:
+            data = os.read(self._fd, 1 << 16)
+            if not data:
+                break
+            self._rbuf += data
+        return self._complete()
 
     def _recv(self):
-        out = pickle.load(self._proc.stdout)
+        while not self._complete():
+            data = os.read(self._fd, 1 << 16)
+            if not data:
+                raise EOFError("permutation helper exited")
+            self._rbuf += data
+        n = struct.unpack_from("<I", self._rbuf)[0]
+        out = pickle.loads(bytes(self._rbuf[4:4 + n]))
+        del self._rbuf[:4 + n]
         self._answered = True
         return out
 

@@ -68,3 +68,29 @@ def test_prefetch_mismatch_falls_back_inline(monkeypatch):
             assert a.rng.integers(7) == t.rng.integers(7)
     finally:
         t.close()
+
+
+def test_prefetch_chain_restarts_after_midrun_mismatch(monkeypatch):
+    """An unpredicted draw in the middle of a run drops the two-ahead chain;
+    the next boundary draws inline, the chain restarts, and the sequence stays
+    identical to drawing every permutation inline."""
+    m, b = 4608, 1536  # exactly 3 batches per epoch
+    a = _sampler(9, m, b, False, monkeypatch)
+    t = _sampler(9, m, b, True, monkeypatch)
+    try:
+        for s in (a, t):
+            for i in range(30):
+                s._next_batch()
+                s.rng.integers(7)
+                if i == 14:
+                    s.rng.integers(5)  # not in the predicted schedule
+                if s is t:
+                    time.sleep(1.0 if i == 0 else 0.03)
+        adopted_before = t._permuter.adopted
+        for _ in range(12):
+            np.testing.assert_array_equal(a._next_batch(), t._next_batch())
+            assert a.rng.integers(7) == t.rng.integers(7)
+            time.sleep(0.03)
+        assert adopted_before >= 3 and t._permuter.adopted > adopted_before  # the chain came back
+    finally:
+        t.close()

@@ -26,7 +26,10 @@ constexpr int kNH = 64;       // hidden width
 constexpr int kNBands = 6;
 constexpr int kNT = 64;       // points per tile
 constexpr int kNThr = 256;    // threads per CTA (4 outputs x 4 points each for a 64 x 64 tile)
-constexpr int kNChunk = 128;  // points per dW staging chunk
+#ifndef MG_NRF_CHUNK
+#define MG_NRF_CHUNK 128
+#endif
+constexpr int kNChunk = MG_NRF_CHUNK;  // points per dW staging chunk (double-buffered: 2 x 2 x chunk x 256 B smem)
 constexpr float kNOutBound = 0.1f;
 #ifndef MG_NRF_UNROLL
 #define MG_NRF_UNROLL 8  // k-loop unroll of the tile GEMMs (4: fwd 0.181 ms, 8: 0.173 ms, 16: 0.176 ms at 131k points)
@@ -343,15 +346,36 @@ __global__ void __launch_bounds__(kNThr) nrf_bwd_kernel(const float* __restrict_
 }
 
 struct NrfDwSmem {
-  float a[kNChunk][kNH];  // point-major A rows (enc padded to 40, or SiLU(z_{l-1}))
-  float d[kNChunk][kNH];  // point-major delta rows
+  float a[2][kNChunk][kNH];  // double-buffered point-major A rows (enc padded to 40, or SiLU(z_{l-1}))
+  float d[2][kNChunk][kNH];  // double-buffered point-major delta rows
 };
+
+__device__ __forceinline__ void cp_async16_zfill(void* dst, const void* src, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes)
+               : "memory");
+}
+
+// One chunk of A and delta rows into buffer `buf` with 16-byte cp.async pieces;
+// rows past n (and A columns past astride) are zero-filled.
+__device__ __forceinline__ void nrf_dw_stage(NrfDwSmem& sm, int buf, const float* A, int astride, const float* D,
+                                             int64_t q0, int n, int tid) {
+  constexpr int kPieces = kNChunk * kNH / 4 / kNThr;
+#pragma unroll
+  for (int u = 0; u < kPieces; ++u) {
+    const int e = tid + u * kNThr, p = e / (kNH / 4), i4 = e - p * (kNH / 4);
+    const bool okA = p < n && 4 * i4 < astride, okD = p < n;
+    cp_async16_zfill(&sm.a[buf][p][4 * i4], okA ? A + (q0 + p) * astride + 4 * i4 : A, okA ? 16 : 0);
+    cp_async16_zfill(&sm.d[buf][p][4 * i4], okD ? D + (q0 + p) * kNH + 4 * i4 : D, okD ? 16 : 0);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
 
 // blockIdx.y = layer (0..3: 64-wide deltas; 4: output layer); each CTA sums
 // chunks blockIdx.x, blockIdx.x + gridDim.x, ... into one partial:
 // part[l] = [gridDim.x][kin * 64 + 64] (dW row-major, then db).  The layer
-// inputs come from the backward pass (enc rows, h = SiLU(z) rows), so staging
-// is a plain copy.
+// inputs come from the backward pass (enc rows, h = SiLU(z) rows); chunk c+1
+// is copied in by cp.async while chunk c is reduced.
 __global__ void __launch_bounds__(kNThr) nrf_dw_kernel(int64_t b, const float* __restrict__ enc,
                                                        const float* __restrict__ h, const float* __restrict__ dz,
                                                        const float* __restrict__ d4g, float* __restrict__ part) {
@@ -363,59 +387,61 @@ __global__ void __launch_bounds__(kNThr) nrf_dw_kernel(int64_t b, const float* _
   const int64_t sz0 = kNE * kNH + kNH, sz = kNH * kNH + kNH;
   float* out = part + (l == 0 ? 0 : G * (sz0 + (int64_t)(l - 1) * sz)) +
                (int64_t)blockIdx.x * (l == 0 ? sz0 : (l < 4 ? sz : 65));
+  const float* A = l == 0 ? enc : h + (int64_t)(l == 4 ? 3 : l - 1) * b * kNH;
+  if (l == 4) {  // dW4[j] = sum_p h3[p][j] d4[p]; db4 = sum_p d4[p] (small: synchronous staging)
+    float s4 = 0.f, sb4 = 0.f;
+    for (int64_t c = blockIdx.x; c < nchunks; c += G) {
+      const int64_t q0 = c * kNChunk;
+      const int n = (int)min((int64_t)kNChunk, b - q0);
+      __syncthreads();
+      for (int e = tid; e < kNChunk * kNH / 4; e += kNThr) {
+        const int p = e / (kNH / 4), i4 = e - p * (kNH / 4);
+        *reinterpret_cast<float4*>(&sm.a[0][p][4 * i4]) =
+            p < n ? *reinterpret_cast<const float4*>(A + (q0 + p) * kNH + 4 * i4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      if (tid < kNChunk) sm.d[0][tid][0] = tid < n ? d4g[q0 + tid] : 0.f;
+      __syncthreads();
+      if (tid < kNH) {
+        for (int p = 0; p < n; ++p) s4 = fmaf(sm.a[0][p][tid], sm.d[0][p][0], s4);
+      } else if (tid == kNH) {
+        for (int p = 0; p < n; ++p) sb4 += sm.d[0][p][0];
+      }
+    }
+    if (tid < kNH) out[tid] = s4;
+    if (tid == kNH) out[kNH] = sb4;
+    return;
+  }
   const int kin = l == 0 ? kNE : kNH;
   const int astride = l == 0 ? kNE + 1 : kNH;  // floats per A row in global memory
-  const float* A = l == 0 ? enc : h + (int64_t)(l == 4 ? 3 : l - 1) * b * kNH;
+  const float* D = dz + (int64_t)l * b * kNH;
   const int ib = tid >> 4, jb = tid & 15;
   f2 acc[4][2];
 #pragma unroll
   for (int ii = 0; ii < 4; ++ii) acc[ii][0] = acc[ii][1] = bc2(0.f);
   f2 dba[2] = {bc2(0.f), bc2(0.f)};
-  float s4 = 0.f, sb4 = 0.f;
-  for (int64_t c = blockIdx.x; c < nchunks; c += G) {
-    const int64_t q0 = c * kNChunk;
-    const int n = (int)min((int64_t)kNChunk, b - q0);
-    __syncthreads();
-    {  // A rows (astride floats each, 16-byte pieces) and delta rows, all loads issued first
-      constexpr int kA = kNChunk * kNH / 4 / kNThr;  // float4 pieces per thread (64-wide rows)
-      float4 av[kA], dv[kA];
-#pragma unroll
-      for (int u = 0; u < kA; ++u) {
-        const int e = tid + u * kNThr, p = e / (kNH / 4), i4 = e - p * (kNH / 4);
-        const int64_t q = q0 + min(p, n - 1);
-        av[u] = 4 * i4 < astride ? *reinterpret_cast<const float4*>(A + q * astride + 4 * i4)
-                                 : make_float4(0.f, 0.f, 0.f, 0.f);
-        dv[u] = l < 4 ? *reinterpret_cast<const float4*>(dz + ((int64_t)l * b + q) * kNH + 4 * i4)
-                      : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-#pragma unroll
-      for (int u = 0; u < kA; ++u) {
-        const int e = tid + u * kNThr, p = e / (kNH / 4), i4 = e - p * (kNH / 4);
-        const bool ok = p < n;
-        *reinterpret_cast<float4*>(&sm.a[p][4 * i4]) = ok ? av[u] : make_float4(0.f, 0.f, 0.f, 0.f);
-        if (l < 4) *reinterpret_cast<float4*>(&sm.d[p][4 * i4]) = ok ? dv[u] : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-      if (l == 4 && tid < kNChunk) sm.d[tid][0] = tid < n ? d4g[q0 + tid] : 0.f;  // only column 0 is used
+  int buf = 0;
+  int64_t c = blockIdx.x;
+  if (c < nchunks) nrf_dw_stage(sm, 0, A, astride, D, c * kNChunk, (int)min((int64_t)kNChunk, b - c * kNChunk), tid);
+  for (; c < nchunks; c += G) {
+    const int64_t cn = c + G;
+    if (cn < nchunks) {
+      nrf_dw_stage(sm, buf ^ 1, A, astride, D, cn * kNChunk, (int)min((int64_t)kNChunk, b - cn * kNChunk), tid);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
-    if (l == 4) {  // dW4[j] = sum_p h3[p][j] d4[p]; db4 = sum_p d4[p]
-      if (tid < kNH) {
-        for (int p = 0; p < n; ++p) s4 = fmaf(sm.a[p][tid], sm.d[p][0], s4);
-      } else if (tid == kNH) {
-        for (int p = 0; p < n; ++p) sb4 += sm.d[p][0];
-      }
-      continue;
-    }
+    const int n = (int)min((int64_t)kNChunk, b - c * kNChunk);
     if (4 * ib < kin) {
-      // padded rows (p >= n) are zero, so groups of 8 points may run past n
+      // rows past n are zero, so groups of 8 points may run past n
 #pragma unroll 1
       for (int p0 = 0; p0 < n; p0 += 8) {
         float4 a[8];
         ulonglong2 dd[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          a[u] = *reinterpret_cast<const float4*>(&sm.a[p0 + u][4 * ib]);
-          dd[u] = *reinterpret_cast<const ulonglong2*>(&sm.d[p0 + u][4 * jb]);
+          a[u] = *reinterpret_cast<const float4*>(&sm.a[buf][p0 + u][4 * ib]);
+          dd[u] = *reinterpret_cast<const ulonglong2*>(&sm.d[buf][p0 + u][4 * jb]);
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
@@ -435,11 +461,8 @@ __global__ void __launch_bounds__(kNThr) nrf_dw_kernel(int64_t b, const float* _
         }
       }
     }
-  }
-  if (l == 4) {
-    if (tid < kNH) out[tid] = s4;
-    if (tid == kNH) out[kNH] = sb4;
-    return;
+    __syncthreads();  // the next iteration stages into this buffer
+    buf ^= 1;
   }
 #pragma unroll
   for (int ii = 0; ii < 4; ++ii) {

@@ -551,7 +551,14 @@ void launch_nrf_forward(const float* x, int64_t b, const float* const* w, const 
 void launch_nrf_backward(const float* x, int64_t b, const float* const* w, const float* const* bias, const float* up,
                          const float* t, const float* z, float* dp, float* const* dw, float* const* db, void* ws,
                          cudaStream_t st) {
-  if (b <= 0) return;
+  if (b <= 0) {  // no points: zero gradients
+    for (int l = 0; l < 5; ++l) {
+      const size_t kin = l == 0 ? kNE : kNH, nout = l == 4 ? 1 : kNH;
+      cudaMemsetAsync(dw[l], 0, kin * nout * sizeof(float), st);
+      cudaMemsetAsync(db[l], 0, nout * sizeof(float), st);
+    }
+    return;
+  }
   nrf_attrs();
   NrfParams P;
   NrfGrads Gd;

@@ -65,3 +65,15 @@ def test_fused_nrf_matches_torch_mirror(n):
     g2 = nrf_backward_fused(f, x, up, c1)
     for a, b in zip(g1[0] + g1[1] + [g1[2]], g2[0] + g2[1] + [g2[2]]):
         assert torch.equal(a, b)
+
+
+def test_fused_nrf_empty_batch_zero_grads():
+    from paper_2603_00145_b200.nrf import ResidualField, nrf_backward_fused, nrf_forward_fused
+
+    f = ResidualField.create(np.random.default_rng(1))
+    x = torch.zeros((0, 3), dtype=torch.float32, device="cuda")
+    r, cache = nrf_forward_fused(f, x)
+    assert r.numel() == 0
+    dws, dbs, dp = nrf_backward_fused(f, x, torch.zeros(0, device="cuda"), cache)
+    assert dp.shape == (0, 3)
+    assert all(float(t.abs().sum()) == 0.0 for t in dws + dbs)

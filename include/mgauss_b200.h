@@ -13,7 +13,8 @@
  *
  * Reference interfaces each group replaces (paths under
  * /root/reference/pkg/src/mgauss):
- *   mg_block_forward / mg_block_backward / mg_dense_forward
+ *   mg_block_forward / mg_block_backward / mg_dense_forward (+ the strict
+ *   float64 mg_block_forward_f64 / mg_block_backward_f64)
  *        -> _kernels.block_forward (_kernels.py:24-27), block_backward
  *           (_kernels.py:73-76), dense_forward (_kernels.py:147-148):
  *           same argument list and meaning, float64/int64 device arrays.
@@ -166,6 +167,12 @@ int mg_sample_volume(const void *grec, int64_t n_gauss, const int32_t *gstart, i
  * predictions (mean), loss_acc += L (float64 device scalar). */
 int mg_smooth_l1(const float *pred, const float *target, int64_t b, float *upstream_out, double *loss_acc,
                  void *stream);
+/* Same with an explicit normaliser: upstream_out = scale * dHuber/dpred,
+ * loss_acc += scale * sum Huber.  A rank holding a share of a sharded batch
+ * passes scale = 1 / (global batch size), so the all-reduced partial sums
+ * are exactly the global mean and its gradient. */
+int mg_smooth_l1_scaled(const float *pred, const float *target, int64_t b, double scale, float *upstream_out,
+                        double *loss_acc, void *stream);
 /* Residual field r(x) = 0.1 tanh(MLP(enc(x))) with the reference widths
  * 39-64-64-64-64-1, SiLU, 6 Fourier bands (nrf.py:23-182; ResidualField.forward /
  * backward).  w[l] are (fan_in, fan_out) row-major float32, bias[l] (fan_out).
@@ -222,6 +229,21 @@ int mg_block_backward(const double *points, const int64_t *slice_ids, int64_t b,
                       int64_t n, const int64_t *cell_starts, const int64_t *cell_indices, int64_t grid_res,
                       int64_t radius, const double *upstream, double *d_mu, double *d_abar6, double *d_alpha,
                       double *out_dpoint, void *ws, size_t ws_bytes, void *stream);
+/* Strict float64 instantiation of the same two kernels (same arguments, same
+ * ownership): every pair is evaluated in IEEE float64 in the reference's
+ * operation order without FMA contraction, so results agree with
+ * _kernels.py to ~1e-15 relative (selected by render.set_strict_fp64). */
+size_t mg_block_f64_workspace_bytes(int64_t b, int64_t n, int64_t grid_res);
+int mg_block_forward_f64(const double *points, const int64_t *slice_ids, int64_t b, const double *rot,
+                         const double *trans, int64_t k, const double *mu, const double *prec6, const double *alpha,
+                         int64_t n, const int64_t *cell_starts, const int64_t *cell_indices, int64_t grid_res,
+                         int64_t radius, double *out_intensity, int64_t *out_counts, double *out_transformed,
+                         void *ws, size_t ws_bytes, void *stream);
+int mg_block_backward_f64(const double *points, const int64_t *slice_ids, int64_t b, const double *rot,
+                          const double *trans, int64_t k, const double *mu, const double *prec6, const double *alpha,
+                          int64_t n, const int64_t *cell_starts, const int64_t *cell_indices, int64_t grid_res,
+                          int64_t radius, const double *upstream, double *d_mu, double *d_abar6, double *d_alpha,
+                          double *out_dpoint, void *ws, size_t ws_bytes, void *stream);
 size_t mg_dense_workspace_bytes(int64_t n);
 int mg_dense_forward(const double *points, int64_t b, const double *mu, const double *prec6, const double *alpha,
                      int64_t n, double *out_intensity, void *ws, size_t ws_bytes, void *stream);

@@ -55,6 +55,7 @@ SIGNATURES = {
     "mg_volume_workspace_bytes": (SZ, [I64, I64, I64]),
     "mg_sample_volume": (ctypes.c_int, [P, I64, P, I64, I64, I64, I64, I64, P, P, I64, I64, P, P, P, SZ, P]),
     "mg_smooth_l1": (ctypes.c_int, [P, P, I64, P, P, P]),
+    "mg_smooth_l1_scaled": (ctypes.c_int, [P, P, I64, D, P, P, P]),
     "mg_nrf_forward": (ctypes.c_int, [P, I64, P, P, P, P, P, P, P]),
     "mg_nrf_backward_workspace_bytes": (SZ, [I64]),
     "mg_nrf_backward": (ctypes.c_int, [P, I64, P, P, P, P, P, P, P, P, P, SZ, P]),
@@ -71,6 +72,10 @@ SIGNATURES = {
     "mg_block_forward": (ctypes.c_int, [P, P, I64, P, P, I64, P, P, P, I64, P, P, I64, I64, P, P, P, P, SZ, P]),
     "mg_block_backward": (ctypes.c_int,
                           [P, P, I64, P, P, I64, P, P, P, I64, P, P, I64, I64, P, P, P, P, P, P, SZ, P]),
+    "mg_block_f64_workspace_bytes": (SZ, [I64, I64, I64]),
+    "mg_block_forward_f64": (ctypes.c_int, [P, P, I64, P, P, I64, P, P, P, I64, P, P, I64, I64, P, P, P, P, SZ, P]),
+    "mg_block_backward_f64": (ctypes.c_int,
+                              [P, P, I64, P, P, I64, P, P, P, I64, P, P, I64, I64, P, P, P, P, P, P, SZ, P]),
     "mg_dense_workspace_bytes": (SZ, [I64]),
     "mg_dense_forward": (ctypes.c_int, [P, I64, P, P, P, I64, P, P, SZ, P]),
 }

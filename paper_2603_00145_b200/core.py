@@ -81,6 +81,10 @@ class TransformSet:
                    translations=np.stack([np.asarray(t.translation, dtype=np.float64)
                                           for t in transforms]))
 
+    def to_list(self):
+        return [RigidTransform(self.quats[k].copy(), self.translations[k].copy(), slice_id=k)
+                for k in range(len(self))]
+
     def rotations(self):
         return quat_to_rotation(self.quats)
 
@@ -123,6 +127,22 @@ class GaussianField:
     @property
     def alphas(self):
         return sigmoid(self.intensity_logits)
+
+    @property
+    def params_per_primitive(self):
+        return 11  # core.py:18
+
+    def validate(self):
+        """Shape checks of core.py:287-301 (N = prod(lattice_dims))."""
+        n = self.count
+        if n != int(np.prod(self.lattice_dims)):
+            raise ValueError("primitive count does not match lattice dims")
+        li = self.lattice_index if self.lattice_index is not None else np.zeros((0, 3))
+        for arr, shape in ((self.positions, (n, 3)), (self.quaternions, (n, 4)), (self.log_scales, (n, 3)),
+                           (self.intensity_logits, (n,)), (li, (n, 3))):
+            if np.asarray(arr).shape != shape:
+                raise ValueError(f"bad array shape {np.asarray(arr).shape}, expected {shape}")
+        return self
 
     def copy(self):
         return GaussianField(np.array(self.positions), np.array(self.quaternions),

@@ -426,7 +426,13 @@ int mg_sample_volume(const void* grec, int64_t n_gauss, const int32_t* gstart, i
 }
 
 int mg_smooth_l1(const float* pred, const float* target, int64_t b, float* up_out, double* loss_acc, void* stream) {
-  launch_smooth_l1(pred, target, b, up_out, loss_acc, S(stream));
+  return mg_smooth_l1_scaled(pred, target, b, b > 0 ? 1.0 / (double)b : 0.0, up_out, loss_acc, stream);
+}
+
+int mg_smooth_l1_scaled(const float* pred, const float* target, int64_t b, double scale, float* up_out,
+                        double* loss_acc, void* stream) {
+  if (b < 0) return fail("mg_smooth_l1: b < 0");
+  launch_smooth_l1(pred, target, b, scale, up_out, loss_acc, S(stream));
   return cuda_status();
 }
 
@@ -572,6 +578,41 @@ int mg_block_backward(const double* points, const int64_t* sids, int64_t b, cons
   if (!upstream) return fail("mg_block_backward: upstream is required");
   return block_common(points, sids, b, rot, trans, k, mu, prec6, alpha, n, cs, ci, g, r, true, nullptr, nullptr,
                       nullptr, upstream, d_mu, d_abar6, d_alpha, out_dp, ws, wsb, S(stream));
+}
+
+// ---- strict float64 instantiation of the same ABI (mg_strict.cu) ----
+size_t mg_block_f64_workspace_bytes(int64_t b, int64_t n, int64_t g) { return strict_workspace_bytes(b, n, g); }
+
+static int strict_common(const double* points, const int64_t* sids, int64_t b, const double* rot, const double* trans,
+                         int64_t k, const double* mu, const double* prec6, const double* alpha, int64_t n,
+                         const int64_t* cs, const int64_t* ci, int64_t g, int64_t r, double* out_i, int64_t* out_cnt,
+                         double* out_x, const double* upstream, double* d_mu, double* d_abar6, double* d_alpha,
+                         double* out_dp, void* ws, size_t wsb, cudaStream_t st) {
+  if (g < 1 || r < 0 || b < 0 || n < 0) return fail("mg_block_f64: bad sizes");
+  if (ncell_of(g) >= (1ll << 31)) return fail("mg_block_f64: grid too large");
+  if (strict_block(points, sids, b, rot, trans, k, mu, prec6, alpha, n, cs, ci, (int)g, (int)r, out_i, out_cnt, out_x,
+                   upstream, d_mu, d_abar6, d_alpha, out_dp, ws, wsb, st))
+    return fail("mg_block_f64: workspace too small");
+  return cuda_status();
+}
+
+int mg_block_forward_f64(const double* points, const int64_t* sids, int64_t b, const double* rot, const double* trans,
+                         int64_t k, const double* mu, const double* prec6, const double* alpha, int64_t n,
+                         const int64_t* cs, const int64_t* ci, int64_t g, int64_t r, double* out_i, int64_t* out_cnt,
+                         double* out_x, void* ws, size_t wsb, void* stream) {
+  if (!out_i || !out_cnt) return fail("mg_block_forward_f64: out_intensity and out_counts are required");
+  return strict_common(points, sids, b, rot, trans, k, mu, prec6, alpha, n, cs, ci, g, r, out_i, out_cnt, out_x,
+                       nullptr, nullptr, nullptr, nullptr, nullptr, ws, wsb, S(stream));
+}
+
+int mg_block_backward_f64(const double* points, const int64_t* sids, int64_t b, const double* rot,
+                          const double* trans, int64_t k, const double* mu, const double* prec6, const double* alpha,
+                          int64_t n, const int64_t* cs, const int64_t* ci, int64_t g, int64_t r,
+                          const double* upstream, double* d_mu, double* d_abar6, double* d_alpha, double* out_dp,
+                          void* ws, size_t wsb, void* stream) {
+  if (!upstream || !d_mu || !d_abar6 || !d_alpha) return fail("mg_block_backward_f64: upstream and accumulators are required");
+  return strict_common(points, sids, b, rot, trans, k, mu, prec6, alpha, n, cs, ci, g, r, nullptr, nullptr, nullptr,
+                       upstream, d_mu, d_abar6, d_alpha, out_dp, ws, wsb, S(stream));
 }
 
 size_t mg_dense_workspace_bytes(int64_t n) { return al((size_t)n * 48) + al((size_t)n * 4) + 512; }

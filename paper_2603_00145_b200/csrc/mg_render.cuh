@@ -56,8 +56,8 @@ void launch_transform_grads(const double* dpoints, const double* coords, const i
                             const double* tap_off, const double* dirs, const double* tq, int k, double* acc12,
                             double* out7, int accumulate, void* ws, cudaStream_t st);
 size_t transform_grads_ws_bytes(int64_t k);
-void launch_smooth_l1(const float* pred, const float* target, int64_t b, float* up_out, double* loss_acc,
-                      cudaStream_t st);
+void launch_smooth_l1(const float* pred, const float* target, int64_t b, double scale, float* up_out,
+                      double* loss_acc, cudaStream_t st);
 // fused residual field (mg_nrf.cu)
 size_t nrf_backward_ws_bytes(int64_t b);
 void launch_nrf_forward(const float* x, int64_t b, const float* const* w, const float* const* bias, float* pred_add,
@@ -79,6 +79,14 @@ void launch_transform_adam(double* tq, double* tt, const double* g7, double* m7,
                            double b1, double b2, double eps, const int* t_dev, cudaStream_t st);
 void launch_upsample(const float* q_old, const float* s_old, const float* l_old, const int* node_of_old, int ro, int rn,
                      float* pos, float* q, float* s, float* l, cudaStream_t st);
+
+// strict float64 reference-order pair kernels (mg_strict.cu)
+size_t strict_workspace_bytes(int64_t b, int64_t n, int64_t g);
+int strict_block(const double* points, const int64_t* sids, int64_t b, const double* rot, const double* trans,
+                 int64_t k, const double* mu, const double* prec6, const double* alpha, int64_t n, const int64_t* cs,
+                 const int64_t* ci, int g, int r, double* out_i, int64_t* out_cnt, double* out_x,
+                 const double* upstream, double* d_mu, double* d_abar6, double* d_alpha, double* out_dp, void* ws,
+                 size_t wsb, cudaStream_t st);
 
 // inference
 size_t volume_workspace_bytes(int nx, int ny, int nz);

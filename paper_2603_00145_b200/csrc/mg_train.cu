@@ -697,9 +697,9 @@ void launch_transform_grads(const double* dpoints, const double* coords, const i
   }
   MG_LAUNCH(transform_chain_kernel<<<gridn(k), 256, 0, st>>>(acc12, tq, k, out7, accumulate));
 }
-void launch_smooth_l1(const float* pred, const float* target, int64_t b, float* up_out, double* loss_acc,
-                      cudaStream_t st) {
-  if (b > 0) MG_LAUNCH(smooth_l1_kernel<<<gridn(b), 256, 0, st>>>(pred, target, b, 1.0 / (double)b, up_out, loss_acc));
+void launch_smooth_l1(const float* pred, const float* target, int64_t b, double scale, float* up_out,
+                      double* loss_acc, cudaStream_t st) {
+  if (b > 0) MG_LAUNCH(smooth_l1_kernel<<<gridn(b), 256, 0, st>>>(pred, target, b, scale, up_out, loss_acc));
 }
 
 __global__ void quat_to_rot_kernel(const double* __restrict__ q, int64_t k, double* __restrict__ rot) {

@@ -2,10 +2,15 @@
 
 r(x) = 0.1 * tanh(MLP(enc(x))), enc = [x, sin(2^k pi x), cos(2^k pi x)]_{k<6}
 (39 dims), hidden widths (64, 64, 64, 64) with SiLU, zero-initialised last
-layer.  The four dense layers are plain fp32 GEMMs (cuBLAS through torch);
-SURVEY §8(a) A16 allows tensor cores only once ncu shows the MLP is a
-dense-contraction bottleneck, and bf16/tf32 would break the 1e-4 parity.
-Manual backward identical to nrf.py:147-182 (including d/dx into transforms).
+layer (nrf.py:23-137).  Forward and the manual backward of nrf.py:147-182
+(weight/bias gradients and d/dx into the slice transforms) run in the fused
+float32 SIMT kernels of csrc/mg_nrf.cu (4 launches per step).
+A16 allows tensor cores only if ncu shows the MLP is a dense-contraction
+bottleneck; profiles/r02_nrf.md has the capture and the decision.  Only the
+reference configuration (6 bands, 64 x 4 hidden, output bound 0.1) exists on
+the device: any other width raises UnsupportedResidualField (no second
+backend).  The torch-op restatement used as a test reference lives in
+tests/nrf_mirror.py.
 """
 
 from __future__ import annotations
@@ -17,7 +22,7 @@ import numpy as np
 import torch
 
 from . import _device as dv
-from .errors import UninitializedField
+from .errors import UninitializedField, UnsupportedResidualField
 
 OUTPUT_BOUND = 0.1
 DEFAULT_BANDS = 6
@@ -64,43 +69,22 @@ class ResidualField:
         return out
 
 
-def _freqs(bands, x):
-    return (2.0 ** torch.arange(bands, dtype=x.dtype, device=x.device)) * np.pi
-
-
-def fourier_encode(x: torch.Tensor, bands: int) -> torch.Tensor:
-    """nrf.py:23-36 on device: [x, sin(2^0 pi x), cos(2^0 pi x), sin(2^1 pi x), ...],
-    all bands in one broadcast (same column order as the reference)."""
-    s = x[:, None, :] * _freqs(bands, x)[None, :, None]  # (B, bands, 3)
-    sc = torch.stack((torch.sin(s), torch.cos(s)), dim=2)  # (B, bands, 2, 3)
-    return torch.cat((x, sc.reshape(x.shape[0], 6 * bands)), dim=1)
-
-
-def nrf_forward_cached(field: ResidualField, x: torch.Tensor):
+def _require_fused(field: ResidualField):
     if not field.weights:
         raise UninitializedField("residual field has no weights")
-    h = fourier_encode(x, field.frequency_bands)
-    pre, post = [], [h]
-    depth = len(field.weights)
-    for li in range(depth):
-        z = torch.addmm(field.biases[li], h, field.weights[li])
-        pre.append(z)
-        if li < depth - 1:
-            h = torch.nn.functional.silu(z)  # z * sigmoid(z), one kernel
-            post.append(h)
-    t = torch.tanh(pre[-1][:, 0])
-    return field.output_bound * t, (t, pre, post)
+    if not fused_supported(field):
+        raise UnsupportedResidualField(
+            f"device NRF kernels implement the reference widths {FUSED_WIDTHS} with 6 bands and output bound 0.1; "
+            f"got widths {tuple(field.layer_widths)}, {field.frequency_bands} bands")
 
 
 def nrf_forward_device(field: ResidualField, x: torch.Tensor, chunk=1 << 20):
+    _require_fused(field)
     out = torch.empty(x.shape[0], dtype=torch.float32, device=x.device)
     for lo in range(0, x.shape[0], chunk):
-        if fused_supported(field):
-            xs = x[lo:lo + chunk].contiguous()
-            t = torch.empty(xs.shape[0], dtype=torch.float32, device=x.device)
-            _fused_forward(field, xs, None, out[lo:lo + chunk], t, None)
-        else:
-            out[lo:lo + chunk] = nrf_forward_cached(field, x[lo:lo + chunk])[0]
+        xs = x[lo:lo + chunk].contiguous()
+        t = torch.empty(xs.shape[0], dtype=torch.float32, device=x.device)
+        _fused_forward(field, xs, None, out[lo:lo + chunk], t, None)
     return out
 
 
@@ -130,6 +114,7 @@ def _fused_forward(field, x, pred_add, r_out, t_out, z_out):
 def nrf_forward_fused(field: ResidualField, x: torch.Tensor, pred_add: torch.Tensor | None = None):
     """nrf_forward_cached on the fused kernel: (r or None, cache).  With
     ``pred_add`` the residual is added into it in place and r is not returned."""
+    _require_fused(field)
     x = x.contiguous()
     n = x.shape[0]
     t = torch.empty(n, dtype=torch.float32, device=x.device)
@@ -164,63 +149,8 @@ def nrf_backward_fused(field: ResidualField, x: torch.Tensor, upstream: torch.Te
     return dws, dbs, dp
 
 
-def _split_k(n_rows, parts=128, min_rows=512):
-    q = n_rows // parts
-    return (parts, q) if q >= min_rows else (0, 0)
-
-
-def _tn_matmul(a, b):
-    """a^T @ b for tall (K x m), (K x n) operands: split-K over equal row
-    chunks as one batched GEMM plus a fixed-order sum (a plain K = 131k GEMM
-    with a 64 x 64 output runs on a handful of CTAs)."""
-    parts, q = _split_k(a.shape[0])
-    if not parts:
-        return a.T @ b
-    main = parts * q
-    out = torch.bmm(a[:main].reshape(parts, q, a.shape[1]).transpose(1, 2),
-                    b[:main].reshape(parts, q, b.shape[1])).sum(dim=0)
-    if main < a.shape[0]:
-        out = out + a[main:].T @ b[main:]
-    return out
-
-
-def _col_sum(a):
-    """a.sum(dim=0) as a two-stage reduction over equal row chunks."""
-    parts, q = _split_k(a.shape[0])
-    if not parts:
-        return a.sum(dim=0)
-    main = parts * q
-    out = a[:main].reshape(parts, q, a.shape[1]).sum(dim=1).sum(dim=0)
-    if main < a.shape[0]:
-        out = out + a[main:].sum(dim=0)
-    return out
-
-
-def nrf_backward(field: ResidualField, x: torch.Tensor, upstream: torch.Tensor, cache):
-    """(d_weights, d_biases, d_points) of sum_b upstream_b r(x_b)."""
-    t, pre, post = cache
-    depth = len(field.weights)
-    dws, dbs = [None] * depth, [None] * depth
-    dz = (upstream * field.output_bound * (1.0 - t * t))[:, None]
-    d_enc = None
-    for li in range(depth - 1, -1, -1):
-        dws[li] = _tn_matmul(post[li], dz)
-        dbs[li] = _col_sum(dz)
-        dh = dz @ field.weights[li].T
-        if li > 0:  # dh * s (1 + z (1 - s)), s = sigmoid(z): one fused kernel
-            dz = torch.ops.aten.silu_backward(dh, pre[li - 1])
-        else:
-            d_enc = dh
-    bands = field.frequency_bands
-    f = _freqs(bands, x)[None, :, None]  # (1, bands, 1)
-    s = x[:, None, :] * f
-    de = d_enc[:, 3:].reshape(x.shape[0], bands, 2, 3)
-    dp = d_enc[:, :3] + (f * (torch.cos(s) * de[:, :, 0] - torch.sin(s) * de[:, :, 1])).sum(dim=1)
-    return dws, dbs, dp
-
-
 def nrf_forward(field: ResidualField, x):
     """Host-facing r(x) (numpy in, numpy out), nrf.py:132-137."""
     xt = dv.to_dev(np.atleast_2d(np.asarray(x, dtype=np.float64)), torch.float32)
-    r = dv.to_host(nrf_forward_cached(field, xt)[0]).astype(np.float64)
+    r = dv.to_host(nrf_forward_device(field, xt)).astype(np.float64)
     return float(r[0]) if np.asarray(x).ndim == 1 else r

@@ -13,6 +13,7 @@ through-plane slice profile, I_psf(p) = sum_t w_t I(T_k(p + off_t * dir_k)).
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -25,6 +26,38 @@ from .errors import DegenerateQuaternion, InconsistentGrid, OutOfMemoryRequest
 from .spatial import PartitionGrid
 
 MAX_VOLUME_VOXELS = 2 ** 27  # render.py:35
+
+_num_threads = 1
+_strict_fp64 = os.environ.get("MGAUSS_STRICT_FP64", "0") not in ("", "0")
+
+
+def set_num_threads(n):
+    """Worker count of the reference's CPU kernels (render.py:44-55).
+
+    Kept for API compatibility (the reference CLI calls it, cli.py:472-479).
+    The device kernels have no host worker threads and their reductions are
+    fixed-order, so results do not depend on this value."""
+    global _num_threads
+    _num_threads = max(1, int(n))
+
+
+def get_num_threads():
+    return _num_threads
+
+
+def set_strict_fp64(on=True):
+    """Select the strict float64 pair kernels (mg_block_forward_f64 /
+    mg_block_backward_f64) for render_points, render_backward,
+    render_points_dense and sample_volume: every pair in IEEE float64 in the
+    reference's operation order (_kernels.py:24-162), ~1e-15 relative to the
+    reference.  Default off: the float32 kernels (rel. error ~1e-6, within the
+    1e-4 contract) are 10-20x faster.  MGAUSS_STRICT_FP64=1 sets it at import."""
+    global _strict_fp64
+    _strict_fp64 = bool(on)
+
+
+def get_strict_fp64():
+    return _strict_fp64
 
 
 @dataclass
@@ -182,6 +215,8 @@ def render_points(field, grid, transforms, samples, radius=None, prepared=None, 
     gd = _grid_dev(grid)
     L = N.lib()
     st = dv.sptr()
+    if _strict_fp64:
+        return _strict_render(field, gd, p6, al, coords, sids, rot, trans, k, g, r, slice_psf)
     c_d = dv.to_dev(coords, torch.float64)
     s_d = dv.to_dev(sids, torch.int64)
     rot_d = dv.to_dev(rot, torch.float64)
@@ -202,6 +237,62 @@ def render_points(field, grid, transforms, samples, radius=None, prepared=None, 
     t = slice_psf.ntaps
     return RenderBatch(points=dv.to_host(stg["x"]).reshape(b, t, 3), intensities=dv.to_host(stg["I"]),
                        contributor_counts=dv.to_host(stg["cnt"]))
+
+
+def _psf_expand(coords, sids, psf):
+    """(b*t, 3) tap points p + off_t * dir_k in (b, t) order, as the oracle
+    composes them (I_psf = sum_t w_t I(T_k(p + off_t dir_k)))."""
+    dirs = np.asarray(psf.through_dirs, dtype=np.float64).reshape(-1, 3)
+    shift = dirs[np.clip(sids, 0, None)] * (sids >= 0)[:, None]
+    taps = [coords + off * shift for off in np.asarray(psf.offsets, dtype=np.float64)]
+    return np.ascontiguousarray(np.stack(taps, axis=1).reshape(-1, 3)), np.repeat(sids, psf.ntaps)
+
+
+def _strict_call(fn, field, gd, p6, al, coords, sids, rot, trans, k, g, r, up=None, acc=None):
+    """One strict float64 kernel call (mg_block_forward_f64 / _backward_f64)."""
+    L = N.lib()
+    n, b = field.count, coords.shape[0]
+    mu = dv.to_dev(field.positions, torch.float64, (n, 3))
+    c_d = dv.to_dev(coords, torch.float64)
+    s_d = dv.to_dev(sids, torch.int64)
+    rot_d = dv.to_dev(rot, torch.float64)
+    tr_d = dv.to_dev(trans, torch.float64)
+    ws = dv.workspace(L.mg_block_f64_workspace_bytes(b, n, g), "strict")
+    if up is None:
+        out_i = dv.empty((b,), torch.float64)
+        out_c = dv.empty((b,), torch.int64)
+        out_x = dv.empty((b, 3), torch.float64)
+        N.check(L.mg_block_forward_f64(N.ptr(c_d), N.ptr(s_d), b, N.ptr(rot_d), N.ptr(tr_d), k, N.ptr(mu),
+                                       N.ptr(p6), N.ptr(al), n, N.ptr(gd["starts64"]), N.ptr(gd["order64"]), g, r,
+                                       N.ptr(out_i), N.ptr(out_c), N.ptr(out_x), N.ptr(ws), ws.numel(), dv.sptr()),
+                "block_forward_f64")
+        return out_i, out_c, out_x
+    d_mu, d_ab, d_al = acc
+    u_d = dv.to_dev(up, torch.float64)
+    d_pts = dv.empty((b, 3), torch.float64)
+    N.check(L.mg_block_backward_f64(N.ptr(c_d), N.ptr(s_d), b, N.ptr(rot_d), N.ptr(tr_d), k, N.ptr(mu), N.ptr(p6),
+                                    N.ptr(al), n, N.ptr(gd["starts64"]), N.ptr(gd["order64"]), g, r, N.ptr(u_d),
+                                    N.ptr(d_mu), N.ptr(d_ab), N.ptr(d_al), N.ptr(d_pts), N.ptr(ws), ws.numel(),
+                                    dv.sptr()), "block_backward_f64")
+    return d_pts
+
+
+def _strict_render(field, gd, p6, al, coords, sids, rot, trans, k, g, r, psf):
+    b = coords.shape[0]
+    if psf is None:
+        out_i, out_c, out_x = _strict_call(None, field, gd, p6, al, coords, sids, rot, trans, k, g, r)
+        return RenderBatch(points=dv.to_host(out_x), intensities=dv.to_host(out_i),
+                           contributor_counts=dv.to_host(out_c))
+    t = psf.ntaps
+    xc, xs = _psf_expand(coords, sids, psf)
+    out_i, out_c, out_x = _strict_call(None, field, gd, p6, al, xc, xs, rot, trans, k, g, r)
+    it = dv.to_host(out_i).reshape(b, t)
+    ct = dv.to_host(out_c).reshape(b, t)
+    inten = np.zeros(b)
+    for j, w in enumerate(np.asarray(psf.weights, dtype=np.float64)):
+        inten += w * it[:, j]
+    return RenderBatch(points=dv.to_host(out_x).reshape(b, t, 3), intensities=inten,
+                       contributor_counts=ct.sum(axis=1))
 
 
 def _stage_psf(field, gd, p6, al, c_d, s_d, rot_d, tr_d, k, g, psf, with_h, radius):
@@ -249,6 +340,13 @@ def render_points_dense(field, samples, transforms=None):
             coords = np.where(sids[:, None] >= 0, moved, coords)
     _, _, _, p6, al = _activate_dev(field)
     n = field.count
+    if _strict_fp64:  # one cell holding every primitive in index order: all pairs, _kernels.py:147-162
+        gd = {"starts64": dv.to_dev(np.array([0, n], np.int64), torch.int64),
+              "order64": dv.to_dev(np.arange(n, dtype=np.int64), torch.int64)}
+        c = np.ascontiguousarray(coords, dtype=np.float64)
+        out_i, _, _ = _strict_call(None, field, gd, p6, al, c, np.full(c.shape[0], -1, np.int64),
+                                   np.zeros((1, 3, 3)), np.zeros((1, 3)), 0, 1, 0)
+        return dv.to_host(out_i)
     L = N.lib()
     mu = dv.to_dev(field.positions, torch.float64, (n, 3))
     pts = dv.to_dev(coords, torch.float64)
@@ -315,7 +413,14 @@ def render_backward(field, grid, transforms, samples, upstream, radius=None, pre
     d_al = dv.zeros((n,), torch.float64)
     t = 1 if slice_psf is None else slice_psf.ntaps
     off = dirs = None
-    if slice_psf is None:
+    if _strict_fp64:
+        if slice_psf is None:
+            d_pts = _strict_call(None, field, gd, p6, al, coords, sids, rot, trans, k, g, r, up, (d_mu, d_ab, d_al))
+        else:
+            xc, xs = _psf_expand(coords, sids, slice_psf)
+            upt = (up[:, None] * np.asarray(slice_psf.weights, dtype=np.float64)[None, :]).reshape(-1)
+            d_pts = _strict_call(None, field, gd, p6, al, xc, xs, rot, trans, k, g, r, upt, (d_mu, d_ab, d_al))
+    elif slice_psf is None:
         mu = dv.to_dev(field.positions, torch.float64, (n, 3))
         d_pts = dv.empty((b, 3), torch.float64)
         ws = dv.workspace(L.mg_block_workspace_bytes(b, n, g))
@@ -336,6 +441,9 @@ def render_backward(field, grid, transforms, samples, upstream, radius=None, pre
                 "backward")
         N.check(L.mg_backward_accumulators(N.ptr(acc), N.ptr(gd["order"]), n, N.ptr(al), N.ptr(d_mu), N.ptr(d_ab),
                                            N.ptr(d_al), st), "backward_accumulators")
+    if _strict_fp64 and slice_psf is not None and k:
+        off = dv.to_dev(np.asarray(slice_psf.offsets, dtype=np.float64), torch.float64)
+        dirs = dv.to_dev(np.asarray(slice_psf.through_dirs, dtype=np.float64).reshape(-1, 3), torch.float64)
     q = dv.to_dev(field.quaternions, torch.float64, (n, 4))
     s = dv.to_dev(field.log_scales, torch.float64, (n, 3))
     lg = dv.to_dev(field.intensity_logits, torch.float64, (n,))
@@ -409,6 +517,20 @@ def sample_volume(field, grid, residual, dims, bounds=((-1.0, -1.0, -1.0), (1.0,
         return Volume(data=np.zeros(dims), spacing=spacing, origin=origin)
     _, _, _, p6, al = _activate_dev(field)
     gd = _grid_dev(grid)
+    if _strict_fp64:  # render.py:394-408: render_points over voxel chunks, float64
+        gx, gy, gz = np.meshgrid(axes[0], axes[1], axes[2], indexing="ij")
+        pts = np.stack([gx.ravel(), gy.ravel(), gz.ravel()], axis=1)
+        out = np.empty(total)
+        for c0 in range(0, total, max(1, int(chunk))):
+            c1 = min(total, c0 + max(1, int(chunk)))
+            oi, _, _ = _strict_call(None, field, gd, p6, al, np.ascontiguousarray(pts[c0:c1]),
+                                    np.full(c1 - c0, -1, np.int64), np.zeros((1, 3, 3)), np.zeros((1, 3)), 0, g, r)
+            out[c0:c1] = dv.to_host(oi)
+        if residual is not None:
+            from .nrf import nrf_forward_device
+
+            out += dv.to_host(nrf_forward_device(residual, dv.to_dev(pts, torch.float32))).astype(np.float64)
+        return Volume(data=np.clip(out, 0.0, 1.0).reshape(dims), spacing=spacing, origin=origin)
     _, grec = _records(field, gd, p6, al)
     res_d = None
     if residual is not None:

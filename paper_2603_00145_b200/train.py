@@ -73,21 +73,27 @@ def _stream(name):
     return st
 
 
-def _freeze_gc_once():
-    """Move everything alive at the first Trainer construction (torch, numpy
-    and the caller's module state: several hundred thousand objects) out of
-    the cyclic collector's reach.  A full collection over them took 0.1-0.4 s
-    and landed at random inside the step loop (measured as 0.3 s stalls in a
-    0.7 s desk-scale reconstruction).  Objects created later are collected as
-    usual.  MGAUSS_GC_FREEZE=0 disables this."""
+def freeze_gc():
+    """Move everything alive now (torch, numpy and the caller's module state:
+    several hundred thousand objects) out of the cyclic collector's reach.  A
+    full collection over them took 0.1-0.4 s and landed at random inside a
+    step loop (measured as 0.3 s stalls in a 0.7 s desk-scale reconstruction).
+    Objects created later are collected as usual.  Process-wide, so it is
+    opt-in: the bench and reconstruction entry points call it; a Trainer calls
+    it at construction only when MGAUSS_GC_FREEZE=1."""
     global _GC_FROZEN
-    if _GC_FROZEN or os.environ.get("MGAUSS_GC_FREEZE", "1") == "0":
+    if _GC_FROZEN:
         return
     import gc
 
     gc.collect()
     gc.freeze()
     _GC_FROZEN = True
+
+
+def _freeze_gc_once():
+    if os.environ.get("MGAUSS_GC_FREEZE", "0") == "1":
+        freeze_gc()
 
 
 _PERM_PREFETCH_MIN = 1 << 16  # pools from this size draw epoch permutations ahead
@@ -259,17 +265,29 @@ def progressive_upsample_device(field: DeviceField, new_r: int) -> DeviceField:
     return DeviceField(pos, q, s, lg, new_r, torch.arange(n, dtype=torch.int32, device=pos.device))
 
 
-class _StepBuffers:
-    """Fixed-shape device buffers for one (N, B, HW, taps) configuration."""
+def _hyper_array(cfg):
+    """Host hyper-parameter block read by mg_gauss_update (9 doubles)."""
+    return np.array([cfg.lr_position, cfg.lr_rotation, cfg.lr_scale, cfg.lr_intensity, cfg.adam_beta1,
+                     cfg.adam_beta2, cfg.adam_eps, cfg.lambda_aniso, cfg.lambda_ratio], dtype=np.float64)
 
-    def __init__(self, n, g, b_total, ntaps, k):
+
+class _StepBuffers:
+    """Fixed-shape device buffers for one (N, rendered points, taps, K, NRF)
+    configuration.  Everything a distributed step all-reduces lives in two
+    flat buffers (acc10 + the NRF gradients in float32; the loss partials and
+    the per-slice transform gradients in float64), so the collective runs
+    in place on them with no copy in or out."""
+
+    def __init__(self, n, g, b_render, b_gather, ntaps, k, nrf_numel=0):
         L = N.lib()
-        ns = b_total * ntaps
+        ns = b_render * ntaps
         self.gkey = dv.empty((n,), torch.int32)
         self.gorder = dv.empty((n,), torch.int32)
         self.gstart = dv.empty((g ** 3 + 1,), torch.int32)
         self.grec = dv.empty((n, 12), torch.float32)
-        self.acc10 = dv.empty((n, 10), torch.float32)
+        self.flat32 = dv.empty((10 * n + nrf_numel,), torch.float32)
+        self.acc10 = self.flat32[:10 * n].view(n, 10)
+        self.nrf_numel = nrf_numel
         self.pkey = dv.empty((ns,), torch.int32)
         self.pinv = dv.empty((ns,), torch.int32)
         self.pstart = dv.empty((g ** 3 + 1,), torch.int32)
@@ -277,13 +295,15 @@ class _StepBuffers:
         self.xout = dv.empty((ns, 3), torch.float64)
         self.out4 = dv.empty((ns, 4), torch.float32)
         self.cnt = dv.empty((ns,), torch.int32)
-        self.pred = dv.empty((b_total,), torch.float32)
-        self.up = dv.empty((b_total,), torch.float32)
+        self.pred = dv.empty((b_render,), torch.float32)
+        self.up = dv.empty((b_render,), torch.float32)
         self.dpts = dv.empty((ns, 3), torch.float64)
         self.rot = dv.empty((max(k, 1), 3, 3), torch.float64)
-        self.g7 = dv.empty((max(k, 1), 7), torch.float64)
-        self.scratch12 = dv.empty((max(k, 1), 12), torch.float64)
-        self.scalars = dv.zeros((4,), torch.float64)  # data loss, aniso loss, ssim sum, spare
+        kk = max(k, 1)
+        self.flat64 = dv.zeros((4 + 7 * kk,), torch.float64)
+        self.scalars = self.flat64[:4]  # data loss, aniso loss, ssim sum, spare (non-reporting ranks' ssim)
+        self.g7 = self.flat64[4:].view(kk, 7)
+        self.scratch12 = dv.empty((kk, 12), torch.float64)
         self.err = dv.zeros((1,), torch.int32)
         wsb = max(L.mg_bin_workspace_bytes(n, g), L.mg_points_workspace_bytes(ns, g),
                   L.mg_forward_workspace_bytes(ns), L.mg_backward_workspace_bytes(n, g),
@@ -292,14 +312,73 @@ class _StepBuffers:
         self.ws_gauss = None  # side-stream workspaces (Gaussian binning, transform reduction)
         self.ws_tr = None
         self.ssim_ws = None
+        self.slice_pred = None  # strong-sharded SSIM: full-slice prediction / upstream
+        self.slice_up = None
+        self.idx = dv.empty((b_gather,), torch.int64)
+        self.coords = dv.empty((b_gather, 3), torch.float64)
+        self.sids = dv.empty((b_gather,), torch.int64)
+        self.tgt = dv.empty((b_gather,), torch.float32)
+        self.pairs = dv.zeros((1,), torch.int64)
+        # two pinned index staging slots (a slot is rewritten only after its
+        # previous H2D copy has completed)
+        self.idx_host = [torch.empty((b_gather,), dtype=torch.int64, pin_memory=True) for _ in range(2)]
+        self.idx_done = [None, None]
+        self.slot = 0
+        # device landing slots for the H2D copies, which run on a copy stream
+        # under the previous step; the step itself reads B.idx (a fixed
+        # address for the graph), filled by a short D2D copy
+        self.idx_stage = [dv.empty((b_gather,), torch.int64) for _ in range(2)]
+        self.stage_free = [None, None]
+        # two pinned loss-readback slots (pipelined steps read one while the next fills)
+        self.scalars_host = [torch.empty((4,), dtype=torch.float64, pin_memory=True) for _ in range(2)]
+        self.err_host = [torch.empty((1,), dtype=torch.int32, pin_memory=True) for _ in range(2)]
+        self.r_done = [None, None]
+        self.rslot = 0
+
+    def nrf_grad_flat(self):
+        return self.flat32[self.flat32.numel() - self.nrf_numel:]
+
+
+@dataclass(frozen=True)
+class StepPlan:
+    """Point layout of one step on this rank (SURVEY §8(e) sharding).
+
+    The pool-index list is [batch share (nbl) | slice pixels [s_lo, s_hi) |
+    the full slice (hw_full, target only: strong-sharded SSIM)]; the first
+    nbl + (s_hi - s_lo) points are rendered.  nb_norm is the GLOBAL batch size
+    the smooth-L1 mean divides by, so the all-reduced sums are the gradient
+    of the global loss."""
+
+    nbl: int
+    nb_norm: int
+    hw: tuple | None = None
+    s_lo: int = 0
+    s_hi: int = 0
+    full_slice: bool = False
+
+    @property
+    def render(self):
+        return self.nbl + (self.s_hi - self.s_lo)
+
+    @property
+    def gather(self):
+        return self.render + (self.hw[0] * self.hw[1] if self.full_slice else 0)
 
 
 class Trainer:
     """Owns the device field, transforms, optimizer state and the batch stream."""
 
     def __init__(self, cloud, transforms: TransformSet, config: TrainConfig, slice_grids=None,
-                 slice_psf: SlicePSF | None = None, graph=False, dist=None):
+                 slice_psf: SlicePSF | None = None, graph=False, dist=None, shard="strong"):
+        """``dist``: a torch.distributed group (NCCL on GPUs) for data
+        parallelism.  ``shard="strong"`` splits every step's global batch and
+        SSIM slice into contiguous per-rank shares (all ranks draw the same
+        batch from the reference's RNG stream), so N ranks train exactly the
+        reference's model; ``"weak"`` gives every rank its own full batch and
+        SSIM slice (its own RNG stream; global batch N x batch_points)."""
         config.validate()
+        if shard not in ("strong", "weak"):
+            raise ValueError("shard must be 'strong' or 'weak'")
         _freeze_gc_once()
         if config.use_ssim and not slice_grids:
             raise ValueError("use_ssim requires slice sample grids")
@@ -307,6 +386,13 @@ class Trainer:
         self.psf = slice_psf
         self.graph = graph
         self.dist = dist  # optional torch.distributed group for gradient all-reduce
+        self.shard = shard
+        if dist is not None:
+            import torch.distributed as tdist
+
+            self.rank, self.world = tdist.get_rank(dist), tdist.get_world_size(dist)
+        else:
+            self.rank, self.world = 0, 1
         self.coords = dv.to_dev(cloud.coords, torch.float64)
         self.intens = dv.to_dev(cloud.intensities, torch.float32)
         self.sids = dv.to_dev(cloud.slice_ids, torch.int64)
@@ -321,6 +407,8 @@ class Trainer:
         self.tv = dv.zeros((max(self.k, 1), 7), torch.float64)
         root = np.random.SeedSequence(config.seed)
         batch_ss, nrf_ss = root.spawn(2)
+        if shard == "weak" and self.rank > 0:  # rank 0 keeps the reference stream
+            batch_ss = np.random.SeedSequence(batch_ss.entropy, spawn_key=batch_ss.spawn_key + (1 << 20, self.rank))
         self.rng = np.random.default_rng(batch_ss)
         self.nrf = None
         if config.use_nrf:
@@ -351,9 +439,7 @@ class Trainer:
         self._bufs_key = None
         self._graph = None
         self._graph_key = None
-        self._hyper = np.array([config.lr_position, config.lr_rotation, config.lr_scale, config.lr_intensity,
-                                config.adam_beta1, config.adam_beta2, config.adam_eps, config.lambda_aniso,
-                                config.lambda_ratio], dtype=np.float64)
+        self._hyper = _hyper_array(config)
         if slice_psf is not None:
             self._psf_off = dv.to_dev(np.asarray(slice_psf.offsets, dtype=np.float64), torch.float64)
             self._psf_w = dv.to_dev(np.asarray(slice_psf.weights, dtype=np.float64), torch.float64)
@@ -443,12 +529,33 @@ class Trainer:
             self.src_coords, self.src_sids, self.src_tgt = self.coords, self.sids, self.intens
 
     def host_indices(self, idx, slice_j):
-        """Pool indices of one step: the batch, then the SSIM slice's pixels."""
+        """Pool indices of one step on this rank and its StepPlan: the batch
+        (share), then the SSIM slice's pixels (share), then -- strong sharding
+        over several ranks -- the whole slice again for the SSIM target."""
+        from .parallel import shard_range
+
         idx = np.asarray(idx, dtype=np.int64)
+        strong = self.world > 1 and self.shard == "strong"
+        nb_norm = len(idx) * (self.world if self.shard == "weak" else 1)
+        if strong:
+            lo, hi = shard_range(len(idx), self.rank, self.world)
+            idx = idx[lo:hi]
         if slice_j is None:
-            return idx, None
+            return idx, StepPlan(len(idx), nb_norm)
         hw = self._sg_shape[slice_j]
-        return np.concatenate([idx, self._sg_off[slice_j] + np.arange(hw[0] * hw[1], dtype=np.int64)]), hw
+        pix = self._sg_off[slice_j] + np.arange(hw[0] * hw[1], dtype=np.int64)
+        if strong:
+            s_lo, s_hi = shard_range(len(pix), self.rank, self.world)
+            return (np.concatenate([idx, pix[s_lo:s_hi], pix]),
+                    StepPlan(len(idx), nb_norm, hw, s_lo, s_hi, True))
+        return np.concatenate([idx, pix]), StepPlan(len(idx), nb_norm, hw, 0, len(pix))
+
+    def draw_step(self):
+        """Draw the next step's batch and SSIM slice from the host RNG stream
+        (train.py:348-363,408) -> (pool indices, StepPlan)."""
+        idx = self._next_batch()
+        slice_j = int(self.rng.integers(len(self.slice_grids))) if self.config.use_ssim else None
+        return self.host_indices(idx, slice_j)
 
     # -- one optimizer step ----------------------------------------------------
     # -- checkpoint state: the reference Trainer's tree (train.py:514-583) ----
@@ -504,6 +611,7 @@ class Trainer:
 
         cfg = TrainConfig.from_dict(state["config"])
         self.config = cfg
+        self._hyper = _hyper_array(cfg)  # the fused Gaussian Adam reads the resumed config's values
         f = state["field"]
         dims = tuple(int(d) for d in f["lattice_dims"])
         self.field = DeviceField.from_host(GaussianField(
@@ -572,12 +680,9 @@ class Trainer:
             pass
 
     def step(self, sync=True):
-        cfg = self.config
         self._apply_milestones()
-        idx = self._next_batch()
-        slice_j = int(self.rng.integers(len(self.slice_grids))) if cfg.use_ssim else None
-        all_idx, hw = self.host_indices(idx, slice_j)
-        report = self._device_step(all_idx, len(idx), hw, sync)
+        all_idx, plan = self.draw_step()
+        report = self._device_step(all_idx, plan, sync)
         self.iteration += 1
         self.reports.append(report)
         return report
@@ -588,14 +693,11 @@ class Trainer:
         returns the last one).  The host-side batch draw and index upload of
         this step overlap the device running the previous step; every step
         still uploads its indices and reads back its losses."""
-        cfg = self.config
         self._apply_milestones()
-        idx = self._next_batch()
-        slice_j = int(self.rng.integers(len(self.slice_grids))) if cfg.use_ssim else None
-        all_idx, hw = self.host_indices(idx, slice_j)
+        all_idx, plan = self.draw_step()
         prev = getattr(self, "_pending", None)
-        self._device_step(all_idx, len(idx), hw, sync=False)
-        self._pending = self._enqueue_readback(self._bufs, hw)
+        self._device_step(all_idx, plan, sync=False)
+        self._pending = self._enqueue_readback(self._bufs, plan)
         self.iteration += 1
         rep = None
         if prev is not None:
@@ -612,39 +714,24 @@ class Trainer:
         self.reports.append(rep)
         return rep
 
-    def _buffers(self, b_total):
+    def _buffers(self, plan):
+        """Step buffers for a StepPlan (or a plain rendered-point count)."""
+        if not isinstance(plan, StepPlan):
+            plan = StepPlan(int(plan), int(plan))
         g = self.field.resolution
-        key = (self.field.count, g, b_total, self.ntaps, self.k)
+        nrf_numel = self._nrf_numel() if self.nrf is not None else 0
+        key = (self.field.count, g, plan.render, plan.gather, self.ntaps, self.k, nrf_numel)
         if self._bufs_key != key:
-            self._bufs = _StepBuffers(self.field.count, g, b_total, self.ntaps, self.k)
-            self._bufs.idx = dv.empty((b_total,), torch.int64)
-            self._bufs.coords = dv.empty((b_total, 3), torch.float64)
-            self._bufs.sids = dv.empty((b_total,), torch.int64)
-            self._bufs.tgt = dv.empty((b_total,), torch.float32)
-            self._bufs.pairs = dv.zeros((1,), torch.int64)
-            # two pinned index staging slots (a slot is rewritten only after its
-            # previous H2D copy has completed) and one pinned loss readback slot
-            self._bufs.idx_host = [torch.empty((b_total,), dtype=torch.int64, pin_memory=True) for _ in range(2)]
-            self._bufs.idx_done = [None, None]
-            self._bufs.slot = 0
-            # device landing slots for the H2D copies, which run on a copy
-            # stream under the previous step; the step itself reads B.idx
-            # (a fixed address for the graph), filled by a short D2D copy
-            self._bufs.idx_stage = [dv.empty((b_total,), torch.int64) for _ in range(2)]
-            self._bufs.stage_free = [None, None]
-            # two pinned loss-readback slots (pipelined steps read one while the next fills)
-            self._bufs.scalars_host = [torch.empty((4,), dtype=torch.float64, pin_memory=True) for _ in range(2)]
-            self._bufs.err_host = [torch.empty((1,), dtype=torch.int32, pin_memory=True) for _ in range(2)]
-            self._bufs.r_done = [None, None]
-            self._bufs.rslot = 0
-            self._bufs_key = key
+            self._bufs = None
             self._graph = None
+            self._bufs = _StepBuffers(self.field.count, g, plan.render, plan.gather, self.ntaps, self.k, nrf_numel)
+            self._bufs_key = key
         return self._bufs
 
-    def load_indices(self, all_idx):
+    def load_indices(self, all_idx, plan):
         """Stage one step's pool indices (host array or device tensor) into the
         fixed index buffer, on the current stream."""
-        B = self._buffers(len(all_idx))
+        B = self._buffers(plan)
         if isinstance(all_idx, torch.Tensor):
             B.idx.copy_(all_idx, non_blocking=True)
             return B
@@ -672,35 +759,51 @@ class Trainer:
     def _copy_stream(self):
         return _stream("h2d")
 
-    def _body(self, B, nb, hw):
+    def _body(self, B, plan):
         N.check(N.lib().mg_gather_batch(N.ptr(B.idx), B.idx.numel(), N.ptr(self.src_coords), N.ptr(self.src_sids),
                                         N.ptr(self.src_tgt), N.ptr(B.coords), N.ptr(B.sids), N.ptr(B.tgt),
                                         dv.sptr()), "gather_batch")
-        self._launch(B, B.coords, B.sids, B.tgt, nb, hw)
+        self._launch(B, plan)
 
-    def _device_step(self, all_idx, nb, hw, sync):
-        cfg = self.config
-        B = self.load_indices(all_idx)
+    def run_device_step(self, plan):
+        """Run one step on the indices already staged by ``load_indices``:
+        replay the captured graph of this plan, or enqueue it eagerly."""
+        B = self._bufs
+        if self._graph is not None and self._graph_key == (plan, self.nrf_active):
+            self._graph.replay()
+        else:
+            self._body(B, plan)
+
+    def _device_step(self, all_idx, plan, sync):
+        B = self.load_indices(all_idx, plan)
         # the step (incl. the NCCL all-reduce, whose communicator the eager
         # warm-up step initialises) is captured once per shape and replayed
-        use_graph = self.graph
+        # (a gloo group cannot be captured: distributed gloo steps run eagerly)
+        use_graph = self.graph and not self._gloo()
         if use_graph:
-            key = (nb, hw, self.nrf_active)
+            key = (plan, self.nrf_active)
             if self._graph is None or self._graph_key != key:
-                self._body(B, nb, hw)  # eager warm-up of this shape (also lazily inits kernels)
+                self._body(B, plan)  # eager warm-up of this shape (also lazily inits kernels)
                 torch.cuda.synchronize()
                 self._graph = None  # release the previous shape's graph (and its pool) first
-                self._graph, self._graph_key = self._capture(lambda: self._body(B, nb, hw)), key
+                self._graph, self._graph_key = self._capture(lambda: self._body(B, plan)), key
                 # the warm-up already performed this step's update; undo nothing: the
                 # captured graph is replayed from the next step on.
             else:
                 self._graph.replay()
         else:
-            self._body(B, nb, hw)
+            self._body(B, plan)
         if not sync:
             return LossReport(self.iteration, float("nan"), float("nan"), float("nan"), float("nan"),
                               self.field.resolution, self.nrf_active)
-        return self._resolve(self._enqueue_readback(B, hw))
+        return self._resolve(self._enqueue_readback(B, plan))
+
+    def _gloo(self):
+        if self.dist is None:
+            return False
+        import torch.distributed as tdist
+
+        return tdist.get_backend(self.dist) == "gloo"
 
     def _capture(self, fn):
         """Capture ``fn``'s launches into a CUDA graph on a side stream.
@@ -722,7 +825,7 @@ class Trainer:
         cur.wait_stream(cs)
         return g
 
-    def _enqueue_readback(self, B, hw):
+    def _enqueue_readback(self, B, plan):
         """Async D2H of this step's loss sums and error flag into a pinned slot."""
         k = B.rslot
         B.rslot ^= 1
@@ -733,12 +836,12 @@ class Trainer:
         ev = torch.cuda.Event()
         ev.record()
         B.r_done[k] = ev
-        return (B, k, ev, self.iteration, hw, self.field.resolution, self.nrf_active)
+        return (B, k, ev, self.iteration, plan, self.field.resolution, self.nrf_active)
 
     def _resolve(self, pending):
         """LossReport of a step whose readback was enqueued (waits for it)."""
         cfg = self.config
-        B, k, ev, iteration, hw, res, nrf_on = pending
+        B, k, ev, iteration, plan, res, nrf_on = pending
         ev.synchronize()
         sc = B.scalars_host[k].numpy().copy()
         err = int(B.err_host[k][0])
@@ -749,21 +852,26 @@ class Trainer:
         data = float(sc[0])
         aniso = float(sc[1]) if cfg.use_aniso else 0.0
         ssim = 0.0
-        if hw is not None:
-            ssim = 1.0 - float(sc[2]) / ((hw[0] - 10) * (hw[1] - 10))
+        if plan.hw is not None:
+            h, w = plan.hw
+            # weak sharding: one slice per rank, the loss is their mean
+            nsl = self.world if (self.shard == "weak" and self.dist is not None) else 1
+            ssim = 1.0 - float(sc[2]) / (nsl * (h - 10) * (w - 10))
         total = data + cfg.lambda_ssim * ssim + cfg.lambda_aniso * aniso
         if not np.isfinite(total):
             raise NonFiniteLoss(f"non-finite loss at iteration {iteration}")
         return LossReport(iteration, total, data, ssim, aniso, res, nrf_on)
 
-    def _launch(self, B, coords, sids, tgt, nb, hw):
+    def _launch(self, B, plan):
         """Enqueue the whole step on the current stream (graph-capturable)."""
         cfg = self.config
         L = N.lib()
         st = dv.sptr()
         f = self.field
         n, g, r = f.count, f.resolution, cfg.block_radius
-        bt = coords.shape[0]
+        bt = plan.render
+        nb, hw = plan.nbl, plan.hw
+        coords, sids, tgt = B.coords[:bt], B.sids[:bt], B.tgt[:bt]
         t = self.ntaps
         ns = bt * t
         ws = B.ws
@@ -799,24 +907,15 @@ class Trainer:
                                     N.ptr(B.pred), None, N.ptr(B.pairs), st), "finish")
         nrf_cache = None
         if self.nrf_active:
-            from .nrf import fused_supported, nrf_forward_cached, nrf_forward_fused
+            from .nrf import nrf_forward_fused
 
             xc = self._centre_points(B, bt, t)
-            if fused_supported(self.nrf) and os.environ.get("MGAUSS_NRF_FUSED", "1") != "0":
-                _, nrf_cache = nrf_forward_fused(self.nrf, xc, pred_add=B.pred)  # pred += r in the kernel
-            else:
-                res, nrf_cache = nrf_forward_cached(self.nrf, xc)
-                B.pred.add_(res)
-        # losses (train.py:424-436)
-        N.check(L.mg_smooth_l1(N.ptr(B.pred), N.ptr(tgt), nb, N.ptr(B.up), N.ptr(B.scalars[0:1]), st), "smooth_l1")
+            _, nrf_cache = nrf_forward_fused(self.nrf, xc, pred_add=B.pred)  # pred += r in the kernel
+        # losses (train.py:424-436): smooth-L1 mean over the GLOBAL batch
+        N.check(L.mg_smooth_l1_scaled(N.ptr(B.pred), N.ptr(tgt), nb, 1.0 / plan.nb_norm, N.ptr(B.up),
+                                      N.ptr(B.scalars[0:1]), st), "smooth_l1")
         if hw is not None:
-            h, w = hw
-            need = L.mg_ssim_workspace_bytes(h, w)
-            if B.ssim_ws is None or B.ssim_ws.numel() < need:
-                B.ssim_ws = dv.empty((need,), torch.uint8)
-            N.check(L.mg_ssim_loss_grad(N.ptr(B.pred[nb:]), N.ptr(tgt[nb:]), h, w, cfg.lambda_ssim,
-                                        N.ptr(B.up[nb:]), N.ptr(B.scalars[2:3]), N.ptr(B.ssim_ws),
-                                        B.ssim_ws.numel(), st), "ssim")
+            self._ssim(B, plan, tgt, st)
         # backward (render_backward): upstream -> point records, d_points; Gaussian-major pass
         N.check(L.mg_backward_points(None, N.ptr(B.up), bt, t, N.ptr(wts), N.ptr(B.pinv), N.ptr(B.out4),
                                      N.ptr(B.prec), N.ptr(B.dpts), st), "backward_points")
@@ -836,19 +935,14 @@ class Trainer:
             main.wait_stream(side)
         ng = None
         if nrf_cache is not None:
-            from .nrf import nrf_backward, nrf_backward_fused
+            from .nrf import nrf_backward_fused
 
-            # gradients land in one persistent flat buffer (all-reduced with the
-            # step's other partial sums when distributed, then the fused Adam)
-            gv = self._nrf_grad_views()
+            # gradients land in the step's flat float32 buffer behind acc10
+            # (all-reduced in place with it when distributed, then the fused Adam)
+            gv = self._nrf_grad_views(B)
             nl = len(self.nrf.weights)
             gws, gbs = [gv[f"w{i}"] for i in range(nl)], [gv[f"b{i}"] for i in range(nl)]
-            if isinstance(nrf_cache[0], str):  # ("fused", t, z)
-                _, _, dp = nrf_backward_fused(self.nrf, self._centre_x, B.up, nrf_cache, out=(gws, gbs))
-            else:
-                dws, dbs, dp = nrf_backward(self.nrf, self._centre_x, B.up, nrf_cache)
-                for dst, src in zip(gws + gbs, dws + dbs):
-                    dst.copy_(src)
+            _, _, dp = nrf_backward_fused(self.nrf, self._centre_x, B.up, nrf_cache, out=(gws, gbs))
             ng = True
             if self.k:
                 dp64 = dp.double().contiguous()
@@ -870,7 +964,43 @@ class Trainer:
                                         self.k, cfg.lr_transform, cfg.adam_beta1, cfg.adam_beta2, cfg.adam_eps,
                                         N.ptr(self.counters[1:2]), st), "transform_adam")
         if ng is not None:
-            self._nrf_adam()
+            self._nrf_adam(B)
+
+    def _ssim(self, B, plan, tgt, st):
+        """SSIM loss + upstream of the step's slice (ssim.py:59-122).
+
+        Unsharded / weak: this rank rendered the whole slice.  Strong over N
+        ranks: each rank rendered pixels [s_lo, s_hi); the full prediction is
+        assembled by an all-reduce(sum) of zero-padded shares (exact: one
+        non-zero term per pixel), every rank evaluates the identical SSIM
+        gradient and keeps its own pixels' upstream; rank 0 alone reports the
+        SSIM sum."""
+        L = N.lib()
+        h, w = plan.hw
+        nb = plan.nbl
+        need = L.mg_ssim_workspace_bytes(h, w)
+        if B.ssim_ws is None or B.ssim_ws.numel() < need:
+            B.ssim_ws = dv.empty((need,), torch.uint8)
+        weak = self.dist is not None and self.shard == "weak"
+        scale = self.config.lambda_ssim / (self.world if weak else 1)
+        if not plan.full_slice:
+            N.check(L.mg_ssim_loss_grad(N.ptr(B.pred[nb:]), N.ptr(tgt[nb:]), h, w, scale, N.ptr(B.up[nb:]),
+                                        N.ptr(B.scalars[2:3]), N.ptr(B.ssim_ws), B.ssim_ws.numel(), st), "ssim")
+            return
+        import torch.distributed as tdist
+
+        hw_n = h * w
+        if B.slice_pred is None or B.slice_pred.numel() != hw_n:
+            B.slice_pred = dv.empty((hw_n,), torch.float32)
+            B.slice_up = dv.empty((hw_n,), torch.float32)
+        B.slice_pred.zero_()
+        B.slice_pred[plan.s_lo:plan.s_hi].copy_(B.pred[nb:])
+        tdist.all_reduce(B.slice_pred, op=tdist.ReduceOp.SUM, group=self.dist)
+        full_tgt = B.tgt[plan.render:plan.render + hw_n]
+        acc = B.scalars[2:3] if self.rank == 0 else B.scalars[3:4]
+        N.check(L.mg_ssim_loss_grad(N.ptr(B.slice_pred), N.ptr(full_tgt), h, w, scale, N.ptr(B.slice_up),
+                                    N.ptr(acc), N.ptr(B.ssim_ws), B.ssim_ws.numel(), st), "ssim")
+        B.up[nb:].copy_(B.slice_up[plan.s_lo:plan.s_hi])
 
     def _side_stream(self):
         return _stream("side")
@@ -895,20 +1025,22 @@ class Trainer:
     def nrf_t(self, value):
         self._nrf_tdev = torch.full((), float(value), dtype=torch.float64, device=dv.device())
 
-    def _nrf_grad_views(self):
-        """Persistent flat NRF gradient buffer with one view per parameter."""
+    def _nrf_numel(self):
+        return sum(v.numel() for v in self.nrf.parameter_arrays().values())
+
+    def _nrf_grad_views(self, B):
+        """One view per NRF parameter into the tail of B's flat float32 buffer."""
         params = self.nrf.parameter_arrays()
-        key = tuple((k, tuple(v.shape)) for k, v in params.items())
-        if getattr(self, "_nrf_gkey", None) != key:
-            self._nrf_gflat = dv.zeros((sum(v.numel() for v in params.values()),), torch.float32)
+        flat = B.nrf_grad_flat()
+        if getattr(B, "nrf_views", None) is None:
             views, off = {}, 0
             for k, v in params.items():
-                views[k] = self._nrf_gflat[off:off + v.numel()].view(v.shape)
+                views[k] = flat[off:off + v.numel()].view(v.shape)
                 off += v.numel()
-            self._nrf_gviews, self._nrf_gkey = views, key
-        return self._nrf_gviews
+            B.nrf_views = views
+        return B.nrf_views
 
-    def _nrf_adam(self):
+    def _nrf_adam(self, B):
         """AdamState.step("nrf", ...) (train.py:251-271): one launch over all
         NRF tensors, with the device step counter read and advanced in the
         kernel so the update replays inside the graph."""
@@ -917,7 +1049,7 @@ class Trainer:
         cfg = self.config
         params = self.nrf.parameter_arrays()
         keys = list(params)
-        gv = self._nrf_grad_views()
+        gv = self._nrf_grad_views(B)
 
         def arr(ts):
             return (ctypes.c_void_p * len(ts))(*[t.data_ptr() for t in ts])
@@ -930,18 +1062,14 @@ class Trainer:
                                     cfg.lr_nrf, cfg.adam_beta1, cfg.adam_beta2, cfg.adam_eps, dv.sptr()), "nrf_adam")
 
     def _allreduce(self, B):
-        """One flat all-reduce(sum) of the step's partial sums (parallel.py)."""
-        from .parallel import FlatAllReduce
+        """All-reduce(sum) in place of the step's two flat partial-sum buffers:
+        acc10 (+ the NRF gradients while the NRF is active) in float32, the
+        loss partials and per-slice transform gradients in float64 (parallel.py)."""
+        import torch.distributed as tdist
 
-        nrf_g = self._nrf_gflat if (self.nrf_active and getattr(self, "_nrf_gflat", None) is not None) else None
-        key = (id(B), None if nrf_g is None else id(nrf_g))
-        if getattr(self, "_ar_key", None) != key:
-            f32 = [B.acc10] + ([nrf_g] if nrf_g is not None else [])
-            f64 = [B.scalars] + ([B.g7] if self.k else [])
-            self._ar = (FlatAllReduce(f32, self.dist), FlatAllReduce(f64, self.dist))
-            self._ar_key = key
-        for ar in self._ar:
-            ar()
+        n32 = B.flat32.numel() if self.nrf_active else 10 * self.field.count
+        tdist.all_reduce(B.flat32[:n32], op=tdist.ReduceOp.SUM, group=self.dist)
+        tdist.all_reduce(B.flat64, op=tdist.ReduceOp.SUM, group=self.dist)
 
     def run(self, iterations=None):
         target = self.config.total_iters if iterations is None else self.iteration + iterations

@@ -39,9 +39,13 @@ def test_fused_nrf_matches_reference_golden():
     assert_grad_close(_h(dp), z["d_points"], name="d_points")
 
 
-@pytest.mark.parametrize("n", [1, 63, 5000])
+@pytest.mark.parametrize("n", [1, 63, 5000, 20000, 70001])
 def test_fused_nrf_matches_torch_mirror(n):
-    from paper_2603_00145_b200.nrf import nrf_backward, nrf_backward_fused, nrf_forward_cached, nrf_forward_fused
+    """n >= 8192 makes CTAs of the dW pass take several 128-point chunks, so
+    the double-buffered cp.async prefetch (wait_group 1) is exercised; 70001
+    is ragged."""
+    from nrf_mirror import nrf_backward, nrf_forward_cached
+    from paper_2603_00145_b200.nrf import nrf_backward_fused, nrf_forward_fused
 
     rng = np.random.default_rng(n)
     widths = (39, 64, 64, 64, 64, 1)
@@ -65,6 +69,15 @@ def test_fused_nrf_matches_torch_mirror(n):
     g2 = nrf_backward_fused(f, x, up, c1)
     for a, b in zip(g1[0] + g1[1] + [g1[2]], g2[0] + g2[1] + [g2[2]]):
         assert torch.equal(a, b)
+
+
+def test_unsupported_width_raises():
+    from paper_2603_00145_b200.errors import UnsupportedResidualField
+    from paper_2603_00145_b200.nrf import ResidualField, nrf_forward_device
+
+    f = ResidualField.create(np.random.default_rng(1), hidden=(32, 32))
+    with pytest.raises(UnsupportedResidualField):
+        nrf_forward_device(f, torch.zeros((4, 3), dtype=torch.float32, device="cuda"))
 
 
 def test_fused_nrf_empty_batch_zero_grads():

@@ -1,20 +1,84 @@
 """Data parallelism for the Gaussian path.
 
 Training: the field, grid and transforms are replicated on every rank; each
-rank renders its own share of the step's sample points and produces partial
-per-Gaussian accumulators (acc10 = {S, T, A6}), per-slice transform
-gradients and loss partial sums.  All of these are plain sums over points,
-so ONE all-reduce(sum) of a flat buffer per step gives every rank the exact
-full-batch totals; every rank then runs the identical (deterministic)
-epilogue + Adam, so no parameter broadcast is needed.  Backend: NCCL over
-NVLink on GPUs, gloo on CPU (tests).
+rank renders its share of the step's sample points and produces partial
+per-Gaussian accumulators (acc10 = {S, T, A6}), NRF gradients, per-slice
+transform gradients and loss partial sums.  All of these are plain sums over
+points (the smooth-L1 mean divides by the GLOBAL batch size on every rank),
+so one in-place all-reduce(sum) of the step's flat buffers gives every rank
+the exact global-batch totals; every rank then runs the identical
+(deterministic) epilogue + Adam, so no parameter broadcast is needed.
 
-Inference: z-slab (axis-0) ownership of the output volume, no collective.
+Two ways to share the points (plan_step):
+  strong -- every rank draws the SAME global batch from the reference's RNG
+            stream and renders a contiguous share of it and of the SSIM
+            slice (the reference's own contiguous point chunks,
+            render.py:60-77, 296-317); the SSIM slice prediction is
+            assembled by one small all-reduce.  N ranks train exactly the
+            model one rank (and the reference) trains.
+  weak   -- every rank draws its own batch and SSIM slice (own RNG stream):
+            the global batch is N x batch_points, the data loss their mean
+            and the SSIM loss the mean over the N slices.
+
+Backend: NCCL over NVLink on GPUs (captured in the step's CUDA graph), gloo
+for CPU tests and for several ranks sharing one GPU (eager steps).
+
+Inference: z-slab (axis-0) ownership of the output volume, no collective
+until the optional gather (volume_slabs).
 """
 
 from __future__ import annotations
 
+from dataclasses import dataclass
+
+import numpy as np
 import torch
+
+
+@dataclass(frozen=True)
+class StepPlan:
+    """Point layout of one step on one rank.
+
+    The pool-index list is [batch share (nbl) | slice pixels [s_lo, s_hi) |
+    the whole slice again (target only; strong sharding over >1 rank)]; the
+    first nbl + (s_hi - s_lo) points are rendered.  nb_norm is the GLOBAL
+    batch size the smooth-L1 mean divides by."""
+
+    nbl: int
+    nb_norm: int
+    hw: tuple | None = None
+    s_lo: int = 0
+    s_hi: int = 0
+    full_slice: bool = False
+
+    @property
+    def render(self):
+        return self.nbl + (self.s_hi - self.s_lo)
+
+    @property
+    def gather(self):
+        return self.render + (self.hw[0] * self.hw[1] if self.full_slice else 0)
+
+
+def plan_step(idx, pix, hw, rank: int, world: int, shard: str):
+    """(pool indices, StepPlan) of one step on `rank` of `world`.
+
+    idx: the batch drawn by this rank (strong: the global batch, identical on
+    every rank); pix: pool indices of the SSIM slice's pixels (or None)."""
+    idx = np.asarray(idx, dtype=np.int64)
+    strong = world > 1 and shard == "strong"
+    nb_norm = len(idx) * (world if shard == "weak" else 1)
+    if strong:
+        lo, hi = shard_range(len(idx), rank, world)
+        idx = idx[lo:hi]
+    if pix is None:
+        return idx, StepPlan(len(idx), nb_norm)
+    pix = np.asarray(pix, dtype=np.int64)
+    hw = tuple(int(v) for v in hw)
+    if strong:
+        s_lo, s_hi = shard_range(len(pix), rank, world)
+        return np.concatenate([idx, pix[s_lo:s_hi], pix]), StepPlan(len(idx), nb_norm, hw, s_lo, s_hi, True)
+    return np.concatenate([idx, pix]), StepPlan(len(idx), nb_norm, hw, 0, len(pix))
 
 
 def shard_range(n: int, rank: int, world: int):

@@ -30,6 +30,7 @@ from . import _device as dv
 from . import _native as N
 from .core import TransformSet, lattice_node_index, lattice_node_positions  # noqa: F401
 from .errors import NonFiniteLoss, ShrinkNotAllowed
+from .parallel import StepPlan, plan_step
 from .render import SlicePSF, sample_volume_device
 
 DEFAULT_SCHEDULE = ((0, 70), (500, 100), (1000, 130), (2000, 165), (3000, 200))
@@ -339,32 +340,6 @@ class _StepBuffers:
         return self.flat32[self.flat32.numel() - self.nrf_numel:]
 
 
-@dataclass(frozen=True)
-class StepPlan:
-    """Point layout of one step on this rank (SURVEY §8(e) sharding).
-
-    The pool-index list is [batch share (nbl) | slice pixels [s_lo, s_hi) |
-    the full slice (hw_full, target only: strong-sharded SSIM)]; the first
-    nbl + (s_hi - s_lo) points are rendered.  nb_norm is the GLOBAL batch size
-    the smooth-L1 mean divides by, so the all-reduced sums are the gradient
-    of the global loss."""
-
-    nbl: int
-    nb_norm: int
-    hw: tuple | None = None
-    s_lo: int = 0
-    s_hi: int = 0
-    full_slice: bool = False
-
-    @property
-    def render(self):
-        return self.nbl + (self.s_hi - self.s_lo)
-
-    @property
-    def gather(self):
-        return self.render + (self.hw[0] * self.hw[1] if self.full_slice else 0)
-
-
 class Trainer:
     """Owns the device field, transforms, optimizer state and the batch stream."""
 
@@ -532,23 +507,11 @@ class Trainer:
         """Pool indices of one step on this rank and its StepPlan: the batch
         (share), then the SSIM slice's pixels (share), then -- strong sharding
         over several ranks -- the whole slice again for the SSIM target."""
-        from .parallel import shard_range
-
-        idx = np.asarray(idx, dtype=np.int64)
-        strong = self.world > 1 and self.shard == "strong"
-        nb_norm = len(idx) * (self.world if self.shard == "weak" else 1)
-        if strong:
-            lo, hi = shard_range(len(idx), self.rank, self.world)
-            idx = idx[lo:hi]
-        if slice_j is None:
-            return idx, StepPlan(len(idx), nb_norm)
-        hw = self._sg_shape[slice_j]
-        pix = self._sg_off[slice_j] + np.arange(hw[0] * hw[1], dtype=np.int64)
-        if strong:
-            s_lo, s_hi = shard_range(len(pix), self.rank, self.world)
-            return (np.concatenate([idx, pix[s_lo:s_hi], pix]),
-                    StepPlan(len(idx), nb_norm, hw, s_lo, s_hi, True))
-        return np.concatenate([idx, pix]), StepPlan(len(idx), nb_norm, hw, 0, len(pix))
+        pix, hw = None, None
+        if slice_j is not None:
+            hw = self._sg_shape[slice_j]
+            pix = self._sg_off[slice_j] + np.arange(hw[0] * hw[1], dtype=np.int64)
+        return plan_step(idx, pix, hw, self.rank, self.world, self.shard)
 
     def draw_step(self):
         """Draw the next step's batch and SSIM slice from the host RNG stream
@@ -1078,8 +1041,18 @@ class Trainer:
         return self.reports
 
     # -- inference (train.py:509-512, render.py:379-408) -------------------------
-    def render_volume(self, dims, bounds, include_nrf=True):
+    def render_volume(self, dims, bounds, include_nrf=True, dist=None, gather=True):
+        """Inference sampling of the trained field (train.py:509-512,
+        render.py:379-408) on a node-inclusive grid, clipped to [0, 1].
+
+        With ``dist`` (a torch.distributed group) every rank
+        samples only its z-slab [i0, i1) of axis 0 (parallel.slab_ranges), so
+        the sampling has no collective.  ``gather=True`` then all-gathers the
+        slabs (one collective of the padded slabs) and every rank returns the
+        whole Volume; ``gather=False`` returns this rank's slab as a Volume
+        whose origin is the slab's first plane."""
         from .core import Volume
+        from .parallel import slab_ranges
         from .render import grid_coordinates
 
         f = self.field
@@ -1092,16 +1065,33 @@ class Trainer:
                               f.count, N.ptr(B.gorder), N.ptr(B.grec), N.ptr(B.err), dv.sptr()), "activate")
         dims = tuple(int(d) for d in dims)
         axes, spacing = grid_coordinates(dims, bounds)
+        rank, world = 0, 1
+        if dist is not None:
+            import torch.distributed as tdist
+
+            rank, world = tdist.get_rank(dist), tdist.get_world_size(dist)
+        slabs = slab_ranges(dims[0], world)
+        i0, i1 = slabs[rank]
         res = None
-        if include_nrf and self.nrf_active:
+        if include_nrf and self.nrf_active and i1 > i0:
             from .nrf import nrf_forward_device
 
-            gx, gy, gz = np.meshgrid(axes[0], axes[1], axes[2], indexing="ij")
+            gx, gy, gz = np.meshgrid(axes[0][i0:i1], axes[1], axes[2], indexing="ij")
             pts = dv.to_dev(np.stack([gx.ravel(), gy.ravel(), gz.ravel()], 1), torch.float32)
-            res = nrf_forward_device(self.nrf, pts).reshape(dims)
-        out = sample_volume_device(B.grec, f.count, B.gstart, g, r, dims, bounds, residual=res)
-        return Volume(data=dv.to_host(out).astype(np.float64), spacing=spacing,
-                      origin=np.array([axes[0][0], axes[1][0], axes[2][0]]))
+            res = nrf_forward_device(self.nrf, pts).reshape((i1 - i0,) + dims[1:])
+        out = sample_volume_device(B.grec, f.count, B.gstart, g, r, dims, bounds, i0=i0, i1=i1, residual=res)
+        if world > 1 and gather:
+            import torch.distributed as tdist
+
+            pmax = max(b - a for a, b in slabs)
+            pad = torch.zeros((pmax,) + dims[1:], dtype=torch.float32, device=out.device)
+            pad[:i1 - i0].copy_(out)
+            parts = [torch.empty_like(pad) for _ in range(world)]
+            tdist.all_gather(parts, pad, group=dist)
+            out = torch.cat([parts[q][:b - a] for q, (a, b) in enumerate(slabs)])
+            i0 = 0
+        origin = np.array([axes[0][min(i0, dims[0] - 1)], axes[1][0], axes[2][0]])
+        return Volume(data=dv.to_host(out).astype(np.float64), spacing=spacing, origin=origin)
 
     def transforms_host(self):
         return TransformSet(dv.to_host(self.tq), dv.to_host(self.tt))

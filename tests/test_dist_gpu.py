@@ -1,9 +1,17 @@
-"""The data-parallel training path (parallel.py FlatAllReduce over NCCL,
-captured in the step's CUDA graph) at world size 1: the all-reduce is then
-an identity, so the trainer must evolve bit-identically to the plain one
-(the step is deterministic).  Multi-rank sums are covered on CPU by
-tests/test_parallel_cpu.py (gloo, world size 2)."""
+"""The data-parallel training path (parallel.py).
 
+* world size 1 over NCCL (the all-reduce captured in the step's CUDA graph):
+  an identity, so the trainer must evolve bit-identically to the plain one;
+* world size 2 (two processes sharing the box's one GPU over gloo, eager
+  steps, host-side collectives): strong sharding must train the SAME model
+  as one rank -- losses and parameters within fp32 reduction-order noise --
+  and weak sharding must keep the ranks' replicas identical; the z-slab
+  sharded volume must equal the single-rank volume.
+"""
+
+import os
+import subprocess
+import sys
 from types import SimpleNamespace
 
 import numpy as np
@@ -49,3 +57,51 @@ def test_nccl_path_world1_matches_plain_trainer():
         b.close()
     finally:
         tdist.destroy_process_group()
+
+
+def _spawn_world(tmp_path, world, shard, steps, use_nrf):
+    port = str(29600 + (os.getpid() % 200))
+    out = str(tmp_path / f"{shard}")
+    worker = os.path.join(os.path.dirname(os.path.abspath(__file__)), "dist_worker.py")
+    procs = [subprocess.Popen([sys.executable, worker, str(r), str(world), port, shard, str(steps),
+                               "1" if use_nrf else "0", out]) for r in range(world)]
+    for p in procs:
+        assert p.wait(timeout=600) == 0
+    return [dict(np.load(f"{out}_r{r}.npz")) for r in range(world)]
+
+
+@pytest.mark.parametrize("use_nrf", [False, True])
+def test_strong_sharding_world2_matches_world1(tmp_path, use_nrf):
+    """2 ranks x half the batch and half the SSIM slice == 1 rank x the whole
+    batch: every loss term (smooth-L1 over the global batch, SSIM of the
+    assembled slice, aniso once) and every parameter group, through a lattice
+    milestone (step 3) and the NRF switch (step 2)."""
+    from dist_worker import make_trainer, snapshot
+
+    z = load_golden("io")
+    steps = 5
+    ranks = _spawn_world(tmp_path, 2, "strong", steps, use_nrf)
+    tr = make_trainer(z, None, "strong", use_nrf)
+    ref = snapshot(tr, [tr.step() for _ in range(steps)])
+    vol = tr.render_volume((13, 9, 7), ((-1.0,) * 3, (1.0,) * 3)).data
+    tr.close()
+    for res in ranks:
+        np.testing.assert_allclose(res["losses"], ref["losses"], rtol=2e-6, atol=1e-9)
+        for name in ("positions", "quaternions", "log_scales", "logits", "tq", "tt"):
+            np.testing.assert_allclose(res[name], ref[name], rtol=0, atol=2e-6, err_msg=name)
+        if use_nrf:
+            np.testing.assert_allclose(res["nrf_w2"], ref["nrf_w2"], rtol=0, atol=2e-6)
+        np.testing.assert_allclose(res["volume"], vol, rtol=1e-5, atol=1e-6)
+    for name in ("positions", "logits", "tq"):  # replicas stay identical
+        np.testing.assert_array_equal(ranks[0][name], ranks[1][name])
+
+
+def test_weak_sharding_world2_replicas_agree(tmp_path):
+    """Weak sharding: own batches per rank, one all-reduce of the partial sums
+    -> every rank applies the identical update (no parameter broadcast)."""
+    ranks = _spawn_world(tmp_path, 2, "weak", 4, True)
+    for name in ("positions", "quaternions", "log_scales", "logits", "tq", "tt", "nrf_w2"):
+        np.testing.assert_array_equal(ranks[0][name], ranks[1][name], err_msg=name)
+    np.testing.assert_array_equal(ranks[0]["losses"], ranks[1]["losses"])
+    assert np.all(np.isfinite(ranks[0]["losses"]))
+    assert np.all(ranks[0]["losses"][:, 2] < 1.0)  # mean SSIM loss of the two ranks' slices

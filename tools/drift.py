@@ -22,16 +22,10 @@ def main():
 
     from paper_2603_00145_b200.train import Trainer
 
-    data, cloud, grids, psf, cfg = bench.make_workload(a.config, 0)
+    data, cloud, grids, psf, cfg = bench.make_workload(a.config, 0, final_only=True)
     tr = Trainer(cloud, data.transforms, cfg, slice_grids=grids, slice_psf=psf, graph=True)
     for r in range(a.rounds + 1):
-        idx_list = []
-        for _ in range(5):
-            idx = tr._next_batch()
-            j = int(tr.rng.integers(len(tr.slice_grids)))
-            all_idx, hw = tr.host_indices(idx, j)
-            idx_list.append(torch.from_numpy(all_idx).cuda())
-        kt = bench.kernel_times(tr, idx_list, cfg.batch_points, hw)
+        kt = bench.kernel_times(tr, 5)
         gk = tr._bufs.gkey[: tr.field.count].cpu().numpy().astype(np.int64) if hasattr(tr._bufs, "gkey") else None
         extra = ""
         if gk is not None:

@@ -18,31 +18,26 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--config", default="C2")
+    ap.add_argument("--train", type=int, default=3, help="training steps before timing (drifted field)")
     a = ap.parse_args()
     import torch
 
     from paper_2603_00145_b200.train import Trainer
 
-    data, cloud, grids, psf, cfg = bench.make_workload(a.config, 0)
+    data, cloud, grids, psf, cfg = bench.make_workload(a.config, 0, final_only=True)
     tr = Trainer(cloud, data.transforms, cfg, slice_grids=grids, slice_psf=psf, graph=False)
-    for _ in range(3):
-        tr.step()
-    idx_list = []
-    for _ in range(a.reps):
-        idx = tr._next_batch()
-        j = int(tr.rng.integers(len(tr.slice_grids)))
-        all_idx, hw = tr.host_indices(idx, j)
-        idx_list.append(torch.from_numpy(all_idx).cuda())
-    kt = bench.kernel_times(tr, idx_list, cfg.batch_points, hw)
-    B = tr._bufs
+    for _ in range(max(3, a.train)):
+        tr.step(sync=False)
+    kt = bench.kernel_times(tr, a.reps)
+    steps = [tr.draw_step() for _ in range(a.reps)]
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for ix in idx_list:
-        tr.load_indices(ix)
-        tr._body(B, cfg.batch_points, hw)
+    for all_idx, plan in steps:
+        B = tr.load_indices(torch.from_numpy(all_idx).cuda(), plan)
+        tr._body(B, plan)
     e1.record()
     torch.cuda.synchronize()
-    kt["step_ms_eager"] = e0.elapsed_time(e1) / len(idx_list)
+    kt["step_ms_eager"] = e0.elapsed_time(e1) / len(steps)
     p = kt["pairs_per_launch"]
     kt["fwd_gpairs_s"] = p / kt["forward_ms"] / 1e6
     kt["bwd_gpairs_s"] = p / kt["backward_ms"] / 1e6

@@ -26,7 +26,7 @@ def main():
 
     from paper_2603_00145_b200.train import Trainer
 
-    data, cloud, grids, psf, cfg = bench.make_workload(a.config, 0)
+    data, cloud, grids, psf, cfg = bench.make_workload(a.config, 0, final_only=True)
     tr = Trainer(cloud, data.transforms, cfg, slice_grids=grids, slice_psf=psf, graph=True)
     for _ in range(a.train):
         tr.step_pipelined()

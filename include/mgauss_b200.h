@@ -173,6 +173,14 @@ int mg_smooth_l1(const float *pred, const float *target, int64_t b, float *upstr
  * are exactly the global mean and its gradient. */
 int mg_smooth_l1_scaled(const float *pred, const float *target, int64_t b, double scale, float *upstream_out,
                         double *loss_acc, void *stream);
+/* aniso_loss_grad (train.py:128-147), float64: grad (n,3) overwritten with
+ * d(loss)/d(log_scales), loss_acc += loss. */
+int mg_aniso_loss_grad_f64(const double *log_scales, int64_t n, double lambda_ratio, double *grad,
+                           double *loss_acc, void *stream);
+/* AdamState.step on one float64 tensor (train.py:251-271); t = the group's
+ * post-increment step count.  param, m, v updated in place. */
+int mg_adam_f64(double *param, const double *grad, double *m, double *v, int64_t n, int64_t t, double lr,
+                double beta1, double beta2, double eps, void *stream);
 /* Residual field r(x) = 0.1 tanh(MLP(enc(x))) with the reference widths
  * 39-64-64-64-64-1, SiLU, 6 Fourier bands (nrf.py:23-182; ResidualField.forward /
  * backward).  w[l] are (fan_in, fan_out) row-major float32, bias[l] (fan_out).

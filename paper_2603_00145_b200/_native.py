@@ -56,6 +56,8 @@ SIGNATURES = {
     "mg_sample_volume": (ctypes.c_int, [P, I64, P, I64, I64, I64, I64, I64, P, P, I64, I64, P, P, P, SZ, P]),
     "mg_smooth_l1": (ctypes.c_int, [P, P, I64, P, P, P]),
     "mg_smooth_l1_scaled": (ctypes.c_int, [P, P, I64, D, P, P, P]),
+    "mg_aniso_loss_grad_f64": (ctypes.c_int, [P, I64, D, P, P, P]),
+    "mg_adam_f64": (ctypes.c_int, [P, P, P, P, I64, I64, D, D, D, D, P]),
     "mg_nrf_forward": (ctypes.c_int, [P, I64, P, P, P, P, P, P, P]),
     "mg_nrf_backward_workspace_bytes": (SZ, [I64]),
     "mg_nrf_backward": (ctypes.c_int, [P, I64, P, P, P, P, P, P, P, P, P, SZ, P]),

@@ -429,6 +429,20 @@ int mg_smooth_l1(const float* pred, const float* target, int64_t b, float* up_ou
   return mg_smooth_l1_scaled(pred, target, b, b > 0 ? 1.0 / (double)b : 0.0, up_out, loss_acc, stream);
 }
 
+int mg_aniso_loss_grad_f64(const double* log_scales, int64_t n, double lambda_ratio, double* grad,
+                           double* loss_acc, void* stream) {
+  if (n < 0) return fail("mg_aniso_loss_grad_f64: n < 0");
+  launch_aniso_f64(log_scales, n, lambda_ratio, grad, loss_acc, S(stream));
+  return cuda_status();
+}
+
+int mg_adam_f64(double* param, const double* grad, double* m, double* v, int64_t n, int64_t t, double lr,
+                double beta1, double beta2, double eps, void* stream) {
+  if (n < 0 || t < 1) return fail("mg_adam_f64: need n >= 0 and t >= 1");
+  launch_adam_f64(param, grad, m, v, n, t, lr, beta1, beta2, eps, S(stream));
+  return cuda_status();
+}
+
 int mg_smooth_l1_scaled(const float* pred, const float* target, int64_t b, double scale, float* up_out,
                         double* loss_acc, void* stream) {
   if (b < 0) return fail("mg_smooth_l1: b < 0");

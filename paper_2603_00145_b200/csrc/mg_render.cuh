@@ -58,6 +58,10 @@ void launch_transform_grads(const double* dpoints, const double* coords, const i
 size_t transform_grads_ws_bytes(int64_t k);
 void launch_smooth_l1(const float* pred, const float* target, int64_t b, double scale, float* up_out,
                       double* loss_acc, cudaStream_t st);
+void launch_aniso_f64(const double* ls, int64_t n, double lambda_ratio, double* grad, double* loss_acc,
+                      cudaStream_t st);
+void launch_adam_f64(double* p, const double* g, double* m, double* v, int64_t n, int64_t t, double lr, double b1,
+                     double b2, double eps, cudaStream_t st);
 // fused residual field (mg_nrf.cu)
 size_t nrf_backward_ws_bytes(int64_t b);
 void launch_nrf_forward(const float* x, int64_t b, const float* const* w, const float* const* bias, float* pred_add,

@@ -697,6 +697,67 @@ void launch_transform_grads(const double* dpoints, const double* coords, const i
   }
   MG_LAUNCH(transform_chain_kernel<<<gridn(k), 256, 0, st>>>(acc12, tq, k, out7, accumulate));
 }
+// Standalone aniso_loss_grad (train.py:128-147) in float64: grad (n,3) is
+// overwritten, loss_acc += sum(excess) / n.
+__global__ void aniso_f64_kernel(const double* __restrict__ ls, int64_t n, double lambda_ratio,
+                                 double* __restrict__ grad, double* __restrict__ loss_acc) {
+  double local = 0.0;
+  GRID_LOOP(i, n) {
+    const double s[3] = {ls[3 * i], ls[3 * i + 1], ls[3 * i + 2]};
+    int hi = 0, lo = 0;
+    for (int a = 1; a < 3; ++a) {
+      if (s[a] > s[hi]) hi = a;
+      if (s[a] < s[lo]) lo = a;
+    }
+    const double ratio = exp(s[hi] - s[lo]);
+    const double excess = ratio - lambda_ratio;
+    double gr[3] = {0.0, 0.0, 0.0};
+    if (excess > 0) {
+      local += excess;
+      const double c = ratio / (double)n;
+      gr[hi] += c;
+      gr[lo] -= c;
+    }
+    for (int a = 0; a < 3; ++a) grad[3 * i + a] = gr[a];
+  }
+  __shared__ double s_red[32];
+  for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(MG_FULL, local, o);
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = local;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? s_red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(MG_FULL, v, o);
+    if (threadIdx.x == 0 && v != 0.0) atomicAdd(loss_acc, v / (double)n);
+  }
+}
+void launch_aniso_f64(const double* ls, int64_t n, double lambda_ratio, double* grad, double* loss_acc,
+                      cudaStream_t st) {
+  if (n > 0) MG_LAUNCH(aniso_f64_kernel<<<gridn(n), 256, 0, st>>>(ls, n, lambda_ratio, grad, loss_acc));
+}
+
+// AdamState.step on one float64 tensor (train.py:251-271), t = the
+// post-increment step count of the group.
+__global__ void adam_f64_kernel(double* __restrict__ p, const double* __restrict__ g, double* __restrict__ m,
+                                double* __restrict__ v, int64_t n, double lr, double b1, double b2, double eps,
+                                double bc1, double bc2) {
+  GRID_LOOP(i, n) {
+    const double gi = g[i];
+    double mi = m[i] * b1;
+    mi += (1.0 - b1) * gi;
+    double vi = v[i] * b2;
+    vi += (1.0 - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    p[i] -= lr * (mi / bc1) / (sqrt(vi / bc2) + eps);
+  }
+}
+void launch_adam_f64(double* p, const double* g, double* m, double* v, int64_t n, int64_t t, double lr, double b1,
+                     double b2, double eps, cudaStream_t st) {
+  if (n > 0)
+    MG_LAUNCH(adam_f64_kernel<<<gridn(n), 256, 0, st>>>(p, g, m, v, n, lr, b1, b2, eps, 1.0 - pow(b1, (double)t),
+                                                        1.0 - pow(b2, (double)t)));
+}
+
 void launch_smooth_l1(const float* pred, const float* target, int64_t b, double scale, float* up_out,
                       double* loss_acc, cudaStream_t st) {
   if (b > 0) MG_LAUNCH(smooth_l1_kernel<<<gridn(b), 256, 0, st>>>(pred, target, b, scale, up_out, loss_acc));

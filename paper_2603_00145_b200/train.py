@@ -1124,3 +1124,114 @@ def ssim_loss_grad(pred, target):
     N.check(N.lib().mg_ssim_loss_grad(N.ptr(p), N.ptr(t), h, w, 1.0, N.ptr(up), N.ptr(acc), N.ptr(ws), ws.numel(),
                                       dv.sptr()), "ssim")
     return 1.0 - float(acc.item()) / ((h - 10) * (w - 10)), dv.to_host(up).astype(np.float64).reshape(h, w)
+
+
+# ---------------------------------------------------------------------------
+# The reference's host-level training API (train.py:108-290), same names and
+# semantics, computed by the device kernels: float64 numpy in and out.
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class SliceGrid:
+    """Full native in-plane sample grid of one acquired slice (train.py:282-290)."""
+
+    coords: np.ndarray  # (H * W, 3), C-order matching target.ravel()
+    target: np.ndarray  # (H, W)
+    slice_id: int
+
+
+def smooth_l1(pred, target):
+    """Huber loss (delta 1), mean over the batch (train.py:108-113); mg_smooth_l1."""
+    return smooth_l1_loss_grad(pred, target)[0]
+
+
+def smooth_l1_grad(pred, target):
+    """d(mean Huber)/dpred (train.py:116-120); mg_smooth_l1."""
+    return smooth_l1_loss_grad(pred, target)[1].reshape(np.shape(pred))
+
+
+def aniso_loss_grad(field, lambda_ratio):
+    """(loss, d loss / d log_scales) of the anisotropy hinge (train.py:128-147),
+    float64 on the device (mg_aniso_loss_grad_f64)."""
+    s = dv.to_dev(np.asarray(field.log_scales, dtype=np.float64).reshape(-1, 3), torch.float64)
+    n = s.shape[0]
+    grad = dv.empty((n, 3), torch.float64)
+    acc = dv.zeros((1,), torch.float64)
+    N.check(N.lib().mg_aniso_loss_grad_f64(N.ptr(s), n, float(lambda_ratio), N.ptr(grad), N.ptr(acc), dv.sptr()),
+            "aniso_loss_grad")
+    return float(acc.item()), dv.to_host(grad)
+
+
+def aniso_loss(field, lambda_ratio):
+    """train.py:123-125."""
+    return aniso_loss_grad(field, lambda_ratio)[0]
+
+
+def progressive_upsample(field, new_resolution):
+    """train.py:157-218 on the device (mg_upsample): trilinear logits and
+    log-scales, sign-aligned NLERP quaternions, positions on the new lattice.
+    Interpolation runs in float32 (the trainer's parameter precision)."""
+    from .core import GaussianField
+
+    new_r = int(new_resolution)
+    old_r = int(field.lattice_dims[0])
+    if new_r < old_r:
+        raise ShrinkNotAllowed(f"cannot shrink lattice {old_r} -> {new_r}")
+    up = progressive_upsample_device(DeviceField.from_host(field), new_r).to_host()
+    return GaussianField(lattice_node_positions(new_r), up.quaternions, up.log_scales, up.intensity_logits,
+                         (new_r, new_r, new_r), lattice_node_index(new_r))
+
+
+def init_field(cloud, resolution, logit_eps=1e-4):
+    """Uniform lattice field with logit(mean sample intensity) per cell
+    (train.py:221-236) on the device (mg_cell_keys_f64 + segmented means)."""
+    from .core import GaussianField
+
+    r = int(resolution)
+    f = init_field_device(dv.to_dev(np.asarray(cloud.coords, np.float64).reshape(-1, 3), torch.float64),
+                          dv.to_dev(np.asarray(cloud.intensities, np.float64).ravel(), torch.float32), r,
+                          logit_eps).to_host()
+    return GaussianField(lattice_node_positions(r), f.quaternions, f.log_scales, f.intensity_logits, (r, r, r),
+                         lattice_node_index(r))
+
+
+class AdamState:
+    """Named parameter groups with first/second moments and step counters
+    (train.py:239-279).  ``step`` updates the caller's float64 arrays in place;
+    the update runs in float64 on the device (mg_adam_f64)."""
+
+    def __init__(self, beta1=0.9, beta2=0.999, eps=1e-8):
+        self.beta1, self.beta2, self.eps = beta1, beta2, eps
+        self.groups = {}
+
+    def reset_group(self, name):
+        self.groups.pop(name, None)
+
+    def step(self, name, params, grads, lr):
+        g = self.groups.setdefault(name, {"t": 0, "m": {}, "v": {}})
+        g["t"] += 1
+        t = g["t"]
+        L = N.lib()
+        for key, param in params.items():
+            if key not in g["m"]:
+                g["m"][key] = np.zeros_like(param, dtype=np.float64)
+                g["v"][key] = np.zeros_like(param, dtype=np.float64)
+            p = dv.to_dev(param, torch.float64)
+            gr = dv.to_dev(np.asarray(grads[key], dtype=np.float64), torch.float64)
+            m = dv.to_dev(g["m"][key], torch.float64)
+            v = dv.to_dev(g["v"][key], torch.float64)
+            N.check(L.mg_adam_f64(N.ptr(p), N.ptr(gr), N.ptr(m), N.ptr(v), p.numel(), t, float(lr), self.beta1,
+                                  self.beta2, self.eps, dv.sptr()), "adam")
+            param[...] = dv.to_host(p).reshape(param.shape)
+            g["m"][key][...] = dv.to_host(m).reshape(param.shape)
+            g["v"][key][...] = dv.to_host(v).reshape(param.shape)
+
+    def state_dict(self):
+        return {name: {"t": g["t"], "m": {k: a.copy() for k, a in g["m"].items()},
+                       "v": {k: a.copy() for k, a in g["v"].items()}} for name, g in self.groups.items()}
+
+    def load_state_dict(self, state):
+        self.groups = {name: {"t": int(g["t"]), "m": {k: np.array(a, dtype=np.float64) for k, a in g["m"].items()},
+                              "v": {k: np.array(a, dtype=np.float64) for k, a in g["v"].items()}}
+                       for name, g in state.items()}

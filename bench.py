@@ -312,7 +312,7 @@ def kernel_times(tr, n=3):
 
     L = N.lib()
     fwd, bwd, upd, pairs, launches = [], [], [], [], []
-    orig = L.mg_forward, L.mg_backward, L.mg_gauss_update
+    orig = L.mg_forward, L.mg_backward, L.mg_gauss_update_inv, L.mg_gauss_update
 
     class Timed:
         def __init__(self, fn, sink):
@@ -327,7 +327,8 @@ def kernel_times(tr, n=3):
             return rc
 
     try:
-        L.mg_forward, L.mg_backward, L.mg_gauss_update = Timed(orig[0], fwd), Timed(orig[1], bwd), Timed(orig[2], upd)
+        L.mg_forward, L.mg_backward = Timed(orig[0], fwd), Timed(orig[1], bwd)
+        L.mg_gauss_update_inv, L.mg_gauss_update = Timed(orig[2], upd), Timed(orig[3], upd)
         for _ in range(n):
             all_idx, plan = tr.draw_step()
             B = tr.load_indices(torch.from_numpy(all_idx).cuda(), plan)
@@ -337,7 +338,7 @@ def kernel_times(tr, n=3):
             torch.cuda.synchronize()
             pairs.append(int(B.cnt.sum().item()))
     finally:
-        L.mg_forward, L.mg_backward, L.mg_gauss_update = orig
+        L.mg_forward, L.mg_backward, L.mg_gauss_update_inv, L.mg_gauss_update = orig
     torch.cuda.synchronize()
     return {"forward_ms": float(np.mean([a.elapsed_time(b) for a, b in fwd])),
             "backward_ms": float(np.mean([a.elapsed_time(b) for a, b in bwd])),

@@ -218,6 +218,14 @@ int mg_gather_batch(const int64_t *idx, int64_t n, const double *pool_coords, co
 int mg_gauss_update(const float *acc10, const int32_t *cell_indices, int64_t n, float *pos, float *quat,
                     float *log_scales, float *logits, float *m, float *v, const double *hyper_host,
                     int32_t use_aniso, const int32_t *t_dev, double *aniso_acc, void *stream);
+/* Same update walking the ORIGINAL Gaussian order (coalesced parameter and
+ * moment rows): inv[i] = the sorted position of Gaussian i (the inverse of
+ * cell_indices, mg_invert_permutation).  Bit-identical results. */
+int mg_gauss_update_inv(const float *acc10, const int32_t *inv, int64_t n, float *pos, float *quat,
+                        float *log_scales, float *logits, float *m, float *v, const double *hyper_host,
+                        int32_t use_aniso, const int32_t *t_dev, double *aniso_acc, void *stream);
+/* inv[perm[p]] = p for a permutation of 0..n-1 (int32). */
+int mg_invert_permutation(const int32_t *perm, int64_t n, int32_t *inv, void *stream);
 int mg_transform_adam(double *t_quats, double *t_trans, const double *grad7, double *m7, double *v7, int64_t k,
                       double lr, double beta1, double beta2, double eps, const int32_t *t_dev, void *stream);
 /* node_of_old[(i*R+j)*R+k] = primitive id at lattice node (i,j,k) */

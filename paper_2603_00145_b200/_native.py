@@ -68,6 +68,8 @@ SIGNATURES = {
     "mg_counter_incr": (ctypes.c_int, [P, I32, P]),
     "mg_gather_batch": (ctypes.c_int, [P, I64, P, P, P, P, P, P, P]),
     "mg_gauss_update": (ctypes.c_int, [P, P, I64, P, P, P, P, P, P, P, I32, P, P, P]),
+    "mg_gauss_update_inv": (ctypes.c_int, [P, P, I64, P, P, P, P, P, P, P, I32, P, P, P]),
+    "mg_invert_permutation": (ctypes.c_int, [P, I64, P, P]),
     "mg_transform_adam": (ctypes.c_int, [P, P, P, P, P, I64, D, D, D, D, P, P]),
     "mg_upsample": (ctypes.c_int, [P, P, P, P, I64, I64, P, P, P, P, P]),
     "mg_block_workspace_bytes": (SZ, [I64, I64, I64]),

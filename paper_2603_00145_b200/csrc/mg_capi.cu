@@ -508,7 +508,20 @@ int mg_counter_incr(int32_t* c, int32_t n, void* stream) {
 int mg_gauss_update(const float* acc10, const int32_t* order, int64_t n, float* pos, float* quat, float* ls,
                     float* lg, float* m, float* v, const double* hyper, int32_t use_aniso, const int32_t* t_dev,
                     double* aniso_acc, void* stream) {
-  launch_gauss_update(acc10, order, n, pos, quat, ls, lg, m, v, hyper, use_aniso, t_dev, aniso_acc, S(stream));
+  launch_gauss_update(acc10, order, 0, n, pos, quat, ls, lg, m, v, hyper, use_aniso, t_dev, aniso_acc, S(stream));
+  return cuda_status();
+}
+
+int mg_gauss_update_inv(const float* acc10, const int32_t* inv, int64_t n, float* pos, float* quat, float* ls,
+                        float* lg, float* m, float* v, const double* hyper, int32_t use_aniso, const int32_t* t_dev,
+                        double* aniso_acc, void* stream) {
+  launch_gauss_update(acc10, inv, 1, n, pos, quat, ls, lg, m, v, hyper, use_aniso, t_dev, aniso_acc, S(stream));
+  return cuda_status();
+}
+
+int mg_invert_permutation(const int32_t* perm, int64_t n, int32_t* inv, void* stream) {
+  if (n < 0) return fail("mg_invert_permutation: n < 0");
+  launch_invert_perm(perm, n, inv, S(stream));
   return cuda_status();
 }
 

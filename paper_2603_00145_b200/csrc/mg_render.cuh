@@ -76,9 +76,10 @@ void launch_ssim(const float* pred, const float* tgt, int H, int W, double scale
                  void* ws, cudaStream_t st);
 void launch_quat_to_rot(const double* q, int64_t k, double* rot, cudaStream_t st);
 void launch_counter_incr(int* c, int n, cudaStream_t st);
-void launch_gauss_update(const float* acc10, const int* order, int64_t n, float* pos, float* quat, float* ls,
-                         float* lg, float* mom_m, float* mom_v, const double* hyper, int use_aniso,
+void launch_gauss_update(const float* acc10, const int* perm, int by_inv, int64_t n, float* pos, float* quat,
+                         float* ls, float* lg, float* mom_m, float* mom_v, const double* hyper, int use_aniso,
                          const int* t_dev, double* aniso_acc, cudaStream_t st);
+void launch_invert_perm(const int* perm, int64_t n, int* inv, cudaStream_t st);
 void launch_transform_adam(double* tq, double* tt, const double* g7, double* m7, double* v7, int k, double lr,
                            double b1, double b2, double eps, const int* t_dev, cudaStream_t st);
 void launch_upsample(const float* q_old, const float* s_old, const float* l_old, const int* node_of_old, int ro, int rn,

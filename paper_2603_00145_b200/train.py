@@ -97,7 +97,8 @@ def _freeze_gc_once():
         freeze_gc()
 
 
-_PERM_PREFETCH_MIN = 1 << 16  # pools from this size draw epoch permutations ahead
+_PERM_PREFETCH_MIN = 1 << 16
+_UPD_SORTED = os.environ.get("MGAUSS_UPD_SORTED", "0") == "1"  # A/B: update walking the sorted order  # pools from this size draw epoch permutations ahead
 
 
 @dataclass
@@ -284,6 +285,7 @@ class _StepBuffers:
         ns = b_render * ntaps
         self.gkey = dv.empty((n,), torch.int32)
         self.gorder = dv.empty((n,), torch.int32)
+        self.ginv = dv.empty((n,), torch.int32)  # sorted position of each Gaussian (coalesced update walk)
         self.gstart = dv.empty((g ** 3 + 1,), torch.int32)
         self.grec = dv.empty((n, 12), torch.float32)
         self.flat32 = dv.empty((10 * n + nrf_numel,), torch.float32)
@@ -853,6 +855,7 @@ class Trainer:
                              N.ptr(B.ws_gauss), B.ws_gauss.numel(), ss), "bin")
         N.check(L.mg_activate(N.ptr(f.positions), N.ptr(f.quaternions), N.ptr(f.log_scales), N.ptr(f.logits), n,
                               N.ptr(B.gorder), N.ptr(B.grec), N.ptr(B.err), ss), "activate")
+        N.check(L.mg_invert_permutation(N.ptr(B.gorder), n, N.ptr(B.ginv), ss), "invert_permutation")
         # points: transforms, PSF taps, bin
         if self.k:
             N.check(L.mg_quat_to_rot_f64(N.ptr(self.tq), self.k, N.ptr(B.rot), st))
@@ -918,7 +921,8 @@ class Trainer:
         # updates (train.py:461-477): epilogue + aniso + Adam fused; transforms; NRF
         N.check(L.mg_counter_incr(N.ptr(self.counters), 2, st))
         hyper = self._hyper
-        N.check(L.mg_gauss_update(N.ptr(B.acc10), N.ptr(B.gorder), n, N.ptr(f.positions), N.ptr(f.quaternions),
+        upd, perm = (L.mg_gauss_update, B.gorder) if _UPD_SORTED else (L.mg_gauss_update_inv, B.ginv)
+        N.check(upd(N.ptr(B.acc10), N.ptr(perm), n, N.ptr(f.positions), N.ptr(f.quaternions),
                                   N.ptr(f.log_scales), N.ptr(f.logits), N.ptr(self.m), N.ptr(self.v),
                                   hyper.ctypes.data_as(N.P), 1 if cfg.use_aniso else 0, N.ptr(self.counters[0:1]),
                                   N.ptr(B.scalars[1:2]), st), "gauss_update")

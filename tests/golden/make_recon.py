@@ -1,7 +1,13 @@
 """Reference desk-scale reconstruction (configs/desk64.cfg) -> tests/golden/recon_desk64.npz.
 
     PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \\
-        python tests/golden/make_recon.py [threads]
+        python tests/golden/make_recon.py [threads] [--long]
+
+--long: the same data with the reference's default training length (4,000
+iterations, train.py:56) -- lattice 0:16,500:24,1000:32,1800:40,2800:48, NRF
+from 1,600 -- written to recon_desk64_long.npz (trajectory, PSNR, runtime and
+the reconstructed volume only; the inputs are recon_desk64.npz's, which the
+same seed reproduces).
 
 Runs the REFERENCE pipeline exactly as `mgauss reconstruct` does
 (cli.py:111-141: simulate, devoxelize, estimated transforms, slice grids,
@@ -35,10 +41,20 @@ OUT = os.path.dirname(os.path.abspath(__file__))
 CFG = "/root/reference/pkg/configs/desk64.cfg"
 
 
+LONG = dict(total_iters=4000, resolution_schedule=((0, 16), (500, 24), (1000, 32), (1800, 40), (2800, 48)),
+            nrf_activation_iter=1600)
+
+
 def main():
-    threads = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+    import dataclasses
+
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    long_run = "--long" in sys.argv
+    threads = int(args[0]) if args else 1
     render.set_num_threads(threads)
     bundle = mio.load_config(CFG)
+    if long_run:
+        bundle = dataclasses.replace(bundle, train=dataclasses.replace(bundle.train, **LONG))
     gt, stacks = simulate_stacks(bundle.sim, bundle.train.seed)
     cloud = devoxelize(stacks, bundle.sim.foreground_threshold)
     ts = normalized_transforms(stacks, cloud.world_map, "estimated")
@@ -63,6 +79,13 @@ def main():
     pred = (vol.data * cloud.intensity_scale).astype(np.float32).astype(np.float64)
     db = psnr(pred, gt.data.astype(np.float32).astype(np.float64))
     print(f"PSNR {db:.4f} dB, {runtime:.1f} s on {threads} thread(s)")
+    if long_run:
+        np.savez_compressed(
+            os.path.join(OUT, "recon_desk64_long.npz"), psnr_db=db, runtime_s=runtime, threads=threads,
+            losses=np.array(losses), recon=pred.astype(np.float32), schedule=np.array(LONG["resolution_schedule"]),
+            nrf_activation_iter=LONG["nrf_activation_iter"], total_iters=LONG["total_iters"],
+            batch_points=bundle.train.batch_points, seed=bundle.train.seed)
+        return
     np.savez_compressed(
         os.path.join(OUT, "recon_desk64.npz"),
         coords=cloud.coords, intensities=cloud.intensities, slice_ids=cloud.slice_ids,

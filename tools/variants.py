@@ -14,6 +14,10 @@ LIBDIR = os.path.join(ROOT, "paper_2603_00145_b200", "_lib")
 
 def main():
     mode, specs = sys.argv[1], sys.argv[2:]
+    extra = []
+    if "--" in specs:  # run: arguments after -- go to kbench
+        extra = specs[specs.index("--") + 1:]
+        specs = specs[:specs.index("--")]
     if mode == "build":
         from paper_2603_00145_b200 import _build
         for sp in specs:
@@ -24,7 +28,7 @@ def main():
     else:
         for name in specs:
             env = dict(os.environ, MGAUSS_B200_LIB=os.path.join(LIBDIR, f"var_{name}.so"))
-            r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "kbench.py")], env=env,
+            r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "kbench.py"), *extra], env=env,
                                capture_output=True, text=True)
             print("==", name, (r.stdout.strip().splitlines() or [r.stderr[-400:]])[-1], flush=True)
 

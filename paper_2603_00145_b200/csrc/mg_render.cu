@@ -209,11 +209,35 @@ struct Window {
   float inv_nj;  // exact column -> (i, j) split for ncol < 2^22
 };
 
+// cell -> (ci, cj, ck) with two float-reciprocal divisions: (n + 0.5) * (1/g)
+// is exact after truncation while the quotient's fractional part (>= 0.5/g
+// away from an integer) exceeds the float rounding, n * 2^-23 / g: holds for
+// every n < 2^21 at g <= 2^10 (host-guarded: larger grids take the integer
+// path).  Replaces two integer div/mod sequences per item (~45 instructions).
+#ifndef MG_FAST_SPLIT
+#define MG_FAST_SPLIT 1
+#endif
+#ifndef MG_BWD_SMEM_STORE
+#define MG_BWD_SMEM_STORE 0  // smem f2 reduction: fewer instructions but 2.27 -> 2.32 ms at C4 (latency)
+#endif
+__device__ __forceinline__ void split_cell(int cell, int g, int& ci, int& cj, int& ck) {
+  if (MG_FAST_SPLIT && g * g * g <= (1 << 21)) {
+    const float inv_g = 1.0f / (float)g;
+    const int t = (int)(((float)cell + 0.5f) * inv_g);
+    ck = cell - t * g;
+    ci = (int)(((float)t + 0.5f) * inv_g);
+    cj = t - ci * g;
+  } else {
+    ck = cell % g;
+    const int t = cell / g;
+    cj = t % g;
+    ci = t / g;
+  }
+}
+
 __device__ __noinline__ Window make_window(int cell, int g, int r) {
-  int ck = cell % g;
-  int t = cell / g;
-  int cj = t % g;
-  int ci = t / g;
+  int ci, cj, ck;
+  split_cell(cell, g, ci, cj, ck);
   Window w;
   w.ilo = max(ci - r, 0);
   int ihi = min(ci + r, g - 1);
@@ -1065,6 +1089,78 @@ __device__ __noinline__ LaneSegs build_lane_segs_pair(const Window& w, int c0, i
   return L;
 }
 
+#ifndef MG_PAIR_INLINE
+#define MG_PAIR_INLINE 1
+#endif
+// Inlined pair builder: the window arrives as scalars in registers (the
+// noinline form took it by reference, i.e. from local memory, reloading six
+// fields per column, and rebuilt the global-memory descriptor for every
+// load), and the four CSR bounds of a column are int32-indexed from one base.
+// Per item ~335 -> ~120 instructions at C4.
+__device__ __forceinline__ LaneSegs build_lane_segs_pair_inl(int ilo, int jlo, int nj, int ncol, float inv_nj,
+                                                             int klo, int kend, int kae, int kbs, int g,
+                                                             const int* __restrict__ starts, PairSmem& ps,
+                                                             int lane) {
+  LaneSegs L;
+  int2 t[4];
+  int sum = 0, ne = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int col = lane * 4 + k;
+    L.st[k] = 0;
+    L.len[k] = 0;
+    t[k] = make_int2(0, 0);
+    if (col < ncol) {
+      const int q = (int)(((float)col + 0.5f) * inv_nj);  // == col / nj
+      const int base = ((ilo + q) * g + jlo + (col - q * nj)) * g;
+      const int a = __ldg(starts + (base + klo));
+      const int b = __ldg(starts + (base + kend));
+      t[k] = make_int2(__ldg(starts + (base + kae)), __ldg(starts + (base + kbs)));
+      L.st[k] = a;
+      L.len[k] = b - a;
+    }
+    sum += L.len[k];
+    ne += L.len[k] > 0;
+  }
+  int tot, netot;
+  int off = warp_excl_scan(sum, lane, &tot);
+  const int nbefore = warp_excl_scan(ne, lane, &netot);
+  int e = nbefore;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    L.pre[k] = off;
+    if (L.len[k] > 0) {
+      const int d = L.st[k] - off;
+      ps.dt[e++] = make_int4(d, t[k].x - d, t[k].y - d, 0);
+    }
+    off += L.len[k];
+  }
+  L.nonempty_before = nbefore;
+  L.tot = tot;
+  return L;
+}
+
+__device__ __forceinline__ int build_window_inl(const LaneSegs& L, int w0, uint32_t* bits, int lane) {
+#pragma unroll
+  for (int i = 0; i < kBmWords / 32; ++i) bits[lane + 32 * i] = 0u;
+  __syncwarp();
+  int before = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (L.len[k] > 0) {
+      const int p = L.pre[k] - w0;
+      if (p < 0)
+        ++before;
+      else if (p < 32 * kBmWords)
+        atomicOr(&bits[p >> 5], 1u << (p & 31));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) before += __shfl_xor_sync(MG_FULL, before, o);
+  __syncwarp();
+  return before;
+}
+
 // Cursor4 that also classifies each candidate against its column's
 // thresholds: m bit 0 = B-only cell (not A's), bit 1 = A-only cell (not B's).
 struct Cursor4P {
@@ -1161,6 +1257,65 @@ struct GaussPairAcc {
   }
 };
 
+// Warp reduction of the pair's 10 f32x2 accumulators through the warp's
+// (no longer needed) shared memory: every lane stores its 10 packed sums, lane
+// c < 10 adds column c over the 32 lanes as 64-bit loads + FADD2 (both
+// Gaussians at once, 4 independent chains), T = P' D1 is formed once on
+// lanes 1..3.  ~90 instructions where the 20-value shuffle transpose took 165.
+__device__ __forceinline__ void bwd_store_pair(const GaussPairAcc& acc, int j, float* __restrict__ acc10,
+                                               PairSmem& ps, int lane) {
+  static_assert(sizeof(PairSmem) >= 32 * 10 * sizeof(unsigned long long), "pair reduction buffer");
+  unsigned long long* red = reinterpret_cast<unsigned long long*>(&ps);
+  __syncwarp();  // the window loop's last shared-memory reads are done
+  {
+    unsigned long long* row = red + lane * 10;
+    row[0] = acc.S.v;
+    row[1] = acc.T[0].v;
+    row[2] = acc.T[1].v;
+    row[3] = acc.T[2].v;
+#pragma unroll
+    for (int c = 0; c < 6; ++c) row[4 + c] = acc.A6[c].v;
+  }
+  __syncwarp();
+  const int c = lane < 10 ? lane : 0;
+  f2 s0, s1, s2, s3;
+  s0.v = red[0 * 10 + c];
+  s1.v = red[1 * 10 + c];
+  s2.v = red[2 * 10 + c];
+  s3.v = red[3 * 10 + c];
+#pragma unroll
+  for (int l = 4; l < 32; l += 4) {
+    f2 a, b, d, e;
+    a.v = red[(l + 0) * 10 + c];
+    b.v = red[(l + 1) * 10 + c];
+    d.v = red[(l + 2) * 10 + c];
+    e.v = red[(l + 3) * 10 + c];
+    s0 = add2(s0, a);
+    s1 = add2(s1, b);
+    s2 = add2(s2, d);
+    s3 = add2(s3, e);
+  }
+  f2 v = add2(add2(s0, s1), add2(s2, s3));
+  // D1 = -sum u g (mu - x) on lanes 1..3 -> T = P' D1 (rows of the symmetric P')
+  const float lo1 = __shfl_sync(MG_FULL, lo(v), 1), hi1 = __shfl_sync(MG_FULL, hi(v), 1);
+  const float lo2 = __shfl_sync(MG_FULL, lo(v), 2), hi2 = __shfl_sync(MG_FULL, hi(v), 2);
+  const float lo3 = __shfl_sync(MG_FULL, lo(v), 3), hi3 = __shfl_sync(MG_FULL, hi(v), 3);
+  if (lane >= 1 && lane <= 3) {
+    const f2 d1x = mk2(-lo1, -hi1), d1y = mk2(-lo2, -hi2), d1z = mk2(-lo3, -hi3);
+    const f2 half = bc2(0.5f);
+    const f2 h01 = mul2(half, acc.P[3]), h02 = mul2(half, acc.P[4]), h12 = mul2(half, acc.P[5]);
+    // row (lane - 1) of P' = [[p00, h01, h02], [h01, p11, h12], [h02, h12, p22]]
+    const f2 ra = lane == 1 ? acc.P[0] : (lane == 2 ? h01 : h02);
+    const f2 rb = lane == 1 ? h01 : (lane == 2 ? acc.P[1] : h12);
+    const f2 rc = lane == 1 ? h02 : (lane == 2 ? h12 : acc.P[2]);
+    v = fma2(rc, d1z, fma2(rb, d1y, mul2(ra, d1x)));
+  }
+  if (lane < 10) {
+    acc10[(int64_t)j * 10 + lane] = lo(v);
+    acc10[(int64_t)(j + 1) * 10 + lane] = hi(v);
+  }
+}
+
 __device__ __forceinline__ void pair_masked(GaussPairAcc& acc, const float4& a, const float4& b, int ma, int mb) {
   acc.point(a, mk2((ma & 1) ? 0.f : a.w, (ma & 2) ? 0.f : a.w));
   acc.point(b, mk2((mb & 1) ? 0.f : b.w, (mb & 2) ? 0.f : b.w));
@@ -1192,10 +1347,21 @@ __device__ __forceinline__ void bwd_pair_item(const GaussSoA grec, int j, int ce
   const PairCols cols{pstart, max(kb - r, 0), min(ka + r, g - 1) + 1};
   const unsigned upto = 0xffffffffu >> (31 - lane);
   for (int c0 = 0; c0 < w.ncol; c0 += 128) {
+#if MG_PAIR_INLINE
+    // r <= 5 windows have <= 121 columns: one table (c0 == 0) per item
+    const LaneSegs L = w.ncol <= 128 ? build_lane_segs_pair_inl(w.ilo, w.jlo, w.nj, w.ncol, w.inv_nj, w.klo,
+                                                                w.khi + 1, cols.kae, cols.kbs, g, pstart, ps, lane)
+                                     : build_lane_segs_pair(w, c0, g, cols, ps, lane);
+#else
     const LaneSegs L = build_lane_segs_pair(w, c0, g, cols, ps, lane);
+#endif
     const int tot = L.tot;
     for (int w0 = 0; w0 < tot; w0 += 32 * kBmWords) {
+#if MG_PAIR_INLINE
+      Cursor4P cur{build_window_inl(L, w0, ps.bits, lane)};
+#else
       Cursor4P cur{build_window(L, w0, reinterpret_cast<SegSmem&>(ps), lane)};
+#endif
       const int wend = min(tot, w0 + 32 * kBmWords);
       const int nfull = (wend - w0) >> 7;
       int v[4], e[4], m[4];
@@ -1219,7 +1385,11 @@ __device__ __forceinline__ void bwd_pair_item(const GaussSoA grec, int j, int ce
       __syncwarp();
     }
   }
+#if MG_BWD_PAIR_GPACK && MG_BWD_SMEM_STORE
+  bwd_store_pair(acc, j, acc10, ps, lane);
+#else
   bwd_store<2>(acc, j, 2, acc10, lane);
+#endif
 }
 
 #ifndef MG_BWD_PAIR_DMAX
@@ -1242,7 +1412,10 @@ __global__ void __launch_bounds__(kBwdWarps * 32, PAIR ? MG_BWD_PAIR_MINB : MG_B
                                                                   const int4* __restrict__ items,
                                                                   const int* __restrict__ nitems_dev,
                                                                   int n_implicit, float* __restrict__ acc10) {
-  __shared__ WarpSmem s_ws[kBwdWarps];  // per warp: SegSmem for single items, PairSmem for pairs (aliased)
+  // per warp: SegSmem for single items, PairSmem for pairs (aliased); dynamic,
+  // so more than 16 warps fit (static shared memory stops at 48 KB)
+  extern __shared__ __align__(16) unsigned char bwd_dyn[];
+  WarpSmem* s_ws = reinterpret_cast<WarpSmem*>(bwd_dyn);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;  // kBwdWarps, or 8 for small launches
   // implicit pair items: sorted Gaussians (2j, 2j+1)
@@ -1726,6 +1899,19 @@ void launch_forward(bool with_h, const float* grec_raw, int64_t n_gauss, const i
   MG_LAUNCH(k<<<blocks, nw * 32, smem, st>>>(grec, gstart, g, r, prec, pkey, pstart, items, nitems, out4, cnt));
 }
 
+static size_t bwd_smem_bytes(int nw) {
+  const size_t b = sizeof(WarpSmem) * (size_t)nw;
+  static bool done = false;  // opt in above 48 KB once per process
+  if (!done) {
+    cudaFuncSetAttribute(backward_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(WarpSmem) * kBwdWarps));
+    cudaFuncSetAttribute(backward_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(WarpSmem) * kBwdWarps));
+    done = true;
+  }
+  return b;
+}
+
 size_t staged_smem_bytes() { return sizeof(float4) * kSbCap + sizeof(SegSmem) * kSbS + sizeof(StageSmem); }
 
 size_t backward_staged_ws_bytes(int64_t n, int g) {
@@ -1776,9 +1962,10 @@ void launch_backward_staged(const float* grec_raw, int64_t n_gauss, const uint32
   MG_LAUNCH(item_compact_kernel<<<grid_for(n_gauss), 256, 0, st>>>(oflags, oscan, gkey, gstart, n_gauss, 1, 0,
                                                                     oitems, counts + 1, 1));
   const int64_t want = (n_gauss / 2 + kBwdWarps) / kBwdWarps;
-  MG_LAUNCH(backward_kernel<false><<<(unsigned)persistent_blocks(backward_kernel<false>, kBwdWarps * 32, want),
-                                     kBwdWarps * 32, 0, st>>>(grec, gkey, gstart, g, r, prec, pstart, oitems,
-                                                              counts + 1, 0, acc10));
+  const size_t dsm = bwd_smem_bytes(kBwdWarps);
+  MG_LAUNCH(backward_kernel<false><<<(unsigned)persistent_blocks(backward_kernel<false>, kBwdWarps * 32, want, dsm),
+                                     kBwdWarps * 32, dsm, st>>>(grec, gkey, gstart, g, r, prec, pstart, oitems,
+                                                                counts + 1, 0, acc10));
 }
 
 void launch_backward(const float* grec_raw, int64_t n_gauss, const uint32_t* gkey, const int* gstart, int g, int r,
@@ -1790,7 +1977,8 @@ void launch_backward(const float* grec_raw, int64_t n_gauss, const uint32_t* gke
   const int nw = block_warps(kBwdWarps, pairs ? (max_items + 1) / 2 : max_items);
   const int64_t want = (max_items + nw - 1) / nw;
   auto k = pairs ? backward_kernel<true> : backward_kernel<false>;
-  MG_LAUNCH(k<<<(unsigned)persistent_blocks(k, nw * 32, want), nw * 32, 0, st>>>(
+  const size_t dsm = bwd_smem_bytes(nw);
+  MG_LAUNCH(k<<<(unsigned)persistent_blocks(k, nw * 32, want, dsm), nw * 32, dsm, st>>>(
       grec, gkey, gstart, g, r, prec, pstart, items, nitems, (int)n_gauss, acc10));
 }
 

@@ -48,9 +48,11 @@ def reconstruct(trainer, dims, first, last, intensity_scale, progress=None):
     return out, t_train, time.perf_counter() - t0
 
 
-def load_recon_fixture(path):
+def load_recon_fixture(path, long_path=None):
     """(cloud, TransformSet, slice grids, TrainConfig, target) from a
-    make_recon.py fixture."""
+    make_recon.py fixture; ``long_path`` (make_recon.py --long) replaces the
+    schedule, length and the reference's results with those of the
+    4,000-iteration run on the same data."""
     from .core import TransformSet
     from .train import TrainConfig
 
@@ -68,4 +70,11 @@ def load_recon_fixture(path):
                              intensity_scale=float(z["intensity_scale"]), gt=z["gt"],
                              ref_psnr_db=float(z["psnr_db"]), ref_seconds=float(z["runtime_s"]),
                              ref_threads=int(z["threads"]), ref_losses=z["losses"])
+    if long_path is not None:
+        zl = np.load(long_path)
+        cfg = TrainConfig(resolution_schedule=tuple((int(i), int(r)) for i, r in zl["schedule"]),
+                          nrf_activation_iter=int(zl["nrf_activation_iter"]), total_iters=int(zl["total_iters"]),
+                          batch_points=int(zl["batch_points"]), seed=int(zl["seed"]))
+        target.ref_psnr_db, target.ref_seconds = float(zl["psnr_db"]), float(zl["runtime_s"])
+        target.ref_threads, target.ref_losses = int(zl["threads"]), zl["losses"]
     return cloud, TransformSet(z["t_quats"], z["t_trans"]), grids, cfg, target

@@ -70,12 +70,34 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-// Cutoff-masked weight: 2^{m'} if m' >= cut (i.e. m <= 64) else exactly 0.
-__device__ __forceinline__ float gauss_w(float ms) {
-  float e = ex2(ms);
-  return ms >= kCutScaled ? e : 0.0f;
+// Cutoff by flush-to-zero.  2^{m'} is scaled by kCutScale = 2^-79.83 with an
+// FTZ multiply: the product is subnormal -- flushed to exactly 0 -- precisely
+// when m' < -46.17, i.e. m > 64 (_kernels.py:21: the reference's skip), so the
+// cutoff costs one packed FMUL2.FTZ per two pairs instead of a compare and a
+// select per pair, and 2^{m'} itself keeps full precision (biasing the exponent
+// argument instead lost ~3e-6 relative in the float32 add).  The weights that
+// multiply the Gaussian factor carry the inverse scale kWeightScale ~ 1.08e24:
+// the intensity alpha in the records (A.w) and the upstream in the point
+// records (prec.w), so alpha' g' = alpha g and u' g' = u g.  Point upstreams
+// must stay below ~3e14 in magnitude (the host layer checks).
+static constexpr float kCutScale = 9.28205098304025e-25f;        // float(2^(-126 + 32 log2 e))
+static constexpr double kWeightScaleD = 1.0773481010039219e24;  // 1 / kCutScale (float64)
+static constexpr float kWeightScale = (float)kWeightScaleD;
+
+__device__ __forceinline__ float mul_ftz(float a, float b) {
+  float d;
+  asm("mul.rn.ftz.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+  return d;
 }
-__device__ __forceinline__ f2 gauss_w2(f2 m) { return mk2(gauss_w(lo(m)), gauss_w(hi(m))); }
+__device__ __forceinline__ f2 mul2_ftz(f2 a, f2 b) {
+  f2 d;
+  asm("mul.rn.ftz.f32x2 %0, %1, %2;" : "=l"(d.v) : "l"(a.v), "l"(b.v));
+  return d;
+}
+
+// Cutoff-masked weight g' = 2^{m'} * kCutScale (0 when m > 64).
+__device__ __forceinline__ float gauss_w(float ms) { return mul_ftz(ex2(ms), kCutScale); }
+__device__ __forceinline__ f2 gauss_w2(f2 m) { return mul2_ftz(mk2(ex2(lo(m)), ex2(hi(m))), bc2(kCutScale)); }
 
 // ---------------------------------------------------------------------------
 // Warp reductions

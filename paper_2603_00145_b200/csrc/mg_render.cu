@@ -83,7 +83,7 @@ __device__ __forceinline__ void activate_one(const float* pos, const float* quat
     P[k] = kMScaleD * (R[3 * a] * e[0] * R[3 * b] + R[3 * a + 1] * e[1] * R[3 * b + 1] + R[3 * a + 2] * e[2] * R[3 * b + 2]);
   }
   double alpha = 1.0 / (1.0 + exp(-(double)lg[i]));  // core.py:21-26
-  rec.A[p] = make_float4(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], (float)alpha);
+  rec.A[p] = make_float4(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], (float)(alpha * kWeightScaleD));
   rec.B[p] = make_float4((float)P[0], (float)P[1], (float)P[2], (float)P[3]);
   rec.C[p] = make_float2((float)P[4], (float)P[5]);
 }
@@ -106,7 +106,8 @@ __global__ void gauss_pack_prepared_kernel(const double* __restrict__ mu, const 
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
     int64_t i = order[p];
     const double* P = prec6 + 6 * i;
-    grec.A[p] = make_float4((float)mu[3 * i], (float)mu[3 * i + 1], (float)mu[3 * i + 2], (float)alpha[i]);
+    grec.A[p] = make_float4((float)mu[3 * i], (float)mu[3 * i + 1], (float)mu[3 * i + 2],
+                            (float)(alpha[i] * kWeightScaleD));
     grec.B[p] = make_float4((float)(kMScaleD * P[0]), (float)(kMScaleD * P[3]), (float)(kMScaleD * P[5]),
                             (float)(kMScaleD * P[1]));
     grec.C[p] = make_float2((float)(kMScaleD * P[2]), (float)(kMScaleD * P[4]));

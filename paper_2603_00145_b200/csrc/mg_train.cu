@@ -74,7 +74,7 @@ __global__ void backward_points_kernel(const double* __restrict__ up64, const fl
     double u = up64 ? up64[pb] : (double)up32[pb];
     double us = u * (tap_w ? tap_w[t] : 1.0);
     int p = inv[j];
-    prec[p].w = (float)us;
+    prec[p].w = (float)(us * kWeightScaleD);  // u' = u / kCutScale (FTZ cutoff, mg_common.cuh)
     if (dpoints) {
       float4 H = out4[p];
       dpoints[3 * j + 0] = -us * (double)H.x;

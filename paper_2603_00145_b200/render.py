@@ -394,6 +394,9 @@ def render_backward(field, grid, transforms, samples, upstream, radius=None, pre
     up = np.ascontiguousarray(upstream, dtype=np.float64).reshape(-1)
     if up.shape[0] != coords.shape[0]:
         raise ValueError("upstream length does not match sample count")
+    if not _strict_fp64 and up.size and np.abs(up).max() > 1e14:
+        # the float32 kernels carry u * 2^79.8 in the point records (exponent-offset cutoff, mg_common.cuh)
+        raise ValueError("|upstream| > 1e14 exceeds the float32 kernels' range; use render.set_strict_fp64(True)")
     rot, trans, k, ts = _transform_arrays(transforms)
     r = grid.block_radius if radius is None else int(radius)
     g = grid.grid_resolution

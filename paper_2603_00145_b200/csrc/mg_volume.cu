@@ -171,6 +171,9 @@ __global__ void __launch_bounds__(kVolWarps * 32) volume_kernel(const GaussSoA g
 #define MG_VOL_TZ 6  // runs per tile along k: 2 x 2 x 6 cells over 12 warps, 2 CTAs (2 x 104 KB) per SM
                      // (2 x 2 x 4 over 8 warps: 130 ms at C5; this shape: 116 ms)
 #endif
+#ifndef MG_VOL_LPT
+#define MG_VOL_LPT 1
+#endif
 #ifndef MG_VOL_WARPS
 #define MG_VOL_WARPS 12  // warps per tile CTA; the tile's 2 x 2 x TZ cells are dealt round-robin
 #endif
@@ -188,6 +191,8 @@ struct VolTileSmem {
   int off[kTileCols][kTileK];  // absolute CSR index of union cell (column, KZ0 + k)
   int sb[kTileCols + 1];       // staged base of each column
   int geom[8];                 // UI0, UJ0, KZ0, ni, nj, nk, total, ok
+  int order[4 * kTileTZ];      // the tile's cells, most voxel slots first (LPT hand-out)
+  int next;                    // hand-out counter
 };
 
 template <int V>
@@ -343,9 +348,47 @@ __global__ void __launch_bounds__(kVolTileWarps * 32) volume_tile_kernel(const G
         __syncthreads();
       }
     }
+#if MG_VOL_LPT
+    // cells handed out dynamically, largest first (longest-processing-time):
+    // 64-voxel cells take one 64-slot pass, larger ones 128-slot passes, so a
+    // fixed round-robin deal left warps idle at the end-of-tile barrier
+    if (threadIdx.x == 0) {
+      int cost[4 * kTileTZ];
+      for (int c = 0; c < 4 * kTileTZ; ++c) {
+        const int rx = rx0 + ((c >> 2) & 1), ry = ry0 + ((c >> 1) & 1), rz = rz0 + (c & 1) + 2 * (c >> 3);
+        int w = 0;
+        if (rx < nrx && ry < nry && rz < nrz) {
+          const int nv = (ax.rs[0][rx + 1] - ax.rs[0][rx]) * (ax.rs[1][ry + 1] - ax.rs[1][ry]) *
+                         (ax.rs[2][rz + 1] - ax.rs[2][rz]);
+          w = nv <= 64 ? 1 : 2 * ((nv + 127) / 128);
+        }
+        cost[c] = w;
+        sm.order[c] = c;
+      }
+      for (int a = 1; a < 4 * kTileTZ; ++a) {  // insertion sort, descending cost
+        const int v = sm.order[a];
+        int b = a - 1;
+        while (b >= 0 && cost[sm.order[b]] < cost[v]) {
+          sm.order[b + 1] = sm.order[b];
+          --b;
+        }
+        sm.order[b + 1] = v;
+      }
+      sm.next = 0;
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (;;) {
+    int slot = 0;
+    if (lane == 0) slot = atomicAdd(&sm.next, 1);
+    slot = __shfl_sync(MG_FULL, slot, 0);
+    if (slot >= 4 * kTileTZ) break;
+    const int c = sm.order[slot];
+#else
     // this warp's runs (cells) of the tile's 2 x 2 x TZ, dealt round-robin
 #pragma unroll 1
     for (int c = warp; c < 4 * kTileTZ; c += kVolTileWarps) {
+#endif
     const int rx = rx0 + ((c >> 2) & 1), ry = ry0 + ((c >> 1) & 1), rz = rz0 + (c & 1) + 2 * (c >> 3);
     if (rx < nrx && ry < nry && rz < nrz) {
       const int bx0 = ax.rs[0][rx], nbx = ax.rs[0][rx + 1] - bx0;

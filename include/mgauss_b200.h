@@ -245,6 +245,10 @@ int mg_block_backward(const double *points, const int64_t *slice_ids, int64_t b,
                       int64_t n, const int64_t *cell_starts, const int64_t *cell_indices, int64_t grid_res,
                       int64_t radius, const double *upstream, double *d_mu, double *d_abar6, double *d_alpha,
                       double *out_dpoint, void *ws, size_t ws_bytes, void *stream);
+/* Self-test of the tcgen05 tensor-core path (kind::tf32, TMEM accumulator) the
+ * NRF layers use: D (128 x 64) = A (128 x 64, row-major) * B where Bt (64 x 64)
+ * holds B transposed; split != 0 evaluates 3xTF32 (hi*hi + hi*lo + lo*hi). */
+int mg_tc_selftest(const float *A, const float *Bt, float *D, int32_t split, void *stream);
 /* Strict float64 instantiation of the same two kernels (same arguments, same
  * ownership): every pair is evaluated in IEEE float64 in the reference's
  * operation order without FMA contraction, so results agree with

@@ -76,6 +76,7 @@ SIGNATURES = {
     "mg_block_forward": (ctypes.c_int, [P, P, I64, P, P, I64, P, P, P, I64, P, P, I64, I64, P, P, P, P, SZ, P]),
     "mg_block_backward": (ctypes.c_int,
                           [P, P, I64, P, P, I64, P, P, P, I64, P, P, I64, I64, P, P, P, P, P, P, SZ, P]),
+    "mg_tc_selftest": (ctypes.c_int, [P, P, P, I32, P]),
     "mg_block_f64_workspace_bytes": (SZ, [I64, I64, I64]),
     "mg_block_forward_f64": (ctypes.c_int, [P, P, I64, P, P, I64, P, P, P, I64, P, P, I64, I64, P, P, P, P, SZ, P]),
     "mg_block_backward_f64": (ctypes.c_int,

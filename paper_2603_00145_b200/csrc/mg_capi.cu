@@ -607,6 +607,12 @@ int mg_block_backward(const double* points, const int64_t* sids, int64_t b, cons
                       nullptr, upstream, d_mu, d_abar6, d_alpha, out_dp, ws, wsb, S(stream));
 }
 
+// ---- tensor-core self-test (mg_nrf_tc.cu) ----
+int mg_tc_selftest(const float* A, const float* Bt, float* D, int32_t split, void* stream) {
+  launch_tc_selftest(A, Bt, D, split, S(stream));
+  return cuda_status();
+}
+
 // ---- strict float64 instantiation of the same ABI (mg_strict.cu) ----
 size_t mg_block_f64_workspace_bytes(int64_t b, int64_t n, int64_t g) { return strict_workspace_bytes(b, n, g); }
 

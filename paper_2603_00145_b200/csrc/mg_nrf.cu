@@ -17,6 +17,8 @@
 //   nrf_reduce_kernel  fixed-order sum of the partials -> deterministic grads
 //
 // Everything is float32 like the torch path it replaces (nrf.py host mirror).
+#include <stdlib.h>
+
 #include "mg_render.cuh"
 
 namespace mg {
@@ -537,9 +539,23 @@ static unsigned nrf_tile_grid(const void* kern, size_t smem, int64_t b) {
   return (unsigned)(tiles < g ? (tiles < 1 ? 1 : tiles) : g);
 }
 
+// MGAUSS_NRF_TC=0 selects the SIMT layer kernels (A/B); the tcgen05 layers are the default.
+bool nrf_use_tc() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MGAUSS_NRF_TC");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 void launch_nrf_forward(const float* x, int64_t b, const float* const* w, const float* const* bias, float* pred_add,
                         float* r_out, float* t_out, float* z_out, cudaStream_t st) {
   if (b <= 0) return;
+  if (nrf_use_tc()) {
+    launch_nrf_forward_tc(x, b, w, bias, pred_add, r_out, t_out, z_out, st);
+    return;
+  }
   nrf_attrs();
   NrfParams P;
   for (int l = 0; l < 5; ++l) P.w[l] = w[l], P.b[l] = bias[l];
@@ -574,9 +590,13 @@ void launch_nrf_backward(const float* x, int64_t b, const float* const* w, const
   float* enc = (float*)p;
   p += al((size_t)b * (kNE + 1) * sizeof(float));
   float* part = (float*)p;
-  const size_t smem = sizeof(NrfBwdSmem);
-  MG_LAUNCH(nrf_bwd_kernel<<<nrf_tile_grid((const void*)nrf_bwd_kernel, smem, b), kNThr, smem, st>>>(
-      x, b, P, up, t, z, dz, d4, dp, hb, enc));
+  if (nrf_use_tc()) {
+    launch_nrf_bwd_chain_tc(x, b, w, bias, up, t, z, dz, d4, dp, hb, enc, st);
+  } else {
+    const size_t smem = sizeof(NrfBwdSmem);
+    MG_LAUNCH(nrf_bwd_kernel<<<nrf_tile_grid((const void*)nrf_bwd_kernel, smem, b), kNThr, smem, st>>>(
+        x, b, P, up, t, z, dz, d4, dp, hb, enc));
+  }
   const int G = nrf_dw_grid(b);
   MG_LAUNCH(nrf_dw_kernel<<<dim3(G, 5), kNThr, sizeof(NrfDwSmem), st>>>(b, enc, hb, dz, d4, part));
   const int64_t total = (kNE * kNH + kNH) + 3 * (kNH * kNH + kNH) + 65;

@@ -85,6 +85,15 @@ void launch_transform_adam(double* tq, double* tt, const double* g7, double* m7,
 void launch_upsample(const float* q_old, const float* s_old, const float* l_old, const int* node_of_old, int ro, int rn,
                      float* pos, float* q, float* s, float* l, cudaStream_t st);
 
+// tensor-core (tcgen05) NRF layers and the self-test GEMM (mg_nrf_tc.cu)
+bool nrf_use_tc();
+void launch_nrf_forward_tc(const float* x, int64_t b, const float* const* w, const float* const* bias,
+                           float* pred_add, float* r_out, float* t_out, float* z_out, cudaStream_t st);
+void launch_nrf_bwd_chain_tc(const float* x, int64_t b, const float* const* w, const float* const* bias,
+                             const float* up, const float* t, const float* z, float* dz, float* d4, float* dp,
+                             float* hout, float* enc, cudaStream_t st);
+void launch_tc_selftest(const float* A, const float* Bt, float* D, int split, cudaStream_t st);
+
 // strict float64 reference-order pair kernels (mg_strict.cu)
 size_t strict_workspace_bytes(int64_t b, int64_t n, int64_t g);
 int strict_block(const double* points, const int64_t* sids, int64_t b, const double* rot, const double* trans,

@@ -50,6 +50,9 @@ def main():
 
     args = [a for a in sys.argv[1:] if not a.startswith("--")]
     long_run = "--long" in sys.argv
+    perturb = None
+    if "--perturb" in sys.argv:  # rounding-level perturbation of the samples (tools/recon_ensemble.py's)
+        perturb = int(args.pop(-1))
     threads = int(args[0]) if args else 1
     render.set_num_threads(threads)
     bundle = mio.load_config(CFG)
@@ -59,7 +62,12 @@ def main():
     cloud = devoxelize(stacks, bundle.sim.foreground_threshold)
     ts = normalized_transforms(stacks, cloud.world_map, "estimated")
     grids = build_slice_grids(stacks, cloud.world_map, cloud.intensity_scale)
-    for g in grids:  # grid k == cloud rows of slice k (foreground threshold -1)
+    if perturb is not None:
+        cloud.intensities = cloud.intensities * (1.0 + 1e-7 * np.random.default_rng(perturb).normal(
+            size=cloud.intensities.shape))
+        for g in grids:
+            g.target = cloud.intensities[cloud.slice_ids == g.slice_id].reshape(np.asarray(g.target).shape)
+    for g in grids if perturb is None else []:  # grid k == cloud rows of slice k (foreground threshold -1)
         rows = cloud.slice_ids == g.slice_id
         assert np.array_equal(cloud.coords[rows], np.asarray(g.coords).reshape(-1, 3))
         assert np.array_equal(cloud.intensities[rows], np.asarray(g.target).ravel())
@@ -79,6 +87,10 @@ def main():
     pred = (vol.data * cloud.intensity_scale).astype(np.float32).astype(np.float64)
     db = psnr(pred, gt.data.astype(np.float32).astype(np.float64))
     print(f"PSNR {db:.4f} dB, {runtime:.1f} s on {threads} thread(s)")
+    if perturb is not None:
+        with open(os.path.join(OUT, "recon_desk64_long_perturbed.txt"), "a") as fh:
+            fh.write(f"{perturb} {db:.6f} {runtime:.1f} {threads}\n")
+        return
     if long_run:
         np.savez_compressed(
             os.path.join(OUT, "recon_desk64_long.npz"), psnr_db=db, runtime_s=runtime, threads=threads,

@@ -702,27 +702,36 @@ def recon_desk64():
             "reference_threads": tgt.ref_threads}
 
 
-def inference_c5(reps=3):
-    """C5 (BASELINE.json configs[4]): sample a 512^3 node-inclusive volume over
-    [-1, 1]^3 from a 2,000,376-Gaussian field (R = G = 126, r = 5).  Synthetic
-    field per SURVEY §8(d): lattice positions + N(0, 0.1/R) jitter, identity +
-    N(0, 0.1) quaternions, log-scales log(1/R) + N(0, 0.1), logits N(0, 1)."""
-    import torch
-
-    from paper_2603_00145_b200 import _native as N
+def _c5_field(kind, R=126):
+    """C5 fields (SURVEY §8(d) option 2, seed 7): lattice positions + N(0, 0.1/R) jitter, identity + N(0, 0.1)
+    quaternions, log-scales log(1/R) + N(0, 0.1), logits N(0, 1).  'drifted' jitters by half a cell (cell
+    occupancy 0..4, like a trained field); 'clustered' squeezes the field into the central eighth (~8 Gaussians
+    per occupied cell: every central tile overflows the shared-memory staging -> the global-walk path)."""
     from paper_2603_00145_b200.core import lattice_node_positions
-    from paper_2603_00145_b200.render import sample_volume_device
-    from paper_2603_00145_b200.spatial import build_device
 
-    R = 126
     n = R ** 3
     rng = np.random.default_rng(7)
-    pos = lattice_node_positions(R) + rng.normal(0, 0.1 / R, (n, 3))
+    sig = {"lattice": 0.1, "drifted": 0.5, "clustered": 0.1}[kind]
+    pos = lattice_node_positions(R) + rng.normal(0, sig / R, (n, 3))
     q = np.zeros((n, 4))
     q[:, 0] = 1.0
     q += rng.normal(0, 0.1, (n, 4))
     ls = np.log(1.0 / R) + rng.normal(0, 0.1, (n, 3))
     lg = rng.normal(0, 1, n)
+    if kind == "clustered":
+        pos *= 0.5
+        ls += np.log(0.5)
+    return pos, q, ls, lg
+
+
+def _c5_time(pos, q, ls, lg, R, reps):
+    import torch
+
+    from paper_2603_00145_b200 import _native as N
+    from paper_2603_00145_b200.render import sample_volume_device
+    from paper_2603_00145_b200.spatial import build_device
+
+    n = pos.shape[0]
     dev = torch.device("cuda")
     pos_d = torch.from_numpy(pos).float().to(dev)
     q_d = torch.from_numpy(q).float().to(dev)
@@ -744,6 +753,7 @@ def inference_c5(reps=3):
         out = sample_volume_device(grec, n, d["starts"], R, 5, dims, bounds)
     e1.record()
     torch.cuda.synchronize()
+    del out
     ms = e0.elapsed_time(e1) / reps
     # exact candidate-pair count: sum over voxels of the Gaussians within Chebyshev 5 cells of the voxel's cell
     starts = d["starts"].cpu().numpy().astype(np.int64)
@@ -760,10 +770,20 @@ def inference_c5(reps=3):
     vc = np.bincount(np.clip(np.floor((ax + 1.0) * (R / 2.0)).astype(np.int64), 0, R - 1), minlength=R)
     pairs = float(np.einsum("i,j,k,ijk->", vc, vc, vc, cand.astype(np.float64)))
     peak = peak_fp32(L.mg_device_sm_count(), 1965.0)
-    return {"workload": "C5: 512^3 volume from 2,000,376 Gaussians (R=G=126, r=5), synthetic lattice field",
-            "ms": ms, "voxels_per_s": 512 ** 3 / (ms / 1e3), "pairs_per_s": pairs / (ms / 1e3),
-            "pairs": pairs, "roofline_frac_fp32": pairs * FLOP_FWD / (ms / 1e3) / peak}
+    return {"ms": ms, "voxels_per_s": 512 ** 3 / (ms / 1e3), "pairs_per_s": pairs / (ms / 1e3), "pairs": pairs,
+            "roofline_frac_fp32": pairs * FLOP_FWD / (ms / 1e3) / peak,
+            "max_gaussians_per_cell": int(cnt.max()), "occupied_cells": float((cnt > 0).mean())}
 
+
+def inference_c5(reps=3):
+    """C5 (BASELINE.json configs[4]): sample a 512^3 node-inclusive volume over
+    [-1, 1]^3 from a 2,000,376-Gaussian field (R = G = 126, r = 5): the headline
+    numbers on the jittered lattice, plus a drifted and a clustered field."""
+    R = 126
+    out = {"workload": "C5: 512^3 volume from 2,000,376 Gaussians (R=G=126, r=5), synthetic lattice field"}
+    out.update(_c5_time(*_c5_field("lattice", R), R, reps))
+    out["other_fields"] = {k: _c5_time(*_c5_field(k, R), R, max(1, reps - 1)) for k in ("drifted", "clustered")}
+    return out
 
 
 def main():

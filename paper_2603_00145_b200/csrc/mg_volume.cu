@@ -171,6 +171,9 @@ __global__ void __launch_bounds__(kVolWarps * 32) volume_kernel(const GaussSoA g
 #define MG_VOL_TZ 6  // runs per tile along k: 2 x 2 x 6 cells over 12 warps, 2 CTAs (2 x 104 KB) per SM
                      // (2 x 2 x 4 over 8 warps: 130 ms at C5; this shape: 116 ms)
 #endif
+#ifndef MG_VOL_FD
+#define MG_VOL_FD 0  // forward-differencing cell pairs: 108 -> 115 ms at C5 (one pair per warp per tile: end-of-tile imbalance)
+#endif
 #ifndef MG_VOL_LPT
 #define MG_VOL_LPT 1
 #endif
@@ -258,6 +261,90 @@ __device__ __forceinline__ void vol_chunk_tile(const VolTileSmem& sm, int g, int
       out[o] = fminf(fmaxf(val, 0.f), 1.f);
     }
   }
+}
+
+// Forward-differencing pair walk (MG_VOL_FD): a warp takes two x-adjacent
+// cells of the tile (same y and z runs); a lane owns one (x, y) column of
+// voxels of one of them with all its z voxels (<= 6, packed in f32x2 pairs).
+// Along a column dx, dy are shared, so per candidate the lane forms the
+// (dx, dy) part of the quadratic form once,
+//   m = [dx (P00 dx + 2 P01 dy) + P11 dy^2] + dz (2 P02 dx + 2 P12 dy + P22 dz),
+// and each z voxel costs one packed subtract and two packed FMAs (~4.75 FP32-pipe
+// instructions per pair instead of 6.5).  The walk covers the union of the two
+// cells' windows (one extra i-column); a lane whose cell does not see a
+// column weights it by 0.  Returns false (nothing written) when a run exceeds 6
+// voxels along z -- the per-cell path handles those.
+__device__ __forceinline__ bool vol_pair_fd(const VolTileSmem& sm, int g, int r, const VolAxes& ax, int rxA,
+                                            int nrx, int ry, int rz, const float* __restrict__ residual,
+                                            float* __restrict__ out, int lane) {
+  const int by0 = ax.rs[1][ry], nby = ax.rs[1][ry + 1] - by0;
+  const int bz0 = ax.rs[2][rz], nbz = ax.rs[2][rz + 1] - bz0;
+  if (nbz > 6) return false;
+  const bool hasB = rxA + 1 < nrx;
+  const int bx0A = ax.rs[0][rxA], nbxA = ax.rs[0][rxA + 1] - bx0A;
+  const int bx0B = hasB ? ax.rs[0][rxA + 1] : 0, nbxB = hasB ? ax.rs[0][rxA + 2] - bx0B : 0;
+  const int ciA = ax.rc[0][rxA], ciB = hasB ? ax.rc[0][rxA + 1] : ciA;
+  const int cj = ax.rc[1][ry], ck = ax.rc[2][rz];
+  const int ncA = nbxA * nby, ntot = ncA + nbxB * nby;
+  const int UI0 = sm.geom[0], UJ0 = sm.geom[1], KZ0 = sm.geom[2], nj = sm.geom[4];
+  const int iu0 = max(min(ciA, ciB) - r, 0), iu1 = min(max(ciA, ciB) + r, g - 1);
+  const int jlo = max(cj - r, 0), jhi = min(cj + r, g - 1);
+  const int klo = max(ck - r, 0) - KZ0, khi = min(ck + r, g - 1) - KZ0 + 1;
+  float zc[6];
+#pragma unroll
+  for (int t = 0; t < 6; ++t) zc[t] = (float)axis_coord(bz0 + min(t, nbz - 1), ax.n[2], ax.lo[2], ax.hi[2], ax.sp[2]);
+  const f2 pz[3] = {mk2(zc[0], zc[1]), mk2(zc[2], zc[3]), mk2(zc[4], zc[5])};
+  const int np = (nbz + 1) >> 1;  // packed z pairs in use (warp-uniform)
+  for (int c0 = 0; c0 < ntot; c0 += 32) {
+    const int c = c0 + lane;
+    const bool active = c < ntot;
+    const bool isB = c >= ncA;
+    const int cc = active ? (isB ? c - ncA : c) : 0;
+    const int bx = cc / nby, by = cc - bx * nby;
+    const int i = (isB ? bx0B : bx0A) + bx, j = by0 + by;
+    const float x = (float)axis_coord(ax.v0[0] + i, ax.n[0], ax.lo[0], ax.hi[0], ax.sp[0]);
+    const float y = (float)axis_coord(j, ax.n[1], ax.lo[1], ax.hi[1], ax.sp[1]);
+    const int ci = isB ? ciB : ciA;
+    f2 acc[3] = {bc2(0.f), bc2(0.f), bc2(0.f)};
+    for (int ii = iu0; ii <= iu1; ++ii) {
+      const bool sees = active && ii >= ci - r && ii <= ci + r;
+      for (int jj = jlo; jj <= jhi; ++jj) {
+        const int col = (ii - UI0) * nj + (jj - UJ0);
+        const int o0 = sm.off[col][0];
+        const int a = sm.sb[col] + sm.off[col][klo] - o0, b = sm.sb[col] + sm.off[col][khi] - o0;
+        for (int gi = a; gi < b; ++gi) {
+          const float4 A = sm.A[gi], B = sm.B[gi];
+          const float2 C = sm.C[gi];  // staged pre-doubled: B.w = 2P'01, C = (2P'02, 2P'12)
+          const float al = sees ? A.w : 0.f;
+          const float dx = x - A.x, dy = y - A.y;
+          const float qa = fmaf(dy, B.y * dy, dx * fmaf(B.w, dy, B.x * dx));
+          const float qb = fmaf(C.y, dy, C.x * dx);
+          const f2 QA = bc2(qa), QB = bc2(qb);
+#pragma unroll
+          for (int q = 0; q < 3; ++q) {
+            if (q < np) {
+              const f2 dz = sub2(pz[q], bc2(A.z));
+              const f2 sz = fma2(dz, bc2(B.z), QB);
+              const f2 m = fma2(dz, sz, QA);
+              acc[q] = fma2(gauss_w2(m), bc2(al), acc[q]);
+            }
+          }
+        }
+      }
+    }
+    if (active) {
+      const int64_t base = ((int64_t)i * ax.n[1] + j) * ax.n[2] + bz0;
+#pragma unroll
+      for (int t = 0; t < 6; ++t) {
+        if (t < nbz) {
+          float val = (t & 1) ? hi(acc[t >> 1]) : lo(acc[t >> 1]);
+          if (residual) val += residual[base + t];
+          out[base + t] = fminf(fmaxf(val, 0.f), 1.f);
+        }
+      }
+    }
+  }
+  return true;
 }
 
 __device__ __forceinline__ void cpa16(void* dst, const void* src) {
@@ -348,6 +435,33 @@ __global__ void __launch_bounds__(kVolTileWarps * 32) volume_tile_kernel(const G
         __syncthreads();
       }
     }
+#if MG_VOL_FD
+    if (ok) {  // x-adjacent cell pairs, handed out from a shared counter
+      if (threadIdx.x == 0) sm.next = 0;
+      __syncthreads();
+#pragma unroll 1
+      for (;;) {
+        int slot = 0;
+        if (lane == 0) slot = atomicAdd(&sm.next, 1);
+        slot = __shfl_sync(MG_FULL, slot, 0);
+        if (slot >= 2 * kTileTZ) break;
+        const int ry = ry0 + (slot & 1), rz = rz0 + (slot >> 1);
+        if (ry < nry && rz < nrz && !vol_pair_fd(sm, g, r, ax, rx0, nrx, ry, rz, residual, out, lane)) {
+          for (int rx = rx0; rx <= min(rx0 + 1, nrx - 1); ++rx) {  // long z runs: per-cell path
+            const int bx0 = ax.rs[0][rx], nbx = ax.rs[0][rx + 1] - bx0;
+            const int by0 = ax.rs[1][ry], nby = ax.rs[1][ry + 1] - by0;
+            const int bz0 = ax.rs[2][rz], nbz = ax.rs[2][rz + 1] - bz0;
+            const int cell = flat_cell(ax.rc[0][rx], ax.rc[1][ry], ax.rc[2][rz], g);
+            const int nvox = nbx * nby * nbz;
+            for (int l0 = 0; l0 < nvox; l0 += 128)
+              vol_chunk_tile<4>(sm, g, r, ax, bx0, by0, bz0, nbx, nby, nbz, cell, l0, nvox, residual, out, lane);
+          }
+        }
+      }
+      __syncthreads();  // the staged tile is overwritten by the next one
+      continue;
+    }
+#endif
 #if MG_VOL_LPT
     // cells handed out dynamically, largest first (longest-processing-time):
     // 64-voxel cells take one 64-slot pass, larger ones 128-slot passes, so a

@@ -72,6 +72,8 @@ def parse():
     ap.add_argument("--no-recon", action="store_true", help="skip the desk64 reconstruction-to-PSNR run")
     ap.add_argument("--no-secondary", action="store_true", help="skip the secondary C2 line")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: run the N-rank path with all ranks on GPU 0 (control-flow check; eager steps)")
     ap.add_argument("--force-dist", action="store_true",
                     help="use the NCCL data-parallel path even at world size 1 (exercises the N>1 code path)")
     return ap.parse_args()
@@ -432,6 +434,8 @@ def run_ours(args):
     import torch
 
     rank, world, local = dist_info()
+    if args.backend == "gloo":  # control-flow check of the N-rank path on a one-GPU box (ranks share GPU 0)
+        local = 0
     torch.cuda.set_device(local)
     group = None
     dist_on = world > 1 or args.force_dist
@@ -441,7 +445,10 @@ def run_ours(args):
         if not tdist.is_initialized():
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             os.environ.setdefault("MASTER_PORT", "29517")
-            tdist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+            if args.backend == "gloo":
+                tdist.init_process_group("gloo", rank=rank, world_size=world)
+            else:
+                tdist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
         group = tdist.group.WORLD
     from paper_2603_00145_b200 import _native as N
     from paper_2603_00145_b200.train import Trainer, freeze_gc
@@ -475,7 +482,7 @@ def run_ours(args):
         ms, pairs, h2d, plan = timed_window(tr, k, dist_on)
         ms_max = _allsum(ms, dist_on, "max")
         pairs_all = _allsum(pairs, dist_on)
-        kt = kernel_times(tr) if rank == 0 else None
+        kt = kernel_times(tr)  # every rank: the eager steps carry the step's collectives
         levels.append({"level": li, "resolution": res, "gaussians": res ** 3, "iterations": [it0, it_end],
                        "timed_steps": k, "ms": ms_max, "ms_per_step": ms_max / k, "pairs_per_step": pairs_all / k,
                        "value": pairs_all / (ms_max / 1e3), "kernels": kt,

@@ -214,7 +214,8 @@ int mg_counter_incr(int32_t *counters, int32_t n, void *stream);
 int mg_gather_batch(const int64_t *idx, int64_t n, const double *pool_coords, const int64_t *pool_slice_ids,
                     const float *pool_target, double *coords, int64_t *slice_ids, float *target, void *stream);
 /* hyper (host, 9 doubles): lr_pos, lr_quat, lr_scale, lr_logit, beta1, beta2, eps, lambda_aniso, lambda_ratio.
- * t_dev: device int32 post-increment Adam step.  Moments m, v are (n, 11) float32. */
+ * t_dev: device int32 post-increment Adam step.  Moments m, v are float32 structure-of-arrays (11, n)
+ * (slot rows: position 3, quaternion 4, log-scale 3, logit 1); the Adam arithmetic is float32. */
 int mg_gauss_update(const float *acc10, const int32_t *cell_indices, int64_t n, float *pos, float *quat,
                     float *log_scales, float *logits, float *m, float *v, const double *hyper_host,
                     int32_t use_aniso, const int32_t *t_dev, double *aniso_acc, void *stream);

@@ -426,8 +426,9 @@ class Trainer:
     # -- state --------------------------------------------------------------
     def _reset_gauss_adam(self):
         n = self.field.count
-        self.m = dv.zeros((n, 11), torch.float32)
-        self.v = dv.zeros((n, 11), torch.float32)
+        # Adam moments, structure-of-arrays [11][n] (slots: pos 3, quat 4, log-scale 3, logit 1)
+        self.m = dv.zeros((11, n), torch.float32)
+        self.v = dv.zeros((11, n), torch.float32)
         if hasattr(self, "counters"):
             self.counters[0].zero_()
 
@@ -535,8 +536,8 @@ class Trainer:
         t_gauss, t_tr = (int(x) for x in dv.to_host(self.counters))
         adam = {}
         if t_gauss > 0:
-            m = dv.to_host(self.m).astype(np.float64)
-            v = dv.to_host(self.v).astype(np.float64)
+            m = dv.to_host(self.m).astype(np.float64).T
+            v = dv.to_host(self.v).astype(np.float64).T
             for name, key, lo, hi in self._GAUSS_GROUPS:
                 cut = (lambda a: np.ascontiguousarray(a[:, lo])) if hi - lo == 1 else \
                     (lambda a: np.ascontiguousarray(a[:, lo:hi]))
@@ -599,8 +600,8 @@ class Trainer:
                 g = adam[name]
                 m[:, lo:hi] = np.asarray(g["m"][key], np.float64).reshape(self.field.count, hi - lo)
                 v[:, lo:hi] = np.asarray(g["v"][key], np.float64).reshape(self.field.count, hi - lo)
-            self.m.copy_(torch.from_numpy(m))
-            self.v.copy_(torch.from_numpy(v))
+            self.m.copy_(torch.from_numpy(np.ascontiguousarray(m.T)))
+            self.v.copy_(torch.from_numpy(np.ascontiguousarray(v.T)))
             self.counters[0] = int(adam["positions"]["t"])
         self.tm.zero_()
         self.tv.zero_()

@@ -265,6 +265,27 @@ int mg_block_backward_f64(const double *points, const int64_t *slice_ids, int64_
                           int64_t n, const int64_t *cell_starts, const int64_t *cell_indices, int64_t grid_res,
                           int64_t radius, const double *upstream, double *d_mu, double *d_abar6, double *d_alpha,
                           double *out_dpoint, void *ws, size_t ws_bytes, void *stream);
+/* Float64 variants of the training-step pieces for strict-float64 training
+ * (train.StrictTrainer): Huber loss (train.py:108-120), SSIM loss/gradient
+ * (ssim.py:82-122), progressive upsample (train.py:157-218), and the residual
+ * field forward / manual backward (nrf.py:23-182) in float64 like the
+ * reference's numpy code.  mg_nrf_forward_f64 fills `ws` with the forward
+ * cache (encoding, activations) that mg_nrf_backward_f64 consumes, the role
+ * of nrf_forward_cached's cache (nrf.py:140-145); weights are (fan_in,
+ * fan_out) row-major float64, widths 39-64-64-64-64-1. */
+int mg_smooth_l1_f64(const double *pred, const double *target, int64_t b, double *upstream_out, double *loss_acc,
+                     void *stream);
+int mg_ssim_loss_grad_f64(const double *pred, const double *target, int64_t h, int64_t w, double scale,
+                          double *upstream_out, double *ssim_sum, void *ws, size_t ws_bytes, void *stream);
+int mg_upsample_f64(const double *quat_old, const double *log_scales_old, const double *logits_old,
+                    const int32_t *node_of_old, int64_t r_old, int64_t r_new, double *pos, double *quat,
+                    double *log_scales, double *logits, void *stream);
+size_t mg_nrf_f64_workspace_bytes(int64_t b);
+int mg_nrf_forward_f64(const double *x, int64_t b, const double *const *w, const double *const *bias,
+                       double *r_out, void *ws, size_t ws_bytes, void *stream);
+int mg_nrf_backward_f64(const double *x, int64_t b, const double *const *w, const double *const *bias,
+                        const double *upstream, double *d_points, double *const *d_w, double *const *d_b, void *ws,
+                        size_t ws_bytes, void *stream);
 size_t mg_dense_workspace_bytes(int64_t n);
 int mg_dense_forward(const double *points, int64_t b, const double *mu, const double *prec6, const double *alpha,
                      int64_t n, double *out_intensity, void *ws, size_t ws_bytes, void *stream);

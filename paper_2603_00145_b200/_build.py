@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libmgauss_b200.so")
-SOURCES = ["mg_sort.cu", "mg_render.cu", "mg_train.cu", "mg_volume.cu", "mg_ssim.cu", "mg_nrf.cu", "mg_strict.cu", "mg_nrf_tc.cu", "mg_capi.cu"]
+SOURCES = ["mg_sort.cu", "mg_render.cu", "mg_train.cu", "mg_volume.cu", "mg_ssim.cu", "mg_nrf.cu", "mg_strict.cu", "mg_nrf_tc.cu", "mg_nrf64.cu", "mg_capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -488,6 +488,49 @@ int mg_ssim_loss_grad(const float* pred, const float* target, int64_t h, int64_t
   return cuda_status();
 }
 
+// ---- float64 variants for strict-float64 training ----
+int mg_smooth_l1_f64(const double* pred, const double* target, int64_t b, double* up_out, double* loss_acc,
+                     void* stream) {
+  if (b < 0) return fail("mg_smooth_l1_f64: b < 0");
+  launch_smooth_l1_f64(pred, target, b, (double)b, up_out, loss_acc, S(stream));
+  return cuda_status();
+}
+
+int mg_ssim_loss_grad_f64(const double* pred, const double* target, int64_t h, int64_t w, double scale, double* up,
+                          double* ssim_sum, void* ws, size_t wsb, void* stream) {
+  if (h < 11 || w < 11) return fail("mg_ssim_loss_grad_f64: slice smaller than the 11-tap window");
+  if (wsb < ssim_workspace_bytes((int)h, (int)w)) return fail("mg_ssim_loss_grad_f64: workspace too small");
+  launch_ssim_f64(pred, target, (int)h, (int)w, scale, up, ssim_sum, ws, S(stream));
+  return cuda_status();
+}
+
+int mg_upsample_f64(const double* q_old, const double* s_old, const double* l_old, const int32_t* node_of_old,
+                    int64_t ro, int64_t rn, double* pos, double* q, double* s, double* l, void* stream) {
+  if (rn < ro || ro < 1) return fail("mg_upsample_f64: bad resolutions");
+  launch_upsample_f64(q_old, s_old, l_old, node_of_old, (int)ro, (int)rn, pos, q, s, l, S(stream));
+  return cuda_status();
+}
+
+size_t mg_nrf_f64_workspace_bytes(int64_t b) { return b < 0 ? 0 : nrf64_workspace_bytes(b); }
+
+int mg_nrf_forward_f64(const double* x, int64_t b, const double* const* w, const double* const* bias, double* r_out,
+                       void* ws, size_t wsb, void* stream) {
+  if (b < 0 || !w || !bias) return fail("mg_nrf_forward_f64: bad arguments");
+  if (wsb < nrf64_workspace_bytes(b)) return fail("mg_nrf_forward_f64: workspace too small");
+  if (b == 0) return 0;
+  launch_nrf64_forward(x, b, w, bias, r_out, ws, S(stream));
+  return cuda_status();
+}
+
+int mg_nrf_backward_f64(const double* x, int64_t b, const double* const* w, const double* const* bias,
+                        const double* upstream, double* d_points, double* const* dw, double* const* db, void* ws,
+                        size_t wsb, void* stream) {
+  if (b < 0 || !w || !bias || !dw || !db) return fail("mg_nrf_backward_f64: bad arguments");
+  if (wsb < nrf64_workspace_bytes(b)) return fail("mg_nrf_backward_f64: workspace too small");
+  launch_nrf64_backward(x, b, w, bias, upstream, d_points, dw, db, ws, S(stream));
+  return cuda_status();
+}
+
 int mg_quat_to_rot_f64(const double* q, int64_t k, double* rot, void* stream) {
   launch_quat_to_rot(q, k, rot, S(stream));
   return cuda_status();

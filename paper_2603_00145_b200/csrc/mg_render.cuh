@@ -85,6 +85,20 @@ void launch_transform_adam(double* tq, double* tt, const double* g7, double* m7,
 void launch_upsample(const float* q_old, const float* s_old, const float* l_old, const int* node_of_old, int ro, int rn,
                      float* pos, float* q, float* s, float* l, cudaStream_t st);
 
+// float64 variants for the strict-float64 training path
+void launch_smooth_l1_f64(const double* pred, const double* target, int64_t b, double divisor, double* up_out,
+                          double* loss_acc, cudaStream_t st);
+void launch_ssim_f64(const double* pred, const double* tgt, int H, int W, double scale, double* up,
+                     double* ssim_sum, void* ws, cudaStream_t st);
+void launch_upsample_f64(const double* q_old, const double* s_old, const double* l_old, const int* node_of_old,
+                         int ro, int rn, double* pos, double* q, double* s, double* l, cudaStream_t st);
+size_t nrf64_workspace_bytes(int64_t b);
+void launch_nrf64_forward(const double* x, int64_t b, const double* const* w, const double* const* bias, double* r,
+                          void* ws, cudaStream_t st);
+void launch_nrf64_backward(const double* x, int64_t b, const double* const* w, const double* const* bias,
+                           const double* up, double* d_points, double* const* dw, double* const* db, void* ws,
+                           cudaStream_t st);
+
 // tensor-core (tcgen05) NRF layers and the self-test GEMM (mg_nrf_tc.cu)
 bool nrf_use_tc();
 void launch_nrf_forward_tc(const float* x, int64_t b, const float* const* w, const float* const* bias,

@@ -15,7 +15,8 @@ __constant__ double c_w[kWin];
 #define GL(i, n) for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
 
 // pass 1: horizontal valid correlation of the 5 moment fields, (H, Wv, 5)
-__global__ void ssim_h_kernel(const float* __restrict__ pred, const float* __restrict__ tgt, int H, int W,
+template <typename T>
+__global__ void ssim_h_kernel(const T* __restrict__ pred, const T* __restrict__ tgt, int H, int W,
                               double* __restrict__ h5) {
   const int Wv = W - kWin + 1;
   GL(e, (int64_t)H * Wv) {
@@ -79,8 +80,9 @@ __global__ void ssim_ah_kernel(const double* __restrict__ g3, int H, int W, doub
 }
 
 // pass 4: adjoint vertical + combine -> upstream[y*W + x] = scale * dloss/dpred
-__global__ void ssim_av_kernel(const double* __restrict__ a3, const float* __restrict__ pred,
-                               const float* __restrict__ tgt, int H, int W, double scale, float* __restrict__ up) {
+template <typename T>
+__global__ void ssim_av_kernel(const double* __restrict__ a3, const T* __restrict__ pred,
+                               const T* __restrict__ tgt, int H, int W, double scale, T* __restrict__ up) {
   const int Hv = H - kWin + 1;
   GL(e, (int64_t)H * W) {
     int y = (int)(e / W), x = (int)(e % W);
@@ -92,7 +94,7 @@ __global__ void ssim_av_kernel(const double* __restrict__ a3, const float* __res
       for (int f = 0; f < 3; ++f) s[f] += c_w[i] * r[f];
     }
     double gr = s[0] + s[1] * 2.0 * (double)pred[e] + s[2] * (double)tgt[e];
-    up[e] = (float)(scale * gr);
+    up[e] = (T)(scale * gr);
   }
 }
 
@@ -111,8 +113,9 @@ static unsigned gs(int64_t n) {
   return (unsigned)(b < 1 ? 1 : b);
 }
 
-void launch_ssim(const float* pred, const float* tgt, int H, int W, double scale, float* up, double* ssim_sum,
-                 void* ws, cudaStream_t st) {
+template <typename T>
+static void launch_ssim_t(const T* pred, const T* tgt, int H, int W, double scale, T* up, double* ssim_sum,
+                          void* ws, cudaStream_t st) {
   if (!g_w_init) {
     double w[kWin], s = 0.0;
     for (int i = 0; i < kWin; ++i) {
@@ -135,6 +138,17 @@ void launch_ssim(const float* pred, const float* tgt, int H, int W, double scale
   MG_LAUNCH(ssim_v_kernel<<<gs((int64_t)Hv * Wv), 256, 0, st>>>(h5, H, W, g3, ssim_sum));
   MG_LAUNCH(ssim_ah_kernel<<<gs((int64_t)Hv * W), 256, 0, st>>>(g3, H, W, a3));
   MG_LAUNCH(ssim_av_kernel<<<gs((int64_t)H * W), 256, 0, st>>>(a3, pred, tgt, H, W, scale, up));
+}
+
+void launch_ssim(const float* pred, const float* tgt, int H, int W, double scale, float* up, double* ssim_sum,
+                 void* ws, cudaStream_t st) {
+  launch_ssim_t(pred, tgt, H, W, scale, up, ssim_sum, ws, st);
+}
+
+// float64 prediction / target / gradient (strict-float64 training)
+void launch_ssim_f64(const double* pred, const double* tgt, int H, int W, double scale, double* up,
+                     double* ssim_sum, void* ws, cudaStream_t st) {
+  launch_ssim_t(pred, tgt, H, W, scale, up, ssim_sum, ws, st);
 }
 
 }  // namespace mg

@@ -439,15 +439,19 @@ __global__ void transform_finish_kernel(const double* __restrict__ partials, int
 // ---------------------------------------------------------------------------
 // Smooth-L1 (train.py:108-120): mean Huber (delta 1) and its gradient.
 // ---------------------------------------------------------------------------
-__global__ void smooth_l1_kernel(const float* __restrict__ pred, const float* __restrict__ target, int64_t b,
-                                 double scale, float* __restrict__ up_out, double* __restrict__ loss_acc) {
+// DIV: the gradient is g / scale (the reference's `g / x.size`) instead of g * scale.
+template <typename T, bool DIV>
+__global__ void smooth_l1_kernel(const T* __restrict__ pred, const T* __restrict__ target, int64_t b,
+                                 double scale, T* __restrict__ up_out, double* __restrict__ loss_acc) {
   double local = 0.0;
   GRID_LOOP(pb, b) {
     double x = (double)pred[pb] - (double)target[pb];
     double ax = fabs(x);
     local += ax < 1.0 ? 0.5 * x * x : ax - 0.5;
-    up_out[pb] = (float)((ax < 1.0 ? x : (x > 0 ? 1.0 : (x < 0 ? -1.0 : 0.0))) * scale);
+    const double g = ax < 1.0 ? x : (x > 0 ? 1.0 : (x < 0 ? -1.0 : 0.0));
+    up_out[pb] = (T)(DIV ? g / scale : g * scale);
   }
+  if (DIV) local /= scale;
   __shared__ double s_red[32];
   for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(MG_FULL, local, o);
   if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = local;
@@ -455,7 +459,7 @@ __global__ void smooth_l1_kernel(const float* __restrict__ pred, const float* __
   if (threadIdx.x < 32) {
     double v = threadIdx.x < (blockDim.x >> 5) ? s_red[threadIdx.x] : 0.0;
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(MG_FULL, v, o);
-    if (threadIdx.x == 0) atomicAdd(loss_acc, v * scale);
+    if (threadIdx.x == 0) atomicAdd(loss_acc, DIV ? v : v * scale);
   }
 }
 
@@ -611,10 +615,11 @@ __global__ void transform_adam_kernel(double* __restrict__ tq, double* __restric
 // Progressive upsample (train.py:157-218), lattice-index addressed.
 // Input arrays are indexed by the (C-ordered) lattice node id old_id.
 // ---------------------------------------------------------------------------
-__global__ void upsample_kernel(const float* __restrict__ q_old, const float* __restrict__ s_old,
-                                const float* __restrict__ l_old, const int* __restrict__ node_of_old, int ro,
-                                int rn, float* __restrict__ pos, float* __restrict__ q, float* __restrict__ s,
-                                float* __restrict__ l) {
+template <typename T>
+__global__ void upsample_kernel(const T* __restrict__ q_old, const T* __restrict__ s_old,
+                                const T* __restrict__ l_old, const int* __restrict__ node_of_old, int ro,
+                                int rn, T* __restrict__ pos, T* __restrict__ q, T* __restrict__ s,
+                                T* __restrict__ l) {
   const int64_t nn = (int64_t)rn * rn * rn;
   GRID_LOOP(id, nn) {
     int c3[3] = {(int)(id / ((int64_t)rn * rn)), (int)((id / rn) % rn), (int)(id % rn)};
@@ -649,10 +654,10 @@ __global__ void upsample_kernel(const float* __restrict__ q_old, const float* __
         }
     double nrm = sqrt(qs[0] * qs[0] + qs[1] * qs[1] + qs[2] * qs[2] + qs[3] * qs[3]);
     if (!(nrm > 1e-12)) nrm = 1.0;
-    for (int a = 0; a < 4; ++a) q[4 * id + a] = (float)(qs[a] / nrm);
-    for (int a = 0; a < 3; ++a) s[3 * id + a] = (float)sc[a];
-    l[id] = (float)lo;
-    for (int a = 0; a < 3; ++a) pos[3 * id + a] = (float)(-1.0 + ((double)c3[a] + 0.5) * (2.0 / rn));
+    for (int a = 0; a < 4; ++a) q[4 * id + a] = (T)(qs[a] / nrm);
+    for (int a = 0; a < 3; ++a) s[3 * id + a] = (T)sc[a];
+    l[id] = (T)lo;
+    for (int a = 0; a < 3; ++a) pos[3 * id + a] = (T)(-1.0 + ((double)c3[a] + 0.5) * (2.0 / rn));
   }
 }
 
@@ -792,7 +797,11 @@ void launch_adam_f64(double* p, const double* g, double* m, double* v, int64_t n
 
 void launch_smooth_l1(const float* pred, const float* target, int64_t b, double scale, float* up_out,
                       double* loss_acc, cudaStream_t st) {
-  if (b > 0) MG_LAUNCH(smooth_l1_kernel<<<gridn(b), 256, 0, st>>>(pred, target, b, scale, up_out, loss_acc));
+  if (b > 0) MG_LAUNCH((smooth_l1_kernel<float, false><<<gridn(b), 256, 0, st>>>(pred, target, b, scale, up_out, loss_acc)));
+}
+void launch_smooth_l1_f64(const double* pred, const double* target, int64_t b, double divisor, double* up_out,
+                          double* loss_acc, cudaStream_t st) {
+  if (b > 0) MG_LAUNCH((smooth_l1_kernel<double, true><<<gridn(b), 256, 0, st>>>(pred, target, b, divisor, up_out, loss_acc)));
 }
 
 __global__ void quat_to_rot_kernel(const double* __restrict__ q, int64_t k, double* __restrict__ rot) {
@@ -839,6 +848,11 @@ void launch_transform_adam(double* tq, double* tt, const double* g7, double* m7,
 }
 void launch_upsample(const float* q_old, const float* s_old, const float* l_old, const int* node_of_old, int ro, int rn,
                      float* pos, float* q, float* s, float* l, cudaStream_t st) {
+  int64_t nn = (int64_t)rn * rn * rn;
+  if (nn > 0) MG_LAUNCH(upsample_kernel<<<gridn(nn), 256, 0, st>>>(q_old, s_old, l_old, node_of_old, ro, rn, pos, q, s, l));
+}
+void launch_upsample_f64(const double* q_old, const double* s_old, const double* l_old, const int* node_of_old,
+                         int ro, int rn, double* pos, double* q, double* s, double* l, cudaStream_t st) {
   int64_t nn = (int64_t)rn * rn * rn;
   if (nn > 0) MG_LAUNCH(upsample_kernel<<<gridn(nn), 256, 0, st>>>(q_old, s_old, l_old, node_of_old, ro, rn, pos, q, s, l));
 }

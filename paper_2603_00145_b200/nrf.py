@@ -29,6 +29,24 @@ DEFAULT_BANDS = 6
 DEFAULT_HIDDEN = (64, 64, 64, 64)
 
 
+def init_arrays(rng=None, frequency_bands=DEFAULT_BANDS, hidden=DEFAULT_HIDDEN):
+    """(widths, weights, biases) as float64 numpy arrays drawn from ``rng`` in
+    the reference's order (nrf.py:58-83)."""
+    rng = np.random.default_rng(rng)
+    widths = (3 + 6 * int(frequency_bands),) + tuple(hidden) + (1,)
+    ws, bs = [], []
+    for li in range(len(widths) - 1):
+        fi, fo = widths[li], widths[li + 1]
+        if li == len(widths) - 2:
+            w = np.zeros((fi, fo))
+        else:
+            bound = np.sqrt(6.0 / (fi + fo))
+            w = rng.uniform(-bound, bound, size=(fi, fo))
+        ws.append(w)
+        bs.append(np.zeros(fo))
+    return widths, ws, bs
+
+
 @dataclass
 class ResidualField:
     frequency_bands: int = DEFAULT_BANDS
@@ -40,19 +58,9 @@ class ResidualField:
     @classmethod
     def create(cls, rng=None, frequency_bands=DEFAULT_BANDS, hidden=DEFAULT_HIDDEN):
         """Same initialisation stream as nrf.py:58-83 (uniform +-sqrt(6/(fi+fo)), last layer 0)."""
-        rng = np.random.default_rng(rng)
-        widths = (3 + 6 * int(frequency_bands),) + tuple(hidden) + (1,)
-        ws, bs = [], []
-        for li in range(len(widths) - 1):
-            fi, fo = widths[li], widths[li + 1]
-            if li == len(widths) - 2:
-                w = np.zeros((fi, fo))
-            else:
-                bound = np.sqrt(6.0 / (fi + fo))
-                w = rng.uniform(-bound, bound, size=(fi, fo))
-            ws.append(dv.to_dev(w, torch.float32))
-            bs.append(dv.zeros((fo,), torch.float32))
-        return cls(int(frequency_bands), widths, ws, bs)
+        widths, ws, bs = init_arrays(rng, frequency_bands, hidden)
+        return cls(int(frequency_bands), widths, [dv.to_dev(w, torch.float32) for w in ws],
+                   [dv.to_dev(b, torch.float32) for b in bs])
 
     @classmethod
     def from_numpy(cls, weights, biases, frequency_bands=DEFAULT_BANDS):
@@ -154,3 +162,89 @@ def nrf_forward(field: ResidualField, x):
     xt = dv.to_dev(np.atleast_2d(np.asarray(x, dtype=np.float64)), torch.float32)
     r = dv.to_host(nrf_forward_device(field, xt)).astype(np.float64)
     return float(r[0]) if np.asarray(x).ndim == 1 else r
+
+
+# ---------------------------------------------------------------------------
+# float64 residual field for strict-float64 training (csrc/mg_nrf64.cu)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class ResidualField64:
+    """The residual network with float64 host weights (the reference's own
+    representation, nrf.py:49-101), evaluated by the float64 kernels of
+    mg_nrf64.cu.  Used by train.StrictTrainer."""
+
+    frequency_bands: int = DEFAULT_BANDS
+    layer_widths: tuple = ()
+    weights: list = dc_field(default_factory=list)  # (fan_in, fan_out) float64 numpy
+    biases: list = dc_field(default_factory=list)
+    output_bound: float = OUTPUT_BOUND
+
+    @classmethod
+    def create(cls, rng=None, frequency_bands=DEFAULT_BANDS, hidden=DEFAULT_HIDDEN):
+        widths, ws, bs = init_arrays(rng, frequency_bands, hidden)
+        return cls(int(frequency_bands), widths, ws, bs)
+
+    def parameter_arrays(self):
+        out = {}
+        for li, (w, b) in enumerate(zip(self.weights, self.biases)):
+            out[f"w{li}"] = w
+            out[f"b{li}"] = b
+        return out
+
+
+def _require_f64(field: ResidualField64):
+    if not field.weights:
+        raise UninitializedField("residual field has no weights")
+    if tuple(field.layer_widths) != FUSED_WIDTHS or field.frequency_bands != DEFAULT_BANDS or \
+            field.output_bound != OUTPUT_BOUND:
+        raise UnsupportedResidualField(
+            f"float64 NRF kernels implement the reference widths {FUSED_WIDTHS} with 6 bands and output bound 0.1")
+
+
+class Nrf64Cache:
+    """Device-resident forward activations (the reference's ``cache``,
+    nrf.py:140-145) plus the uploaded weights, consumed by nrf_backward_f64."""
+
+    def __init__(self, field: ResidualField64, x: torch.Tensor):
+        from . import _native as N
+
+        self.x = x
+        self.n = int(x.shape[0])
+        self.w = [dv.to_dev(np.ascontiguousarray(w), torch.float64) for w in field.weights]
+        self.b = [dv.to_dev(np.ascontiguousarray(b), torch.float64) for b in field.biases]
+        self.ws = torch.empty((max(1, N.lib().mg_nrf_f64_workspace_bytes(self.n)),), dtype=torch.uint8,
+                              device=x.device)
+
+
+def nrf_forward_cached_f64(field: ResidualField64, x: torch.Tensor):
+    """(r (n,) float64 device tensor, cache) -- nrf.py:140-145 in float64."""
+    _require_f64(field)
+    x = x.to(torch.float64).contiguous()
+    c = Nrf64Cache(field, x)
+    from . import _native as N
+
+    r = torch.empty((c.n,), dtype=torch.float64, device=x.device)
+    w, b = _ptr_array(c.w), _ptr_array(c.b)  # kept alive across the call
+    N.check(N.lib().mg_nrf_forward_f64(N.ptr(x), c.n, ctypes.addressof(w), ctypes.addressof(b), N.ptr(r),
+                                       N.ptr(c.ws), c.ws.numel(), dv.sptr()), "nrf_forward_f64")
+    return r, c
+
+
+def nrf_backward_f64(cache: Nrf64Cache, upstream: torch.Tensor):
+    """(d_weights, d_biases as float64 numpy, d_points (n, 3) float64 device)
+    of sum_b upstream[b] r(x_b) -- nrf.py:147-182 in float64."""
+    up = upstream.to(torch.float64).contiguous()
+    if up.numel() != cache.n:
+        raise ValueError("upstream length does not match the cached batch")
+    dws = [torch.empty_like(w) for w in cache.w]
+    dbs = [torch.empty_like(b) for b in cache.b]
+    from . import _native as N
+
+    dp = torch.empty((cache.n, 3), dtype=torch.float64, device=up.device)
+    w, b, gw, gb = _ptr_array(cache.w), _ptr_array(cache.b), _ptr_array(dws), _ptr_array(dbs)
+    N.check(N.lib().mg_nrf_backward_f64(N.ptr(cache.x), cache.n, ctypes.addressof(w), ctypes.addressof(b), N.ptr(up),
+                                        N.ptr(dp), ctypes.addressof(gw), ctypes.addressof(gb), N.ptr(cache.ws),
+                                        cache.ws.numel(), dv.sptr()), "nrf_backward_f64")
+    return [dv.to_host(w) for w in dws], [dv.to_host(b) for b in dbs], dp

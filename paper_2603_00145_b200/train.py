@@ -237,6 +237,11 @@ def uniform_lattice_device(r, logits=None):
 
 def init_field_device(coords: torch.Tensor, intensities: torch.Tensor, r: int, logit_eps=1e-4):
     """Logit of the mean sample intensity per lattice cell, 0 where empty (train.py:221-236)."""
+    return uniform_lattice_device(r, _init_logits(coords, intensities, r, logit_eps))
+
+
+def _init_logits(coords: torch.Tensor, intensities: torch.Tensor, r: int, logit_eps):
+    """float64 (r^3,) logits of the per-cell mean intensity (0 where empty)."""
     n = r ** 3
     keys = dv.empty((coords.shape[0],), torch.int32)
     N.check(N.lib().mg_cell_keys_f64(N.ptr(coords), coords.shape[0], r, N.ptr(keys), dv.sptr()), "cell_keys")
@@ -246,8 +251,7 @@ def init_field_device(coords: torch.Tensor, intensities: torch.Tensor, r: int, l
     occ = cnts > 0
     mean = torch.where(occ, sums / cnts.clamp(min=1), torch.full_like(sums, 0.5))
     mean = mean.clamp(logit_eps, 1.0 - logit_eps)
-    lg = torch.where(occ, torch.log(mean) - torch.log1p(-mean), torch.zeros_like(mean))
-    return uniform_lattice_device(r, lg)
+    return torch.where(occ, torch.log(mean) - torch.log1p(-mean), torch.zeros_like(mean))
 
 
 def progressive_upsample_device(field: DeviceField, new_r: int) -> DeviceField:
@@ -1108,7 +1112,18 @@ class Trainer:
 
 
 def smooth_l1_loss_grad(pred, target):
-    """(mean Huber loss, d/dpred) computed by the device kernel."""
+    """(mean Huber loss, d/dpred) computed by the device kernel (float64 in
+    strict mode, render.set_strict_fp64)."""
+    from . import render
+
+    if render.get_strict_fp64():
+        p = dv.to_dev(np.asarray(pred, dtype=np.float64).ravel(), torch.float64)
+        t = dv.to_dev(np.asarray(target, dtype=np.float64).ravel(), torch.float64)
+        up = dv.empty(p.shape, torch.float64)
+        acc = dv.zeros((1,), torch.float64)
+        N.check(N.lib().mg_smooth_l1_f64(N.ptr(p), N.ptr(t), p.numel(), N.ptr(up), N.ptr(acc), dv.sptr()),
+                "smooth_l1_f64")
+        return float(acc.item()), dv.to_host(up)
     p = dv.to_dev(np.asarray(pred, dtype=np.float64).ravel(), torch.float32)
     t = dv.to_dev(np.asarray(target, dtype=np.float64).ravel(), torch.float32)
     up = dv.empty(p.shape, torch.float32)
@@ -1118,16 +1133,21 @@ def smooth_l1_loss_grad(pred, target):
 
 
 def ssim_loss_grad(pred, target):
-    """(1 - mean SSIM, d/dpred) of an (H, W) slice computed by the device kernels."""
+    """(1 - mean SSIM, d/dpred) of an (H, W) slice computed by the device
+    kernels (float64 prediction and gradient in strict mode)."""
+    from . import render
+
     pred = np.asarray(pred, dtype=np.float64)
     h, w = pred.shape
-    p = dv.to_dev(pred.ravel(), torch.float32)
-    t = dv.to_dev(np.asarray(target, dtype=np.float64).ravel(), torch.float32)
-    up = dv.empty(p.shape, torch.float32)
+    strict = render.get_strict_fp64()
+    ty = torch.float64 if strict else torch.float32
+    p = dv.to_dev(pred.ravel(), ty)
+    t = dv.to_dev(np.asarray(target, dtype=np.float64).ravel(), ty)
+    up = dv.empty(p.shape, ty)
     acc = dv.zeros((1,), torch.float64)
     ws = dv.empty((N.lib().mg_ssim_workspace_bytes(h, w),), torch.uint8)
-    N.check(N.lib().mg_ssim_loss_grad(N.ptr(p), N.ptr(t), h, w, 1.0, N.ptr(up), N.ptr(acc), N.ptr(ws), ws.numel(),
-                                      dv.sptr()), "ssim")
+    fn = N.lib().mg_ssim_loss_grad_f64 if strict else N.lib().mg_ssim_loss_grad
+    N.check(fn(N.ptr(p), N.ptr(t), h, w, 1.0, N.ptr(up), N.ptr(acc), N.ptr(ws), ws.numel(), dv.sptr()), "ssim")
     return 1.0 - float(acc.item()) / ((h - 10) * (w - 10)), dv.to_host(up).astype(np.float64).reshape(h, w)
 
 
@@ -1179,10 +1199,24 @@ def progressive_upsample(field, new_resolution):
     Interpolation runs in float32 (the trainer's parameter precision)."""
     from .core import GaussianField
 
+    from . import render
+
     new_r = int(new_resolution)
     old_r = int(field.lattice_dims[0])
     if new_r < old_r:
         raise ShrinkNotAllowed(f"cannot shrink lattice {old_r} -> {new_r}")
+    if render.get_strict_fp64():  # float64 interpolation (mg_upsample_f64)
+        li = np.asarray(field.lattice_index, dtype=np.int64)
+        node_of = np.empty(field.count, np.int32)
+        node_of[(li[:, 0] * old_r + li[:, 1]) * old_r + li[:, 2]] = np.arange(field.count, dtype=np.int32)
+        n = new_r ** 3
+        out = [dv.empty((n, c), torch.float64) for c in (3, 4, 3, 1)]
+        src = [dv.to_dev(field.quaternions, torch.float64), dv.to_dev(field.log_scales, torch.float64),
+               dv.to_dev(field.intensity_logits, torch.float64), dv.to_dev(node_of, torch.int32)]
+        N.check(N.lib().mg_upsample_f64(*[N.ptr(t) for t in src], old_r, new_r, *[N.ptr(o) for o in out],
+                                        dv.sptr()), "upsample_f64")
+        pos, q, sc, lg = (dv.to_host(o) for o in out)
+        return GaussianField(pos, q, sc, lg.reshape(n), (new_r, new_r, new_r), lattice_node_index(new_r))
     up = progressive_upsample_device(DeviceField.from_host(field), new_r).to_host()
     return GaussianField(lattice_node_positions(new_r), up.quaternions, up.log_scales, up.intensity_logits,
                          (new_r, new_r, new_r), lattice_node_index(new_r))
@@ -1193,9 +1227,19 @@ def init_field(cloud, resolution, logit_eps=1e-4):
     (train.py:221-236) on the device (mg_cell_keys_f64 + segmented means)."""
     from .core import GaussianField
 
+    from . import render
+
     r = int(resolution)
-    f = init_field_device(dv.to_dev(np.asarray(cloud.coords, np.float64).reshape(-1, 3), torch.float64),
-                          dv.to_dev(np.asarray(cloud.intensities, np.float64).ravel(), torch.float32), r,
+    coords = dv.to_dev(np.asarray(cloud.coords, np.float64).reshape(-1, 3), torch.float64)
+    if render.get_strict_fp64():  # float64 cell means and logits
+        lg = _init_logits(coords, dv.to_dev(np.asarray(cloud.intensities, np.float64).ravel(), torch.float64), r,
+                          logit_eps)
+        n = r ** 3
+        q = np.zeros((n, 4))
+        q[:, 0] = 1.0
+        return GaussianField(lattice_node_positions(r), q, np.full((n, 3), np.log(1.0 / r)), dv.to_host(lg),
+                             (r, r, r), lattice_node_index(r))
+    f = init_field_device(coords, dv.to_dev(np.asarray(cloud.intensities, np.float64).ravel(), torch.float32), r,
                           logit_eps).to_host()
     return GaussianField(lattice_node_positions(r), f.quaternions, f.log_scales, f.intensity_logits, (r, r, r),
                          lattice_node_index(r))
@@ -1240,3 +1284,6 @@ class AdamState:
         self.groups = {name: {"t": int(g["t"]), "m": {k: np.array(a, dtype=np.float64) for k, a in g["m"].items()},
                               "v": {k: np.array(a, dtype=np.float64) for k, a in g["v"].items()}}
                        for name, g in state.items()}
+
+
+from .strict_train import StrictTrainer  # noqa: E402,F401  (strict-float64 parity path)

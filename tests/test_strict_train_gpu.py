@@ -69,12 +69,14 @@ def test_strict_nrf_matches_reference_golden():
     np.testing.assert_allclose(dv.to_host(dp), z["d_points"], rtol=1e-11, atol=1e-14 * np.abs(z["d_points"]).max())
 
 
-def _run(long_run):
+def _run(long_run, seed=0):
     from paper_2603_00145_b200.recon import load_recon_fixture, psnr
     from paper_2603_00145_b200.strict_train import StrictTrainer
+    from test_recon_gpu import _perturbed
 
     cloud, ts, grids, cfg, tgt = load_recon_fixture(os.path.join(G, "recon_desk64.npz"),
                                                     os.path.join(G, "recon_desk64_long.npz") if long_run else None)
+    cloud, grids = _perturbed(cloud, grids, seed)
     tr = StrictTrainer(cloud, ts, cfg, slice_grids=grids)
     losses = []
     while tr.iteration < cfg.total_iters:
@@ -116,3 +118,23 @@ def test_strict_trainer_follows_reference_long_run():
     # (float32 training is O(1) apart by then); PSNR 27.239721 vs 27.239707 dB
     assert dev.max() < 1e-3
     assert abs(db - tgt.ref_psnr_db) < 1e-3
+
+
+PERTURBED = os.path.join(G, "recon_desk64_long_perturbed.txt")
+
+
+@pytest.mark.skipif(not os.path.exists(PERTURBED), reason="perturbed reference runs missing")
+@pytest.mark.parametrize("seed", [1, 2])
+def test_strict_trainer_reproduces_perturbed_reference_runs(seed):
+    """Rounding-level input perturbations (1e-7 relative) move the
+    reference's own 4,000-iteration PSNR by up to 0.12 dB; the strict path
+    given the same perturbed inputs lands on the same PSNR as the reference
+    did (measured: seed 1 27.232160 vs 27.232404, seed 2 27.178454 vs 27.178436)."""
+    from test_recon_gpu import _reference_ensemble
+
+    ref = _reference_ensemble()
+    if seed not in ref:
+        pytest.skip(f"reference run for seed {seed} not recorded")
+    _, db, _ = _run(True, seed)
+    print(f"seed {seed}: strict {db:.6f} dB, reference {ref[seed]:.6f} dB")
+    assert abs(db - ref[seed]) < 1e-3

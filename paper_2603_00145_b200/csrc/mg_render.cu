@@ -253,6 +253,58 @@ __device__ __noinline__ Window make_window(int cell, int g, int r) {
 }
 
 // ---------------------------------------------------------------------------
+// Cutoff culling for the Gaussian-major backward.  A pair whose Mahalanobis
+// form exceeds 64 contributes nothing (_kernels.py:21, 106-110: skipped), and
+// {d : d^T P d <= 64} lies inside the axis box |d_a| <= 8 sqrt(Sigma_aa).  A
+// Gaussian's candidate points therefore only need the cells of that box
+// intersected with its Chebyshev window.  The box is padded by 1% (m by 2%),
+// far beyond the float32 rounding of m, so every culled pair is one the
+// kernel would have flushed to an exact zero: the accumulators are
+// bit-identical with and without culling, only the candidate walk shrinks.
+// Sigma_aa = kMScale cof_aa(P') / det(P') from the float32 record, in float64.
+// ---------------------------------------------------------------------------
+#ifndef MG_BWD_CULL
+#define MG_BWD_CULL 1
+#endif
+struct CellBox {
+  int lo[3], hi[3];
+};
+
+__device__ __forceinline__ CellBox cutoff_box(const float4 A, const float4 B, const float2 C, int g) {
+  const double p00 = B.x, p11 = B.y, p22 = B.z, p01 = B.w, p02 = C.x, p12 = C.y;
+  const double c00 = p11 * p22 - p12 * p12, c11 = p00 * p22 - p02 * p02, c22 = p00 * p11 - p01 * p01;
+  const double det = p00 * c00 - p01 * (p01 * p22 - p12 * p02) + p02 * (p01 * p12 - p11 * p02);
+  const double s = kMScaleD / det, half_g = 0.5 * (double)g;
+  const double sig[3] = {s * c00, s * c11, s * c22}, mu[3] = {A.x, A.y, A.z};
+  CellBox b;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    b.lo[a] = 0;
+    b.hi[a] = g - 1;
+    if (sig[a] > 0.0 && sig[a] < 1e30) {  // else (degenerate / non-finite): no culling on this axis
+      const double e = 8.08 * sqrt(sig[a]) + 1e-6;
+      const double l = floor((mu[a] - e + 1.0) * half_g), h = floor((mu[a] + e + 1.0) * half_g);
+      b.lo[a] = (int)fmin(fmax(l, 0.0), (double)(g - 1));
+      b.hi[a] = (int)fmin(fmax(h, 0.0), (double)(g - 1));
+    }
+  }
+  return b;
+}
+
+// Shrink a window to (its intersection with) a cell box.
+__device__ __forceinline__ void cull_window(Window& w, const CellBox& b) {
+  const int ihi = min(w.ilo + (int)(((float)w.ncol + 0.5f) * w.inv_nj) - 1, b.hi[0]);
+  const int jhi = min(w.jlo + w.nj - 1, b.hi[1]);
+  w.ilo = max(w.ilo, b.lo[0]);
+  w.jlo = max(w.jlo, b.lo[1]);
+  w.klo = max(w.klo, b.lo[2]);
+  w.khi = min(w.khi, b.hi[2]);
+  w.nj = max(jhi - w.jlo + 1, 0);
+  w.ncol = w.nj > 0 && ihi >= w.ilo && w.khi >= w.klo ? (ihi - w.ilo + 1) * w.nj : 0;
+  w.inv_nj = 1.0f / (float)max(w.nj, 1);
+}
+
+// ---------------------------------------------------------------------------
 // Bitmap segment cursor.  For a batch of <= 128 columns the candidate list is
 // the concatenation of the non-empty column segments.  Each warp keeps, in
 // shared memory, delta[seg] = (segment start element) - (segment start in the
@@ -995,7 +1047,9 @@ __device__ __forceinline__ void bwd_item(const GaussSoA grec, int g0, int ng, in
   GaussAcc<QG> acc;
 #pragma unroll
   for (int k = 0; k < QG; ++k) acc.load(grec, k, g0 + min(k, ng - 1));
-  bwd_window_loop(acc, make_window(cell, g, r), g, prec, pstart, sm, lane);
+  Window w = make_window(cell, g, r);
+  if (MG_BWD_CULL && QG == 1) cull_window(w, cutoff_box(grec.A[g0], grec.B[g0], grec.C[g0], g));
+  bwd_window_loop(acc, w, g, prec, pstart, sm, lane);
   bwd_store<QG>(acc, g0, ng, acc10, lane);
 }
 
@@ -1345,6 +1399,16 @@ __device__ __forceinline__ void bwd_pair_item(const GaussSoA grec, int j, int ce
   Window w = make_window(cell_a, g, r);
   const int ka = cell_a % g, kb = ka + (cell_b - cell_a);
   w.khi = min(kb + r, g - 1);
+  if (MG_BWD_CULL) {  // union of the two cutoff boxes (lane 0: A, lane 1: B)
+    const int jj = j + (lane & 1);
+    CellBox b = cutoff_box(grec.A[jj], grec.B[jj], grec.C[jj], g);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      b.lo[a] = min(b.lo[a], __shfl_xor_sync(MG_FULL, b.lo[a], 1));
+      b.hi[a] = max(b.hi[a], __shfl_xor_sync(MG_FULL, b.hi[a], 1));
+    }
+    cull_window(w, b);
+  }
   const PairCols cols{pstart, max(kb - r, 0), min(ka + r, g - 1) + 1};
   const unsigned upto = 0xffffffffu >> (31 - lane);
   for (int c0 = 0; c0 < w.ncol; c0 += 128) {

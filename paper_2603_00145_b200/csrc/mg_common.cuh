@@ -1,5 +1,6 @@
 // mg_common.cuh -- shared device helpers for the B200 (sm_100a) Gaussian path.
 #pragma once
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -153,25 +154,29 @@ __device__ __forceinline__ int flat_cell(int ci, int cj, int ck, int g) { return
 
 // Gaussian records, structure-of-arrays inside one float buffer of 12*N:
 // A = float4[N] {mu.xyz, alpha} at 0, B = float4[N] {P'00,P'11,P'22,P'01} at
-// 4N, C = float2[N] {P'02,P'12} at 8N.  Warp-wide loads of consecutive
-// records are fully coalesced (4 + 4 + 2 sectors per 32 records).
+// 4N, C = float2[N] {P'02,P'12} at 8N, E = uint2[N] at 10N: the half-extents
+// of the cutoff ellipsoid's axis box (three fp16, rounded up; +inf = no
+// culling), read by the backward's candidate-window culling.  Warp-wide loads
+// of consecutive records are fully coalesced (4 + 4 + 2 sectors per 32).
 struct GaussSoA {
   const float4* A;
   const float4* B;
   const float2* C;
+  const uint2* E;
 };
 struct GaussOut {
   float4* A;
   float4* B;
   float2* C;
+  uint2* E;
 };
 inline GaussSoA gauss_soa(const float* base, int64_t n) {
   return GaussSoA{reinterpret_cast<const float4*>(base), reinterpret_cast<const float4*>(base + 4 * n),
-                  reinterpret_cast<const float2*>(base + 8 * n)};
+                  reinterpret_cast<const float2*>(base + 8 * n), reinterpret_cast<const uint2*>(base + 10 * n)};
 }
 inline GaussOut gauss_out(float* base, int64_t n) {
   return GaussOut{reinterpret_cast<float4*>(base), reinterpret_cast<float4*>(base + 4 * n),
-                  reinterpret_cast<float2*>(base + 8 * n)};
+                  reinterpret_cast<float2*>(base + 8 * n), reinterpret_cast<uint2*>(base + 10 * n)};
 }
 
 // Host-side count of kernel launches issued by this library (all streams),

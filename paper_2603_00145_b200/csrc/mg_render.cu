@@ -57,6 +57,19 @@ __device__ __forceinline__ void quat_rot_d(double w, double x, double y, double 
   R[8] = 1.0 - 2.0 * (x * x + y * y);
 }
 
+// Cutoff box half-extents from Sigma_aa (m <= 64 <=> |d_a| <= 8 sqrt(Sigma_aa)),
+// padded by 1% (+1e-6) and rounded up to fp16; cond > 1e4 or non-finite: +inf.
+__device__ __forceinline__ uint2 pack_extents(const double (&sig)[3], double cond) {
+  unsigned short h[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double e = 8.08 * sqrt(sig[a]) + 1e-6;
+    const bool ok = sig[a] > 0.0 && e < 6.0e4 && cond < 1e4;
+    h[a] = __half_as_ushort(ok ? __float2half_ru((float)e) : __ushort_as_half((unsigned short)0x7c00));
+  }
+  return make_uint2((unsigned)h[0] | ((unsigned)h[1] << 16), (unsigned)h[2]);
+}
+
 __device__ __forceinline__ void activate_one(const float* pos, const float* quat, const float* ls, const float* lg,
                                              int64_t i, GaussOut rec, int64_t p, int* err) {
   double qw = quat[4 * i], qx = quat[4 * i + 1], qy = quat[4 * i + 2], qz = quat[4 * i + 3];
@@ -86,6 +99,12 @@ __device__ __forceinline__ void activate_one(const float* pos, const float* quat
   rec.A[p] = make_float4(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], (float)(alpha * kWeightScaleD));
   rec.B[p] = make_float4((float)P[0], (float)P[1], (float)P[2], (float)P[3]);
   rec.C[p] = make_float2((float)P[4], (float)P[5]);
+  // Sigma = R diag(1/e) R^T
+  double sig[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) sig[a] = R[3 * a] * R[3 * a] / e[0] + R[3 * a + 1] * R[3 * a + 1] / e[1] + R[3 * a + 2] * R[3 * a + 2] / e[2];
+  const double emax = fmax(e[0], fmax(e[1], e[2])), emin = fmin(e[0], fmin(e[1], e[2]));
+  rec.E[p] = pack_extents(sig, emax / emin);
 }
 
 __global__ void gauss_activate_kernel(const float* __restrict__ pos, const float* __restrict__ quat,
@@ -111,6 +130,12 @@ __global__ void gauss_pack_prepared_kernel(const double* __restrict__ mu, const 
     grec.B[p] = make_float4((float)(kMScaleD * P[0]), (float)(kMScaleD * P[3]), (float)(kMScaleD * P[5]),
                             (float)(kMScaleD * P[1]));
     grec.C[p] = make_float2((float)(kMScaleD * P[2]), (float)(kMScaleD * P[4]));
+    // Sigma_aa = cof_aa(P) / det(P); Sigma_aa * P_aa >= 1 grows with the condition number
+    const double c00 = P[3] * P[5] - P[4] * P[4], c11 = P[0] * P[5] - P[2] * P[2], c22 = P[0] * P[3] - P[1] * P[1];
+    const double det = P[0] * c00 - P[1] * (P[1] * P[5] - P[4] * P[2]) + P[2] * (P[1] * P[4] - P[3] * P[2]);
+    double sig[3] = {c00 / det, c11 / det, c22 / det};
+    const double cond = fmax(sig[0] * P[0], fmax(sig[1] * P[3], sig[2] * P[5]));
+    grec.E[p] = pack_extents(sig, cond);
   }
 }
 
@@ -255,13 +280,14 @@ __device__ __noinline__ Window make_window(int cell, int g, int r) {
 // ---------------------------------------------------------------------------
 // Cutoff culling for the Gaussian-major backward.  A pair whose Mahalanobis
 // form exceeds 64 contributes nothing (_kernels.py:21, 106-110: skipped), and
-// {d : d^T P d <= 64} lies inside the axis box |d_a| <= 8 sqrt(Sigma_aa).  A
+// {d : d^T P d <= 64} lies inside the axis box |d_a| <= 8 sqrt(Sigma_aa)
+// (precomputed per Gaussian with the records, GaussSoA::E).  A
 // Gaussian's candidate points therefore only need the cells of that box
 // intersected with its Chebyshev window.  The box is padded by 1% (m by 2%),
 // far beyond the float32 rounding of m, so every culled pair is one the
-// kernel would have flushed to an exact zero: the accumulators are
-// bit-identical with and without culling, only the candidate walk shrinks.
-// Sigma_aa = kMScale cof_aa(P') / det(P') from the float32 record, in float64.
+// kernel would have flushed to an exact zero: culling drops no contribution
+// (the sums differ from the unculled walk only in float32 summation order,
+// as the shorter candidate list hands points to different lanes).
 // ---------------------------------------------------------------------------
 #ifndef MG_BWD_CULL
 #define MG_BWD_CULL 1
@@ -270,29 +296,55 @@ struct CellBox {
   int lo[3], hi[3];
 };
 
-__device__ __forceinline__ CellBox cutoff_box(const float4 A, const float4 B, const float2 C, int g) {
-  const double p00 = B.x, p11 = B.y, p22 = B.z, p01 = B.w, p02 = C.x, p12 = C.y;
-  const double c00 = p11 * p22 - p12 * p12, c11 = p00 * p22 - p02 * p02, c22 = p00 * p11 - p01 * p01;
-  const double det = p00 * c00 - p01 * (p01 * p22 - p12 * p02) + p02 * (p01 * p12 - p11 * p02);
-  const double s = kMScaleD / det, half_g = 0.5 * (double)g;
-  const double sig[3] = {s * c00, s * c11, s * c22}, mu[3] = {A.x, A.y, A.z};
+__device__ __forceinline__ CellBox cutoff_box(const float4 A, const uint2 E, int g) {
+  const float e[3] = {__half2float(__ushort_as_half((unsigned short)(E.x & 0xffffu))),
+                      __half2float(__ushort_as_half((unsigned short)(E.x >> 16))),
+                      __half2float(__ushort_as_half((unsigned short)(E.y & 0xffffu)))};
+  const float mu[3] = {A.x, A.y, A.z}, hg = 0.5f * (float)g;
   CellBox b;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    b.lo[a] = 0;
-    b.hi[a] = g - 1;
-    if (sig[a] > 0.0 && sig[a] < 1e30) {  // else (degenerate / non-finite): no culling on this axis
-      const double e = 8.08 * sqrt(sig[a]) + 1e-6;
-      const double l = floor((mu[a] - e + 1.0) * half_g), h = floor((mu[a] + e + 1.0) * half_g);
-      b.lo[a] = (int)fmin(fmax(l, 0.0), (double)(g - 1));
-      b.hi[a] = (int)fmin(fmax(h, 0.0), (double)(g - 1));
-    }
+    // +inf extents clamp to the whole grid; float rounding of the box edges is
+    // ~1e-7 relative, far inside the 1% padding
+    b.lo[a] = (int)fminf(fmaxf(floorf((mu[a] + 1.0f - e[a]) * hg), 0.0f), (float)(g - 1));
+    b.hi[a] = (int)fminf(fmaxf(floorf((mu[a] + 1.0f + e[a]) * hg), 0.0f), (float)(g - 1));
   }
   return b;
 }
 
+// Can the box trim the window at all?  Only if some half-extent is below r
+// cells: a box reaches floor(frac + e) >= floor(e) cells either side (fp16
+// bit patterns of non-negative values order like integers);
+// fields whose Gaussians all reach past the window (upsampled levels) then
+// skip the out-of-line call.
+__device__ __forceinline__ bool may_cull(uint2 E, int g, int r) {
+  const unsigned thr = __half_as_ushort(__float2half_ru(2.0f * (float)r / (float)g));
+  const unsigned m = min(min(E.x & 0xffffu, E.x >> 16), E.y & 0xffffu);
+  return m < thr;
+}
+
+// Kept out of line so the item loops' register allocation is unaffected.
+__device__ __forceinline__ void cull_window(Window& w, const CellBox& b);
+__device__ __noinline__ Window cull_single_window(Window w, const GaussSoA grec, int j, int g) {
+  cull_window(w, cutoff_box(grec.A[j], grec.E[j], g));
+  return w;
+}
+// union of the pair's two boxes (even lanes: Gaussian j, odd lanes: j + 1)
+__device__ __noinline__ Window cull_pair_window(Window w, const GaussSoA grec, int j, int g, int lane) {
+  const int jj = j + (lane & 1);
+  CellBox b = cutoff_box(grec.A[jj], grec.E[jj], g);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    b.lo[a] = min(b.lo[a], __shfl_xor_sync(MG_FULL, b.lo[a], 1));
+    b.hi[a] = max(b.hi[a], __shfl_xor_sync(MG_FULL, b.hi[a], 1));
+  }
+  cull_window(w, b);
+  return w;
+}
+
 // Shrink a window to (its intersection with) a cell box.
 __device__ __forceinline__ void cull_window(Window& w, const CellBox& b) {
+  if (MG_BWD_CULL == 2) return;  // A/B: boxes computed, not applied
   const int ihi = min(w.ilo + (int)(((float)w.ncol + 0.5f) * w.inv_nj) - 1, b.hi[0]);
   const int jhi = min(w.jlo + w.nj - 1, b.hi[1]);
   w.ilo = max(w.ilo, b.lo[0]);
@@ -1044,11 +1096,11 @@ template <int QG>
 __device__ __forceinline__ void bwd_item(const GaussSoA grec, int g0, int ng, int cell, int g, int r,
                                          const float4* __restrict__ prec, const int* __restrict__ pstart,
                                          float* __restrict__ acc10, SegSmem& sm, int lane) {
+  Window w = make_window(cell, g, r);
+  if (MG_BWD_CULL && QG == 1 && may_cull(grec.E[g0], g, r)) w = cull_single_window(w, grec, g0, g);
   GaussAcc<QG> acc;
 #pragma unroll
   for (int k = 0; k < QG; ++k) acc.load(grec, k, g0 + min(k, ng - 1));
-  Window w = make_window(cell, g, r);
-  if (MG_BWD_CULL && QG == 1) cull_window(w, cutoff_box(grec.A[g0], grec.B[g0], grec.C[g0], g));
   bwd_window_loop(acc, w, g, prec, pstart, sm, lane);
   bwd_store<QG>(acc, g0, ng, acc10, lane);
 }
@@ -1388,6 +1440,12 @@ __device__ __forceinline__ void pair_masked(GaussAcc<2>& acc, const float4& a, c
 __device__ __forceinline__ void bwd_pair_item(const GaussSoA grec, int j, int cell_a, int cell_b, int g, int r,
                                               const float4* __restrict__ prec, const int* __restrict__ pstart,
                                               float* __restrict__ acc10, PairSmem& ps, int lane) {
+  // window first: the out-of-line cull call then has few live registers
+  Window w = make_window(cell_a, g, r);
+  const int ka = cell_a % g, kb = ka + (cell_b - cell_a);
+  w.khi = min(kb + r, g - 1);
+  if (MG_BWD_CULL && (may_cull(grec.E[j], g, r) || may_cull(grec.E[j + 1], g, r)))
+    w = cull_pair_window(w, grec, j, g, lane);
 #if MG_BWD_PAIR_GPACK
   GaussPairAcc acc;
   acc.load(grec, j, j + 1, &ps.stage[0], lane);
@@ -1396,19 +1454,6 @@ __device__ __forceinline__ void bwd_pair_item(const GaussSoA grec, int j, int ce
   acc.load(grec, 0, j);
   acc.load(grec, 1, j + 1);
 #endif
-  Window w = make_window(cell_a, g, r);
-  const int ka = cell_a % g, kb = ka + (cell_b - cell_a);
-  w.khi = min(kb + r, g - 1);
-  if (MG_BWD_CULL) {  // union of the two cutoff boxes (lane 0: A, lane 1: B)
-    const int jj = j + (lane & 1);
-    CellBox b = cutoff_box(grec.A[jj], grec.B[jj], grec.C[jj], g);
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      b.lo[a] = min(b.lo[a], __shfl_xor_sync(MG_FULL, b.lo[a], 1));
-      b.hi[a] = max(b.hi[a], __shfl_xor_sync(MG_FULL, b.hi[a], 1));
-    }
-    cull_window(w, b);
-  }
   const PairCols cols{pstart, max(kb - r, 0), min(ka + r, g - 1) + 1};
   const unsigned upto = 0xffffffffu >> (31 - lane);
   for (int c0 = 0; c0 < w.ncol; c0 += 128) {

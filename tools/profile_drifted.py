@@ -21,12 +21,14 @@ def main():
     ap.add_argument("--config", default="C4")
     ap.add_argument("--train", type=int, default=200)
     ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--schedule", action="store_true",
+                    help="train through the config's resolution schedule instead of starting at its final level")
     a = ap.parse_args()
     import torch
 
     from paper_2603_00145_b200.train import Trainer
 
-    data, cloud, grids, psf, cfg = bench.make_workload(a.config, 0, final_only=True)
+    data, cloud, grids, psf, cfg = bench.make_workload(a.config, 0, final_only=not a.schedule)
     tr = Trainer(cloud, data.transforms, cfg, slice_grids=grids, slice_psf=psf, graph=True)
     for _ in range(a.train):
         tr.step_pipelined()

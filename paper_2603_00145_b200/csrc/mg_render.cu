@@ -295,6 +295,13 @@ __device__ __noinline__ Window make_window(int cell, int g, int r) {
 struct CellBox {
   int lo[3], hi[3];
 };
+// MGAUSS_BWD_CULL=0 turns culling off at launch time (A/B and the test that
+// checks culling drops no contribution); read at every launch, so a graph
+// keeps the value it was captured with.
+static inline int bwd_cull_enabled() {
+  const char* e = getenv("MGAUSS_BWD_CULL");
+  return (e && e[0] == '0') ? 0 : 1;
+}
 
 __device__ __forceinline__ CellBox cutoff_box(const float4 A, const uint2 E, int g) {
   const float e[3] = {__half2float(__ushort_as_half((unsigned short)(E.x & 0xffffu))),
@@ -344,7 +351,6 @@ __device__ __noinline__ Window cull_pair_window(Window w, const GaussSoA grec, i
 
 // Shrink a window to (its intersection with) a cell box.
 __device__ __forceinline__ void cull_window(Window& w, const CellBox& b) {
-  if (MG_BWD_CULL == 2) return;  // A/B: boxes computed, not applied
   const int ihi = min(w.ilo + (int)(((float)w.ncol + 0.5f) * w.inv_nj) - 1, b.hi[0]);
   const int jhi = min(w.jlo + w.nj - 1, b.hi[1]);
   w.ilo = max(w.ilo, b.lo[0]);
@@ -1095,9 +1101,9 @@ __device__ __forceinline__ void bwd_store(const Acc& acc, int g0, int ng, float*
 template <int QG>
 __device__ __forceinline__ void bwd_item(const GaussSoA grec, int g0, int ng, int cell, int g, int r,
                                          const float4* __restrict__ prec, const int* __restrict__ pstart,
-                                         float* __restrict__ acc10, SegSmem& sm, int lane) {
+                                         float* __restrict__ acc10, SegSmem& sm, int lane, bool cull = false) {
   Window w = make_window(cell, g, r);
-  if (MG_BWD_CULL && QG == 1 && may_cull(grec.E[g0], g, r)) w = cull_single_window(w, grec, g0, g);
+  if (MG_BWD_CULL && QG == 1 && cull && may_cull(grec.E[g0], g, r)) w = cull_single_window(w, grec, g0, g);
   GaussAcc<QG> acc;
 #pragma unroll
   for (int k = 0; k < QG; ++k) acc.load(grec, k, g0 + min(k, ng - 1));
@@ -1439,12 +1445,12 @@ __device__ __forceinline__ void pair_masked(GaussAcc<2>& acc, const float4& a, c
 
 __device__ __forceinline__ void bwd_pair_item(const GaussSoA grec, int j, int cell_a, int cell_b, int g, int r,
                                               const float4* __restrict__ prec, const int* __restrict__ pstart,
-                                              float* __restrict__ acc10, PairSmem& ps, int lane) {
+                                              float* __restrict__ acc10, PairSmem& ps, int lane, bool cull) {
   // window first: the out-of-line cull call then has few live registers
   Window w = make_window(cell_a, g, r);
   const int ka = cell_a % g, kb = ka + (cell_b - cell_a);
   w.khi = min(kb + r, g - 1);
-  if (MG_BWD_CULL && (may_cull(grec.E[j], g, r) || may_cull(grec.E[j + 1], g, r)))
+  if (MG_BWD_CULL && cull && (may_cull(grec.E[j], g, r) || may_cull(grec.E[j + 1], g, r)))
     w = cull_pair_window(w, grec, j, g, lane);
 #if MG_BWD_PAIR_GPACK
   GaussPairAcc acc;
@@ -1521,7 +1527,8 @@ __global__ void __launch_bounds__(kBwdWarps * 32, PAIR ? MG_BWD_PAIR_MINB : MG_B
                                                                   const int* __restrict__ pstart,
                                                                   const int4* __restrict__ items,
                                                                   const int* __restrict__ nitems_dev,
-                                                                  int n_implicit, float* __restrict__ acc10) {
+                                                                  int n_implicit, float* __restrict__ acc10,
+                                                                  int cull) {
   // per warp: SegSmem for single items, PairSmem for pairs (aliased); dynamic,
   // so more than 16 warps fit (static shared memory stops at 48 KB)
   extern __shared__ __align__(16) unsigned char bwd_dyn[];
@@ -1540,10 +1547,10 @@ __global__ void __launch_bounds__(kBwdWarps * 32, PAIR ? MG_BWD_PAIR_MINB : MG_B
       const int cb = j + 1 < n_implicit ? (int)gkey[j + 1] : -1;
       const int dk = cb - ca;  // cells of one column, dk apart (sorted, so dk >= 0 when cb >= 0)
       if (cb >= 0 && dk <= MG_BWD_PAIR_DMAX && ca % g + dk <= g - 1) {
-        bwd_pair_item(grec, j, ca, cb, g, r, prec, pstart, acc10, s_ws[warp].pair, lane);
+        bwd_pair_item(grec, j, ca, cb, g, r, prec, pstart, acc10, s_ws[warp].pair, lane, cull != 0);
       } else {
-        bwd_item<1>(grec, j, 1, ca, g, r, prec, pstart, acc10, s_ws[warp].seg, lane);
-        if (cb >= 0) bwd_item<1>(grec, j + 1, 1, cb, g, r, prec, pstart, acc10, s_ws[warp].seg, lane);
+        bwd_item<1>(grec, j, 1, ca, g, r, prec, pstart, acc10, s_ws[warp].seg, lane, cull != 0);
+        if (cb >= 0) bwd_item<1>(grec, j + 1, 1, cb, g, r, prec, pstart, acc10, s_ws[warp].seg, lane, cull != 0);
       }
     }
     return;
@@ -1561,7 +1568,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, PAIR ? MG_BWD_PAIR_MINB : MG_B
   for (; it < nitems; it += stride) {
     const int4 item = MG_BWD_IPF ? next : load_item(it);  // {first, cell, count, 0}
     if (MG_BWD_IPF && it + stride < nitems) next = load_item(it + stride);  // loads under this item
-    bwd_item<1>(grec, item.x, 1, item.y, g, r, prec, pstart, acc10, s_ws[warp].seg, lane);
+    bwd_item<1>(grec, item.x, 1, item.y, g, r, prec, pstart, acc10, s_ws[warp].seg, lane, cull != 0);
   }
 }
 
@@ -2075,7 +2082,7 @@ void launch_backward_staged(const float* grec_raw, int64_t n_gauss, const uint32
   const size_t dsm = bwd_smem_bytes(kBwdWarps);
   MG_LAUNCH(backward_kernel<false><<<(unsigned)persistent_blocks(backward_kernel<false>, kBwdWarps * 32, want, dsm),
                                      kBwdWarps * 32, dsm, st>>>(grec, gkey, gstart, g, r, prec, pstart, oitems,
-                                                                counts + 1, 0, acc10));
+                                                                counts + 1, 0, acc10, bwd_cull_enabled()));
 }
 
 void launch_backward(const float* grec_raw, int64_t n_gauss, const uint32_t* gkey, const int* gstart, int g, int r,
@@ -2089,7 +2096,7 @@ void launch_backward(const float* grec_raw, int64_t n_gauss, const uint32_t* gke
   auto k = pairs ? backward_kernel<true> : backward_kernel<false>;
   const size_t dsm = bwd_smem_bytes(nw);
   MG_LAUNCH(k<<<(unsigned)persistent_blocks(k, nw * 32, want, dsm), nw * 32, dsm, st>>>(
-      grec, gkey, gstart, g, r, prec, pstart, items, nitems, (int)n_gauss, acc10));
+      grec, gkey, gstart, g, r, prec, pstart, items, nitems, (int)n_gauss, acc10, bwd_cull_enabled()));
 }
 
 }  // namespace mg

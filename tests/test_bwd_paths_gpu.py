@@ -8,6 +8,10 @@ cloud (several Gaussians per cell, odd N, non-adjacent cells):
 - staged strips (MGAUSS_STAGED_BWD=1, opt-in): TMA bulk copies of each strip's
   point neighbourhood into shared memory under an mbarrier.
 
+Cutoff culling (on by default in all of them) is checked separately: with
+and without it (MGAUSS_BWD_CULL=0) the gradients agree to float32 summation
+order (measured <= 2e-7 of the largest entry).
+
 The switches are read once per process, so every variant runs in a
 subprocess; the oracle gradients come from the committed golden (lattice) and
 the CPU oracle (random cloud)."""
@@ -82,3 +86,23 @@ def test_backward_path_matches_reference(tmp_path, variant, name):
     got, want = np.load(out), _want(name)
     for k in ("dp", "dq", "ds", "dl"):
         assert_grad_close(got[k], want[k], name=f"{variant}:{name}:{k}")
+
+
+@pytest.mark.parametrize("name", ["lattice", "random"])
+@pytest.mark.parametrize("pairs", ["1", "0"])
+def test_cutoff_culling_drops_no_contribution(tmp_path, name, pairs):
+    """Cutoff culling (MGAUSS_BWD_CULL, default on) only skips pairs the
+    kernel would flush to exact zeros: with and without it the accumulators
+    differ by float32 summation order alone -- far below the contract
+    tolerance, and no gradient entry may move beyond that."""
+    got = {}
+    for cull in ("1", "0"):
+        out = tmp_path / f"cull{cull}_{pairs}_{name}.npz"
+        env = dict(os.environ, MGAUSS_STAGED_BWD="0", MGAUSS_BWD_PAIRS=pairs, MGAUSS_BWD_CULL=cull)
+        subprocess.run([sys.executable, "-c", SCRIPT, ROOT, str(out), name], env=env, check=True, timeout=600)
+        got[cull] = np.load(out)
+    for k in ("dp", "dq", "ds", "dl"):
+        on, off = got["1"][k], got["0"][k]
+        dev = np.abs(on - off).max() / np.abs(off).max()
+        print(f"{name} pairs={pairs} {k}: max |culled - unculled| / max |unculled| = {dev:.2e}")
+        assert dev <= 2e-6

@@ -75,3 +75,38 @@ def test_own_checkpoint_resumes_bit_exactly(tmp_path):
     assert a.rng.bit_generator.state == b.rng.bit_generator.state
     a.close()
     b.close()
+
+
+def test_resume_takes_the_checkpoint_config(tmp_path):
+    """A trainer constructed with other learning rates / loss weights resumes
+    on the checkpoint's config, as the reference CLI's --resume does
+    (cli.py:121-123): every optimizer group -- including the fused Gaussian
+    Adam + anisotropy kernel, whose hyperparameters live on the device --
+    continues bit-exactly like the uninterrupted run."""
+    import dataclasses
+
+    from paper_2603_00145_b200 import _device as dv
+    from paper_2603_00145_b200 import io as mio
+    from paper_2603_00145_b200.train import TrainConfig
+
+    z = load_golden("io")
+    cfg = TrainConfig(resolution_schedule=((0, 8),), use_nrf=False, use_ssim=True, batch_points=2048, seed=5,
+                      total_iters=8)
+    other = dataclasses.replace(cfg, lr_position=0.01, lr_rotation=0.02, lr_scale=0.03, lr_intensity=0.2,
+                                lambda_aniso=0.7, lambda_ratio=1.1, adam_beta1=0.8)
+    a = _trainer(z, cfg)
+    for _ in range(3):
+        a.step()
+    p = tmp_path / "ck.mgss"
+    mio.save_checkpoint(p, {"trainer": a.state_dict()})
+    b = _trainer(z, other)
+    b.load_state_dict(mio.load_checkpoint(p)["trainer"])
+    assert b.config.lr_position == cfg.lr_position and b.config.lambda_aniso == cfg.lambda_aniso
+    for _ in range(3):
+        a.step()
+        b.step()
+    for x, y in [(a.field.positions, b.field.positions), (a.field.log_scales, b.field.log_scales),
+                 (a.field.logits, b.field.logits), (a.m, b.m), (a.v, b.v), (a.tq, b.tq)]:
+        np.testing.assert_array_equal(dv.to_host(x), dv.to_host(y))
+    a.close()
+    b.close()

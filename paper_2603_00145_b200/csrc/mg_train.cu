@@ -694,7 +694,10 @@ void launch_epilogue_f64(const double* d_mu, const double* d_abar6, const double
 }
 // Deterministic reduction geometry: blocks of kTrWarps warps, at most
 // kTrBlocks blocks; the per-warp slice tables must fit in shared memory.
-constexpr int kTrWarps = 4, kTrBlocks = 148;
+#ifndef MG_TR_BLOCKS
+#define MG_TR_BLOCKS 296  // two blocks per SM (smem-bound tables): C4 -28 us, C2 -8 us per step vs 148; 592 slower
+#endif
+constexpr int kTrWarps = 4, kTrBlocks = MG_TR_BLOCKS;
 constexpr size_t kTrSmemMax = 200 * 1024;
 static size_t tr_smem(int k) { return sizeof(double) * ((size_t)kTrWarps * 12 * k + (size_t)kTrWarps * 32 * 12); }
 static bool tr_deterministic(int k) { return tr_smem(k) <= kTrSmemMax; }

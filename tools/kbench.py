@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--config", default="C2")
     ap.add_argument("--train", type=int, default=3, help="training steps before timing (drifted field)")
+    ap.add_argument("--radius", type=int, default=None, help="override the candidate radius (what-if timing only)")
     ap.add_argument("--schedule", action="store_true",
                     help="train through the config's resolution schedule (upsampled fields) instead of its final level")
     a = ap.parse_args()
@@ -27,6 +28,10 @@ def main():
     from paper_2603_00145_b200.train import Trainer
 
     data, cloud, grids, psf, cfg = bench.make_workload(a.config, 0, final_only=not a.schedule)
+    if a.radius is not None:
+        import dataclasses
+
+        cfg = dataclasses.replace(cfg, block_radius=a.radius)
     tr = Trainer(cloud, data.transforms, cfg, slice_grids=grids, slice_psf=psf, graph=False)
     for _ in range(max(3, a.train)):
         tr.step(sync=False)

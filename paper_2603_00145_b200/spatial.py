@@ -3,9 +3,9 @@
 query_local).
 
 The bucket assignment is evaluated in float64 exactly as numpy does
-(floor((x + 1) * (G / 2)), clamped), and the stable radix sort keeps
-ascending primitive order inside a cell, so ``cell_starts`` and
-``cell_indices`` are bit-identical to the reference.
+(floor((x + 1) * (G / 2)), clamped), and the counting sort's in-cell rank
+pass (csrc/mg_sort.cu) keeps ascending primitive order inside a cell, so
+``cell_starts`` and ``cell_indices`` are bit-identical to the reference.
 """
 
 from __future__ import annotations

@@ -2,11 +2,12 @@
 /root/reference/pkg/src/mgauss/train.py (TrainConfig, losses, AdamState,
 progressive_upsample, init_field, Trainer.step / run / render_volume).
 
-One step runs entirely on the B200: Gaussian binning (radix sort) and
+One step runs entirely on the B200: Gaussian binning (counting sort) and
 activation, point transform + PSF taps + binning, the cell-exact forward
 (with H = sum alpha g P d for d_points), smooth-L1 and SSIM gradients,
-the Gaussian-major backward, transform gradients, and one fused kernel for
-the chain rule + anisotropy penalty + Adam on the four Gaussian groups.
+the Gaussian-major backward (cutoff-culled windows), transform gradients,
+the NRF on tensor cores, and one fused kernel for the chain rule +
+anisotropy penalty + Adam on the four Gaussian groups.
 The host only draws batch indices from the reference's RNG stream
 (SeedSequence(seed).spawn(2), train.py:332-335,348-363,408) so batches are
 identical to the reference's.  With ``graph=True`` the step is captured
@@ -15,6 +16,9 @@ once per lattice level and replayed as a CUDA graph.
 Multi-GPU: Gaussians replicated, sample points sharded; the
 only exchange is an all-reduce(sum) of the per-Gaussian accumulators, the
 transform accumulators and the loss partials.
+
+StrictTrainer (strict_train.py, re-exported here) is the same step on float64
+kernels in the reference's operation order, for parity runs.
 """
 
 from __future__ import annotations

@@ -557,6 +557,12 @@ def run_ours(args):
             recon = recon_desk64()
         except Exception as exc:
             recon = {"error": repr(exc)[:200]}
+    speed = None
+    if not args.no_recon and world == 1:
+        try:
+            speed = speedup_c7()
+        except Exception as exc:
+            speed = {"error": repr(exc)[:200]}
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_tot / args.steps,
@@ -592,6 +598,7 @@ def run_ours(args):
         "secondary": secondary,
         "inference": infer,
         "recon": recon,
+        "block_speedup": speed,
         "clocks": clocks,
         "gpu_launches": nlaunch * args.steps,
         "gpu_launches_note": "library kernels per step (mg_launch_count over one eager step) x timed steps; "
@@ -670,6 +677,23 @@ def run_reference(args):
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
+
+
+def speedup_c7():
+    """The reference's bench_speedup at its acceptance-criterion-7 inputs (cli.py:258-299,
+    tests/test_acceptance.py:327-337): 216k primitives, 1M points, G = 70, r = 5, seed 7, wall clock around the
+    host-level render_points / render_points_dense calls (numpy in and out), as the reference times them."""
+    from paper_2603_00145_b200.speedup import bench_speedup
+
+    row = bench_speedup(num_primitives=216000, num_points=1_000_000, grid_resolution=70, radius=5,
+                        dense_sample=10000, seed=7)
+    b, d = row.pop("block_intensities_sample"), row.pop("dense_intensities_sample")
+    row["block_vs_dense_max_rel"] = float(np.abs(b - d).max() / max(np.abs(d).max(), 1e-30))
+    row["block_pairs_per_s"] = row["candidate_pairs"] / row["block_seconds"]
+    row["reference"] = {"block_seconds": 64.3, "dense_seconds_total": 1007.0, "threads": 1,
+                        "source": "BASELINE.md section 2 (survey measurement of the reference, not published)"}
+    row["vs_reference_block"] = 64.3 / row["block_seconds"]
+    return row
 
 
 def recon_desk64():

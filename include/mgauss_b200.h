@@ -272,7 +272,9 @@ int mg_block_backward_f64(const double *points, const int64_t *slice_ids, int64_
  * reference's numpy code.  mg_nrf_forward_f64 fills `ws` with the forward
  * cache (encoding, activations) that mg_nrf_backward_f64 consumes, the role
  * of nrf_forward_cached's cache (nrf.py:140-145); weights are (fan_in,
- * fan_out) row-major float64, widths 39-64-64-64-64-1. */
+ * fan_out) row-major float64; widths[0..depth] = (3 + 6 bands, hidden...,
+ * 1), every width <= 64, depth <= 8 (any ResidualField.create configuration
+ * of that size, nrf.py:58-83). */
 int mg_smooth_l1_f64(const double *pred, const double *target, int64_t b, double *upstream_out, double *loss_acc,
                      void *stream);
 int mg_ssim_loss_grad_f64(const double *pred, const double *target, int64_t h, int64_t w, double scale,
@@ -282,8 +284,10 @@ int mg_upsample_f64(const double *quat_old, const double *log_scales_old, const 
                     double *log_scales, double *logits, void *stream);
 size_t mg_nrf_f64_workspace_bytes(int64_t b);
 int mg_nrf_forward_f64(const double *x, int64_t b, const double *const *w, const double *const *bias,
-                       double *r_out, void *ws, size_t ws_bytes, void *stream);
+                       const int32_t *widths, int32_t depth, int32_t bands, double output_bound, double *r_out,
+                       void *ws, size_t ws_bytes, void *stream);
 int mg_nrf_backward_f64(const double *x, int64_t b, const double *const *w, const double *const *bias,
+                        const int32_t *widths, int32_t depth, int32_t bands, double output_bound,
                         const double *upstream, double *d_points, double *const *d_w, double *const *d_b, void *ws,
                         size_t ws_bytes, void *stream);
 size_t mg_dense_workspace_bytes(int64_t n);

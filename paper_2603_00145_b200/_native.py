@@ -76,8 +76,8 @@ SIGNATURES = {
     "mg_ssim_loss_grad_f64": (ctypes.c_int, [P, P, I64, I64, D, P, P, P, SZ, P]),
     "mg_upsample_f64": (ctypes.c_int, [P, P, P, P, I64, I64, P, P, P, P, P]),
     "mg_nrf_f64_workspace_bytes": (SZ, [I64]),
-    "mg_nrf_forward_f64": (ctypes.c_int, [P, I64, P, P, P, P, SZ, P]),
-    "mg_nrf_backward_f64": (ctypes.c_int, [P, I64, P, P, P, P, P, P, P, SZ, P]),
+    "mg_nrf_forward_f64": (ctypes.c_int, [P, I64, P, P, P, I32, I32, D, P, P, SZ, P]),
+    "mg_nrf_backward_f64": (ctypes.c_int, [P, I64, P, P, P, I32, I32, D, P, P, P, P, P, SZ, P]),
     "mg_block_workspace_bytes": (SZ, [I64, I64, I64]),
     "mg_block_forward": (ctypes.c_int, [P, P, I64, P, P, I64, P, P, P, I64, P, P, I64, I64, P, P, P, P, SZ, P]),
     "mg_block_backward": (ctypes.c_int,

@@ -513,21 +513,25 @@ int mg_upsample_f64(const double* q_old, const double* s_old, const double* l_ol
 
 size_t mg_nrf_f64_workspace_bytes(int64_t b) { return b < 0 ? 0 : nrf64_workspace_bytes(b); }
 
-int mg_nrf_forward_f64(const double* x, int64_t b, const double* const* w, const double* const* bias, double* r_out,
-                       void* ws, size_t wsb, void* stream) {
-  if (b < 0 || !w || !bias) return fail("mg_nrf_forward_f64: bad arguments");
+int mg_nrf_forward_f64(const double* x, int64_t b, const double* const* w, const double* const* bias,
+                       const int32_t* widths, int32_t depth, int32_t bands, double bound, double* r_out, void* ws,
+                       size_t wsb, void* stream) {
+  if (b < 0 || !w || !bias || !widths) return fail("mg_nrf_forward_f64: bad arguments");
   if (wsb < nrf64_workspace_bytes(b)) return fail("mg_nrf_forward_f64: workspace too small");
   if (b == 0) return 0;
-  launch_nrf64_forward(x, b, w, bias, r_out, ws, S(stream));
+  if (!launch_nrf64_forward(x, b, w, bias, widths, depth, bands, bound, r_out, ws, S(stream)))
+    return fail("mg_nrf_forward_f64: unsupported widths (<= 8 layers, widths <= 64, input 3 + 6 bands, output 1)");
   return cuda_status();
 }
 
 int mg_nrf_backward_f64(const double* x, int64_t b, const double* const* w, const double* const* bias,
-                        const double* upstream, double* d_points, double* const* dw, double* const* db, void* ws,
-                        size_t wsb, void* stream) {
-  if (b < 0 || !w || !bias || !dw || !db) return fail("mg_nrf_backward_f64: bad arguments");
+                        const int32_t* widths, int32_t depth, int32_t bands, double bound, const double* upstream,
+                        double* d_points, double* const* dw, double* const* db, void* ws, size_t wsb,
+                        void* stream) {
+  if (b < 0 || !w || !bias || !dw || !db || !widths) return fail("mg_nrf_backward_f64: bad arguments");
   if (wsb < nrf64_workspace_bytes(b)) return fail("mg_nrf_backward_f64: workspace too small");
-  launch_nrf64_backward(x, b, w, bias, upstream, d_points, dw, db, ws, S(stream));
+  if (!launch_nrf64_backward(x, b, w, bias, widths, depth, bands, bound, upstream, d_points, dw, db, ws, S(stream)))
+    return fail("mg_nrf_backward_f64: unsupported widths (<= 8 layers, widths <= 64, input 3 + 6 bands, output 1)");
   return cuda_status();
 }
 

@@ -9,32 +9,39 @@
 // order (warp-strided partial sums + a shuffle tree), so results are
 // run-to-run deterministic.
 //
-// Workspace (the reference's `cache`, nrf.py:140-145), doubles:
-//   enc  [39][b]        fourier_encode(x)                        (nrf.py:23-36)
-//   post [4][64][b]     silu(pre[l])  for the four hidden layers (nrf.py:121-125)
-//   pre  [4][64][b]     hidden pre-activations z = h W + b
+// Any reference configuration with widths <= 64 and <= 8 layers (the
+// production 39-64-64-64-64-1 and e.g. the acceptance suite's 15-8-8-1).
+// Workspace (the reference's `cache`, nrf.py:140-145), doubles, sized for the
+// maximum shape:
+//   enc  [64][b]        fourier_encode(x)                        (nrf.py:23-36)
+//   post [7][64][b]     silu(pre[l])  for the hidden layers      (nrf.py:121-125)
+//   pre  [7][64][b]     hidden pre-activations z = h W + b
 //   t    [b]            tanh of the output pre-activation        (nrf.py:126)
-//   dz   [4][64][b]     d/dz of the hidden layers (backward)     (nrf.py:165-172)
+//   dz   [7][64][b]     d/dz of the hidden layers (backward)     (nrf.py:165-172)
 //   dzo  [b]            d/dz of the output layer
 #include "mg_render.cuh"
 
 namespace mg {
 
 namespace {
-constexpr int kIn = 39, kH = 64, kDepth = 5, kBands = 6;
-constexpr double kBound = 0.1;
+constexpr int kMaxW = 64, kMaxDepth = 8;
 
+// Widths (fan_in of layer 0 = 3 + 6 bands, hidden <= 64, output 1), up to 8
+// layers: the reference's ResidualField.create(frequency_bands, hidden)
+// (nrf.py:58-83) for any such configuration.
 struct Nrf64Params {
-  const double* w[kDepth];
-  const double* b[kDepth];
+  const double* w[kMaxDepth];
+  const double* b[kMaxDepth];
+  int width[kMaxDepth + 1];
+  int depth, bands;
+  double bound;
+  __host__ __device__ int fan_in(int l) const { return width[l]; }
+  __host__ __device__ int fan_out(int l) const { return width[l + 1]; }
 };
 struct Nrf64Grads {
-  double* w[kDepth];
-  double* b[kDepth];
+  double* w[kMaxDepth];
+  double* b[kMaxDepth];
 };
-
-__host__ __device__ constexpr int fan_in(int l) { return l == 0 ? kIn : kH; }
-__host__ __device__ constexpr int fan_out(int l) { return l == kDepth - 1 ? 1 : kH; }
 
 struct Ws64 {
   double *enc, *post, *pre, *t, *dz, *dzo;
@@ -43,15 +50,15 @@ __host__ __device__ inline Ws64 carve64(void* ws, int64_t b) {
   double* p = (double*)ws;
   Ws64 w;
   w.enc = p;
-  p += (int64_t)kIn * b;
+  p += (int64_t)kMaxW * b;
   w.post = p;
-  p += (int64_t)4 * kH * b;
+  p += (int64_t)(kMaxDepth - 1) * kMaxW * b;
   w.pre = p;
-  p += (int64_t)4 * kH * b;
+  p += (int64_t)(kMaxDepth - 1) * kMaxW * b;
   w.t = p;
   p += b;
   w.dz = p;
-  p += (int64_t)4 * kH * b;
+  p += (int64_t)(kMaxDepth - 1) * kMaxW * b;
   w.dzo = p;
   return w;
 }
@@ -60,7 +67,7 @@ __device__ __forceinline__ double sigmoid64(double z) { return 1.0 / (1.0 + exp(
 
 // h(l): the input activations of layer l for point p, feature-major.
 __device__ __forceinline__ const double* layer_input(const Ws64& W, int l, int64_t b) {
-  return l == 0 ? W.enc : W.post + (int64_t)(l - 1) * kH * b;
+  return l == 0 ? W.enc : W.post + (int64_t)(l - 1) * kMaxW * b;
 }
 
 __global__ void __launch_bounds__(128) nrf64_fwd_kernel(const double* __restrict__ x, int64_t b, Nrf64Params P,
@@ -69,7 +76,7 @@ __global__ void __launch_bounds__(128) nrf64_fwd_kernel(const double* __restrict
     // fourier_encode (nrf.py:23-36): [x, sin(2^k pi x), cos(2^k pi x)]
     double xs[3] = {x[3 * p], x[3 * p + 1], x[3 * p + 2]};
     for (int a = 0; a < 3; ++a) W.enc[(int64_t)a * b + p] = xs[a];
-    for (int k = 0; k < kBands; ++k) {
+    for (int k = 0; k < P.bands; ++k) {
       const double f = ldexp(3.141592653589793, k);  // (2.0**k) * np.pi, exact
       for (int a = 0; a < 3; ++a) {
         double s, c;
@@ -78,20 +85,20 @@ __global__ void __launch_bounds__(128) nrf64_fwd_kernel(const double* __restrict
         W.enc[(int64_t)(6 + 6 * k + a) * b + p] = c;
       }
     }
-    for (int l = 0; l < kDepth; ++l) {
+    for (int l = 0; l < P.depth; ++l) {
       const double* h = layer_input(W, l, b);
-      const int fi = fan_in(l), fo = fan_out(l);
+      const int fi = P.fan_in(l), fo = P.fan_out(l);
       for (int j = 0; j < fo; ++j) {
         double z = 0.0;
         for (int i = 0; i < fi; ++i) z = fma(h[(int64_t)i * b + p], P.w[l][i * fo + j], z);
         z += P.b[l][j];
-        if (l < kDepth - 1) {
-          W.pre[((int64_t)l * kH + j) * b + p] = z;
-          W.post[((int64_t)l * kH + j) * b + p] = z * sigmoid64(z);
+        if (l < P.depth - 1) {
+          W.pre[((int64_t)l * kMaxW + j) * b + p] = z;
+          W.post[((int64_t)l * kMaxW + j) * b + p] = z * sigmoid64(z);
         } else {
           const double t = tanh(z);
           W.t[p] = t;
-          r_out[p] = kBound * t;
+          r_out[p] = P.bound * t;
         }
       }
     }
@@ -101,39 +108,49 @@ __global__ void __launch_bounds__(128) nrf64_fwd_kernel(const double* __restrict
 __global__ void __launch_bounds__(128) nrf64_bwd_kernel(const double* __restrict__ x, int64_t b, Nrf64Params P,
                                                         Ws64 W, const double* __restrict__ up,
                                                         double* __restrict__ d_points) {
+  const int L = P.depth;
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < b; p += (int64_t)gridDim.x * blockDim.x) {
     const double t = W.t[p];
-    const double dzo = up[p] * kBound * (1.0 - t * t);  // nrf.py:164
+    const double dzo = up[p] * P.bound * (1.0 - t * t);  // nrf.py:164
     W.dzo[p] = dzo;
-    // hidden layer 3 from the output layer (fan_out 1)
-    for (int i = 0; i < kH; ++i) {
-      const double z = W.pre[((int64_t)3 * kH + i) * b + p], s = sigmoid64(z);
-      W.dz[((int64_t)3 * kH + i) * b + p] = dzo * P.w[4][i] * (s * (1.0 + z * (1.0 - s)));
+    // last hidden layer (L - 2) from the output layer (fan_out 1)
+    if (L >= 2) {
+      const int fo = P.fan_out(L - 2);
+      for (int i = 0; i < fo; ++i) {
+        const double z = W.pre[((int64_t)(L - 2) * kMaxW + i) * b + p], s = sigmoid64(z);
+        W.dz[((int64_t)(L - 2) * kMaxW + i) * b + p] = dzo * P.w[L - 1][i] * (s * (1.0 + z * (1.0 - s)));
+      }
     }
-    for (int l = 3; l >= 1; --l) {  // dh = dz W^T, dz_prev = dh * silu'(pre)   (nrf.py:165-172)
-      for (int i = 0; i < kH; ++i) {
+    for (int l = L - 2; l >= 1; --l) {  // dh = dz W^T, dz_prev = dh * silu'(pre)   (nrf.py:165-172)
+      const int fi = P.fan_in(l), fo = P.fan_out(l);
+      for (int i = 0; i < fi; ++i) {
         double dh = 0.0;
-        for (int j = 0; j < kH; ++j) dh = fma(W.dz[((int64_t)l * kH + j) * b + p], P.w[l][i * kH + j], dh);
-        const double z = W.pre[((int64_t)(l - 1) * kH + i) * b + p], s = sigmoid64(z);
-        W.dz[((int64_t)(l - 1) * kH + i) * b + p] = dh * (s * (1.0 + z * (1.0 - s)));
+        for (int j = 0; j < fo; ++j) dh = fma(W.dz[((int64_t)l * kMaxW + j) * b + p], P.w[l][i * fo + j], dh);
+        const double z = W.pre[((int64_t)(l - 1) * kMaxW + i) * b + p], s = sigmoid64(z);
+        W.dz[((int64_t)(l - 1) * kMaxW + i) * b + p] = dh * (s * (1.0 + z * (1.0 - s)));
       }
     }
     // d_enc = dz0 W0^T, then the encoding Jacobian (nrf.py:174-181)
+    const int fi0 = P.fan_in(0), fo0 = P.fan_out(0);
     double dp[3] = {0.0, 0.0, 0.0};
-    double denc[kIn];
-    for (int i = 0; i < kIn; ++i) {
+    for (int i = 0; i < fi0; ++i) {
       double dh = 0.0;
-      for (int j = 0; j < kH; ++j) dh = fma(W.dz[(int64_t)j * b + p], P.w[0][i * kH + j], dh);
-      denc[i] = dh;
-    }
-    for (int a = 0; a < 3; ++a) dp[a] = denc[a];
-    for (int k = 0; k < kBands; ++k) {
-      const double f = ldexp(3.141592653589793, k);
-      for (int a = 0; a < 3; ++a) {
+      if (L == 1) {
+        dh = dzo * P.w[0][i];
+      } else {
+        for (int j = 0; j < fo0; ++j) dh = fma(W.dz[(int64_t)j * b + p], P.w[0][i * fo0 + j], dh);
+      }
+      if (i < 3) {
+        dp[i] += dh;
+      } else {
+        const int k = (i - 3) / 6, a = (i - 3) % 6;
+        const double f = ldexp(3.141592653589793, k);
         double s, c;
-        sincos(f * x[3 * p + a], &s, &c);
-        dp[a] += f * c * denc[3 + 6 * k + a];
-        dp[a] -= f * s * denc[6 + 6 * k + a];
+        sincos(f * x[3 * p + (a % 3)], &s, &c);
+        if (a < 3)
+          dp[a] += f * c * dh;
+        else
+          dp[a - 3] -= f * s * dh;
       }
     }
     for (int a = 0; a < 3; ++a) d_points[3 * p + a] = dp[a];
@@ -142,19 +159,19 @@ __global__ void __launch_bounds__(128) nrf64_bwd_kernel(const double* __restrict
 
 // dW[l][i][j] = sum_p h_l[i][p] dz_l[j][p];  db[l][j] = sum_p dz_l[j][p].
 // One warp per output element (output index = global warp id over all layers).
-__global__ void __launch_bounds__(256) nrf64_dw_kernel(int64_t b, Ws64 W, Nrf64Grads G) {
+__global__ void __launch_bounds__(256) nrf64_dw_kernel(int64_t b, Nrf64Params P, Ws64 W, Nrf64Grads G) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int64_t e = warp;
   int l = 0;
-  for (; l < kDepth; ++l) {
-    const int64_t nl = (int64_t)(fan_in(l) + 1) * fan_out(l);  // weights + biases of layer l
+  for (; l < P.depth; ++l) {
+    const int64_t nl = (int64_t)(P.fan_in(l) + 1) * P.fan_out(l);  // weights + biases of layer l
     if (e < nl) break;
     e -= nl;
   }
-  if (l >= kDepth) return;
-  const int fi = fan_in(l), fo = fan_out(l);
-  const double* dz = l == kDepth - 1 ? W.dzo : W.dz + (int64_t)l * kH * b;
+  if (l >= P.depth) return;
+  const int fi = P.fan_in(l), fo = P.fan_out(l);
+  const double* dz = l == P.depth - 1 ? W.dzo : W.dz + (int64_t)l * kMaxW * b;
   const int j = (int)(e % fo);
   const int i = (int)(e / fo);  // i == fi: bias
   const double* dzj = dz + (int64_t)j * b;
@@ -179,28 +196,48 @@ unsigned grid_for(int64_t n, int thr) {
   if (g > 148 * 16) g = 148 * 16;
   return (unsigned)(g < 1 ? 1 : g);
 }
+
+bool make_params(Nrf64Params& P, const double* const* w, const double* const* bias, const int* widths, int depth,
+                 int bands, double bound) {
+  if (depth < 1 || depth > kMaxDepth || bands < 0 || 3 + 6 * bands > kMaxW) return false;
+  if (widths[0] != 3 + 6 * bands || widths[depth] != 1) return false;
+  for (int l = 0; l <= depth; ++l)
+    if (widths[l] < 1 || widths[l] > kMaxW) return false;
+  for (int l = 0; l < depth; ++l) P.w[l] = w[l], P.b[l] = bias[l];
+  for (int l = 0; l <= depth; ++l) P.width[l] = widths[l];
+  P.depth = depth;
+  P.bands = bands;
+  P.bound = bound;
+  return true;
+}
 }  // namespace
 
-size_t nrf64_workspace_bytes(int64_t b) { return (size_t)(kIn + 12 * kH + 2) * (size_t)b * sizeof(double) + 256; }
-
-void launch_nrf64_forward(const double* x, int64_t b, const double* const* w, const double* const* bias, double* r,
-                          void* ws, cudaStream_t st) {
-  Nrf64Params P;
-  for (int l = 0; l < kDepth; ++l) P.w[l] = w[l], P.b[l] = bias[l];
-  MG_LAUNCH(nrf64_fwd_kernel<<<grid_for(b, 128), 128, 0, st>>>(x, b, P, carve64(ws, b), r));
+size_t nrf64_workspace_bytes(int64_t b) {
+  return (size_t)(kMaxW + 3 * (kMaxDepth - 1) * kMaxW + 2) * (size_t)b * sizeof(double) + 256;
 }
 
-void launch_nrf64_backward(const double* x, int64_t b, const double* const* w, const double* const* bias,
-                           const double* up, double* d_points, double* const* dw, double* const* db, void* ws,
-                           cudaStream_t st) {
+bool launch_nrf64_forward(const double* x, int64_t b, const double* const* w, const double* const* bias,
+                          const int* widths, int depth, int bands, double bound, double* r, void* ws,
+                          cudaStream_t st) {
   Nrf64Params P;
+  if (!make_params(P, w, bias, widths, depth, bands, bound)) return false;
+  MG_LAUNCH(nrf64_fwd_kernel<<<grid_for(b, 128), 128, 0, st>>>(x, b, P, carve64(ws, b), r));
+  return true;
+}
+
+bool launch_nrf64_backward(const double* x, int64_t b, const double* const* w, const double* const* bias,
+                           const int* widths, int depth, int bands, double bound, const double* up,
+                           double* d_points, double* const* dw, double* const* db, void* ws, cudaStream_t st) {
+  Nrf64Params P;
+  if (!make_params(P, w, bias, widths, depth, bands, bound)) return false;
   Nrf64Grads G;
-  for (int l = 0; l < kDepth; ++l) P.w[l] = w[l], P.b[l] = bias[l], G.w[l] = dw[l], G.b[l] = db[l];
+  for (int l = 0; l < depth; ++l) G.w[l] = dw[l], G.b[l] = db[l];
   const Ws64 W = carve64(ws, b);
   MG_LAUNCH(nrf64_bwd_kernel<<<grid_for(b, 128), 128, 0, st>>>(x, b, P, W, up, d_points));
   int64_t outs = 0;
-  for (int l = 0; l < kDepth; ++l) outs += (int64_t)(fan_in(l) + 1) * fan_out(l);
-  MG_LAUNCH(nrf64_dw_kernel<<<(unsigned)((outs * 32 + 255) / 256), 256, 0, st>>>(b, W, G));
+  for (int l = 0; l < depth; ++l) outs += (int64_t)(widths[l] + 1) * widths[l + 1];
+  MG_LAUNCH(nrf64_dw_kernel<<<(unsigned)((outs * 32 + 255) / 256), 256, 0, st>>>(b, P, W, G));
+  return true;
 }
 
 }  // namespace mg

@@ -93,11 +93,12 @@ void launch_ssim_f64(const double* pred, const double* tgt, int H, int W, double
 void launch_upsample_f64(const double* q_old, const double* s_old, const double* l_old, const int* node_of_old,
                          int ro, int rn, double* pos, double* q, double* s, double* l, cudaStream_t st);
 size_t nrf64_workspace_bytes(int64_t b);
-void launch_nrf64_forward(const double* x, int64_t b, const double* const* w, const double* const* bias, double* r,
-                          void* ws, cudaStream_t st);
-void launch_nrf64_backward(const double* x, int64_t b, const double* const* w, const double* const* bias,
-                           const double* up, double* d_points, double* const* dw, double* const* db, void* ws,
-                           cudaStream_t st);
+bool launch_nrf64_forward(const double* x, int64_t b, const double* const* w, const double* const* bias,
+                          const int* widths, int depth, int bands, double bound, double* r, void* ws,
+                          cudaStream_t st);
+bool launch_nrf64_backward(const double* x, int64_t b, const double* const* w, const double* const* bias,
+                           const int* widths, int depth, int bands, double bound, const double* up,
+                           double* d_points, double* const* dw, double* const* db, void* ws, cudaStream_t st);
 
 // tensor-core (tcgen05) NRF layers and the self-test GEMM (mg_nrf_tc.cu)
 bool nrf_use_tc();

@@ -173,7 +173,8 @@ def nrf_forward(field: ResidualField, x):
 class ResidualField64:
     """The residual network with float64 host weights (the reference's own
     representation, nrf.py:49-101), evaluated by the float64 kernels of
-    mg_nrf64.cu.  Used by train.StrictTrainer."""
+    mg_nrf64.cu: any widths <= 64 with <= 8 layers.  Used by
+    train.StrictTrainer and the host-level nrf_forward64 / nrf_backward64."""
 
     frequency_bands: int = DEFAULT_BANDS
     layer_widths: tuple = ()
@@ -197,10 +198,11 @@ class ResidualField64:
 def _require_f64(field: ResidualField64):
     if not field.weights:
         raise UninitializedField("residual field has no weights")
-    if tuple(field.layer_widths) != FUSED_WIDTHS or field.frequency_bands != DEFAULT_BANDS or \
-            field.output_bound != OUTPUT_BOUND:
+    w = tuple(int(x) for x in field.layer_widths)
+    if (len(w) < 2 or len(w) > 9 or w[0] != 3 + 6 * int(field.frequency_bands) or w[-1] != 1
+            or max(w) > 64 or min(w) < 1):
         raise UnsupportedResidualField(
-            f"float64 NRF kernels implement the reference widths {FUSED_WIDTHS} with 6 bands and output bound 0.1")
+            f"float64 NRF kernels take widths <= 64 and <= 8 layers (input 3 + 6 bands, output 1); got {w}")
 
 
 class Nrf64Cache:
@@ -212,6 +214,10 @@ class Nrf64Cache:
 
         self.x = x
         self.n = int(x.shape[0])
+        self.widths = (ctypes.c_int32 * len(field.layer_widths))(*[int(v) for v in field.layer_widths])
+        self.depth = len(field.layer_widths) - 1
+        self.bands = int(field.frequency_bands)
+        self.bound = float(field.output_bound)
         self.w = [dv.to_dev(np.ascontiguousarray(w), torch.float64) for w in field.weights]
         self.b = [dv.to_dev(np.ascontiguousarray(b), torch.float64) for b in field.biases]
         self.ws = torch.empty((max(1, N.lib().mg_nrf_f64_workspace_bytes(self.n)),), dtype=torch.uint8,
@@ -227,8 +233,9 @@ def nrf_forward_cached_f64(field: ResidualField64, x: torch.Tensor):
 
     r = torch.empty((c.n,), dtype=torch.float64, device=x.device)
     w, b = _ptr_array(c.w), _ptr_array(c.b)  # kept alive across the call
-    N.check(N.lib().mg_nrf_forward_f64(N.ptr(x), c.n, ctypes.addressof(w), ctypes.addressof(b), N.ptr(r),
-                                       N.ptr(c.ws), c.ws.numel(), dv.sptr()), "nrf_forward_f64")
+    N.check(N.lib().mg_nrf_forward_f64(N.ptr(x), c.n, ctypes.addressof(w), ctypes.addressof(b),
+                                       ctypes.addressof(c.widths), c.depth, c.bands, c.bound, N.ptr(r), N.ptr(c.ws),
+                                       c.ws.numel(), dv.sptr()), "nrf_forward_f64")
     return r, c
 
 
@@ -244,7 +251,25 @@ def nrf_backward_f64(cache: Nrf64Cache, upstream: torch.Tensor):
 
     dp = torch.empty((cache.n, 3), dtype=torch.float64, device=up.device)
     w, b, gw, gb = _ptr_array(cache.w), _ptr_array(cache.b), _ptr_array(dws), _ptr_array(dbs)
-    N.check(N.lib().mg_nrf_backward_f64(N.ptr(cache.x), cache.n, ctypes.addressof(w), ctypes.addressof(b), N.ptr(up),
-                                        N.ptr(dp), ctypes.addressof(gw), ctypes.addressof(gb), N.ptr(cache.ws),
-                                        cache.ws.numel(), dv.sptr()), "nrf_backward_f64")
+    N.check(N.lib().mg_nrf_backward_f64(N.ptr(cache.x), cache.n, ctypes.addressof(w), ctypes.addressof(b),
+                                        ctypes.addressof(cache.widths), cache.depth, cache.bands, cache.bound,
+                                        N.ptr(up), N.ptr(dp), ctypes.addressof(gw), ctypes.addressof(gb),
+                                        N.ptr(cache.ws), cache.ws.numel(), dv.sptr()), "nrf_backward_f64")
     return [dv.to_host(w) for w in dws], [dv.to_host(b) for b in dbs], dp
+
+
+def nrf_forward64(field: ResidualField64, x):
+    """Host-facing r(x), float64 numpy in and out (nrf.py:132-137)."""
+    xt = dv.to_dev(np.atleast_2d(np.asarray(x, dtype=np.float64)), torch.float64)
+    r, _ = nrf_forward_cached_f64(field, xt)
+    r = dv.to_host(r)
+    return float(r[0]) if np.asarray(x).ndim == 1 else r
+
+
+def nrf_backward64(field: ResidualField64, x, upstream):
+    """(d_weights, d_biases, d_points) of sum_b upstream[b] r(x_b), float64
+    numpy (nrf.py:147-182)."""
+    xt = dv.to_dev(np.atleast_2d(np.asarray(x, dtype=np.float64)), torch.float64)
+    _, cache = nrf_forward_cached_f64(field, xt)
+    dws, dbs, dp = nrf_backward_f64(cache, dv.to_dev(np.asarray(upstream, np.float64).reshape(-1), torch.float64))
+    return dws, dbs, dv.to_host(dp)

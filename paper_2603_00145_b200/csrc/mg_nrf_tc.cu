@@ -145,7 +145,7 @@ constexpr int kTE = 39;       // encoding width
 constexpr int kTK0 = 48;      // padded layer-0 K (multiple of 16)
 constexpr int kTBands = 6;
 constexpr int kTThr = 256;
-constexpr float kTOut = 0.1f;
+constexpr float kTOut = 0.099999994f;  // the largest float32 not above 0.1 (see mg_nrf.cu)
 
 struct NrfTcSmem {
   unsigned short w[4][3][kTN * kTN];  // B operands (K-major core-matrix layout), three bf16 parts

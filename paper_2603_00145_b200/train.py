@@ -205,6 +205,14 @@ class DeviceField:
     def count(self):
         return int(self.positions.shape[0])
 
+    @property
+    def lattice_dims(self):  # GaussianField's name (core.py:250-301)
+        return (self.resolution,) * 3
+
+    @property
+    def intensity_logits(self):
+        return self.logits
+
     def to_host(self):
         from .core import GaussianField
 
@@ -1116,43 +1124,23 @@ class Trainer:
 
 
 def smooth_l1_loss_grad(pred, target):
-    """(mean Huber loss, d/dpred) computed by the device kernel (float64 in
-    strict mode, render.set_strict_fp64)."""
-    from . import render
-
-    if render.get_strict_fp64():
-        p = dv.to_dev(np.asarray(pred, dtype=np.float64).ravel(), torch.float64)
-        t = dv.to_dev(np.asarray(target, dtype=np.float64).ravel(), torch.float64)
-        up = dv.empty(p.shape, torch.float64)
-        acc = dv.zeros((1,), torch.float64)
-        N.check(N.lib().mg_smooth_l1_f64(N.ptr(p), N.ptr(t), p.numel(), N.ptr(up), N.ptr(acc), dv.sptr()),
-                "smooth_l1_f64")
-        return float(acc.item()), dv.to_host(up)
-    p = dv.to_dev(np.asarray(pred, dtype=np.float64).ravel(), torch.float32)
-    t = dv.to_dev(np.asarray(target, dtype=np.float64).ravel(), torch.float32)
-    up = dv.empty(p.shape, torch.float32)
+    """(mean Huber loss, d/dpred) in float64 on the device (mg_smooth_l1_f64):
+    the host-level API takes and returns float64 like the reference."""
+    p = dv.to_dev(np.asarray(pred, dtype=np.float64).ravel(), torch.float64)
+    t = dv.to_dev(np.asarray(target, dtype=np.float64).ravel(), torch.float64)
+    up = dv.empty(p.shape, torch.float64)
     acc = dv.zeros((1,), torch.float64)
-    N.check(N.lib().mg_smooth_l1(N.ptr(p), N.ptr(t), p.numel(), N.ptr(up), N.ptr(acc), dv.sptr()), "smooth_l1")
-    return float(acc.item()), dv.to_host(up).astype(np.float64)
+    N.check(N.lib().mg_smooth_l1_f64(N.ptr(p), N.ptr(t), p.numel(), N.ptr(up), N.ptr(acc), dv.sptr()),
+            "smooth_l1_f64")
+    return float(acc.item()), dv.to_host(up)
 
 
 def ssim_loss_grad(pred, target):
-    """(1 - mean SSIM, d/dpred) of an (H, W) slice computed by the device
-    kernels (float64 prediction and gradient in strict mode)."""
-    from . import render
+    """(1 - mean SSIM, d/dpred) of an (H, W) slice, float64 on the device
+    (ssim.ssim_loss_grad)."""
+    from .ssim import ssim_loss_grad as _ssim
 
-    pred = np.asarray(pred, dtype=np.float64)
-    h, w = pred.shape
-    strict = render.get_strict_fp64()
-    ty = torch.float64 if strict else torch.float32
-    p = dv.to_dev(pred.ravel(), ty)
-    t = dv.to_dev(np.asarray(target, dtype=np.float64).ravel(), ty)
-    up = dv.empty(p.shape, ty)
-    acc = dv.zeros((1,), torch.float64)
-    ws = dv.empty((N.lib().mg_ssim_workspace_bytes(h, w),), torch.uint8)
-    fn = N.lib().mg_ssim_loss_grad_f64 if strict else N.lib().mg_ssim_loss_grad
-    N.check(fn(N.ptr(p), N.ptr(t), h, w, 1.0, N.ptr(up), N.ptr(acc), N.ptr(ws), ws.numel(), dv.sptr()), "ssim")
-    return 1.0 - float(acc.item()) / ((h - 10) * (w - 10)), dv.to_host(up).astype(np.float64).reshape(h, w)
+    return _ssim(pred, target)
 
 
 # ---------------------------------------------------------------------------
@@ -1198,54 +1186,43 @@ def aniso_loss(field, lambda_ratio):
 
 
 def progressive_upsample(field, new_resolution):
-    """train.py:157-218 on the device (mg_upsample): trilinear logits and
-    log-scales, sign-aligned NLERP quaternions, positions on the new lattice.
-    Interpolation runs in float32 (the trainer's parameter precision)."""
+    """train.py:157-218 on the device (mg_upsample_f64): trilinear logits and
+    log-scales, sign-aligned NLERP quaternions, positions on the new lattice,
+    in float64 like the reference (the trainer's own float32 state uses
+    progressive_upsample_device)."""
     from .core import GaussianField
-
-    from . import render
 
     new_r = int(new_resolution)
     old_r = int(field.lattice_dims[0])
     if new_r < old_r:
         raise ShrinkNotAllowed(f"cannot shrink lattice {old_r} -> {new_r}")
-    if render.get_strict_fp64():  # float64 interpolation (mg_upsample_f64)
-        li = np.asarray(field.lattice_index, dtype=np.int64)
-        node_of = np.empty(field.count, np.int32)
-        node_of[(li[:, 0] * old_r + li[:, 1]) * old_r + li[:, 2]] = np.arange(field.count, dtype=np.int32)
-        n = new_r ** 3
-        out = [dv.empty((n, c), torch.float64) for c in (3, 4, 3, 1)]
-        src = [dv.to_dev(field.quaternions, torch.float64), dv.to_dev(field.log_scales, torch.float64),
-               dv.to_dev(field.intensity_logits, torch.float64), dv.to_dev(node_of, torch.int32)]
-        N.check(N.lib().mg_upsample_f64(*[N.ptr(t) for t in src], old_r, new_r, *[N.ptr(o) for o in out],
-                                        dv.sptr()), "upsample_f64")
-        pos, q, sc, lg = (dv.to_host(o) for o in out)
-        return GaussianField(pos, q, sc, lg.reshape(n), (new_r, new_r, new_r), lattice_node_index(new_r))
-    up = progressive_upsample_device(DeviceField.from_host(field), new_r).to_host()
-    return GaussianField(lattice_node_positions(new_r), up.quaternions, up.log_scales, up.intensity_logits,
-                         (new_r, new_r, new_r), lattice_node_index(new_r))
+    li = np.asarray(field.lattice_index, dtype=np.int64)
+    node_of = np.empty(field.count, np.int32)
+    node_of[(li[:, 0] * old_r + li[:, 1]) * old_r + li[:, 2]] = np.arange(field.count, dtype=np.int32)
+    n = new_r ** 3
+    out = [dv.empty((n, c), torch.float64) for c in (3, 4, 3, 1)]
+    src = [dv.to_dev(field.quaternions, torch.float64), dv.to_dev(field.log_scales, torch.float64),
+           dv.to_dev(field.intensity_logits, torch.float64), dv.to_dev(node_of, torch.int32)]
+    N.check(N.lib().mg_upsample_f64(*[N.ptr(t) for t in src], old_r, new_r, *[N.ptr(o) for o in out], dv.sptr()),
+            "upsample_f64")
+    pos, q, sc, lg = (dv.to_host(o) for o in out)
+    return GaussianField(pos, q, sc, lg.reshape(n), (new_r, new_r, new_r), lattice_node_index(new_r))
 
 
 def init_field(cloud, resolution, logit_eps=1e-4):
     """Uniform lattice field with logit(mean sample intensity) per cell
-    (train.py:221-236) on the device (mg_cell_keys_f64 + segmented means)."""
+    (train.py:221-236) on the device (mg_cell_keys_f64 + segmented float64
+    means)."""
     from .core import GaussianField
-
-    from . import render
 
     r = int(resolution)
     coords = dv.to_dev(np.asarray(cloud.coords, np.float64).reshape(-1, 3), torch.float64)
-    if render.get_strict_fp64():  # float64 cell means and logits
-        lg = _init_logits(coords, dv.to_dev(np.asarray(cloud.intensities, np.float64).ravel(), torch.float64), r,
-                          logit_eps)
-        n = r ** 3
-        q = np.zeros((n, 4))
-        q[:, 0] = 1.0
-        return GaussianField(lattice_node_positions(r), q, np.full((n, 3), np.log(1.0 / r)), dv.to_host(lg),
-                             (r, r, r), lattice_node_index(r))
-    f = init_field_device(coords, dv.to_dev(np.asarray(cloud.intensities, np.float64).ravel(), torch.float32), r,
-                          logit_eps).to_host()
-    return GaussianField(lattice_node_positions(r), f.quaternions, f.log_scales, f.intensity_logits, (r, r, r),
+    lg = _init_logits(coords, dv.to_dev(np.asarray(cloud.intensities, np.float64).ravel(), torch.float64), r,
+                      logit_eps)
+    n = r ** 3
+    q = np.zeros((n, 4))
+    q[:, 0] = 1.0
+    return GaussianField(lattice_node_positions(r), q, np.full((n, 3), np.log(1.0 / r)), dv.to_host(lg), (r, r, r),
                          lattice_node_index(r))
 
 

@@ -138,3 +138,41 @@ def test_strict_trainer_reproduces_perturbed_reference_runs(seed):
     _, db, _ = _run(True, seed)
     print(f"seed {seed}: strict {db:.6f} dB, reference {ref[seed]:.6f} dB")
     assert abs(db - ref[seed]) < 1e-3
+
+
+@pytest.mark.parametrize("switch", ["none", "no_ssim", "no_nrf", "no_aniso", "fixed_resolution"])
+def test_strict_trainer_config_switches_track_float32_trainer(switch):
+    """StrictTrainer honours the config switches the reference step branches on
+    (use_ssim, use_nrf, use_aniso, use_progressive; train.py:385-491): over 8
+    steps through a milestone and the NRF switch its losses track the float32
+    device trainer's to float32 rounding."""
+    from types import SimpleNamespace
+
+    from paper_2603_00145_b200.core import TransformSet
+    from paper_2603_00145_b200.strict_train import StrictTrainer
+    from paper_2603_00145_b200.train import TrainConfig, Trainer
+
+    rng = np.random.default_rng(5)
+    coords = rng.uniform(-0.9, 0.9, (6000, 3))
+    cloud = SimpleNamespace(coords=coords, intensities=np.exp(-np.sum(coords ** 2, axis=1) / 0.3) * 0.8,
+                            slice_ids=np.zeros(6000, dtype=np.int64))
+    axis = np.linspace(-0.9, 0.9, 16)
+    gx, gy = np.meshgrid(axis, axis, indexing="ij")
+    grid = SimpleNamespace(coords=np.stack([gx.ravel(), gy.ravel(), np.zeros(256)], axis=1),
+                           target=np.exp(-(gx ** 2 + gy ** 2) / 0.3) * 0.8, slice_id=0)
+    kw = dict(resolution_schedule=((0, 6), (4, 8)), total_iters=8, nrf_activation_iter=3, batch_points=1024, seed=3)
+    kw.update({"none": {}, "no_ssim": dict(use_ssim=False), "no_nrf": dict(use_nrf=False),
+               "no_aniso": dict(use_aniso=False), "fixed_resolution": dict(use_progressive=False)}[switch])
+    cfg = TrainConfig(**kw)
+    grids = [grid] if cfg.use_ssim else None
+    ts = TransformSet.identity(1)
+    a = StrictTrainer(cloud, ts, cfg, slice_grids=grids)
+    b = Trainer(cloud, ts, cfg, slice_grids=grids, graph=False)
+    la, lb = [], []
+    for _ in range(cfg.total_iters):
+        ra, rb = a.step(), b.step()
+        assert ra.resolution == rb.resolution and ra.nrf_active == rb.nrf_active
+        la.append([ra.total, ra.data, ra.ssim, ra.aniso])
+        lb.append([rb.total, rb.data, rb.ssim, rb.aniso])
+    np.testing.assert_allclose(np.array(lb), np.array(la), rtol=2e-3, atol=1e-7)
+    b.close()

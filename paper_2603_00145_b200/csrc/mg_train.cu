@@ -657,7 +657,8 @@ __global__ void upsample_kernel(const T* __restrict__ q_old, const T* __restrict
     for (int a = 0; a < 4; ++a) q[4 * id + a] = (T)(qs[a] / nrm);
     for (int a = 0; a < 3; ++a) s[3 * id + a] = (T)sc[a];
     l[id] = (T)lo;
-    for (int a = 0; a < 3; ++a) pos[3 * id + a] = (T)(-1.0 + ((double)c3[a] + 0.5) * (2.0 / rn));
+    // lattice_node_positions (core.py:304-309): -1 + (c + 0.5) * (2 / r), no FMA contraction
+    for (int a = 0; a < 3; ++a) pos[3 * id + a] = (T)__dadd_rn(-1.0, __dmul_rn((double)c3[a] + 0.5, 2.0 / rn));
   }
 }
 

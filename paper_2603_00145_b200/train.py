@@ -1205,8 +1205,9 @@ def progressive_upsample(field, new_resolution):
            dv.to_dev(field.intensity_logits, torch.float64), dv.to_dev(node_of, torch.int32)]
     N.check(N.lib().mg_upsample_f64(*[N.ptr(t) for t in src], old_r, new_r, *[N.ptr(o) for o in out], dv.sptr()),
             "upsample_f64")
-    pos, q, sc, lg = (dv.to_host(o) for o in out)
-    return GaussianField(pos, q, sc, lg.reshape(n), (new_r, new_r, new_r), lattice_node_index(new_r))
+    _, q, sc, lg = (dv.to_host(o) for o in out)
+    return GaussianField(lattice_node_positions(new_r), q, sc, lg.reshape(n), (new_r, new_r, new_r),
+                         lattice_node_index(new_r))
 
 
 def init_field(cloud, resolution, logit_eps=1e-4):
